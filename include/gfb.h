@@ -1,0 +1,265 @@
+/*
+ * gfb.h -- C ABI of the B200 gradient-program engine (libgfb.so).
+ *
+ * The reference executes forward and reverse-mode programs with a scalar
+ * Python tree-walking interpreter (gradflow, pkg/src/gradflow/interpreter.py).
+ * The host lowering in paper_2509_02197_b200/lowering.py walks the same IR
+ * and issues these entry points instead; each one replaces one interpreter
+ * routine, cited per entry below.
+ *
+ * Conventions
+ *   - plain C types only: device pointers, int64 extents/offsets, doubles;
+ *   - every call is asynchronous on the given cudaStream_t (passed as void*);
+ *   - no allocation inside a call: workspaces are passed in;
+ *   - return 0 on success, a GFB_E* status otherwise (launch/config errors);
+ *   - arithmetic-domain faults inside kernels (x/0, log(<=0), ...) are
+ *     reported through the device error word `err` (GFB_EBIT_* bits), which
+ *     the host reads after the stream synchronises and maps to the
+ *     reference's DomainError (pkg/src/gradflow/errors.py:56).
+ */
+#ifndef GFB_H
+#define GFB_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define GFB_ABI_VERSION 3
+
+#define GFB_MAX_PARAMS 8    /* map parameters (iteration-space rank) */
+#define GFB_MAX_RANK 8      /* array rank */
+#define GFB_MAX_INPUTS 8    /* operands read by one tasklet */
+#define GFB_MAX_OUTPUTS 8   /* outputs written by one tasklet */
+#define GFB_MAX_CODE 128    /* bytecode length (all outputs together) */
+#define GFB_MAX_CONSTS 24
+#define GFB_MAX_TAPS 32     /* taps of one linear stencil */
+#define GFB_MAX_SRCS 4      /* source arrays of one linear stencil */
+
+enum gfb_dtype { GFB_F32 = 0, GFB_F64 = 1 };
+
+enum gfb_status {
+  GFB_OK = 0,
+  GFB_EINVAL = 1,      /* malformed descriptor */
+  GFB_ECUDA = 2,       /* CUDA launch failure */
+  GFB_EUNSUPPORTED = 3 /* shape outside what the kernel family handles */
+};
+
+/* device error word bits (eager domain errors, reference symexpr.py:81-133) */
+#define GFB_EBIT_DIV0 0x1u
+#define GFB_EBIT_LOG 0x2u
+#define GFB_EBIT_SQRT 0x4u
+#define GFB_EBIT_POW 0x8u
+#define GFB_EBIT_IDIV0 0x10u
+#define GFB_EBIT_MOD0 0x20u
+
+/* tasklet bytecode (postfix; one segment per output connector) */
+enum gfb_op {
+  GFB_OP_IN = 0,    /* push input operand [arg] at the current point */
+  GFB_OP_CONST = 1, /* push consts[arg] */
+  GFB_OP_ADD, GFB_OP_SUB, GFB_OP_MUL, GFB_OP_DIV, GFB_OP_IDIV, GFB_OP_MOD,
+  GFB_OP_MIN, GFB_OP_MAX, GFB_OP_POW,
+  GFB_OP_NEG, GFB_OP_SIN, GFB_OP_COS, GFB_OP_EXP, GFB_OP_LOG, GFB_OP_SQRT,
+  GFB_OP_TANH, GFB_OP_ABS, GFB_OP_SIGN,
+  GFB_OP_COUNT
+};
+
+/*
+ * Map iteration space (reference MapNode, ir.py:107-116): parameter p runs
+ * over [lo_p, hi_p) with step st_p, where lo_p / hi_p are affine in the
+ * earlier parameters (triangular spaces):
+ *     lo_p = lo0[p] + sum_{q<p} loc[p][q] * x_q     (same for hi)
+ * box_lo/box_ext is the host-computed bounding box the thread grid covers.
+ */
+typedef struct {
+  int32_t nparams;
+  int32_t triangular; /* 0: ranges independent (box == space) */
+  int64_t lo0[GFB_MAX_PARAMS];
+  int64_t hi0[GFB_MAX_PARAMS];
+  int64_t step[GFB_MAX_PARAMS];
+  int64_t loc[GFB_MAX_PARAMS][GFB_MAX_PARAMS];
+  int64_t hic[GFB_MAX_PARAMS][GFB_MAX_PARAMS];
+  int64_t box_lo[GFB_MAX_PARAMS];
+  int64_t box_ext[GFB_MAX_PARAMS]; /* number of points along p in the box */
+} gfb_space;
+
+/* One memlet endpoint: element offset = c0 + sum_p s[p] * x_p (elements). */
+typedef struct {
+  void *base;
+  int32_t dtype;
+  int32_t _pad;
+  int64_t c0;
+  int64_t s[GFB_MAX_PARAMS];
+} gfb_operand;
+
+/*
+ * Pointwise map: one thread per iteration point, every output written by the
+ * point that computes it (reference Executor._exec_map + _exec_tasklet,
+ * interpreter.py:478-507, :405-426). Host lowering guarantees the outputs are
+ * point-private (injective subsets, no cross-point read-after-write), so the
+ * per-point read-all-then-write order of the reference is preserved.
+ *   wcr[o] = 0 overwrite, 1 sum (plain read-modify-write), 2 sum (atomic)
+ */
+typedef struct {
+  gfb_space space;
+  int32_t n_in, n_out;
+  int32_t compute_f64;
+  int32_t ncode;
+  gfb_operand in[GFB_MAX_INPUTS];
+  gfb_operand out[GFB_MAX_OUTPUTS];
+  int32_t wcr[GFB_MAX_OUTPUTS];
+  int32_t code_start[GFB_MAX_OUTPUTS];
+  int32_t code_len[GFB_MAX_OUTPUTS];
+  uint8_t code[GFB_MAX_CODE];
+  uint8_t arg[GFB_MAX_CODE];
+  double consts[GFB_MAX_CONSTS];
+  uint32_t *err;
+} gfb_map_desc;
+
+/*
+ * Gather pass: the scatter-add outputs of one map that land in one array D
+ * (wcr="sum" memlets, reference autodiff.py:1053-1060) executed output-
+ * stationary and atomic-free. Thread groups own target elements y of D inside
+ * ybox; for each contributing output memlet ("term") the map parameters are
+ * split into pivots (solved from y) and free parameters (looped):
+ *     x_piv = (y_row - off_row - sum_{q != piv} C[row][q] x_q) / C[row][piv]
+ * Every candidate point is range- and step-checked against the space.
+ * Result: D[y] = base(y) + sum_terms sum_points body(x), where base(y) is
+ *     clear_mode 0: D[y]                    (accumulate)
+ *     clear_mode 1: 0                       (target known zero: overwrite)
+ *     clear_mode 2: y in clear box ? 0 : D[y]  (folded pending gradient clear)
+ * Large free loops split over `nsplit` CTAs per target tile; partials then go
+ * to `workspace` ([nsplit][|ybox|] of the target dtype) and gfb_gather_launch
+ * finishes them with a deterministic second pass.
+ */
+typedef struct {
+  int32_t row_of[GFB_MAX_PARAMS];   /* -1: free parameter, else pivot row */
+  int32_t order[GFB_MAX_PARAMS];    /* evaluation order of the pivots */
+  int32_t npiv;
+  int32_t code_start, code_len;
+  int32_t _pad;
+  int64_t C[GFB_MAX_RANK][GFB_MAX_PARAMS]; /* subset coefficients (-1,0,1) */
+  int64_t off[GFB_MAX_RANK];
+} gfb_term;
+
+typedef struct {
+  gfb_space space;
+  int32_t rank;        /* rank of D */
+  int32_t dtype;       /* dtype of D */
+  int32_t compute_f64;
+  int32_t n_in;
+  int32_t n_terms;
+  int32_t clear_mode;
+  int32_t lanes_on_free; /* 1: a warp cooperates on one target (coalesced free loop) */
+  int32_t nsplit;
+  void *dst;
+  int64_t dst_strides[GFB_MAX_RANK];
+  int64_t ybox_lo[GFB_MAX_RANK];
+  int64_t ybox_ext[GFB_MAX_RANK];
+  int64_t clear_lo[GFB_MAX_RANK];
+  int64_t clear_hi[GFB_MAX_RANK];
+  int64_t free_lo[GFB_MAX_PARAMS];  /* per term-free parameter loop box */
+  int64_t free_ext[GFB_MAX_PARAMS];
+  gfb_operand in[GFB_MAX_INPUTS];
+  gfb_term terms[4];
+  uint8_t code[GFB_MAX_CODE];
+  uint8_t arg[GFB_MAX_CODE];
+  double consts[GFB_MAX_CONSTS];
+  void *workspace;
+  uint32_t *err;
+} gfb_gather_desc;
+
+/*
+ * Linear stencil sweep (fast path for maps whose tasklet is a constant-
+ * coefficient linear combination of shifted reads, and for the gather form
+ * of their adjoints; reference adj_map autodiff.py:962-1081):
+ *     D[y] = base(y) + sum_t [y in mask_t] * coef_t * S_{src_t}[y + delta_t]
+ * for y in [lo, hi) (rank <= 3, row-major, innermost dimension contiguous).
+ * base(y) follows gfb_gather_desc.clear_mode; mode 3 = pure overwrite of the
+ * region (forward sweep).
+ */
+typedef struct {
+  int32_t rank;
+  int32_t dtype;
+  int32_t clear_mode; /* 0 acc, 1/3 overwrite, 2 folded clear */
+  int32_t ntaps;
+  void *dst;
+  const void *src[GFB_MAX_SRCS];
+  int64_t dims[3];    /* dims of D (all arrays share the same dims) */
+  int64_t lo[3], hi[3];
+  int64_t clear_lo[3], clear_hi[3];
+  int32_t tap_src[GFB_MAX_TAPS];
+  int32_t tap_masked[GFB_MAX_TAPS];
+  int64_t tap_delta[GFB_MAX_TAPS][3];
+  int64_t tap_mlo[GFB_MAX_TAPS][3];
+  int64_t tap_mhi[GFB_MAX_TAPS][3];
+  double tap_coef[GFB_MAX_TAPS];
+} gfb_stencil_desc;
+
+/* ---- entry points --------------------------------------------------- */
+
+int gfb_abi_version(void);
+const char *gfb_last_error(void);
+int gfb_device_sm_count(void);
+/* sizes of gfb_space, gfb_operand, gfb_map_desc, gfb_term, gfb_gather_desc,
+ * gfb_stencil_desc (binding layout check); returns the count written */
+int gfb_struct_sizes(int64_t *out, int32_t cap);
+
+/* replaces Executor._exec_map / _exec_tasklet (interpreter.py:478-507, 405-426) */
+int gfb_map_launch(const gfb_map_desc *d, void *stream);
+/* replaces the wcr="sum" scatter of _exec_tasklet (interpreter.py:422-423) */
+int gfb_gather_launch(const gfb_gather_desc *d, void *stream);
+int64_t gfb_gather_workspace_bytes(const gfb_gather_desc *d);
+/* linear stencil fast path of _exec_map (interpreter.py:478-507) */
+int gfb_stencil_launch(const gfb_stencil_desc *d, void *stream);
+
+/* reduce_sum library node (interpreter.py:447-451): out (=|+=) sum(x[0:n]).
+ * workspace >= gfb_reduce_workspace_bytes(n) bytes; deterministic order. */
+int64_t gfb_reduce_workspace_bytes(int64_t n);
+int gfb_reduce_sum(const void *x, int32_t xdtype, int64_t n, void *out,
+                   int32_t odtype, int32_t accumulate, void *workspace,
+                   void *stream);
+
+/* ew_unary / ew_binary library nodes (interpreter.py:452-463, 553-597):
+ *   out[i] (= | +=) op(a[i] [, b[i]]); `op` is a gfb_op code, `c` the scale
+ *   constant; a scalar operand (n_a == 1) broadcasts. */
+int gfb_elementwise(int32_t op, double c, const void *a, int64_t n_a,
+                    const void *b, int64_t n_b, void *out, int64_t n,
+                    int32_t dtype, int32_t accumulate, uint32_t *err,
+                    void *stream);
+
+/* fill / broadcast (reduce_sum adjoint map, autodiff.py:940-960; zero-init on
+ * first touch, interpreter.py:171-189): out[i] (= | +=) scale * (*src or 1). */
+int gfb_broadcast(const void *src, int32_t src_dtype, double scale, void *out,
+                  int64_t n, int32_t dtype, int32_t accumulate, void *stream);
+
+/* box fill: D[y] = value for y in [lo, hi) (rank <= 3); materialised
+ * pending gradient clear (autodiff.py:735-740) */
+int gfb_fill_box(void *dst, int32_t dtype, int32_t rank, const int64_t *dims,
+                 const int64_t *lo, const int64_t *hi, double value,
+                 void *stream);
+
+/* matmul library node (interpreter.py:433-446; adjoint jobs autodiff.py:
+ * 780-802): C (= | +=) op(A) @ op(B), row-major, op = transpose if t*.
+ * fp64 runs on the DMMA tensor path, fp32 on the FFMA path. */
+int64_t gfb_matmul_workspace_bytes(int32_t dtype, int32_t ta, int32_t tb, int64_t M,
+                                   int64_t N, int64_t K);
+int gfb_matmul(int32_t dtype, int32_t ta, int32_t tb, int64_t M, int64_t N,
+               int64_t K, const void *A, int64_t lda, const void *B,
+               int64_t ldb, void *C, int64_t ldc, int32_t accumulate,
+               void *workspace, void *stream);
+
+/* device-to-device copy of n elements (tape snapshots, interpreter.py:371-386) */
+int gfb_copy(void *dst, const void *src, int64_t bytes, void *stream);
+
+/* halo planes for slab decomposition (multi-GPU stencils): pack/unpack
+ * `nplanes` contiguous outer-dimension planes starting at plane `p0`. */
+int gfb_plane_copy(void *dst, const void *src, int64_t plane_elems,
+                   int32_t dtype, int64_t nplanes, void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* GFB_H */

@@ -1,0 +1,139 @@
+"""ctypes binding of libgfb.so (the C ABI declared in include/gfb.h).
+
+The structures below mirror the C layouts field by field; ``load()`` checks
+the sizes against ``gfb_struct_sizes`` so a stale build fails loudly. There
+is no fallback: if the library is missing the engine raises EngineError.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+from .errors import EngineError
+
+P = 8   # GFB_MAX_PARAMS
+R = 8   # GFB_MAX_RANK
+MAXIN = 8
+MAXOUT = 8
+MAXCODE = 128
+MAXCONST = 24
+MAXTAPS = 32
+MAXSRCS = 4
+ABI_VERSION = 3
+
+F32, F64 = 0, 1
+
+# bytecode opcodes (enum gfb_op)
+OP_IN, OP_CONST, OP_ADD, OP_SUB, OP_MUL, OP_DIV, OP_IDIV, OP_MOD, OP_MIN, OP_MAX, OP_POW = range(11)
+OP_NEG, OP_SIN, OP_COS, OP_EXP, OP_LOG, OP_SQRT, OP_TANH, OP_ABS, OP_SIGN = range(11, 20)
+BINOP = {"add": OP_ADD, "sub": OP_SUB, "mul": OP_MUL, "div": OP_DIV, "idiv": OP_IDIV, "mod": OP_MOD,
+         "min": OP_MIN, "max": OP_MAX, "pow": OP_POW}
+UNOP = {"neg": OP_NEG, "sin": OP_SIN, "cos": OP_COS, "exp": OP_EXP, "log": OP_LOG, "sqrt": OP_SQRT,
+        "tanh": OP_TANH, "abs": OP_ABS, "sign": OP_SIGN}
+
+EBITS = {0x1: "division by zero", 0x2: "log of non-positive value", 0x4: "sqrt of negative value",
+         0x8: "pow outside its domain", 0x10: "floor division by zero", 0x20: "modulo by zero"}
+
+i32, i64, u8, f64, vp = C.c_int32, C.c_int64, C.c_uint8, C.c_double, C.c_void_p
+
+
+class Space(C.Structure):
+    _fields_ = [("nparams", i32), ("triangular", i32), ("lo0", i64 * P), ("hi0", i64 * P), ("step", i64 * P),
+                ("loc", (i64 * P) * P), ("hic", (i64 * P) * P), ("box_lo", i64 * P), ("box_ext", i64 * P)]
+
+
+class Operand(C.Structure):
+    _fields_ = [("base", vp), ("dtype", i32), ("_pad", i32), ("c0", i64), ("s", i64 * P)]
+
+
+class MapDesc(C.Structure):
+    _fields_ = [("space", Space), ("n_in", i32), ("n_out", i32), ("compute_f64", i32), ("ncode", i32),
+                ("in_", Operand * MAXIN), ("out", Operand * MAXOUT), ("wcr", i32 * MAXOUT),
+                ("code_start", i32 * MAXOUT), ("code_len", i32 * MAXOUT), ("code", u8 * MAXCODE),
+                ("arg", u8 * MAXCODE), ("consts", f64 * MAXCONST), ("err", vp)]
+
+
+class Term(C.Structure):
+    _fields_ = [("row_of", i32 * P), ("order", i32 * P), ("npiv", i32), ("code_start", i32), ("code_len", i32),
+                ("_pad", i32), ("C", (i64 * P) * R), ("off", i64 * R)]
+
+
+class GatherDesc(C.Structure):
+    _fields_ = [("space", Space), ("rank", i32), ("dtype", i32), ("compute_f64", i32), ("n_in", i32),
+                ("n_terms", i32), ("clear_mode", i32), ("lanes_on_free", i32), ("nsplit", i32), ("dst", vp),
+                ("dst_strides", i64 * R), ("ybox_lo", i64 * R), ("ybox_ext", i64 * R), ("clear_lo", i64 * R),
+                ("clear_hi", i64 * R), ("free_lo", i64 * P), ("free_ext", i64 * P), ("in_", Operand * MAXIN),
+                ("terms", Term * 4), ("code", u8 * MAXCODE), ("arg", u8 * MAXCODE), ("consts", f64 * MAXCONST),
+                ("workspace", vp), ("err", vp)]
+
+
+class StencilDesc(C.Structure):
+    _fields_ = [("rank", i32), ("dtype", i32), ("clear_mode", i32), ("ntaps", i32), ("dst", vp),
+                ("src", vp * MAXSRCS), ("dims", i64 * 3), ("lo", i64 * 3), ("hi", i64 * 3),
+                ("clear_lo", i64 * 3), ("clear_hi", i64 * 3), ("tap_src", i32 * MAXTAPS),
+                ("tap_masked", i32 * MAXTAPS), ("tap_delta", (i64 * 3) * MAXTAPS),
+                ("tap_mlo", (i64 * 3) * MAXTAPS), ("tap_mhi", (i64 * 3) * MAXTAPS), ("tap_coef", f64 * MAXTAPS)]
+
+
+_LIB = None
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libgfb.so")
+
+# (name, restype, argtypes)
+_SIGS = [
+    ("gfb_abi_version", i32, []),
+    ("gfb_last_error", C.c_char_p, []),
+    ("gfb_device_sm_count", i32, []),
+    ("gfb_struct_sizes", i32, [C.POINTER(i64), i32]),
+    ("gfb_map_launch", i32, [C.POINTER(MapDesc), vp]),
+    ("gfb_gather_launch", i32, [C.POINTER(GatherDesc), vp]),
+    ("gfb_gather_workspace_bytes", i64, [C.POINTER(GatherDesc)]),
+    ("gfb_stencil_launch", i32, [C.POINTER(StencilDesc), vp]),
+    ("gfb_reduce_workspace_bytes", i64, [i64]),
+    ("gfb_reduce_sum", i32, [vp, i32, i64, vp, i32, i32, vp, vp]),
+    ("gfb_elementwise", i32, [i32, f64, vp, i64, vp, i64, vp, i64, i32, i32, vp, vp]),
+    ("gfb_broadcast", i32, [vp, i32, f64, vp, i64, i32, i32, vp]),
+    ("gfb_fill_box", i32, [vp, i32, i32, C.POINTER(i64), C.POINTER(i64), C.POINTER(i64), f64, vp]),
+    ("gfb_matmul_workspace_bytes", i64, [i32, i32, i32, i64, i64, i64]),
+    ("gfb_matmul", i32, [i32, i32, i32, i64, i64, i64, vp, i64, vp, i64, vp, i64, i32, vp, vp]),
+    ("gfb_copy", i32, [vp, vp, i64, vp]),
+    ("gfb_plane_copy", i32, [vp, vp, i64, i32, i64, vp]),
+]
+
+EXPORTED = tuple(name for name, _, _ in _SIGS)
+
+
+def load(path: str | None = None):
+    """Load libgfb.so and bind every entry point (raises EngineError if absent)."""
+    global _LIB
+    if _LIB is not None and path is None:
+        return _LIB
+    p = path or os.environ.get("GFB_LIBRARY", LIB_PATH)
+    if not os.path.exists(p):
+        raise EngineError(f"CUDA engine library not built: {p} (run __graft_entry__.build())")
+    try:
+        lib = C.CDLL(p)
+    except OSError as exc:
+        raise EngineError(f"cannot load {p}: {exc}") from None
+    for name, res, args in _SIGS:
+        fn = getattr(lib, name)
+        fn.restype = res
+        fn.argtypes = args
+    if lib.gfb_abi_version() != ABI_VERSION:
+        raise EngineError(f"libgfb ABI {lib.gfb_abi_version()} != expected {ABI_VERSION}; rebuild")
+    sizes = (i64 * 8)()
+    n = lib.gfb_struct_sizes(sizes, 8)
+    want = [C.sizeof(Space), C.sizeof(Operand), C.sizeof(MapDesc), C.sizeof(Term), C.sizeof(GatherDesc),
+            C.sizeof(StencilDesc)]
+    got = list(sizes[:n])
+    if got[: len(want)] != want:
+        raise EngineError(f"struct layout mismatch between gfb.h and _lib.py: C {got} vs ctypes {want}")
+    if path is None:
+        _LIB = lib
+    return lib
+
+
+def check(rc: int, what: str):
+    if rc != 0:
+        msg = load().gfb_last_error().decode(errors="replace")
+        raise EngineError(f"{what} failed (status {rc}): {msg}")

@@ -1,0 +1,447 @@
+"""Reference-facing entry points, executed on the B200 engine.
+
+Mirrors the reference signatures so the engine is a drop-in for the hot
+path:
+
+* ``gradient(program, inputs, params=None, *, seed=1.0, trip_limit=None,
+  bundle=None) -> GradientResult`` (reference autodiff.py:1153-1184)
+* ``run_planned(result, inputs, params=None, *, seed=1.0, trip_limit=None)``
+  (reference checkpointing.py:903-957)
+* ``run_forward`` / ``run_backward`` (reference interpreter.py:621-695), the
+  executor-level seam.
+* ``plan(program, limit_mib, params=None, *, trip_limit=None)``: the ILP
+  planner is host code and stays the reference's own (checkpointing.py:
+  863-900); this wrapper calls it when the reference is installed.
+
+The AD transform (``build_backward``) and the planner are host-side and run
+once per (program, params, budget); on a machine without the reference they
+arrive as the reference's own serialized artifacts (``load_bundle``,
+``load_plan``: the ``gradflow diff`` / ``gradflow plan --emit`` files).
+Everything on the data path runs as CUDA launches; there is no CPU
+execution path.
+"""
+from __future__ import annotations
+
+import json
+import os
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from .errors import ShapeMismatch, UnboundName, UnsupportedConstruct
+from .ir import (
+    Program,
+    adopt,
+    adopt_forwarding,
+    dump_program,
+    eval_int,
+    forwarding_from_manifest,
+    load_program,
+    manifest_from_forwarding,
+    number_writes,
+    pristine_inputs,
+)
+from .lowering import Lowering, LTape, ProgramRun, required_record
+from .runtime import NP_DTYPE, Executable
+
+# ---------------------------------------------------------------------------
+# bundles (what the host AD / planner hands to the engine)
+
+
+@dataclass
+class Bundle:
+    """Engine view of the reference ``BackwardBundle`` (autodiff.py:428-436)."""
+
+    backward: Program
+    forwarding: dict
+    required: frozenset
+
+
+@dataclass
+class PlanBundle:
+    """Engine view of a reference ``PlanResult`` (checkpointing.py:852-860):
+    the rewritten forward/backward pair plus what ``run_planned`` derives
+    from it (record set, forwarding subset, names of kept copies)."""
+
+    forward: Program
+    backward: Program
+    keep: frozenset
+    forwarding: dict
+    stored: tuple
+    report: dict = field(default_factory=dict)
+
+
+@dataclass
+class RunResult:
+    env: dict
+    value: object
+    op_count: int
+    tape: object = None
+
+
+@dataclass
+class GradientResult:
+    value: object
+    grads: dict
+    forward: object
+    backward: object
+    bundle: object
+
+
+def _ref_available() -> bool:
+    import importlib.util
+
+    return importlib.util.find_spec("gradflow") is not None
+
+
+def as_bundle(bundle) -> Bundle:
+    if isinstance(bundle, Bundle):
+        return bundle
+    return Bundle(adopt(bundle.backward), adopt_forwarding(bundle.forwarding), frozenset(bundle.required))
+
+
+def host_build_backward(program) -> Bundle:
+    """Run the reference AD transform on the host (it is not on the data
+    path). Needs the reference package; otherwise pass ``bundle=``."""
+    if not _ref_available():
+        raise UnsupportedConstruct(
+            "build_backward is the reference's host-side AD transform and the reference is not installed "
+            "here: pass bundle=load_bundle(<prog>.bwd.json, <prog>.fwdreq.json)")
+    from gradflow.autodiff import build_backward  # type: ignore
+    from gradflow.frontend import parse_program  # type: ignore
+
+    ref_prog = program if not isinstance(program, Program) else parse_program(dump_program(program))
+    return as_bundle(build_backward(ref_prog))
+
+
+def load_bundle(bwd_path: str, manifest_path: str) -> Bundle:
+    with open(manifest_path) as f:
+        fw, required = forwarding_from_manifest(json.load(f))
+    return Bundle(load_program(bwd_path), fw, required)
+
+
+def save_bundle(bundle: Bundle, stem: str):
+    with open(stem + ".bwd.json", "w") as f:
+        f.write(dump_program(bundle.backward))
+    with open(stem + ".fwdreq.json", "w") as f:
+        json.dump(manifest_from_forwarding(bundle.forwarding, bundle.required), f, indent=2)
+
+
+def as_plan(result) -> PlanBundle:
+    if isinstance(result, PlanBundle):
+        return result
+    # reference PlanResult -> the sets run_planned derives (checkpointing.py:917-942)
+    fwd = adopt(result.forward)
+    bwd = adopt(result.backward)
+    fw_all = adopt_forwarding(result.bundle.forwarding)
+    keep = {(fv.data, v) for fv in result.fvs if fv.forced for v in fv.versions}
+    forwarding = {}
+    for name, e in fw_all.items():
+        if len(fwd.descriptors[e.data].shape) == 0:
+            forwarding[name] = e
+            keep |= {(e.data, c.version) for c in e.candidates}
+    for fv in result.fvs:
+        if fv.forced:
+            forwarding[fv.name] = fw_all[fv.name]
+    stored = tuple(fv.name for fv, v in zip(result.fvs, result.solution.assignment) if v and not fv.forced)
+    return PlanBundle(fwd, bwd, frozenset(keep), forwarding, stored, dict(result.report))
+
+
+def save_plan(plan: PlanBundle, stem: str):
+    with open(stem + ".fwd.json", "w") as f:
+        f.write(dump_program(plan.forward))
+    with open(stem + ".bwd.json", "w") as f:
+        f.write(dump_program(plan.backward))
+    doc = {
+        "keep": sorted([d, v] for d, v in plan.keep),
+        "stored": list(plan.stored),
+        "forwarding": manifest_from_forwarding(plan.forwarding, frozenset())["entries"],
+        "report": plan.report,
+    }
+    with open(stem + ".plan.json", "w") as f:
+        json.dump(doc, f, indent=2, default=str)
+
+
+def load_plan(stem: str) -> PlanBundle:
+    with open(stem + ".plan.json") as f:
+        doc = json.load(f)
+    fw, _ = forwarding_from_manifest({"entries": doc["forwarding"]})
+    return PlanBundle(load_program(stem + ".fwd.json"), load_program(stem + ".bwd.json"),
+                      frozenset((d, int(v)) for d, v in doc["keep"]), fw, tuple(doc["stored"]),
+                      doc.get("report", {}))
+
+
+# ---------------------------------------------------------------------------
+# executable construction
+
+
+def _check_inputs(program: Program, inputs: dict, params: dict):
+    shapes = {}
+    for name, value in inputs.items():
+        desc = program.descriptors.get(name)
+        if desc is None:
+            raise UnboundName(f"input '{name}' is not declared")
+        declared = tuple(eval_int(d, params) for d in desc.shape)
+        shape = tuple(getattr(value, "shape", np.shape(value)))
+        if desc.shape and tuple(shape[len(shape) - len(declared):]) != declared:
+            raise ShapeMismatch(f"input '{name}': trailing shape {shape} does not end with {declared}")
+        if len(shape) != len(declared):
+            raise UnsupportedConstruct(f"input '{name}': leading batch dimensions are not supported")
+        shapes[name] = declared
+    return shapes
+
+
+def _init_env(low: Lowering, program: Program, shapes: dict, prefix: str):
+    env, inputs = {}, {}
+    for name, shape in shapes.items():
+        desc = program.descriptors[name]
+        b = low.new_buffer(prefix + name, shape, desc.element_kind, fresh=False)
+        env[name] = b
+        inputs[name] = b
+    return env, inputs
+
+
+@dataclass
+class Lowered:
+    low: Lowering
+    inputs: dict
+    outputs: dict
+    seed_buf: object
+    forward_env: dict
+    backward_env: dict
+    tape: LTape
+    forward_program: Program
+    backward_program: Program
+
+
+def lower_gradient(program: Program, bundle: Bundle, params: dict, shapes: dict, *, trip_limit=None,
+                   record=None, plan: PlanBundle | None = None) -> Lowered:
+    """Forward (recording the tape) + backward as one launch list."""
+    low = Lowering(trip_limit=trip_limit)
+    fwd_prog = plan.forward if plan else program
+    bwd_prog = plan.backward if plan else bundle.backward
+    forwarding = plan.forwarding if plan else bundle.forwarding
+    rec = set(plan.keep) if plan else set(bundle.required if record is None else record)
+    fenv, inputs = _init_env(low, fwd_prog, shapes, "")
+    tape = LTape()
+    for name, b in list(fenv.items()):
+        if (name, 0) in rec:
+            slot = low.new_buffer(f"{name}@v0", b.shape, b.kind, fresh=False)
+            from .lowering import CopyOp
+
+            low.emit(CopyOp(slot, b))
+            tape.values[(name, 0, ())] = slot
+    fr = ProgramRun(low, fwd_prog, params, fenv, record=rec, tape=tape, versions=number_writes(fwd_prog))
+    fr.run()
+    dep = fenv.get(fwd_prog.dependent)
+    if dep is None:
+        raise UnboundName(f"dependent '{fwd_prog.dependent}' was never written")
+    # backward env: pristine caller inputs alias the forward's input buffers
+    benv = {}
+    for name in bwd_prog.descriptors:
+        if name in inputs and name in pristine_inputs(fwd_prog):
+            benv[name] = inputs[name]
+    if plan:
+        for name in plan.stored:
+            if name in bwd_prog.descriptors:
+                if name not in fenv:
+                    raise UnboundName(f"planned copy '{name}' was never written by the forward program")
+                benv[name] = fenv[name]
+    seed_name = fwd_prog.dependent + "__grad"
+    seed_buf = None
+    if seed_name in bwd_prog.descriptors and seed_name not in benv:
+        seed_buf = low.new_buffer(seed_name, (), bwd_prog.descriptors[seed_name].element_kind, fresh=False)
+        benv[seed_name] = seed_buf
+    br = ProgramRun(low, bwd_prog, params, benv, src_tape=tape, forwarding=forwarding)
+    br.run()
+    outputs = {"value": dep}
+    for ind in fwd_prog.independents:
+        g = benv.get(ind + "__grad")
+        if g is not None:
+            outputs["grad:" + ind] = g
+    low.finish(list(outputs.values()))
+    return Lowered(low, inputs, outputs, seed_buf, fenv, benv, tape, fwd_prog, bwd_prog)
+
+
+def build_gradient_executable(program: Program, bundle: Bundle, params: dict, shapes: dict, *, trip_limit=None,
+                              record=None, plan: PlanBundle | None = None) -> Executable:
+    lw = lower_gradient(program, bundle, params, shapes, trip_limit=trip_limit, record=record, plan=plan)
+    exe = Executable(lw.low, lw.inputs, lw.outputs, seed_buf=lw.seed_buf)
+    exe.forward_env, exe.backward_env, exe.tape = lw.forward_env, lw.backward_env, lw.tape
+    exe.forward_program, exe.backward_program = lw.forward_program, lw.backward_program
+    return exe
+
+
+# executable cache: (ids of the host objects, params, shapes) -> Executable
+_CACHE: dict = {}
+_CACHE_MAX = int(os.environ.get("GFB_CACHE", "4"))
+
+
+def _cached(key, keep_alive, build):
+    exe = _CACHE.get(key)
+    if exe is None:
+        exe = build()
+        if len(_CACHE) >= _CACHE_MAX:
+            _CACHE.pop(next(iter(_CACHE)))
+        _CACHE[key] = exe
+        exe._keep_alive = keep_alive
+    return exe
+
+
+def clear_cache():
+    _CACHE.clear()
+
+
+def _result(exe: Executable, program: Program, inputs: dict, bundle) -> GradientResult:
+    value = exe.output_host("value")
+    grads = {}
+    for ind in program.independents:
+        key = "grad:" + ind
+        if key in exe.outputs:
+            grads[ind] = exe.output_host(key)
+        else:
+            ref = np.asarray(inputs[ind])
+            grads[ind] = np.zeros(ref.shape, dtype=NP_DTYPE[program.descriptors[ind].element_kind])
+    fenv = {k: exe.view(b) for k, b in exe.forward_env.items()}
+    benv = {k: exe.view(b) for k, b in exe.backward_env.items()}
+    fwd = RunResult(env=fenv, value=value, op_count=exe.flops, tape=exe.tape)
+    bwd = RunResult(env=benv, value=None, op_count=exe.flops)
+    return GradientResult(value=value, grads=grads, forward=fwd, backward=bwd, bundle=bundle)
+
+
+def gradient(program, inputs: dict, params: dict | None = None, *, seed=1.0, trip_limit=None, bundle=None):
+    """Reference ``gradient`` (autodiff.py:1153) executed on the B200."""
+    params = dict(params or {})
+    prog = adopt(program)
+    if bundle is None:
+        b = _CACHE.get(("bundle", id(program)))
+        if b is None:
+            b = host_build_backward(program)
+            _CACHE[("bundle", id(program))] = b
+        bundle_eng = b
+    else:
+        bundle_eng = as_bundle(bundle)
+    shapes = _check_inputs(prog, inputs, params)
+    key = ("grad", id(program), id(bundle), tuple(sorted(params.items())), tuple(sorted(shapes.items())), trip_limit)
+    exe = _cached(key, (program, bundle),
+                  lambda: build_gradient_executable(prog, bundle_eng, params, shapes, trip_limit=trip_limit))
+    exe.run(inputs, seed)
+    return _result(exe, prog, inputs, bundle if bundle is not None else bundle_eng)
+
+
+def run_planned(result, inputs: dict, params: dict | None = None, *, seed=1.0, trip_limit=None):
+    """Reference ``run_planned`` (checkpointing.py:903) executed on the B200."""
+    params = dict(params or {})
+    pb = as_plan(result)
+    shapes = _check_inputs(pb.forward, inputs, params)
+    key = ("plan", id(result), tuple(sorted(params.items())), tuple(sorted(shapes.items())), trip_limit)
+    exe = _cached(key, (result,),
+                  lambda: build_gradient_executable(pb.forward, None, params, shapes, trip_limit=trip_limit, plan=pb))
+    exe.run(inputs, seed)
+    return _result(exe, pb.forward, inputs, getattr(result, "bundle", None))
+
+
+def plan(program, limit_mib, params=None, *, trip_limit=None):
+    """The reference's host-side ILP planner (checkpointing.py:863); its
+    result runs on the engine through ``run_planned``."""
+    if not _ref_available():
+        raise UnsupportedConstruct("plan() is the reference's host ILP planner; load an emitted plan with load_plan()")
+    from gradflow.checkpointing import plan as ref_plan  # type: ignore
+    from gradflow.frontend import parse_program  # type: ignore
+
+    ref_prog = program if not isinstance(program, Program) else parse_program(dump_program(program))
+    return ref_plan(ref_prog, limit_mib, params, trip_limit=trip_limit)
+
+
+def run_forward(program, inputs: dict, params: dict | None = None, *, record=None, trip_limit=None, vinfo=None):
+    """Reference ``run_forward`` (interpreter.py:621): the forward program
+    alone; ``record`` None, "all" or a set of (name, version)."""
+    params = dict(params or {})
+    prog = adopt(program)
+    shapes = _check_inputs(prog, inputs, params)
+    low = Lowering(trip_limit=trip_limit)
+    env, ins = _init_env(low, prog, shapes, "")
+    tape = LTape() if record is not None else None
+    if tape is not None:
+        from .lowering import CopyOp
+
+        for name, b in list(env.items()):
+            if record == "all" or (name, 0) in record:
+                slot = low.new_buffer(f"{name}@v0", b.shape, b.kind, fresh=False)
+                low.emit(CopyOp(slot, b))
+                tape.values[(name, 0, ())] = slot
+    ProgramRun(low, prog, params, env, record=record, tape=tape, versions=number_writes(prog)).run()
+    dep = env.get(prog.dependent)
+    if dep is None:
+        raise UnboundName(f"dependent '{prog.dependent}' was never written")
+    observed = list(env.values()) + (list(tape.values.values()) if tape else [])
+    low.finish(observed)
+    exe = Executable(low, ins, {"value": dep}, use_graph=False)
+    exe.run(inputs)
+    out_env = {k: exe.view(b) for k, b in env.items()}
+    res = RunResult(env=out_env, value=exe.output_host("value"), op_count=exe.flops, tape=tape)
+    res._exe = exe
+    return res
+
+
+def run_backward(program, backward, inputs: dict, params: dict | None = None, *, tape=None, forwarding=None,
+                 seed=1.0, extra_env=None, trip_limit=None):
+    """Reference ``run_backward`` (interpreter.py:659). ``tape`` must come
+    from this engine's ``run_forward`` (device-resident snapshots)."""
+    params = dict(params or {})
+    prog = adopt(program)
+    bwd = adopt(backward)
+    fw = adopt_forwarding(forwarding) if forwarding and not isinstance(next(iter(forwarding.values())), type(None)) \
+        else {}
+    low = Lowering(trip_limit=trip_limit)
+    pass_in = {k: v for k, v in inputs.items() if k in bwd.descriptors}
+    shapes = _check_inputs(bwd, pass_in, params)
+    env, ins = _init_env(low, bwd, shapes, "")
+    extra_in = {}
+    for k, v in (extra_env or {}).items():
+        if k in bwd.descriptors:
+            b = low.new_buffer(k, tuple(np.shape(v)), bwd.descriptors[k].element_kind, fresh=False)
+            env[k] = b
+            ins[k] = b
+            extra_in[k] = v
+    seed_name = prog.dependent + "__grad"
+    seed_buf = None
+    if seed_name in bwd.descriptors and seed_name not in env:
+        seed_buf = low.new_buffer(seed_name, (), bwd.descriptors[seed_name].element_kind, fresh=False)
+        env[seed_name] = seed_buf
+    ProgramRun(low, bwd, params, env, src_tape=tape, forwarding=fw).run()
+    low.finish(list(env.values()))
+    outputs = {"value": seed_buf} if seed_buf is not None else {}
+    exe = Executable(low, ins, outputs, seed_buf=seed_buf, use_graph=False)
+    exe.run({**pass_in, **extra_in}, seed)
+    out_env = {k: exe.view(b) for k, b in env.items()}
+    return RunResult(env=out_env, value=None if seed_buf is None else exe.output_host("value"), op_count=exe.flops)
+
+
+class Engine:
+    """Device-resident gradient evaluator for one (program, params): the
+    object bench.py drives. ``step(device_inputs)`` runs forward+backward on
+    inputs already in HBM; ``gradient(host_inputs)`` is the end-to-end call."""
+
+    def __init__(self, program, bundle=None, params=None, shapes=None, *, plan: PlanBundle | None = None,
+                 trip_limit=None):
+        self.params = dict(params or {})
+        self.plan = plan
+        self.program = adopt(program) if program is not None else plan.forward
+        self.bundle = None if plan else (as_bundle(bundle) if bundle is not None else host_build_backward(program))
+        if shapes is None:
+            shapes = {n: tuple(eval_int(s, self.params) for s in d.shape)
+                      for n, d in self.program.descriptors.items() if d.role == "input"}
+        self.shapes = dict(shapes)
+        self.exe = build_gradient_executable(self.program, self.bundle, self.params, self.shapes,
+                                             trip_limit=trip_limit, plan=plan)
+
+    def step(self, inputs: dict, seed=1.0, sync=False):
+        self.exe.run(inputs, seed, sync=sync)
+
+    def check(self):
+        self.exe.check()
+
+    def gradient(self, inputs: dict, seed=1.0) -> GradientResult:
+        self.exe.run(inputs, seed)
+        return _result(self.exe, self.program, inputs, self.bundle)

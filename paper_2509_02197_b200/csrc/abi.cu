@@ -1,0 +1,69 @@
+// C-ABI plumbing: status strings, device queries, plain copies.
+#include <cstdio>
+#include <cstring>
+
+#include "gfb_common.cuh"
+#include "gfb_internal.h"
+
+namespace gfb {
+
+static thread_local char g_last_error[512] = "";
+
+int set_error(int code, const char *msg) {
+  std::snprintf(g_last_error, sizeof(g_last_error), "%s", msg);
+  return code;
+}
+
+int check_launch(const char *what) {
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    std::snprintf(g_last_error, sizeof(g_last_error), "%s: %s", what, cudaGetErrorString(e));
+    return GFB_ECUDA;
+  }
+  return GFB_OK;
+}
+
+int sm_count() {
+  static int cached = 0;
+  if (!cached) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (cudaDeviceGetAttribute(&cached, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || cached <= 0)
+      cached = 148;
+  }
+  return cached;
+}
+
+}  // namespace gfb
+
+using namespace gfb;
+
+extern "C" int gfb_abi_version(void) { return GFB_ABI_VERSION; }
+
+extern "C" const char *gfb_last_error(void) { return g_last_error; }
+
+extern "C" int gfb_device_sm_count(void) { return sm_count(); }
+
+extern "C" int gfb_copy(void *dst, const void *src, int64_t bytes, void *stream) {
+  if (bytes <= 0) return GFB_OK;
+  cudaError_t e = cudaMemcpyAsync(dst, src, (size_t)bytes, cudaMemcpyDeviceToDevice, (cudaStream_t)stream);
+  if (e != cudaSuccess) return set_error(GFB_ECUDA, cudaGetErrorString(e));
+  return GFB_OK;
+}
+
+extern "C" int gfb_plane_copy(void *dst, const void *src, int64_t plane_elems, int32_t dtype, int64_t nplanes,
+                              void *stream) {
+  int64_t bytes = plane_elems * nplanes * (dtype == GFB_F64 ? 8 : 4);
+  return gfb_copy(dst, src, bytes, stream);
+}
+
+// Layout self-check for foreign bindings (ctypes in _lib.py): sizes of the
+// descriptor structs in declaration order.
+extern "C" int gfb_struct_sizes(int64_t *out, int32_t cap) {
+  const int64_t s[6] = {(int64_t)sizeof(gfb_space),       (int64_t)sizeof(gfb_operand),
+                        (int64_t)sizeof(gfb_map_desc),    (int64_t)sizeof(gfb_term),
+                        (int64_t)sizeof(gfb_gather_desc), (int64_t)sizeof(gfb_stencil_desc)};
+  int n = cap < 6 ? cap : 6;
+  for (int i = 0; i < n; ++i) out[i] = s[i];
+  return n;
+}

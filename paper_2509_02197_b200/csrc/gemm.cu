@@ -1,0 +1,359 @@
+// matmul library node: C (= | +=) op(A) @ op(B), row-major operands.
+//
+// Reference: Executor._exec_library "matmul" (interpreter.py:433-446) and the
+// adjoint jobs gA += g op(B)^T, gB += op(A)^T g (autodiff.py:780-802).
+// Shape classes (dispatch in gfb_matmul):
+//   K == 1            rank-1 update (outer-product adjoints of matvecs), HBM
+//   N == 1 / M == 1   matrix-vector products (atax / bicg), HBM-bound
+//   otherwise         tiled GEMM: fp64 on the DMMA tensor path
+//                     (mma.sync.m8n8k4.f64 -> DMMA), fp32 on FFMA
+#include "gfb_common.cuh"
+#include "gfb_internal.h"
+
+namespace gfb {
+
+// ---------------------------------------------------------------------------
+// generic SIMT tile GEMM (fp32; also the fp64 fallback for odd shapes)
+
+constexpr int kBM = 64, kBN = 64, kBK = 16, kTM = 4, kTN = 4;
+
+template <typename T>
+__global__ void __launch_bounds__(256) gemm_simt_kernel(int ta, int tb, int64_t M, int64_t N, int64_t K,
+                                                        const T *__restrict__ A, int64_t lda,
+                                                        const T *__restrict__ B, int64_t ldb, T *C, int64_t ldc,
+                                                        int accumulate) {
+  __shared__ T As[kBK][kBM + 1];
+  __shared__ T Bs[kBK][kBN + 1];
+  const int tid = threadIdx.x;
+  const int tx = tid % 16, ty = tid / 16;
+  const int64_t m0 = (int64_t)blockIdx.y * kBM, n0 = (int64_t)blockIdx.x * kBN;
+  T acc[kTM][kTN];
+#pragma unroll
+  for (int a = 0; a < kTM; ++a)
+#pragma unroll
+    for (int b = 0; b < kTN; ++b) acc[a][b] = T(0);
+  for (int64_t k0 = 0; k0 < K; k0 += kBK) {
+    // A tile: kBM x kBK elements, 256 threads -> 4 each
+#pragma unroll
+    for (int r = 0; r < (kBM * kBK) / 256; ++r) {
+      int e = tid + r * 256;
+      int mm, kk;
+      if (ta) {  // A stored [K, M]: walk m fastest for coalescing
+        mm = e % kBM;
+        kk = e / kBM;
+      } else {
+        kk = e % kBK;
+        mm = e / kBK;
+      }
+      int64_t gm = m0 + mm, gk = k0 + kk;
+      T v = T(0);
+      if (gm < M && gk < K) v = ta ? A[gk * lda + gm] : A[gm * lda + gk];
+      As[kk][mm] = v;
+    }
+#pragma unroll
+    for (int r = 0; r < (kBN * kBK) / 256; ++r) {
+      int e = tid + r * 256;
+      int nn, kk;
+      if (tb) {  // B stored [N, K]
+        kk = e % kBK;
+        nn = e / kBK;
+      } else {
+        nn = e % kBN;
+        kk = e / kBN;
+      }
+      int64_t gn = n0 + nn, gk = k0 + kk;
+      T v = T(0);
+      if (gn < N && gk < K) v = tb ? B[gn * ldb + gk] : B[gk * ldb + gn];
+      Bs[kk][nn] = v;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int kk = 0; kk < kBK; ++kk) {
+      T a[kTM], b[kTN];
+#pragma unroll
+      for (int q = 0; q < kTM; ++q) a[q] = As[kk][ty + 16 * q];
+#pragma unroll
+      for (int q = 0; q < kTN; ++q) b[q] = Bs[kk][tx + 16 * q];
+#pragma unroll
+      for (int p = 0; p < kTM; ++p)
+#pragma unroll
+        for (int q = 0; q < kTN; ++q) acc[p][q] = fma(a[p], b[q], acc[p][q]);
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int p = 0; p < kTM; ++p) {
+    int64_t gm = m0 + ty + 16 * p;
+    if (gm >= M) continue;
+#pragma unroll
+    for (int q = 0; q < kTN; ++q) {
+      int64_t gn = n0 + tx + 16 * q;
+      if (gn >= N) continue;
+      T *c = C + gm * ldc + gn;
+      *c = accumulate ? (T)(*c + acc[p][q]) : acc[p][q];
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// fp64 DMMA GEMM: 128x128 CTA tile, BK = 16, 8 warps each owning 64x32,
+// mma.sync.aligned.m8n8k4.row.col.f64 (-> DMMA.884 on sm_100a).
+// Operands are staged through padded shared memory with transposes resolved
+// at load time so both A and B fragments come from [k][m] / [k][n] tiles.
+
+constexpr int kDM = 128, kDN = 128, kDK = 16;
+
+__device__ __forceinline__ void dmma884(double &d0, double &d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(d0), "+d"(d1)
+               : "d"(a), "d"(b));
+}
+
+__global__ void __launch_bounds__(256) dgemm_dmma_kernel(int ta, int tb, int64_t M, int64_t N, int64_t K,
+                                                         const double *__restrict__ A, int64_t lda,
+                                                         const double *__restrict__ B, int64_t ldb, double *C,
+                                                         int64_t ldc, int accumulate) {
+  // row stride 132 = 4 (mod 16) doubles keeps the fragment loads conflict-free
+  __shared__ double As[kDK][kDM + 4];
+  __shared__ double Bs[kDK][kDN + 4];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int wm = (warp >> 2) * 64;  // 2 warps along M
+  const int wn = (warp & 3) * 32;   // 4 warps along N
+  const int64_t m0 = (int64_t)blockIdx.y * kDM, n0 = (int64_t)blockIdx.x * kDN;
+  double acc[8][4][2];
+#pragma unroll
+  for (int a = 0; a < 8; ++a)
+#pragma unroll
+    for (int b = 0; b < 4; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
+
+  double ra[8], rb[8];
+  auto fetch = [&](int64_t k0) {
+#pragma unroll
+    for (int r = 0; r < 8; ++r) {
+      int e = tid + r * 256;
+      int mm = ta ? e % kDM : e / kDK, kk = ta ? e / kDM : e % kDK;
+      int64_t gm = m0 + mm, gk = k0 + kk;
+      ra[r] = (gm < M && gk < K) ? (ta ? A[gk * lda + gm] : A[gm * lda + gk]) : 0.0;
+      int nn = tb ? e / kDK : e % kDN, kb = tb ? e % kDK : e / kDN;
+      int64_t gn = n0 + nn, gkb = k0 + kb;
+      rb[r] = (gn < N && gkb < K) ? (tb ? B[gn * ldb + gkb] : B[gkb * ldb + gn]) : 0.0;
+    }
+  };
+  auto stash = [&]() {
+#pragma unroll
+    for (int r = 0; r < 8; ++r) {
+      int e = tid + r * 256;
+      int mm = ta ? e % kDM : e / kDK, kk = ta ? e / kDM : e % kDK;
+      As[kk][mm] = ra[r];
+      int nn = tb ? e / kDK : e % kDN, kb = tb ? e % kDK : e / kDN;
+      Bs[kb][nn] = rb[r];
+    }
+  };
+
+  // m8n8k4 fragments: A(row) lane -> A[lane/4][lane%4]; B(col) lane ->
+  // B[lane%4][lane/4]; D lane -> D[lane/4][2*(lane%4) + {0,1}]
+  const int fr = lane >> 2, fc = lane & 3;
+  fetch(0);
+  for (int64_t k0 = 0; k0 < K; k0 += kDK) {
+    stash();
+    __syncthreads();
+    if (k0 + kDK < K) fetch(k0 + kDK);  // global loads overlap the DMMA work below
+#pragma unroll
+    for (int ks = 0; ks < kDK; ks += 4) {
+      double af[8], bf[4];
+#pragma unroll
+      for (int a = 0; a < 8; ++a) af[a] = As[ks + fc][wm + a * 8 + fr];
+#pragma unroll
+      for (int b = 0; b < 4; ++b) bf[b] = Bs[ks + fc][wn + b * 8 + fr];
+#pragma unroll
+      for (int a = 0; a < 8; ++a)
+#pragma unroll
+        for (int b = 0; b < 4; ++b) dmma884(acc[a][b][0], acc[a][b][1], af[a], bf[b]);
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int a = 0; a < 8; ++a) {
+    int64_t gm = m0 + wm + a * 8 + fr;
+    if (gm >= M) continue;
+#pragma unroll
+    for (int b = 0; b < 4; ++b) {
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        int64_t gn = n0 + wn + b * 8 + 2 * fc + h;
+        if (gn >= N) continue;
+        double *c = C + gm * ldc + gn;
+        *c = accumulate ? *c + acc[a][b][h] : acc[a][b][h];
+      }
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// matrix-vector: y[i] = sum_k op(A)(i,k) x[k]
+
+// op(A)(i,k) contiguous in k: one warp per output row
+template <typename T>
+__global__ void __launch_bounds__(256) gemv_rowdot_kernel(int64_t M, int64_t K, const T *__restrict__ A,
+                                                          int64_t lda, const T *__restrict__ x, int64_t incx,
+                                                          T *y, int64_t incy, int accumulate) {
+  const int64_t row = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (row >= M) return;
+  const T *a = A + row * lda;
+  T acc = T(0);
+  for (int64_t k = lane; k < K; k += 32) acc = fma(a[k], x[k * incx], acc);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_down_sync(0xffffffffu, acc, o);
+  if (lane == 0) {
+    T *o = y + row * incy;
+    *o = accumulate ? (T)(*o + acc) : acc;
+  }
+}
+
+// op(A)(i,k) = S[k*lds + i] (contiguous in i): split-K column sums.
+// partial[s][i] over k-chunk s; a second pass reduces the splits in order.
+template <typename T>
+__global__ void __launch_bounds__(256) gemv_colsum_kernel(int64_t M, int64_t K, const T *__restrict__ S,
+                                                          int64_t lds, const T *__restrict__ x, int64_t incx,
+                                                          T *partial, int64_t kchunk) {
+  __shared__ T red[8][33];
+  const int64_t i = (int64_t)blockIdx.x * 32 + (threadIdx.x & 31);
+  const int g = threadIdx.x >> 5;
+  const int64_t kb = (int64_t)blockIdx.y * kchunk;
+  const int64_t ke = min(kb + kchunk, K);
+  T acc = T(0);
+  if (i < M)
+    for (int64_t k = kb + g; k < ke; k += 8) acc = fma(S[k * lds + i], x[k * incx], acc);
+  red[g][threadIdx.x & 31] = acc;
+  __syncthreads();
+  if (g == 0 && i < M) {
+    T s = T(0);
+#pragma unroll
+    for (int q = 0; q < 8; ++q) s += red[q][threadIdx.x];
+    partial[(int64_t)blockIdx.y * M + i] = s;
+  }
+}
+
+template <typename T>
+__global__ void splits_finish_kernel(int64_t M, int64_t nsplit, const T *__restrict__ partial, T *y, int64_t incy,
+                                     int accumulate) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= M) return;
+  T s = T(0);
+  for (int64_t q = 0; q < nsplit; ++q) s += partial[q * M + i];
+  T *o = y + i * incy;
+  *o = accumulate ? (T)(*o + s) : s;
+}
+
+// rank-1: C[i,j] (+)= u[i*incu] * v[j*incv]
+template <typename T>
+__global__ void __launch_bounds__(256) rank1_kernel(int64_t M, int64_t N, const T *__restrict__ u, int64_t incu,
+                                                    const T *__restrict__ v, int64_t incv, T *C, int64_t ldc,
+                                                    int accumulate) {
+  const int64_t total = M * N;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t f = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; f < total; f += stride) {
+    int64_t i = f / N, j = f % N;
+    T r = u[i * incu] * v[j * incv];
+    T *c = C + i * ldc + j;
+    *c = accumulate ? (T)(*c + r) : r;
+  }
+}
+
+static int64_t colsum_splits(int64_t M, int64_t K) {
+  int64_t cols_blocks = ceil_div(M, 32);
+  int64_t want = ceil_div((int64_t)sm_count() * 4, cols_blocks);
+  int64_t maxs = ceil_div(K, 64);
+  if (want > maxs) want = maxs;
+  return want < 1 ? 1 : want;
+}
+
+template <typename T>
+static int gemv_colsum(int64_t M, int64_t K, const T *S, int64_t lds, const T *x, int64_t incx, T *y, int64_t incy,
+                       int accumulate, void *ws, cudaStream_t st) {
+  int64_t ns = colsum_splits(M, K);
+  int64_t chunk = ceil_div(K, ns);
+  T *partial = (T *)ws;
+  dim3 grid((unsigned)ceil_div(M, 32), (unsigned)ns);
+  gemv_colsum_kernel<T><<<grid, 256, 0, st>>>(M, K, S, lds, x, incx, partial, chunk);
+  splits_finish_kernel<T><<<(unsigned)ceil_div(M, 256), 256, 0, st>>>(M, ns, partial, y, incy, accumulate);
+  return check_launch("gemv_colsum");
+}
+
+template <typename T>
+static int matmul_t(int ta, int tb, int64_t M, int64_t N, int64_t K, const T *A, int64_t lda, const T *B, int64_t ldb,
+                    T *C, int64_t ldc, int accumulate, void *ws, cudaStream_t st) {
+  if (M <= 0 || N <= 0) return GFB_OK;
+  if (K == 0) {
+    if (!accumulate) {
+      for (int64_t i = 0; i < M; ++i) cudaMemsetAsync(C + i * ldc, 0, (size_t)N * sizeof(T), st);
+    }
+    return check_launch("matmul_k0");
+  }
+  if (K == 1) {
+    // op(A) column 0: element i at A[i*lda] (no ta) or A[i] (ta: A stored [1, M])
+    int64_t incu = ta ? 1 : lda;
+    int64_t incv = tb ? ldb : 1;  // op(B) row 0: B[j] (no tb) or B[j*ldb] (tb: stored [N,1])
+    int64_t total = M * N;
+    unsigned blocks = (unsigned)min(ceil_div(total, 256 * 4), (int64_t)sm_count() * 8);
+    rank1_kernel<T><<<blocks, 256, 0, st>>>(M, N, A, incu, B, incv, C, ldc, accumulate);
+    return check_launch("rank1");
+  }
+  if (N == 1) {
+    // x = op(B)(:,0): B[k*ldb] (no tb) or B[k] (tb)
+    int64_t incx = tb ? 1 : ldb;
+    if (!ta) {
+      gemv_rowdot_kernel<T><<<(unsigned)ceil_div(M, 8), 256, 0, st>>>(M, K, A, lda, B, incx, C, ldc, accumulate);
+      return check_launch("gemv_rowdot");
+    }
+    return gemv_colsum<T>(M, K, A, lda, B, incx, C, ldc, accumulate, ws, st);
+  }
+  if (M == 1) {
+    // y[j] = sum_k op(A)(0,k) op(B)(k,j); op(A) row 0: A[k] (no ta) or A[k*lda] (ta)
+    int64_t incx = ta ? lda : 1;
+    if (tb) {  // op(B)(k,j) = B[j*ldb + k]: row dots
+      gemv_rowdot_kernel<T><<<(unsigned)ceil_div(N, 8), 256, 0, st>>>(N, K, B, ldb, A, incx, C, 1, accumulate);
+      return check_launch("gemv_rowdot");
+    }
+    return gemv_colsum<T>(N, K, B, ldb, A, incx, C, 1, accumulate, ws, st);
+  }
+  return -1;  // general GEMM handled by the caller
+}
+
+}  // namespace gfb
+
+using namespace gfb;
+
+extern "C" int64_t gfb_matmul_workspace_bytes(int32_t dtype, int32_t ta, int32_t tb, int64_t M, int64_t N,
+                                              int64_t K) {
+  int64_t es = dtype == GFB_F64 ? 8 : 4;
+  if (K > 1 && N == 1 && ta) return colsum_splits(M, K) * M * es;
+  if (K > 1 && M == 1 && !tb && N > 1) return colsum_splits(N, K) * N * es;
+  return 0;
+}
+
+extern "C" int gfb_matmul(int32_t dtype, int32_t ta, int32_t tb, int64_t M, int64_t N, int64_t K, const void *A,
+                          int64_t lda, const void *B, int64_t ldb, void *C, int64_t ldc, int32_t accumulate,
+                          void *workspace, void *stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  if (gfb_matmul_workspace_bytes(dtype, ta, tb, M, N, K) > 0 && !workspace)
+    return set_error(GFB_EINVAL, "gfb_matmul: workspace required");
+  int rc;
+  if (dtype == GFB_F64) {
+    rc = matmul_t<double>(ta, tb, M, N, K, (const double *)A, lda, (const double *)B, ldb, (double *)C, ldc,
+                          accumulate, workspace, st);
+    if (rc >= 0) return rc;
+    dim3 grid((unsigned)ceil_div(N, kDN), (unsigned)ceil_div(M, kDM));
+    dgemm_dmma_kernel<<<grid, 256, 0, st>>>(ta, tb, M, N, K, (const double *)A, lda, (const double *)B, ldb,
+                                             (double *)C, ldc, accumulate);
+    return check_launch("dgemm_dmma");
+  }
+  rc = matmul_t<float>(ta, tb, M, N, K, (const float *)A, lda, (const float *)B, ldb, (float *)C, ldc, accumulate,
+                       workspace, st);
+  if (rc >= 0) return rc;
+  dim3 grid((unsigned)ceil_div(N, kBN), (unsigned)ceil_div(M, kBM));
+  gemm_simt_kernel<float><<<grid, 256, 0, st>>>(ta, tb, M, N, K, (const float *)A, lda, (const float *)B, ldb,
+                                                (float *)C, ldc, accumulate);
+  return check_launch("sgemm_simt");
+}

@@ -1,0 +1,111 @@
+// Linear stencil sweeps: the forward stencil maps of jacobi_2d / heat_3d and
+// the gather (transposed-stencil) form of their adjoints.
+//
+// Reference: the forward map is Executor._exec_map over a single tasklet
+// (interpreter.py:478-507); its adjoint is the scatter-add map emitted by
+// adj_map (autodiff.py:962-1081) with `_z` clears (autodiff.py:996-1004).
+// The host lowering rewrites the scatter into a gather over the target array
+// (one output per thread, no atomics) and folds pending clears into the same
+// pass (clear_mode 2), so each sweep reads each source once and writes the
+// target once.
+//
+// Data layout: row-major, innermost dimension contiguous; rank <= 3 (lower
+// ranks are padded with leading unit dimensions). Threads map the innermost
+// dimension to the warp (coalesced 256 B fp64 rows), the middle dimension to
+// the block's y, and each block marches MARCH consecutive outer planes so
+// neighbour planes are re-read from L1/L2 rather than HBM.
+#include "gfb_common.cuh"
+#include "gfb_internal.h"
+
+namespace gfb {
+
+constexpr int kSX = 32, kSY = 8, kMarch = 8;
+
+struct StencilGeom {
+  int64_t d1, d2;                // padded dims of the two inner dimensions
+  int64_t lo0, lo1, lo2, e0, e1, e2;
+  int64_t tap_off[GFB_MAX_TAPS];  // linear offset of each tap
+  int64_t mlo[GFB_MAX_TAPS][3], mhi[GFB_MAX_TAPS][3];
+  int64_t clo[3], chi[3];
+};
+
+template <typename T>
+__global__ void __launch_bounds__(kSX *kSY) stencil_kernel(const __grid_constant__ gfb_stencil_desc d,
+                                                           const __grid_constant__ StencilGeom g) {
+  const int64_t k = g.lo2 + (int64_t)blockIdx.x * kSX + threadIdx.x;
+  const int64_t j = g.lo1 + (int64_t)blockIdx.y * kSY + threadIdx.y;
+  if (k >= g.lo2 + g.e2 || j >= g.lo1 + g.e1) return;
+  const int64_t i_begin = g.lo0 + (int64_t)blockIdx.z * kMarch;
+  const int64_t i_end = min(i_begin + kMarch, g.lo0 + g.e0);
+  T *dst = (T *)d.dst;
+  for (int64_t i = i_begin; i < i_end; ++i) {
+    const int64_t off = (i * g.d1 + j) * g.d2 + k;
+    T acc;
+    if (d.clear_mode == 0) {
+      acc = dst[off];
+    } else if (d.clear_mode == 2) {
+      bool in = i >= g.clo[0] && i < g.chi[0] && j >= g.clo[1] && j < g.chi[1] && k >= g.clo[2] && k < g.chi[2];
+      acc = in ? T(0) : dst[off];
+    } else {
+      acc = T(0);
+    }
+    for (int t = 0; t < d.ntaps; ++t) {
+      if (d.tap_masked[t]) {
+        if (i < g.mlo[t][0] || i >= g.mhi[t][0] || j < g.mlo[t][1] || j >= g.mhi[t][1] || k < g.mlo[t][2] ||
+            k >= g.mhi[t][2])
+          continue;
+      }
+      const T *src = (const T *)d.src[d.tap_src[t]];
+      acc += (T)d.tap_coef[t] * __ldg(src + off + g.tap_off[t]);
+    }
+    dst[off] = acc;
+  }
+}
+
+}  // namespace gfb
+
+using namespace gfb;
+
+extern "C" int gfb_stencil_launch(const gfb_stencil_desc *d, void *stream) {
+  if (!d || d->rank < 1 || d->rank > 3 || d->ntaps < 0 || d->ntaps > GFB_MAX_TAPS || !d->dst)
+    return set_error(GFB_EINVAL, "gfb_stencil_launch: bad descriptor");
+  StencilGeom g;
+  int64_t dims[3] = {1, 1, 1}, lo[3] = {0, 0, 0}, hi[3] = {1, 1, 1};
+  const int pad = 3 - d->rank;
+  for (int r = 0; r < d->rank; ++r) {
+    dims[pad + r] = d->dims[r];
+    lo[pad + r] = d->lo[r];
+    hi[pad + r] = d->hi[r];
+  }
+  g.d1 = dims[1];
+  g.d2 = dims[2];
+  g.lo0 = lo[0];
+  g.lo1 = lo[1];
+  g.lo2 = lo[2];
+  g.e0 = hi[0] - lo[0];
+  g.e1 = hi[1] - lo[1];
+  g.e2 = hi[2] - lo[2];
+  if (g.e0 <= 0 || g.e1 <= 0 || g.e2 <= 0) return GFB_OK;
+  for (int t = 0; t < d->ntaps; ++t) {
+    int64_t dl[3] = {0, 0, 0};
+    for (int r = 0; r < d->rank; ++r) dl[pad + r] = d->tap_delta[t][r];
+    g.tap_off[t] = (dl[0] * g.d1 + dl[1]) * g.d2 + dl[2];
+    for (int r = 0; r < 3; ++r) {
+      g.mlo[t][r] = r < pad ? INT64_MIN / 4 : d->tap_mlo[t][r - pad];
+      g.mhi[t][r] = r < pad ? INT64_MAX / 4 : d->tap_mhi[t][r - pad];
+    }
+  }
+  for (int r = 0; r < 3; ++r) {
+    g.clo[r] = r < pad ? INT64_MIN / 4 : d->clear_lo[r - pad];
+    g.chi[r] = r < pad ? INT64_MAX / 4 : d->clear_hi[r - pad];
+  }
+  dim3 block(kSX, kSY);
+  dim3 grid((unsigned)ceil_div(g.e2, kSX), (unsigned)ceil_div(g.e1, kSY), (unsigned)ceil_div(g.e0, kMarch));
+  if (grid.y > 65535 || grid.z > 65535) return set_error(GFB_EUNSUPPORTED, "gfb_stencil_launch: extent too large");
+  cudaStream_t st = (cudaStream_t)stream;
+  if (d->dtype == GFB_F64)
+    stencil_kernel<double><<<grid, block, 0, st>>>(*d, g);
+  else
+    stencil_kernel<float><<<grid, block, 0, st>>>(*d, g);
+  return check_launch("stencil");
+}

@@ -1,0 +1,1505 @@
+"""Lowering: reference IR + parameter bindings -> a static launch list.
+
+This replaces the reference's interpretation loop (``Executor``,
+interpreter.py:116-550). Because loop headers are resolved from parameters
+(the reference's own static-iteration-space rule, SPEC "static iteration
+space"), the whole forward+backward execution of one gradient unrolls into a
+flat list of kernel launches over preallocated HBM buffers. The runtime
+replays that list directly or as one captured CUDA graph.
+
+Per node kind (reference -> here):
+
+* MapNode with one tasklet (``_exec_map``/``_exec_tasklet``,
+  interpreter.py:478-507/405-426): subsets are required to be affine in the
+  map parameters (probed numerically, checked at several points), bounds are
+  checked statically over the whole iteration space (``OutOfBounds``), and
+  outputs are split into
+    - point-private outputs (injective subsets): one pointwise launch;
+    - scatter-add outputs (``wcr="sum"`` with collisions across points):
+      one atomic-free *gather* pass per target array (output-stationary);
+    - constant-zero clears (the adjoint ``_z`` outputs, autodiff.py:
+      996-1004, and ``scale 0.0`` nodes, :901-906): not launched at all but
+      recorded as a *pending clear* on the target buffer and folded into the
+      next kernel that writes it.
+  Linear constant-coefficient bodies over shifted identity subsets (the
+  stencils and their adjoints) take the stencil fast path.
+* LibraryNode (``_exec_library``, interpreter.py:428-476): reduce / fused
+  elementwise / broadcast / matmul launches.
+* Tape (``_visit_access``, interpreter.py:371-386) and forwarded reads
+  (``_fetch_forwarded``/``_cand_coords``, :511-550): resolved at lowering
+  time to tape slots; a slot whose source is never overwritten afterwards
+  aliases it instead of copying (zero-cost store).
+* Zero-init on first touch (interpreter.py:171-189): every fresh buffer
+  starts with a pending whole-array clear, so the first writer overwrites
+  instead of accumulating and no memset is issued.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import itertools
+import math
+import os
+
+import numpy as np
+
+from . import _lib as L
+from .errors import (
+    DomainError,
+    MissingInverse,
+    MissingTapeValue,
+    NonTermination,
+    OutOfBounds,
+    ShapeMismatch,
+    UnboundName,
+    UnsupportedConstruct,
+)
+from .ir import (
+    AccessNode,
+    Binary,
+    Conditional,
+    Const,
+    LibraryNode,
+    LoopRegion,
+    MapNode,
+    Name,
+    State,
+    Tasklet,
+    Unary,
+    count_ops,
+    eval_int,
+    evaluate,
+    free_names,
+    number_writes,
+    schedule,
+)
+
+KIND_DTYPE = {"real32": L.F32, "real64": L.F64}
+ITEMSIZE = {"real32": 4, "real64": 8}
+MAX_UNROLLED_OPS = int(os.environ.get("GFB_MAX_OPS", "200000"))
+
+
+def default_trip_limit() -> int:
+    raw = os.environ.get("GRADFLOW_TRIP_LIMIT")
+    return int(raw) if raw else 10**9
+
+
+# ---------------------------------------------------------------------------
+# boxes: tuple of (lo, hi) per dimension, hi exclusive
+
+
+def box_contains(outer, inner) -> bool:
+    return all(ol <= il and ih <= oh for (ol, oh), (il, ih) in zip(outer, inner))
+
+
+def box_union_bbox(a, b):
+    return tuple((min(al, bl), max(ah, bh)) for (al, ah), (bl, bh) in zip(a, b))
+
+
+def box_size(b) -> int:
+    n = 1
+    for lo, hi in b:
+        n *= max(0, hi - lo)
+    return n
+
+
+def whole_box(shape):
+    return tuple((0, d) for d in shape)
+
+
+# ---------------------------------------------------------------------------
+# buffers
+
+
+class Buffer:
+    """One device array (an env entry, a tape slot, or scratch)."""
+
+    _ids = itertools.count()
+
+    def __init__(self, name: str, shape: tuple, kind: str, *, fresh: bool):
+        self.bid = next(Buffer._ids)
+        self.name = name
+        self.shape = tuple(int(s) for s in shape)
+        self.kind = kind
+        self.dtype = KIND_DTYPE[kind]
+        self.itemsize = ITEMSIZE[kind]
+        self.numel = int(np.prod(self.shape, dtype=np.int64)) if self.shape else 1
+        self.nbytes = self.numel * self.itemsize
+        # region known to be zero but not yet written (first touch or a
+        # deferred gradient clear); None = contents are materialized
+        self.pending = whole_box(self.shape) if fresh else None
+        self.alias_of: Buffer | None = None
+        self.tensor = None
+        self.strides = tuple(int(np.prod(self.shape[d + 1:], dtype=np.int64)) for d in range(len(self.shape)))
+
+    def root(self) -> "Buffer":
+        b = self
+        while b.alias_of is not None:
+            b = b.alias_of
+        return b
+
+    @property
+    def ptr(self) -> int:
+        t = self.root().tensor
+        if t is None:
+            raise RuntimeError(f"buffer '{self.name}' not allocated")
+        return t.data_ptr()
+
+    def __repr__(self):
+        return f"Buffer({self.name}, {self.shape}, {self.kind})"
+
+
+# ---------------------------------------------------------------------------
+# affine analysis of subsets and ranges
+
+_PROBES = [(3, 7, 11, 13, 17, 19, 23, 29), (-5, 2, 9, -4, 6, 1, -8, 5), (101, 57, -33, 12, 71, -19, 44, 3),
+           (2, 2, 2, 2, 2, 2, 2, 2), (-1, -3, -7, -2, -9, -6, -4, -11)]
+
+
+def affine_form(expr, bind: dict, params: tuple, what: str):
+    """(c0, [s_p]) with expr == c0 + sum_p s_p * x_p for integer x."""
+    base = dict(bind)
+    for p in params:
+        base[p] = 0
+    try:
+        c0 = eval_int(expr, base, what)
+        coefs = []
+        for p in params:
+            b = dict(base)
+            b[p] = 1
+            coefs.append(eval_int(expr, b, what) - c0)
+        if params and (free_names(expr) & set(params)):
+            for pt in _PROBES:
+                b = dict(bind)
+                b.update(zip(params, pt))
+                if eval_int(expr, b, what) != c0 + sum(c * v for c, v in zip(coefs, pt)):
+                    raise UnsupportedConstruct(f"{what} is not affine in the map parameters")
+    except (DomainError, ZeroDivisionError) as exc:
+        if params and (free_names(expr) & set(params)):
+            raise UnsupportedConstruct(f"{what} is not affine in the map parameters") from exc
+        raise
+    return c0, coefs
+
+
+class SpaceInfo:
+    """Iteration space of one map with concrete bindings."""
+
+    def __init__(self, params, lo, hi, step):
+        self.params = tuple(params)
+        self.np = len(params)
+        self.lo = lo      # list of (c0, coefs over earlier params)
+        self.hi = hi
+        self.step = step  # list of int
+        self.triangular = any(any(c) for c, in ((f[1],) for f in lo + hi))
+        # bounding box (first value, last value) per parameter
+        self.first, self.last, self.ext = [], [], []
+        for p in range(self.np):
+            lo_min = self._interval(lo[p], p)[0]
+            hi_max = self._interval(hi[p], p)[1]
+            if self.triangular:
+                first, last = lo_min, hi_max - 1
+                ext = max(0, last - first + 1)
+            else:
+                n = max(0, -(-(hi[p][0] - lo[p][0]) // step[p]))
+                first = lo[p][0]
+                last = first + (n - 1) * step[p]
+                ext = n
+            self.first.append(first)
+            self.last.append(last)
+            self.ext.append(ext)
+        self._npoints = None
+
+    def _interval(self, form, p):
+        c0, coefs = form
+        lo = hi = c0
+        for q in range(p):
+            a, b = coefs[q] * self.first[q], coefs[q] * self.last[q]
+            lo += min(a, b)
+            hi += max(a, b)
+        return lo, hi
+
+    @property
+    def empty(self) -> bool:
+        return any(e <= 0 for e in self.ext)
+
+    def points(self) -> int:
+        if self._npoints is None:
+            if self.empty:
+                self._npoints = 0
+            elif not self.triangular:
+                self._npoints = int(np.prod(self.ext, dtype=np.int64))
+            else:
+                self._npoints = int(self.enumerate_count())
+        return self._npoints
+
+    def enumerate_count(self) -> int:
+        def rec(p, xs):
+            if p == self.np:
+                return 1
+            lo = self.lo[p][0] + sum(c * x for c, x in zip(self.lo[p][1], xs))
+            hi = self.hi[p][0] + sum(c * x for c, x in zip(self.hi[p][1], xs))
+            if p == self.np - 1:
+                return max(0, -(-(hi - lo) // self.step[p]))
+            return sum(rec(p + 1, xs + [v]) for v in range(lo, hi, self.step[p]))
+
+        return rec(0, [])
+
+    def range_of(self, form):
+        """min/max of c0 + sum s_p x_p over the bounding box."""
+        c0, coefs = form
+        lo = hi = c0
+        for p, s in enumerate(coefs):
+            a, b = s * self.first[p], s * self.last[p]
+            lo += min(a, b)
+            hi += max(a, b)
+        return lo, hi
+
+    def box_points(self) -> int:
+        return int(np.prod(self.ext, dtype=np.int64)) if self.np else 1
+
+    def fill(self, sp: L.Space):
+        sp.nparams = self.np
+        sp.triangular = 1 if self.triangular else 0
+        for p in range(self.np):
+            sp.lo0[p] = self.lo[p][0]
+            sp.hi0[p] = self.hi[p][0]
+            sp.step[p] = self.step[p]
+            for q in range(p):
+                sp.loc[p][q] = self.lo[p][1][q]
+                sp.hic[p][q] = self.hi[p][1][q]
+            sp.box_lo[p] = self.first[p]
+            sp.box_ext[p] = self.ext[p]
+
+
+class Access:
+    """One memlet endpoint: buffer + per-dimension affine index forms."""
+
+    def __init__(self, buf: Buffer, forms: list):
+        self.buf = buf
+        self.forms = forms  # per dim (c0, coefs)
+
+    def flat(self, np_: int):
+        c0 = sum(st * f[0] for st, f in zip(self.buf.strides, self.forms))
+        s = [sum(st * f[1][p] for st, f in zip(self.buf.strides, self.forms)) for p in range(np_)]
+        return c0, s
+
+    def matrix(self, np_):
+        return [list(f[1]) for f in self.forms], [f[0] for f in self.forms]
+
+    def key(self):
+        return (self.buf.bid, tuple((f[0], tuple(f[1])) for f in self.forms))
+
+    def identity_offset(self, np_):
+        """Offsets if dim d == x_d + off_d for every d (and rank == np)."""
+        if len(self.forms) != np_:
+            return None
+        offs = []
+        for d, (c0, coefs) in enumerate(self.forms):
+            if any(c != (1 if p == d else 0) for p, c in enumerate(coefs)):
+                return None
+            offs.append(c0)
+        return offs
+
+
+def fill_operand(op: L.Operand, acc: Access, np_: int):
+    op.base = acc.buf.ptr
+    op.dtype = acc.buf.dtype
+    c0, s = acc.flat(np_)
+    op.c0 = c0
+    for p in range(np_):
+        op.s[p] = s[p]
+
+
+# ---------------------------------------------------------------------------
+# tasklet bodies -> bytecode
+
+
+class Code:
+    def __init__(self):
+        self.code, self.arg, self.consts = [], [], []
+
+    def const(self, v: float) -> int:
+        v = float(v)
+        for i, c in enumerate(self.consts):
+            if c == v and math.copysign(1, c) == math.copysign(1, v):
+                return i
+        if len(self.consts) >= L.MAXCONST:
+            raise UnsupportedConstruct("tasklet body has too many constants")
+        self.consts.append(v)
+        return len(self.consts) - 1
+
+    def compile(self, expr, conn_index: dict) -> tuple:
+        start = len(self.code)
+        depth = self._emit(expr, conn_index, 0)
+        if depth > 12:
+            raise UnsupportedConstruct("tasklet body too deep for the device evaluator")
+        if len(self.code) > L.MAXCODE:
+            raise UnsupportedConstruct("tasklet bodies too long for the device evaluator")
+        return start, len(self.code) - start
+
+    def _emit(self, e, ci, depth) -> int:
+        t = type(e)
+        if t is Const:
+            self.code.append(L.OP_CONST)
+            self.arg.append(self.const(e.value))
+            return depth + 1
+        if t is Name:
+            if e.id not in ci:
+                raise UnboundName(f"tasklet body uses unbound connector '{e.id}'")
+            self.code.append(L.OP_IN)
+            self.arg.append(ci[e.id])
+            return depth + 1
+        if t is Unary:
+            d = self._emit(e.x, ci, depth)
+            self.code.append(L.UNOP[e.op])
+            self.arg.append(0)
+            return d
+        if t is Binary:
+            if e.op not in L.BINOP:
+                raise UnsupportedConstruct(f"operator '{e.op}' is not allowed in tasklet bodies")
+            d1 = self._emit(e.x, ci, depth)
+            d2 = self._emit(e.y, ci, depth + 1)
+            self.code.append(L.BINOP[e.op])
+            self.arg.append(0)
+            return max(d1, d2)
+        raise UnsupportedConstruct(f"cannot evaluate {e!r} in a tasklet")
+
+    def fill(self, desc):
+        for i, (c, a) in enumerate(zip(self.code, self.arg)):
+            desc.code[i] = c
+            desc.arg[i] = a
+        for i, v in enumerate(self.consts):
+            desc.consts[i] = v
+
+
+def linearize(expr):
+    """(const, {conn: coef}) if expr is an affine combination of connectors
+    with constant coefficients, else None."""
+    t = type(expr)
+    if t is Const:
+        return float(expr.value), {}
+    if t is Name:
+        return 0.0, {expr.id: 1.0}
+    if t is Unary:
+        if expr.op != "neg":
+            return None
+        r = linearize(expr.x)
+        return None if r is None else (-r[0], {k: -v for k, v in r[1].items()})
+    if t is Binary:
+        a, b = linearize(expr.x), linearize(expr.y)
+        if a is None or b is None:
+            return None
+        if expr.op in ("add", "sub"):
+            sgn = 1.0 if expr.op == "add" else -1.0
+            coef = dict(a[1])
+            for k, v in b[1].items():
+                coef[k] = coef.get(k, 0.0) + sgn * v
+            return a[0] + sgn * b[0], coef
+        if expr.op == "mul":
+            if not a[1]:
+                return a[0] * b[0], {k: a[0] * v for k, v in b[1].items()}
+            if not b[1]:
+                return a[0] * b[0], {k: b[0] * v for k, v in a[1].items()}
+            return None
+        if expr.op == "div" and not b[1] and b[0] != 0:
+            return a[0] / b[0], {k: v / b[0] for k, v in a[1].items()}
+        return None
+    return None
+
+
+# ---------------------------------------------------------------------------
+# operations
+
+
+class Op:
+    family = "op"
+    reads: tuple = ()
+    writes: tuple = ()
+    full_write = False  # True when the op defines every element of its single write
+
+    def prepare(self, rt):
+        pass
+
+    def launch(self, rt, stream):
+        raise NotImplementedError
+
+    def algorithmic_bytes(self) -> int:
+        return sum(b.nbytes for b in set(self.reads)) + sum(b.nbytes for b in set(self.writes))
+
+
+class MapOp(Op):
+    family = "map_pointwise"
+
+    def __init__(self, space: SpaceInfo, ins: list, outs: list, code: Code, segs: list, compute_f64: bool):
+        self.space, self.ins, self.outs, self.code, self.segs = space, ins, outs, code, segs
+        self.compute_f64 = compute_f64
+        self.reads = tuple(a.buf for a in ins) + tuple(a.buf for a, w in outs if w == 1)
+        self.writes = tuple(a.buf for a, _ in outs)
+
+    def prepare(self, rt):
+        d = L.MapDesc()
+        self.space.fill(d.space)
+        d.n_in, d.n_out = len(self.ins), len(self.outs)
+        d.compute_f64 = 1 if self.compute_f64 else 0
+        for k, a in enumerate(self.ins):
+            fill_operand(d.in_[k], a, self.space.np)
+        for o, (a, w) in enumerate(self.outs):
+            fill_operand(d.out[o], a, self.space.np)
+            d.wcr[o] = w
+            d.code_start[o], d.code_len[o] = self.segs[o]
+        self.code.fill(d)
+        d.ncode = len(self.code.code)
+        d.err = rt.err_ptr
+        self.desc = d
+        self._ref = C.byref(d)
+
+    def launch(self, rt, stream):
+        L.check(rt.lib.gfb_map_launch(self._ref, stream), "map")
+
+
+class GatherOp(Op):
+    family = "map_gather"
+
+    def __init__(self, space, dst: Buffer, ybox, clear_mode, clear_box, ins, terms, code, compute_f64,
+                 lanes_on_free, nsplit):
+        self.space, self.dst, self.ybox = space, dst, ybox
+        self.clear_mode, self.clear_box = clear_mode, clear_box
+        self.ins, self.terms, self.code = ins, terms, code
+        self.compute_f64, self.lanes_on_free, self.nsplit = compute_f64, lanes_on_free, nsplit
+        self.reads = tuple(a.buf for a in ins) + ((dst,) if clear_mode in (0, 2) else ())
+        self.writes = (dst,)
+
+    def workspace_bytes(self):
+        return 0 if self.nsplit <= 1 else self.nsplit * box_size(self.ybox) * (8 if self.compute_f64 else 4)
+
+    def prepare(self, rt):
+        d = L.GatherDesc()
+        self.space.fill(d.space)
+        d.rank = len(self.dst.shape)
+        d.dtype = self.dst.dtype
+        d.compute_f64 = 1 if self.compute_f64 else 0
+        d.n_in = len(self.ins)
+        d.n_terms = len(self.terms)
+        d.clear_mode = self.clear_mode
+        d.lanes_on_free = self.lanes_on_free
+        d.nsplit = self.nsplit
+        d.dst = self.dst.ptr
+        for r in range(d.rank):
+            d.dst_strides[r] = self.dst.strides[r]
+            d.ybox_lo[r] = self.ybox[r][0]
+            d.ybox_ext[r] = self.ybox[r][1] - self.ybox[r][0]
+            if self.clear_box is not None:
+                d.clear_lo[r], d.clear_hi[r] = self.clear_box[r]
+        for k, a in enumerate(self.ins):
+            fill_operand(d.in_[k], a, self.space.np)
+        for t, (row_of, order, Cm, off, seg) in enumerate(self.terms):
+            tm = d.terms[t]
+            for p in range(self.space.np):
+                tm.row_of[p] = row_of[p]
+            for k, p in enumerate(order):
+                tm.order[k] = p
+            tm.npiv = len(order)
+            tm.code_start, tm.code_len = seg
+            for r in range(d.rank):
+                tm.off[r] = off[r]
+                for p in range(self.space.np):
+                    tm.C[r][p] = Cm[r][p]
+        self.code.fill(d)
+        d.workspace = rt.workspace_ptr if self.nsplit > 1 else None
+        d.err = rt.err_ptr
+        self.desc = d
+        self._ref = C.byref(d)
+
+    def launch(self, rt, stream):
+        L.check(rt.lib.gfb_gather_launch(self._ref, stream), "gather")
+
+
+class StencilOp(Op):
+    family = "stencil"
+
+    def __init__(self, dst: Buffer, srcs: list, region, clear_mode, clear_box, taps, *, kind="sweep"):
+        # taps: (src index, coef, delta tuple, mask box or None)
+        self.dst, self.srcs, self.region = dst, srcs, region
+        self.clear_mode, self.clear_box, self.taps = clear_mode, clear_box, taps
+        self.kind = kind
+        self.reads = tuple(srcs) + ((dst,) if clear_mode in (0, 2) else ())
+        self.writes = (dst,)
+
+    def prepare(self, rt):
+        d = L.StencilDesc()
+        rank = len(self.dst.shape)
+        d.rank, d.dtype = rank, self.dst.dtype
+        d.clear_mode = self.clear_mode
+        d.ntaps = len(self.taps)
+        d.dst = self.dst.ptr
+        for i, s in enumerate(self.srcs):
+            d.src[i] = s.ptr
+        for r in range(rank):
+            d.dims[r] = self.dst.shape[r]
+            d.lo[r], d.hi[r] = self.region[r]
+            if self.clear_box is not None:
+                d.clear_lo[r], d.clear_hi[r] = self.clear_box[r]
+        for t, (si, coef, delta, mask) in enumerate(self.taps):
+            d.tap_src[t] = si
+            d.tap_coef[t] = coef
+            d.tap_masked[t] = 0 if mask is None else 1
+            for r in range(rank):
+                d.tap_delta[t][r] = delta[r]
+                if mask is not None:
+                    d.tap_mlo[t][r], d.tap_mhi[t][r] = mask[r]
+        self.desc = d
+        self._ref = C.byref(d)
+
+    def launch(self, rt, stream):
+        L.check(rt.lib.gfb_stencil_launch(self._ref, stream), "stencil")
+
+    def algorithmic_bytes(self) -> int:
+        pts = box_size(self.region)
+        per = self.dst.itemsize
+        nsrc = len(self.srcs)
+        return pts * per * (nsrc + 1 + (1 if self.clear_mode == 0 else 0))
+
+
+class FillOp(Op):
+    """D[box] = value (materialized pending clear / zero-init)."""
+
+    family = "fill"
+
+    def __init__(self, dst: Buffer, box, value=0.0):
+        self.dst, self.box, self.value = dst, box, value
+        self.writes = (dst,)
+        self.full_write = box == whole_box(dst.shape)
+
+    def prepare(self, rt):
+        rank = len(self.dst.shape)
+        self.whole = self.full_write or rank == 0
+        if not self.whole and rank > 3:
+            raise UnsupportedConstruct("partial clears of arrays with rank > 3")
+        self._dims = (L.i64 * max(rank, 1))(*self.dst.shape)
+        self._lo = (L.i64 * max(rank, 1))(*[b[0] for b in self.box])
+        self._hi = (L.i64 * max(rank, 1))(*[b[1] for b in self.box])
+
+    def launch(self, rt, stream):
+        if self.whole:
+            L.check(rt.lib.gfb_broadcast(None, 0, self.value, self.dst.ptr, self.dst.numel, self.dst.dtype, 0,
+                                         stream), "fill")
+        else:
+            L.check(rt.lib.gfb_fill_box(self.dst.ptr, self.dst.dtype, len(self.dst.shape), self._dims, self._lo,
+                                        self._hi, self.value, stream), "fill_box")
+
+
+class ReduceOp(Op):
+    family = "reduce_sum"
+
+    def __init__(self, x: Buffer, out: Buffer, accumulate: bool):
+        self.x, self.out, self.accumulate = x, out, accumulate
+        self.reads = (x,) + ((out,) if accumulate else ())
+        self.writes = (out,)
+        self.full_write = not accumulate
+
+    def workspace_bytes(self):
+        return int(L.load().gfb_reduce_workspace_bytes(self.x.numel))
+
+    def launch(self, rt, stream):
+        L.check(rt.lib.gfb_reduce_sum(self.x.ptr, self.x.dtype, self.x.numel, self.out.ptr, self.out.dtype,
+                                      1 if self.accumulate else 0, rt.workspace_ptr, stream), "reduce_sum")
+
+
+class EwOp(Op):
+    family = "elementwise"
+
+    def __init__(self, op: int, const: float, a: Buffer, b: Buffer | None, out: Buffer, accumulate: bool):
+        self.op, self.const, self.a, self.b, self.out, self.accumulate = op, const, a, b, out, accumulate
+        self.reads = (a,) + ((b,) if b is not None else ()) + ((out,) if accumulate else ())
+        self.writes = (out,)
+        self.full_write = not accumulate
+
+    def launch(self, rt, stream):
+        L.check(rt.lib.gfb_elementwise(self.op, self.const, self.a.ptr, self.a.numel,
+                                       None if self.b is None else self.b.ptr,
+                                       0 if self.b is None else self.b.numel, self.out.ptr, self.out.numel,
+                                       self.out.dtype, 1 if self.accumulate else 0, rt.err_ptr, stream),
+                "elementwise")
+
+
+class BroadcastOp(Op):
+    family = "broadcast"
+
+    def __init__(self, src: Buffer | None, scale: float, out: Buffer, accumulate: bool):
+        self.src, self.scale, self.out, self.accumulate = src, scale, out, accumulate
+        self.reads = ((src,) if src is not None else ()) + ((out,) if accumulate else ())
+        self.writes = (out,)
+        self.full_write = not accumulate
+
+    def launch(self, rt, stream):
+        L.check(rt.lib.gfb_broadcast(None if self.src is None else self.src.ptr,
+                                     0 if self.src is None else self.src.dtype, self.scale, self.out.ptr,
+                                     self.out.numel, self.out.dtype, 1 if self.accumulate else 0, stream),
+                "broadcast")
+
+
+class MatmulOp(Op):
+    family = "matmul"
+
+    def __init__(self, a: Buffer, b: Buffer, out: Buffer, ta: bool, tb: bool, M, N, K, accumulate: bool):
+        self.a, self.b, self.out = a, b, out
+        self.ta, self.tb, self.M, self.N, self.K = ta, tb, M, N, K
+        self.accumulate = accumulate
+        self.reads = (a, b) + ((out,) if accumulate else ())
+        self.writes = (out,)
+        self.full_write = not accumulate
+        self.lda = a.shape[1]
+        self.ldb = b.shape[1]
+        self.ldc = N
+
+    def workspace_bytes(self):
+        return int(L.load().gfb_matmul_workspace_bytes(self.out.dtype, int(self.ta), int(self.tb), self.M, self.N,
+                                                       self.K))
+
+    def flops(self):
+        return 2 * self.M * self.N * self.K
+
+    def launch(self, rt, stream):
+        L.check(rt.lib.gfb_matmul(self.out.dtype, int(self.ta), int(self.tb), self.M, self.N, self.K, self.a.ptr,
+                                  self.lda, self.b.ptr, self.ldb, self.out.ptr, self.ldc,
+                                  1 if self.accumulate else 0, rt.workspace_ptr, stream), "matmul")
+
+
+class CopyOp(Op):
+    family = "copy"
+
+    def __init__(self, dst: Buffer, src: Buffer):
+        self.dst, self.src = dst, src
+        self.reads = (src,)
+        self.writes = (dst,)
+        self.full_write = True
+        self.elided = False
+
+    def launch(self, rt, stream):
+        if not self.elided:
+            L.check(rt.lib.gfb_copy(self.dst.ptr, self.src.ptr, self.dst.nbytes, stream), "copy")
+
+
+# ---------------------------------------------------------------------------
+# lowering context
+
+
+class LoopCtx:
+    __slots__ = ("label", "iterates", "pos")
+
+    def __init__(self, label, iterates, pos=0):
+        self.label, self.iterates, self.pos = label, iterates, pos
+
+    @property
+    def current(self):
+        return self.iterates[self.pos]
+
+
+class LTape:
+    """Lowering-time image of the reference Tape (interpreter.py:70-75)."""
+
+    def __init__(self):
+        self.values = {}           # (data, version, coords) -> Buffer
+        self.branch_trace = {}     # label -> [bool]
+        self.iterate_records = {}  # label -> {coords: [int]}
+
+
+class Lowering:
+    """Accumulates launches for one or more program runs over shared buffers."""
+
+    def __init__(self, *, trip_limit=None):
+        self.ops: list[Op] = []
+        self.buffers: list[Buffer] = []
+        self.flops = 0
+        self.trip_limit = trip_limit if trip_limit is not None else default_trip_limit()
+
+    def new_buffer(self, name, shape, kind, *, fresh=True) -> Buffer:
+        b = Buffer(name, shape, kind, fresh=fresh)
+        self.buffers.append(b)
+        return b
+
+    def emit(self, op: Op):
+        if len(self.ops) >= MAX_UNROLLED_OPS:
+            raise UnsupportedConstruct(
+                f"program unrolls to more than {MAX_UNROLLED_OPS} launches (sequential scalar loop nest); "
+                "express the parallel work as a map")
+        self.ops.append(op)
+
+    # -- pending clears -------------------------------------------------------
+
+    def materialize(self, buf: Buffer):
+        if buf.pending is not None:
+            box = buf.pending
+            buf.pending = None
+            if box_size(box) > 0:
+                self.emit(FillOp(buf, box))
+
+    def add_clear(self, buf: Buffer, box):
+        if box_size(box) == 0:
+            return
+        if buf.pending is None or box_contains(box, buf.pending):
+            buf.pending = box
+        elif box_contains(buf.pending, box):
+            pass
+        else:
+            self.materialize(buf)
+            buf.pending = box
+
+    # -- post passes -------------------------------------------------------------
+
+    def finish(self, observed: list):
+        for b in observed:
+            self.materialize(b)
+        self._elide_copies()
+
+    def _elide_copies(self):
+        """Copies whose source and destination are never written afterwards
+        (tape snapshots, plan keep-copies) become aliases."""
+        last_write = {}
+        first_touch = {}
+        for i, op in enumerate(self.ops):
+            for b in op.writes:
+                last_write[b.bid] = i
+            for b in tuple(op.reads) + tuple(op.writes):
+                first_touch.setdefault(b.bid, i)
+        for i, op in enumerate(self.ops):
+            if not isinstance(op, CopyOp):
+                continue
+            src, dst = op.src, op.dst
+            if last_write.get(src.bid, -1) > i or last_write.get(dst.bid, -1) > i:
+                continue
+            if first_touch.get(dst.bid, i) < i or dst.alias_of is not None:
+                continue
+            if src.root() is dst.root():
+                continue
+            dst.alias_of = src
+            op.elided = True
+
+
+class ProgramRun:
+    """Lowers one program execution (the reference Executor.run)."""
+
+    def __init__(self, low: Lowering, program, params: dict, env: dict, *, record=None, tape: LTape | None = None,
+                 src_tape: LTape | None = None, forwarding=None, versions=None):
+        self.low = low
+        self.program = program
+        self.params = dict(params)
+        self.bind = dict(params)
+        self.env = env
+        self.record = record
+        self.tape = tape
+        self.src_tape = src_tape
+        self.forwarding = forwarding or {}
+        self.versions = versions  # (version_of, loops_of) or None
+        self.ctx = {}
+        self.ctx_stack = []
+        self.branch_down = {}
+        self._shapes = {}
+
+    # -- env -------------------------------------------------------------------
+
+    def shape_of(self, name) -> tuple:
+        s = self._shapes.get(name)
+        if s is None:
+            desc = self.program.descriptors[name]
+            s = tuple(eval_int(d, self.params, f"dimension of '{name}'") for d in desc.shape)
+            self._shapes[name] = s
+        return s
+
+    def read(self, name: str) -> Buffer:
+        b = self.env.get(name)
+        if b is not None:
+            return b
+        if name in self.forwarding:
+            return self.fetch_forwarded(name)
+        desc = self.program.descriptors.get(name)
+        if desc is None or desc.role == "input":
+            raise UnboundName(f"no value for input '{name}'")
+        return self._fresh(name)
+
+    def write(self, name: str) -> Buffer:
+        b = self.env.get(name)
+        if b is None:
+            if name not in self.program.descriptors:
+                raise UnboundName(f"'{name}' is not declared")
+            b = self._fresh(name)
+        return b
+
+    def _fresh(self, name) -> Buffer:
+        desc = self.program.descriptors[name]
+        b = self.low.new_buffer(name, self.shape_of(name), desc.element_kind, fresh=True)
+        self.env[name] = b
+        return b
+
+    def fetch_forwarded(self, name) -> Buffer:
+        entry = self.forwarding[name]
+        if self.src_tape is None:
+            raise MissingTapeValue(f"'{name}' requested but no tape is attached")
+        for cand in entry.candidates:
+            coords = self._cand_coords(cand.directives)
+            if coords is None:
+                continue
+            slot = self.src_tape.values.get((entry.data, cand.version, coords))
+            if slot is not None:
+                return slot
+        raise MissingTapeValue(f"no recorded instance of '{entry.data}' matches '{name}' here")
+
+    def _cand_coords(self, directives):
+        coords = []
+        for j, (label, kind) in enumerate(directives):
+            ctx = self.ctx.get(label)
+            if kind == "cur":
+                if ctx is None:
+                    return None
+                coords.append(ctx.current)
+            elif kind == "prev":
+                if ctx is None or ctx.pos == 0:
+                    return None
+                coords.append(ctx.iterates[ctx.pos - 1])
+            elif kind == "last":
+                if ctx is not None:
+                    coords.append(ctx.iterates[-1])
+                else:
+                    recs = (self.src_tape.iterate_records if self.src_tape else {}).get(label)
+                    if not recs:
+                        return None
+                    seq = recs.get(tuple(coords[:j]))
+                    if not seq:
+                        return None
+                    coords.append(seq[-1])
+        return tuple(coords)
+
+    # -- control flow ----------------------------------------------------------
+
+    def run(self):
+        self.region(self.program.region)
+
+    def region(self, blocks):
+        for b in blocks:
+            if isinstance(b, State):
+                self.state(b)
+            elif isinstance(b, LoopRegion):
+                self.loop(b)
+            else:
+                self.branch(b)
+
+    def _header_bind(self, loop):
+        need = (free_names(loop.init) | free_names(loop.bound) | free_names(loop.update)) - {loop.iterator}
+        for name in need:
+            if name not in self.bind and name in self.program.descriptors:
+                raise UnsupportedConstruct(
+                    f"loop '{loop.label}' header reads runtime data '{name}'; the engine needs static headers")
+        return dict(self.bind)
+
+    def simulate(self, loop) -> list:
+        b = self._header_bind(loop)
+        out = []
+        i = eval_int(loop.init, b, f"init of '{loop.label}'")
+        lt = loop.cmp == "<"
+        while True:
+            bound = eval_int(loop.bound, b, f"bound of '{loop.label}'")
+            if not (i < bound if lt else i > bound):
+                break
+            out.append(i)
+            if len(out) > self.low.trip_limit:
+                raise NonTermination(f"loop '{loop.label}' exceeded the trip limit of {self.low.trip_limit}")
+            b[loop.iterator] = i
+            i = eval_int(loop.update, b, f"update of '{loop.label}'")
+        return out
+
+    def loop(self, loop):
+        if loop.replay_of is not None:
+            if self.src_tape is None:
+                raise MissingInverse(
+                    f"loop '{loop.replay_of}' has a non-affine header and no declared inverse; "
+                    "reversing it requires recorded iterates")
+            key = tuple(c.current for c in self.ctx_stack)
+            recs = self.src_tape.iterate_records.get(loop.replay_of, {})
+            if key not in recs:
+                raise MissingTapeValue(f"no recorded iterates for loop '{loop.replay_of}' at {key}")
+            self.iterates(loop, recs[key], loop.replay_of, reverse=True)
+        elif loop.reversed_simulate:
+            fwd = self.simulate(loop)
+            self.inverse(loop, fwd, loop.reverse_of or loop.label)
+        elif loop.reverse_of is not None:
+            order = self.simulate(loop)
+            self.iterates(loop, order[::-1], loop.reverse_of, reverse=True)
+        else:
+            its = self.simulate(loop)
+            if self.tape is not None:
+                key = tuple(c.current for c in self.ctx_stack)
+                self.tape.iterate_records.setdefault(loop.label, {})[key] = list(its)
+            self.iterates(loop, its, loop.label, reverse=False)
+
+    def _enter(self, loop, label, fwd):
+        ctx = LoopCtx(label, fwd)
+        self.ctx[label] = ctx
+        self.ctx_stack.append(ctx)
+        return ctx, loop.iterator in self.bind, self.bind.get(loop.iterator)
+
+    def _leave(self, loop, label, had, saved):
+        self.ctx_stack.pop()
+        del self.ctx[label]
+        if had:
+            self.bind[loop.iterator] = saved
+        else:
+            self.bind.pop(loop.iterator, None)
+
+    def iterates(self, loop, fwd, label, reverse):
+        ctx, had, saved = self._enter(loop, label, fwd)
+        try:
+            positions = range(len(fwd) - 1, -1, -1) if reverse else range(len(fwd))
+            for pos in positions:
+                ctx.pos = pos
+                self.bind[loop.iterator] = fwd[pos]
+                self.region(loop.body)
+        finally:
+            self._leave(loop, label, had, saved)
+
+    def inverse(self, loop, fwd, label):
+        if not fwd:
+            return
+        ctx, had, saved = self._enter(loop, label, fwd)
+        try:
+            i = fwd[-1]
+            for pos in range(len(fwd) - 1, -1, -1):
+                ctx.pos = pos
+                if i != fwd[pos]:
+                    raise DomainError(f"declared inverse of loop '{loop.label}' diverges: expected {fwd[pos]}, got {i}")
+                self.bind[loop.iterator] = i
+                self.region(loop.body)
+                if pos > 0:
+                    i = eval_int(loop.inverse, dict(self.bind), f"inverse of '{loop.label}'")
+        finally:
+            self._leave(loop, label, had, saved)
+
+    def branch(self, br):
+        if br.trace_ref is not None:
+            outcomes = (self.src_tape.branch_trace if self.src_tape else {}).get(br.trace_ref)
+            if not outcomes:
+                raise MissingTapeValue(f"no recorded outcomes for branch '{br.trace_ref}'")
+            cursor = self.branch_down.get(br.trace_ref, len(outcomes)) - 1
+            if cursor < 0:
+                raise MissingTapeValue(f"branch trace of '{br.trace_ref}' exhausted")
+            self.branch_down[br.trace_ref] = cursor
+            outcome = outcomes[cursor]
+        else:
+            data = free_names(br.condition) & set(self.program.descriptors)
+            if data:
+                raise UnsupportedConstruct(
+                    f"branch '{br.label}' depends on runtime data {sorted(data)}; data-dependent control "
+                    "flow is not lowered to the device yet")
+            outcome = bool(evaluate(br.condition, dict(self.bind)))
+            if self.tape is not None:
+                self.tape.branch_trace.setdefault(br.label, []).append(outcome)
+        self.region(br.then_body if outcome else br.else_body)
+
+    # -- states -----------------------------------------------------------------
+
+    def state(self, st: State):
+        by_id = {n.id: n for n in st.graph.nodes}
+        for nid in schedule(st.graph):
+            node = by_id[nid]
+            if isinstance(node, AccessNode):
+                self.visit_access(st.label, node)
+            elif isinstance(node, Tasklet):
+                self.map_like(None, node, st.graph)
+            elif isinstance(node, LibraryNode):
+                self.library(node, st.graph)
+            else:
+                self.map_node(node)
+
+    def visit_access(self, label, node):
+        if self.tape is None or self.versions is None or self.record is None:
+            return
+        version_of, loops_of = self.versions
+        v = version_of.get((label, node.id))
+        if v is None or not self._want(node.data, v):
+            return
+        coords = tuple(self.ctx[l].current for l in loops_of[(node.data, v)])
+        self.snapshot(node.data, v, coords)
+
+    def _want(self, data, v):
+        return self.record == "all" or (data, v) in self.record
+
+    def snapshot(self, data, v, coords):
+        src = self.read(data)
+        self.low.materialize(src)
+        slot = self.low.new_buffer(f"{data}@v{v}{list(coords) if coords else ''}", src.shape, src.kind, fresh=False)
+        self.low.emit(CopyOp(slot, src))
+        self.tape.values[(data, v, coords)] = slot
+
+    # -- maps and tasklets --------------------------------------------------------
+
+    def build_space(self, node: MapNode) -> SpaceInfo:
+        lo, hi, step = [], [], []
+        params = node.params
+        for k, (start, stop, st) in enumerate(node.ranges):
+            lo.append(affine_form(start, self.bind, params[:k], f"map '{node.id}' start"))
+            hi.append(affine_form(stop, self.bind, params[:k], f"map '{node.id}' stop"))
+            s = affine_form(st, self.bind, params[:k], f"map '{node.id}' step")
+            if any(s[1]):
+                raise UnsupportedConstruct(f"map '{node.id}' step depends on map parameters")
+            if s[0] <= 0:
+                raise DomainError(f"map '{node.id}' step must be positive, got {s[0]}")
+            step.append(s[0])
+        return SpaceInfo(params, lo, hi, step)
+
+    def map_node(self, node: MapNode):
+        computes = [n for n in node.body.nodes if not isinstance(n, AccessNode)]
+        if len(computes) != 1 or not isinstance(computes[0], Tasklet):
+            raise UnsupportedConstruct(f"map '{node.id}': the engine lowers single-tasklet map bodies")
+        space = self.build_space(node)
+        saved = {p: self.bind[p] for p in node.params if p in self.bind}
+        try:
+            self.map_like(space, computes[0], node.body, node_id=node.id)
+        finally:
+            for p in node.params:
+                self.bind.pop(p, None)
+            self.bind.update(saved)
+
+    def access(self, buf: Buffer, subset, space: SpaceInfo, what: str) -> Access:
+        params = space.params if space else ()
+        rank = len(buf.shape)
+        if subset is None or len(subset) != rank:
+            raise UnsupportedConstruct(f"{what}: element subset of rank {rank} required")
+        forms = [affine_form(e, self.bind, params, f"subset of '{buf.name}'") for e in subset]
+        # static bounds check over the whole iteration space (reference
+        # checks each access at run time, interpreter.py:396-403)
+        for k, f in enumerate(forms):
+            if space is None:
+                lo = hi = f[0]
+            else:
+                lo, hi = space.range_of(f)
+            if lo < 0 or hi >= buf.shape[k]:
+                if space is not None and space.triangular and space.box_points() <= (1 << 22):
+                    lo, hi = self._exact_range(space, f)
+                if lo < 0 or hi >= buf.shape[k]:
+                    bad = lo if lo < 0 else hi
+                    raise OutOfBounds(f"'{buf.name}' index {bad} outside dimension of size {buf.shape[k]}")
+        return Access(buf, forms)
+
+    @staticmethod
+    def _exact_range(space: SpaceInfo, form):
+        grids = np.meshgrid(*[np.arange(f, l + 1) for f, l in zip(space.first, space.last)], indexing="ij")
+        pts = np.stack([g.reshape(-1) for g in grids], axis=1)
+        ok = np.ones(len(pts), dtype=bool)
+        for p in range(space.np):
+            lo = space.lo[p][0] + sum(c * pts[:, q] for q, c in enumerate(space.lo[p][1]))
+            hi = space.hi[p][0] + sum(c * pts[:, q] for q, c in enumerate(space.hi[p][1]))
+            ok &= (pts[:, p] >= lo) & (pts[:, p] < hi) & ((pts[:, p] - lo) % space.step[p] == 0)
+        v = form[0] + pts[ok] @ np.asarray(form[1], dtype=np.int64)
+        return (int(v.min()), int(v.max())) if v.size else (0, 0)
+
+    def map_like(self, space, t: Tasklet, df, node_id=None):
+        """Lower one tasklet, at state level (space None: a single point) or
+        as the body of a map over ``space``."""
+        what = f"map '{node_id}'" if node_id else f"tasklet '{t.id}'"
+        if space is None:
+            space = SpaceInfo((), [], [], [])
+        npts = space.points()
+        in_edges = df.in_edges(t.id)
+        out_edges = df.out_edges(t.id)
+        self.low.flops += sum(count_ops(t.body[e.src_conn]) for e in out_edges) * npts
+        if npts == 0:
+            return
+        np_ = space.np
+        ins = {}
+        for e in in_edges:
+            buf = self.read(e.data)
+            ins[e.dst_conn] = self.access(buf, e.subset, space, what)
+        outs = []
+        for e in out_edges:
+            buf = self.write(e.data)
+            outs.append((e.src_conn, self.access(buf, e.subset, space, what), e.wcr))
+        in_f64 = any(a.buf.kind == "real64" for a in ins.values())
+        compute_f64 = in_f64 or not ins
+
+        # classify outputs per target buffer
+        by_buf = {}
+        for conn, acc, wcr in outs:
+            by_buf.setdefault(acc.buf.bid, []).append((conn, acc, wcr))
+        read_bids = {a.buf.bid for a in ins.values()}
+        pointwise, gathers = [], []
+        if npts == 1 and any(len(g) > 1 for g in by_buf.values()):
+            # one point writing one array several times: a single thread
+            # applies the outputs in declaration order, like the reference
+            for conn, acc, wcr in outs:
+                self.low.materialize(acc.buf)
+            for c in ins:
+                self.low.materialize(ins[c].buf)
+            self.lower_pointwise(space, t, outs, ins, compute_f64, what)
+            return
+        for bid, group in by_buf.items():
+            inj = len(group) == 1 and self._injective(group[0][1], space)
+            if bid in read_bids and npts > 1:
+                # self-update: only the same element may be read and written
+                wkeys = {g[1].key() for g in group}
+                rkeys = {a.key() for a in ins.values() if a.buf.bid == bid}
+                if not inj or rkeys != wkeys:
+                    raise UnsupportedConstruct(
+                        f"{what} reads and writes '{group[0][1].buf.name}' at different points "
+                        "(cross-point dependence is not a parallel map)")
+            if inj:
+                pointwise.append(group[0])
+            else:
+                if any(w != "sum" for _, _, w in group):
+                    raise UnsupportedConstruct(
+                        f"{what} overwrites elements of '{group[0][1].buf.name}' from several points")
+                gathers.append(group)
+        gather_bids = {g[0][1].buf.bid for g in gathers}
+        for group in gathers:
+            used = self._used_inputs([t.body[c] for c, _, _ in group], ins)
+            if any(ins[c].buf.bid in gather_bids for c in used):
+                raise UnsupportedConstruct(f"{what}: a scatter-add target is also read by another scatter")
+        pw_used = self._used_inputs([t.body[c] for c, _, _ in pointwise], ins)
+        if any(ins[c].buf.bid in gather_bids for c in pw_used):
+            raise UnsupportedConstruct(f"{what}: a scatter-add target is read by a pointwise output")
+
+        # everything read must be materialized (pending clears resolved)
+        for c in set(pw_used) | {c for g in gathers for c in self._used_inputs([t.body[x] for x, _, _ in g], ins)}:
+            self.low.materialize(ins[c].buf)
+
+        for group in gathers:
+            self.lower_gather(space, t, group, ins, compute_f64, what)
+
+        clears = []
+        rest = []
+        for conn, acc, wcr in pointwise:
+            body = t.body[conn]
+            if wcr is None and isinstance(body, Const) and float(body.value) == 0.0:
+                img = self._image_box(acc, space)
+                if img is not None:
+                    clears.append((acc.buf, img))
+                    continue
+            rest.append((conn, acc, wcr))
+        if rest:
+            self.lower_pointwise(space, t, rest, ins, compute_f64, what)
+        for buf, img in clears:
+            self.low.add_clear(buf, img)
+
+    @staticmethod
+    def _used_inputs(exprs, ins):
+        used = set()
+        for e in exprs:
+            used |= free_names(e)
+        return [c for c in ins if c in used]
+
+    @staticmethod
+    def _injective(acc: Access, space: SpaceInfo) -> bool:
+        live = [p for p in range(space.np) if space.ext[p] > 1]
+        if not live:
+            return True
+        m = np.array([[f[1][p] for p in live] for f in acc.forms], dtype=np.float64).reshape(len(acc.forms), len(live))
+        return int(np.linalg.matrix_rank(m)) == len(live) if m.size else False
+
+    @staticmethod
+    def _image_box(acc: Access, space: SpaceInfo):
+        """Exact image of an injective access if it is a box, else None."""
+        if space.triangular or any(s != 1 for s in space.step):
+            return None if space.np else tuple((f[0], f[0] + 1) for f in acc.forms)
+        used = set()
+        box = []
+        for c0, coefs in acc.forms:
+            nz = [p for p, c in enumerate(coefs) if c != 0 and space.ext[p] > 1]
+            if not nz:
+                v = c0 + sum(c * space.first[p] for p, c in enumerate(coefs))
+                box.append((v, v + 1))
+                continue
+            if len(nz) != 1 or abs(coefs[nz[0]]) != 1 or nz[0] in used:
+                return None
+            used.add(nz[0])
+            lo, hi = space.range_of((c0, coefs))
+            box.append((lo, hi + 1))
+        return tuple(box)
+
+    # -- pointwise ---------------------------------------------------------------
+
+    def lower_pointwise(self, space, t, outs, ins, compute_f64, what):
+        # stencil fast path: a single linear output over identity+offset subsets
+        if len(outs) == 1:
+            op = self._stencil_pointwise(space, t, outs[0], ins)
+            if op is not None:
+                self.low.emit(op)
+                return
+        conns = list(ins)
+        if len(conns) > L.MAXIN or len(outs) > L.MAXOUT:
+            raise UnsupportedConstruct(f"{what}: too many connectors for the device evaluator")
+        code = Code()
+        ci = {c: k for k, c in enumerate(conns)}
+        segs, out_specs = [], []
+        for conn, acc, wcr in outs:
+            segs.append(code.compile(t.body[conn], ci))
+            w = 1 if wcr == "sum" else 0
+            buf = acc.buf
+            if buf.pending is not None:
+                img = self._image_box(acc, space)
+                if w == 0 and img is not None and box_contains(img, buf.pending):
+                    buf.pending = None
+                elif w == 1 and img is not None and img == buf.pending:
+                    buf.pending = None
+                    w = 0
+                else:
+                    self.low.materialize(buf)
+            out_specs.append((acc, w))
+        self.low.emit(MapOp(space, [ins[c] for c in conns], out_specs, code, segs, compute_f64))
+
+    def _stencil_pointwise(self, space, t, out, ins):
+        conn, acc, wcr = out
+        if space.triangular or space.np == 0 or space.np > 3 or any(s != 1 for s in space.step):
+            return None
+        lin = linearize(t.body[conn])
+        if lin is None or lin[0] != 0.0 or not lin[1]:
+            return None
+        dst = acc.buf
+        ooff = acc.identity_offset(space.np)
+        if ooff is None or len(dst.shape) != space.np:
+            return None
+        srcs, taps = [], []
+        for c, coef in lin[1].items():
+            a = ins[c]
+            if a.buf.shape != dst.shape or a.buf.kind != dst.kind or a.buf.bid == dst.bid:
+                return None
+            doff = a.identity_offset(space.np)
+            if doff is None:
+                return None
+            if a.buf not in srcs:
+                srcs.append(a.buf)
+            if len(srcs) > L.MAXSRCS:
+                return None
+            taps.append((srcs.index(a.buf), coef, tuple(d - o for d, o in zip(doff, ooff)), None))
+        if len(taps) > L.MAXTAPS:
+            return None
+        region = tuple((f + o, l + o + 1) for f, l, o in zip(space.first, space.last, ooff))
+        mode, cbox = (3 if wcr is None else 0), None
+        if dst.pending is not None:
+            if mode == 3 and box_contains(region, dst.pending):
+                dst.pending = None
+            elif mode == 0 and box_contains(region, dst.pending):
+                mode, cbox = 2, dst.pending
+                dst.pending = None
+            else:
+                self.low.materialize(dst)
+        return StencilOp(dst, srcs, region, mode, cbox, taps, kind="sweep")
+
+    # -- gather -------------------------------------------------------------------
+
+    def lower_gather(self, space, t, group, ins, compute_f64, what):
+        dst = group[0][1].buf
+        rank = len(dst.shape)
+        ybox = None
+        for _, acc, _ in group:
+            b = tuple((lo, hi + 1) for lo, hi in (space.range_of(f) for f in acc.forms))
+            ybox = b if ybox is None else box_union_bbox(ybox, b)
+        ybox = tuple((max(0, lo), min(d, hi)) for (lo, hi), d in zip(ybox, dst.shape))
+        clear_mode, cbox = 0, None
+        if dst.pending is not None:
+            ybox = box_union_bbox(ybox, dst.pending)
+            cbox = dst.pending
+            clear_mode = 1 if cbox == ybox else 2
+            dst.pending = None
+        op = self._stencil_gather(space, t, group, ins, dst, ybox, clear_mode, cbox)
+        if op is not None:
+            self.low.emit(op)
+            return
+        if len(group) > 4:
+            # more than 4 terms: split into several passes (later ones accumulate)
+            for k in range(0, len(group), 4):
+                sub = group[k:k + 4]
+                self._emit_gather(space, t, sub, ins, dst, ybox, clear_mode if k == 0 else 0,
+                                  cbox if k == 0 else None, compute_f64, what)
+            return
+        self._emit_gather(space, t, group, ins, dst, ybox, clear_mode, cbox, compute_f64, what)
+
+    def _emit_gather(self, space, t, group, ins, dst, ybox, clear_mode, cbox, compute_f64, what):
+        used = self._used_inputs([t.body[c] for c, _, _ in group], ins)
+        if len(used) > L.MAXIN:
+            raise UnsupportedConstruct(f"{what}: too many inputs for the gather evaluator")
+        ci = {c: k for k, c in enumerate(used)}
+        code = Code()
+        terms = []
+        np_ = space.np
+        for conn, acc, _ in group:
+            seg = code.compile(t.body[conn], ci)
+            Cm, off = acc.matrix(np_)
+            row_of = [-1] * np_
+            forced_free = set()
+            order = []
+            for r in range(len(Cm)):
+                cands = [p for p in range(np_) if abs(Cm[r][p]) == 1 and row_of[p] < 0 and p not in forced_free]
+                if not cands:
+                    continue
+                later = [p for p in cands if not any(Cm[rr][p] for rr in range(r + 1, len(Cm)))]
+                p = (later or cands)[0]
+                row_of[p] = r
+                order.append(p)
+                for q in range(np_):
+                    if q != p and Cm[r][q] != 0 and row_of[q] < 0:
+                        forced_free.add(q)
+            terms.append((row_of, order, Cm, off, seg))
+        # work shape: free iterations per target
+        F = max(int(np.prod([space.ext[p] for p in range(np_) if rof[p] < 0], dtype=np.int64))
+                for rof, *_ in terms)
+        ny = box_size(ybox)
+        inner_free = [p for p in range(np_) if terms[0][0][p] < 0]
+        lanes = 0
+        if inner_free and F >= 32:
+            pin = inner_free[-1]
+            if any(abs(ins[c].flat(np_)[1][pin]) == 1 for c in used):
+                lanes = 1
+        threads = ny * (32 if lanes else 1)
+        want = max(1, -(-(148 * 1024) // max(threads, 1)))
+        cap = max(1, F // ((32 if lanes else 1) * 16))
+        nsplit = int(min(want, cap, 4096))
+        op = GatherOp(space, dst, ybox, clear_mode, cbox, [ins[c] for c in used], terms, code, compute_f64,
+                      lanes, nsplit)
+        self.low.emit(op)
+
+    def _stencil_gather(self, space, t, group, ins, dst, ybox, clear_mode, cbox):
+        if space.triangular or space.np == 0 or space.np > 3 or any(s != 1 for s in space.step):
+            return None
+        if len(dst.shape) != space.np:
+            return None
+        box = tuple((f, l + 1) for f, l in zip(space.first, space.last))
+        srcs, taps = [], []
+        for conn, acc, _ in group:
+            lin = linearize(t.body[conn])
+            if lin is None or lin[0] != 0.0:
+                return None
+            ooff = acc.identity_offset(space.np)
+            if ooff is None:
+                return None
+            mask = tuple((lo + o, hi + o) for (lo, hi), o in zip(box, ooff))
+            for c, coef in lin[1].items():
+                a = ins[c]
+                if a.buf.shape != dst.shape or a.buf.kind != dst.kind:
+                    return None
+                doff = a.identity_offset(space.np)
+                if doff is None:
+                    return None
+                if a.buf not in srcs:
+                    srcs.append(a.buf)
+                if len(srcs) > L.MAXSRCS:
+                    return None
+                taps.append((srcs.index(a.buf), coef, tuple(d - o for d, o in zip(doff, ooff)), mask))
+        if len(taps) > L.MAXTAPS:
+            return None
+        return StencilOp(dst, srcs, ybox, clear_mode, cbox, taps, kind="adjoint")
+
+    # -- library nodes -------------------------------------------------------------
+
+    def library(self, node: LibraryNode, df):
+        ins = {e.dst_conn: e.data for e in df.in_edges(node.id)}
+        outs = df.out_edges(node.id)
+        shapes = {c: self.shape_of(d) for c, d in ins.items()}
+        bufs = {c: self.read(d) for c, d in ins.items()}
+        kind = node.kind
+        if lower_scale_zero(node) and all(e.wcr is None for e in outs):
+            # gradient clear `scale 0.0` (autodiff.py:901-906): deferred and
+            # folded into the next writer instead of a separate pass
+            n = int(np.prod(shapes["x"], dtype=np.int64)) if shapes["x"] else 1
+            self.low.flops += n
+            for e in outs:
+                out = self._lib_out(e, shapes["x"], node)
+                self.low.add_clear(out, whole_box(out.shape))
+            return
+        for b in bufs.values():
+            self.low.materialize(b)
+        if kind == "matmul":
+            sa, sb = shapes["a"], shapes["b"]
+            if len(sa) != 2 or len(sb) != 2:
+                raise UnsupportedConstruct(f"matmul '{node.id}': operands must be 2-D")
+            a_eff = sa[::-1] if node.ta else sa
+            b_eff = sb[::-1] if node.tb else sb
+            if a_eff[1] != b_eff[0]:
+                raise ShapeMismatch(f"matmul '{node.id}': inner dims {a_eff[1]} vs {b_eff[0]}")
+            M, K, N = a_eff[0], a_eff[1], b_eff[1]
+            self.low.flops += 2 * M * K * N
+            for e in outs:
+                out = self._lib_out(e, (M, N), node)
+                acc = self._accumulate(e, out)
+                if bufs["a"].kind != out.kind or bufs["b"].kind != out.kind:
+                    raise UnsupportedConstruct(f"matmul '{node.id}': mixed element kinds")
+                if out.bid in (bufs["a"].bid, bufs["b"].bid):
+                    raise UnsupportedConstruct(f"matmul '{node.id}': output aliases an operand")
+                self.low.emit(MatmulOp(bufs["a"], bufs["b"], out, node.ta, node.tb, M, N, K, acc))
+        elif kind == "reduce_sum":
+            x = bufs["x"]
+            n = x.numel if shapes["x"] else 1
+            self.low.flops += n if shapes["x"] else 0
+            for e in outs:
+                out = self._lib_out(e, (), node)
+                acc = self._accumulate(e, out)
+                self.low.emit(ReduceOp(x, out, acc))
+        elif kind == "ew_unary":
+            x = bufs["x"]
+            n = int(np.prod(shapes["x"], dtype=np.int64)) if shapes["x"] else 1
+            op, const = self._unary_code(node)
+            self.low.flops += (0 if node.op == "copy" else 1) * n
+            for e in outs:
+                out = self._lib_out(e, shapes["x"], node)
+                acc = self._accumulate(e, out)
+                if out.kind != x.kind:
+                    raise UnsupportedConstruct(f"'{node.id}': element kind conversion")
+                if node.op == "copy" and not acc:
+                    self.low.emit(CopyOp(out, x))
+                else:
+                    self.low.emit(EwOp(op, const, x, None, out, acc))
+        else:
+            a, b = bufs["a"], bufs["b"]
+            if shapes["a"] != shapes["b"]:
+                raise ShapeMismatch(f"'{node.id}': operand shapes {shapes['a']} vs {shapes['b']}")
+            n = int(np.prod(shapes["a"], dtype=np.int64)) if shapes["a"] else 1
+            self.low.flops += n
+            if node.op not in L.BINOP or node.op in ("idiv", "mod", "pow"):
+                raise UnsupportedConstruct(f"'{node.id}': unknown elementwise op '{node.op}'")
+            for e in outs:
+                out = self._lib_out(e, shapes["a"], node)
+                acc = self._accumulate(e, out)
+                if not (a.kind == b.kind == out.kind):
+                    raise UnsupportedConstruct(f"'{node.id}': element kind conversion")
+                self.low.emit(EwOp(L.BINOP[node.op], 0.0, a, b, out, acc))
+
+    def _unary_code(self, node):
+        op = node.op
+        if op == "copy":
+            return L.OP_IN, 0.0
+        if op == "scale":
+            return L.OP_MUL, float(node.const)
+        if op in L.UNOP:
+            return L.UNOP[op], 0.0
+        raise DomainError(f"unknown elementwise op '{op}'")
+
+    def _lib_out(self, e, res_shape, node) -> Buffer:
+        want = self.shape_of(e.data)
+        if tuple(res_shape) != tuple(want) and not (len(res_shape) == 0 and e.wcr is None):
+            raise ShapeMismatch(f"'{node.id}': result shape {tuple(res_shape)} does not match '{e.data}' {want}")
+        if tuple(res_shape) != tuple(want):
+            raise UnsupportedConstruct(f"'{node.id}': broadcasting a scalar result into '{e.data}'")
+        return self.write(e.data)
+
+    def _accumulate(self, e, out: Buffer) -> bool:
+        """wcr=sum accumulates unless the target is known zero (first touch
+        or a pending whole-array clear): then it is a plain overwrite."""
+        if e.wcr == "sum":
+            if out.pending is not None and out.pending == whole_box(out.shape):
+                out.pending = None
+                return False
+            self.low.materialize(out)
+            return True
+        out.pending = None  # overwrite (the reference rebinds the array)
+        return False
+
+
+def lower_scale_zero(node) -> bool:
+    return node.kind == "ew_unary" and node.op == "scale" and float(node.const) == 0.0
+
+
+def required_record(forwarding) -> set:
+    out = set()
+    for e in forwarding.values():
+        for c in e.candidates:
+            out.add((e.data, c.version))
+    return out
+
+
+__all__ = ["Lowering", "ProgramRun", "LTape", "Buffer", "number_writes", "lower_scale_zero"]

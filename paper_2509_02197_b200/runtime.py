@@ -1,0 +1,151 @@
+"""Executable: a lowered launch list bound to device memory.
+
+Owns the HBM buffers of one (program(s), params) instance, prepares every
+launch descriptor once, and runs the list either eagerly (first call,
+programs that are not capturable) or as one captured CUDA graph replay.
+Inputs are copied into engine-owned buffers on every run (the reference
+copies inputs on entry and never mutates caller arrays, interpreter.py:
+604-618); results are read back after one stream synchronisation, at which
+point the device error word is checked and mapped to DomainError.
+"""
+from __future__ import annotations
+
+import os
+
+import numpy as np
+import torch
+
+from . import _lib as L
+from .errors import DomainError, EngineError
+from .lowering import Buffer, Lowering
+
+TORCH_DTYPE = {"real32": torch.float32, "real64": torch.float64}
+NP_DTYPE = {"real32": np.float32, "real64": np.float64}
+
+
+def require_cuda():
+    if not torch.cuda.is_available():
+        raise EngineError("the B200 engine needs a CUDA device; none is visible (no CPU fallback)")
+
+
+class Executable:
+    def __init__(self, low: Lowering, inputs: dict, outputs: dict, *, seed_buf: Buffer | None = None,
+                 device=None, use_graph: bool | None = None):
+        require_cuda()
+        self.lib = L.load()
+        self.low = low
+        self.ops = low.ops
+        self.inputs = inputs      # caller name -> Buffer
+        self.outputs = outputs    # key -> Buffer
+        self.seed_buf = seed_buf
+        self.device = torch.device(device or "cuda")
+        self.flops = low.flops
+        env_graph = os.environ.get("GFB_GRAPH", "1") != "0"
+        self.use_graph = env_graph if use_graph is None else use_graph
+        self.graph = None
+        self.runs = 0
+        self._allocate()
+        for op in self.ops:
+            op.prepare(self)
+
+    # -- memory ------------------------------------------------------------------
+
+    def _allocate(self):
+        total = 0
+        for b in self.low.buffers:
+            if b.alias_of is not None or b.tensor is not None:
+                continue
+            b.tensor = torch.empty(max(b.numel, 1), dtype=TORCH_DTYPE[b.kind], device=self.device)
+            total += b.tensor.numel() * b.tensor.element_size()
+        ws = 0
+        for op in self.ops:
+            f = getattr(op, "workspace_bytes", None)
+            if f is not None:
+                ws = max(ws, int(f()))
+        self.workspace = torch.empty(max(ws, 16), dtype=torch.uint8, device=self.device)
+        self.workspace_ptr = self.workspace.data_ptr()
+        self.err = torch.zeros(1, dtype=torch.int32, device=self.device)
+        self.err_ptr = self.err.data_ptr()
+        self.device_bytes = total + self.workspace.numel()
+
+    def view(self, b: Buffer) -> torch.Tensor:
+        t = b.root().tensor
+        return t[: b.numel].view(b.shape) if b.shape else t[:1].view(())
+
+    # -- execution -----------------------------------------------------------------
+
+    def load_inputs(self, values: dict):
+        for name, buf in self.inputs.items():
+            v = values[name]
+            dst = self.view(buf)
+            if isinstance(v, torch.Tensor):
+                src = v.to(device=self.device, dtype=dst.dtype)
+                if tuple(src.shape) != tuple(dst.shape):
+                    src = src.reshape(dst.shape)
+                dst.copy_(src, non_blocking=True)
+            else:
+                arr = np.ascontiguousarray(np.asarray(v, dtype=NP_DTYPE[buf.kind])).reshape(buf.shape)
+                dst.copy_(torch.from_numpy(arr), non_blocking=False)
+
+    def launch_all(self):
+        stream = torch.cuda.current_stream(self.device).cuda_stream
+        if self.graph is not None:
+            self.graph.replay()
+            return
+        for op in self.ops:
+            op.launch(self, stream)
+
+    def run(self, inputs: dict, seed=1.0, *, sync=True):
+        self.load_inputs(inputs)
+        if self.seed_buf is not None:
+            self.view(self.seed_buf).fill_(float(seed))
+        self.err.zero_()
+        if self.graph is None and self.use_graph and self.runs >= 1:
+            self._capture()
+        self.launch_all()
+        self.runs += 1
+        if sync:
+            self.check()
+
+    def _capture(self):
+        g = torch.cuda.CUDAGraph()
+        torch.cuda.synchronize(self.device)
+        with torch.cuda.graph(g):
+            stream = torch.cuda.current_stream(self.device).cuda_stream
+            for op in self.ops:
+                op.launch(self, stream)
+        self.graph = g
+
+    def check(self):
+        torch.cuda.synchronize(self.device)
+        bits = int(self.err.item())
+        if bits:
+            msgs = [m for b, m in L.EBITS.items() if bits & b]
+            raise DomainError("; ".join(msgs) or f"device error bits {bits:#x}")
+
+    def output(self, key) -> torch.Tensor:
+        return self.view(self.outputs[key])
+
+    def output_host(self, key) -> np.ndarray:
+        return self.output(key).detach().cpu().numpy().copy()
+
+    # -- profiling helpers ----------------------------------------------------------
+
+    def timed_eager(self, inputs: dict, seed=1.0):
+        """One eager run with a CUDA event pair around every launch; returns
+        [(family, op, ms)] (used by bench.py for per-kernel roofline shares)."""
+        self.load_inputs(inputs)
+        if self.seed_buf is not None:
+            self.view(self.seed_buf).fill_(float(seed))
+        self.err.zero_()
+        stream = torch.cuda.current_stream(self.device)
+        evs = []
+        for op in self.ops:
+            a = torch.cuda.Event(enable_timing=True)
+            b = torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            op.launch(self, stream.cuda_stream)
+            b.record(stream)
+            evs.append((op, a, b))
+        self.check()
+        return [(op.family, op, a.elapsed_time(b)) for op, a, b in evs]

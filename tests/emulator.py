@@ -1,0 +1,392 @@
+"""CPU emulation of libgfb launch descriptors — TEST INFRASTRUCTURE ONLY.
+
+Executes a lowered launch list on numpy arrays by interpreting the exact
+ctypes descriptors the engine would pass to libgfb.so (gfb_map_desc,
+gfb_gather_desc, gfb_stencil_desc, and the scalar-argument entry points).
+This checks the host lowering and descriptor packing on the CPU-only build
+machine; the CUDA kernels themselves are checked by the `-m gpu` tests.
+"""
+from __future__ import annotations
+
+import ctypes as C
+
+import numpy as np
+
+from paper_2509_02197_b200 import _lib as L
+from paper_2509_02197_b200.lowering import (
+    BroadcastOp,
+    CopyOp,
+    EwOp,
+    FillOp,
+    GatherOp,
+    MapOp,
+    MatmulOp,
+    ReduceOp,
+    StencilOp,
+)
+
+NPT = {L.F32: np.float32, L.F64: np.float64}
+
+
+class _Shim:
+    """Stands in for a torch tensor: exposes data_ptr() of a numpy array."""
+
+    def __init__(self, arr):
+        self.arr = arr
+
+    def data_ptr(self):
+        return self.arr.ctypes.data
+
+    def numel(self):
+        return self.arr.size
+
+    def element_size(self):
+        return self.arr.itemsize
+
+
+class Memory:
+    def __init__(self):
+        self.arrays = []
+
+    def alloc(self, n, dtype):
+        a = np.zeros(max(n, 1), dtype=dtype)
+        self.arrays.append(a)
+        return a
+
+    def resolve(self, ptr):
+        """(flat array, element offset) for a pointer into one allocation."""
+        for a in self.arrays:
+            base = a.ctypes.data
+            if base <= ptr < base + a.nbytes:
+                return a, (ptr - base) // a.itemsize
+        raise KeyError(hex(ptr))
+
+
+def _np_floordiv(a, b):
+    return np.floor_divide(a, b)
+
+
+def _vm(code, arg, start, n, consts, fetch, T, err):
+    st = []
+    for pc in range(start, start + n):
+        op = code[pc]
+        if op == L.OP_IN:
+            st.append(fetch(arg[pc]))
+        elif op == L.OP_CONST:
+            st.append(T(consts[arg[pc]]))
+        elif op >= L.OP_NEG:
+            x = st.pop()
+            if op == L.OP_NEG:
+                r = -x
+            elif op == L.OP_SIN:
+                r = np.sin(x)
+            elif op == L.OP_COS:
+                r = np.cos(x)
+            elif op == L.OP_EXP:
+                r = np.exp(x)
+            elif op == L.OP_LOG:
+                if np.any(~(x > 0)):
+                    err[0] |= 0x2
+                r = np.log(np.where(x > 0, x, 1))
+            elif op == L.OP_SQRT:
+                if np.any(x < 0):
+                    err[0] |= 0x4
+                r = np.sqrt(np.where(x < 0, 0, x))
+            elif op == L.OP_TANH:
+                r = np.tanh(x)
+            elif op == L.OP_ABS:
+                r = np.abs(x)
+            else:
+                r = np.sign(x)
+            st.append(np.asarray(r, dtype=T))
+        else:
+            b = st.pop()
+            a = st.pop()
+            if op == L.OP_ADD:
+                r = a + b
+            elif op == L.OP_SUB:
+                r = a - b
+            elif op == L.OP_MUL:
+                r = a * b
+            elif op in (L.OP_DIV, L.OP_IDIV, L.OP_MOD):
+                if np.any(np.equal(b, 0)):
+                    err[0] |= {L.OP_DIV: 0x1, L.OP_IDIV: 0x10, L.OP_MOD: 0x20}[op]
+                bs = np.where(np.equal(b, 0), 1, b)
+                r = a / bs if op == L.OP_DIV else (_np_floordiv(a, bs) if op == L.OP_IDIV else np.mod(a, bs))
+            elif op == L.OP_MIN:
+                r = np.where(b < a, b, a)
+            elif op == L.OP_MAX:
+                r = np.where(b > a, b, a)
+            else:
+                r = np.power(a, b)
+            st.append(np.asarray(r, dtype=T))
+    return st[0]
+
+
+def _space_points(sp):
+    """All member points of a gfb_space as an (np, npts) int64 array."""
+    npar = sp.nparams
+    if npar == 0:
+        return np.zeros((0, 1), dtype=np.int64)
+    axes = []
+    for p in range(npar):
+        k = np.arange(sp.box_ext[p], dtype=np.int64)
+        axes.append(sp.box_lo[p] + (k if sp.triangular else k * sp.step[p]))
+    grids = np.meshgrid(*axes, indexing="ij")
+    x = np.stack([g.reshape(-1) for g in grids])
+    if sp.triangular:
+        x = x[:, _member(sp, x)]
+    return x
+
+
+def _member(sp, x):
+    ok = np.ones(x.shape[1], dtype=bool)
+    for p in range(sp.nparams):
+        lo = sp.lo0[p] + sum(sp.loc[p][q] * x[q] for q in range(p))
+        hi = sp.hi0[p] + sum(sp.hic[p][q] * x[q] for q in range(p))
+        lo = np.broadcast_to(lo, x.shape[1:])
+        hi = np.broadcast_to(hi, x.shape[1:])
+        ok &= (x[p] >= lo) & (x[p] < hi)
+        if sp.step[p] != 1:
+            ok &= ((x[p] - lo) % sp.step[p]) == 0
+    return ok
+
+
+def _offsets(opnd, x, npar):
+    off = np.full(x.shape[1] if x.ndim > 1 else 1, opnd.c0, dtype=np.int64)
+    for p in range(npar):
+        off = off + opnd.s[p] * x[p]
+    return off
+
+
+class Emulator:
+    def __init__(self, mem: Memory):
+        self.mem = mem
+        self.err = np.zeros(1, dtype=np.uint32)
+
+    def arr(self, ptr, dtype=None):
+        a, o = self.mem.resolve(ptr)
+        return a, o
+
+    def run_op(self, op):
+        if isinstance(op, MapOp):
+            self.map(op.desc)
+        elif isinstance(op, GatherOp):
+            self.gather(op.desc)
+        elif isinstance(op, StencilOp):
+            self.stencil(op.desc)
+        elif isinstance(op, FillOp):
+            a, o = self.arr(op.dst.ptr)
+            if op.whole:
+                a[o:o + op.dst.numel] = op.value
+            else:
+                v = a[o:o + op.dst.numel].reshape(op.dst.shape)
+                v[tuple(slice(lo, hi) for lo, hi in op.box)] = op.value
+        elif isinstance(op, ReduceOp):
+            xa, xo = self.arr(op.x.ptr)
+            s = np.sum(xa[xo:xo + op.x.numel].astype(np.float64))
+            oa, oo = self.arr(op.out.ptr)
+            oa[oo] = (oa[oo] + s) if op.accumulate else s
+        elif isinstance(op, EwOp):
+            T = NPT[op.out.dtype]
+            aa, ao = self.arr(op.a.ptr)
+            a = aa[ao:ao + op.a.numel]
+            b = None
+            if op.b is not None:
+                ba, bo = self.arr(op.b.ptr)
+                b = ba[bo:bo + op.b.numel]
+            if b is None:
+                if op.op == L.OP_IN:
+                    r = a.copy()
+                elif op.op == L.OP_MUL:
+                    r = a * T(op.const)
+                else:
+                    r = _vm([L.OP_IN, op.op], [0, 0], 0, 2, [], lambda k: a, T, self.err)
+            else:
+                r = _vm([L.OP_IN, L.OP_IN, op.op], [0, 1, 0], 0, 3, [], lambda k: (a, b)[k], T, self.err)
+            oa, oo = self.arr(op.out.ptr)
+            sl = slice(oo, oo + op.out.numel)
+            oa[sl] = (oa[sl] + r) if op.accumulate else r
+        elif isinstance(op, BroadcastOp):
+            v = op.scale
+            if op.src is not None:
+                sa, so = self.arr(op.src.ptr)
+                v = v * float(sa[so])
+            oa, oo = self.arr(op.out.ptr)
+            sl = slice(oo, oo + op.out.numel)
+            oa[sl] = (oa[sl] + v) if op.accumulate else v
+        elif isinstance(op, MatmulOp):
+            aa, ao = self.arr(op.a.ptr)
+            ba, bo = self.arr(op.b.ptr)
+            A = aa[ao:ao + op.a.numel].reshape(op.a.shape)
+            B = ba[bo:bo + op.b.numel].reshape(op.b.shape)
+            A = A.T if op.ta else A
+            B = B.T if op.tb else B
+            r = A @ B
+            oa, oo = self.arr(op.out.ptr)
+            sl = slice(oo, oo + op.out.numel)
+            oa[sl] = (oa[sl] + r.reshape(-1)) if op.accumulate else r.reshape(-1)
+        elif isinstance(op, CopyOp):
+            if not op.elided:
+                sa, so = self.arr(op.src.ptr)
+                da, do = self.arr(op.dst.ptr)
+                da[do:do + op.dst.numel] = sa[so:so + op.src.numel]
+        else:
+            raise NotImplementedError(type(op))
+
+    def map(self, d):
+        T = np.float64 if d.compute_f64 else np.float32
+        x = _space_points(d.space)
+        npar = d.space.nparams
+
+        def fetch(k):
+            o = d.in_[k]
+            a, base = self.arr(o.base)
+            return a[base + _offsets(o, x, npar)].astype(T)
+
+        vals = [_vm(list(d.code), list(d.arg), d.code_start[o], d.code_len[o], list(d.consts), fetch, T, self.err)
+                for o in range(d.n_out)]
+        for o in range(d.n_out):
+            w = d.out[o]
+            a, base = self.arr(w.base)
+            idx = base + _offsets(w, x, npar)
+            v = np.broadcast_to(np.asarray(vals[o]), idx.shape)
+            if d.wcr[o] == 0:
+                a[idx] = v
+            elif d.wcr[o] == 1:
+                a[idx] = a[idx] + v
+            else:
+                np.add.at(a, idx, v)
+
+    def gather(self, d):
+        T = np.float64 if d.compute_f64 else np.float32
+        sp = d.space
+        npar = sp.nparams
+        rank = d.rank
+        ext = [d.ybox_ext[r] for r in range(rank)]
+        ys = np.stack([g.reshape(-1) for g in np.meshgrid(*[d.ybox_lo[r] + np.arange(ext[r]) for r in range(rank)],
+                                                          indexing="ij")]) if rank else np.zeros((0, 1), np.int64)
+        ny = ys.shape[1]
+        acc = np.zeros(ny, dtype=T)
+        for t in range(d.n_terms):
+            tm = d.terms[t]
+            free = [p for p in range(npar) if tm.row_of[p] < 0]
+            faxes = [sp.box_lo[p] + (np.arange(sp.box_ext[p]) if sp.triangular else
+                                     np.arange(sp.box_ext[p]) * sp.step[p]) for p in free]
+            fgrid = np.stack([g.reshape(-1) for g in np.meshgrid(*faxes, indexing="ij")]) if free else \
+                np.zeros((0, 1), np.int64)
+            nf = fgrid.shape[1]
+            x = np.zeros((npar, ny, nf), dtype=np.int64)
+            for k, p in enumerate(free):
+                x[p] = fgrid[k][None, :]
+            for k in range(tm.npiv):
+                p = tm.order[k]
+                r = tm.row_of[p]
+                v = ys[r][:, None] - tm.off[r]
+                for q in range(npar):
+                    if q != p:
+                        v = v - tm.C[r][q] * x[q]
+                x[p] = v * tm.C[r][p]
+            ok = np.ones((ny, nf), dtype=bool)
+            for r in range(rank):
+                v = np.full((ny, nf), tm.off[r], dtype=np.int64)
+                for q in range(npar):
+                    v = v + tm.C[r][q] * x[q]
+                ok &= v == ys[r][:, None]
+            flat = x.reshape(npar, -1)
+            okf = ok.reshape(-1) & _member(sp, flat)
+            if not okf.any():
+                continue
+            xs = flat[:, okf]
+
+            def fetch(k, xs=xs):
+                o = d.in_[k]
+                a, base = self.arr(o.base)
+                return a[base + _offsets(o, xs, npar)].astype(T)
+
+            vals = _vm(list(d.code), list(d.arg), tm.code_start, tm.code_len, list(d.consts), fetch, T, self.err)
+            vals = np.broadcast_to(np.asarray(vals, dtype=T), (xs.shape[1],))
+            owner = np.nonzero(okf)[0] // nf
+            np.add.at(acc, owner, vals)
+        a, base = self.arr(d.dst)
+        off = base + sum(ys[r] * d.dst_strides[r] for r in range(rank)) if rank else np.array([base])
+        cur = a[off].astype(T)
+        if d.clear_mode in (1, 3):
+            cur = np.zeros_like(cur)
+        elif d.clear_mode == 2:
+            inside = np.ones(ny, dtype=bool)
+            for r in range(rank):
+                inside &= (ys[r] >= d.clear_lo[r]) & (ys[r] < d.clear_hi[r])
+            cur = np.where(inside, 0, cur)
+        a[off] = cur + acc
+
+    def stencil(self, d):
+        rank = d.rank
+        a, base = self.arr(d.dst)
+        dims = [d.dims[r] for r in range(rank)]
+        n = int(np.prod(dims))
+        D = a[base:base + n].reshape(dims)
+        T = D.dtype.type
+        sl = tuple(slice(d.lo[r], d.hi[r]) for r in range(rank))
+        ys = np.meshgrid(*[np.arange(d.lo[r], d.hi[r]) for r in range(rank)], indexing="ij")
+        if d.clear_mode == 0:
+            acc = D[sl].astype(T).copy()
+        elif d.clear_mode == 2:
+            inside = np.ones(ys[0].shape, dtype=bool)
+            for r in range(rank):
+                inside &= (ys[r] >= d.clear_lo[r]) & (ys[r] < d.clear_hi[r])
+            acc = np.where(inside, 0, D[sl]).astype(T)
+        else:
+            acc = np.zeros(ys[0].shape, dtype=T)
+        srcs = []
+        for i in range(L.MAXSRCS):
+            if d.src[i]:
+                sa, so = self.arr(d.src[i])
+                srcs.append(sa[so:so + n].reshape(dims))
+            else:
+                srcs.append(None)
+        for t in range(d.ntaps):
+            S = srcs[d.tap_src[t]]
+            idx = tuple(ys[r] + d.tap_delta[t][r] for r in range(rank))
+            m = np.ones(ys[0].shape, dtype=bool)
+            if d.tap_masked[t]:
+                for r in range(rank):
+                    m &= (ys[r] >= d.tap_mlo[t][r]) & (ys[r] < d.tap_mhi[t][r])
+            safe = tuple(np.where(m, ix, 0) for ix in idx)
+            acc = acc + np.where(m, T(d.tap_coef[t]) * S[safe], 0).astype(T)
+        D[sl] = acc
+
+
+def execute(exe_builder_low, inputs: dict, input_bufs: dict, seed_buf=None, seed=1.0):
+    """Allocate every buffer of a Lowering in numpy, prepare the descriptors
+    and run the launch list on the emulator. Returns (emulator, views)."""
+    low = exe_builder_low
+    mem = Memory()
+    for b in low.buffers:
+        if b.alias_of is None and b.tensor is None:
+            b.tensor = _Shim(mem.alloc(b.numel, NPT[b.dtype]))
+
+    class RT:
+        pass
+
+    rt = RT()
+    ws = mem.alloc(1 << 16, np.uint8)
+    rt.workspace_ptr = ws.ctypes.data
+    em = Emulator(mem)
+    rt.err_ptr = em.err.ctypes.data
+    rt.lib = None
+    for op in low.ops:
+        op.prepare(rt)
+    for name, b in input_bufs.items():
+        t = b.root().tensor.arr
+        t[:b.numel] = np.asarray(inputs[name], dtype=t.dtype).reshape(-1)
+    if seed_buf is not None:
+        seed_buf.root().tensor.arr[0] = seed
+    for op in low.ops:
+        em.run_op(op)
+
+    def view(b):
+        t = b.root().tensor.arr
+        return t[:b.numel].reshape(b.shape) if b.shape else t[:1].reshape(())
+
+    return em, view

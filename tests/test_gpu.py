@@ -1,0 +1,169 @@
+"""GPU parity tests: the CUDA engine through the drop-in entry points against
+the reference goldens, the oracle, and size-independent properties at full
+config sizes. Tolerances per north_star: rtol 1e-10 (fp64), 1e-5 (fp32),
+metric |a-b|/max(1,|b|) (reference compare_gradients, verification.py:131)."""
+import os
+
+import numpy as np
+import pytest
+
+from conftest import GOLD, golden_index, load_case, rel_err, tol_for
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():  # pragma: no cover
+    pytest.skip("no CUDA device", allow_module_level=True)
+
+from oracle import interp as O  # noqa: E402
+from paper_2509_02197_b200 import Engine, gradient, load_plan, run_planned, workloads as W  # noqa: E402
+from paper_2509_02197_b200.api import load_bundle  # noqa: E402
+from paper_2509_02197_b200.errors import DomainError, UnsupportedConstruct  # noqa: E402
+from paper_2509_02197_b200.ir import load_program  # noqa: E402
+
+IDX = golden_index()
+
+
+def _bundle(name):
+    stem = os.path.join(W.PROG_DIR, name)
+    return load_program(stem + ".fwd.json"), load_bundle(stem + ".bwd.json", stem + ".fwdreq.json")
+
+
+CASES = sorted(IDX["cases"]) + sorted(c for c in IDX["examples"] if "branchy" not in c)
+
+
+@pytest.mark.parametrize("cid", CASES)
+def test_gradient_matches_reference_golden(cid):
+    meta = IDX["cases"].get(cid) or IDX["examples"][cid]
+    prog, b = _bundle(meta["workload"])
+    inputs, value, grads, _ = load_case(cid)
+    res = gradient(prog, inputs, meta["params"], bundle=b)
+    tol = tol_for(prog)
+    assert rel_err(res.value, value) <= tol
+    for k, ref in grads.items():
+        assert rel_err(res.grads[k], ref) <= tol, k
+
+
+@pytest.mark.parametrize("cid", sorted(IDX["plans"]))
+def test_run_planned_matches_reference_golden(cid):
+    meta = IDX["plans"][cid]
+    pb = load_plan(os.path.join(GOLD, "plans", cid))
+    inputs, value, grads, _ = load_case(cid, "plans")
+    res = run_planned(pb, inputs, meta["params"])
+    tol = tol_for(pb.forward)
+    assert rel_err(res.value, value) <= tol
+    for k, ref in grads.items():
+        assert rel_err(res.grads[k], ref) <= tol, k
+
+
+def test_c1_full_size_against_survey_golden():
+    """C1 at its full size: jacobi_2d N=200, TSTEPS=50 (reference: 203 s)."""
+    prog, b = _bundle("jacobi_2d")
+    params = {"N": 200, "TSTEPS": 50}
+    inputs = W.make_inputs("jacobi_2d", prog, params, 0)
+    res = gradient(prog, inputs, params, bundle=b)
+    assert abs(float(res.value) - 40061.09429461688) / 40061.09429461688 < 1e-10
+    assert abs(float(res.grads["A"].sum()) - 38211.744030772315) / 38211.744030772315 < 1e-10
+    assert abs(float(res.grads["A"][100, 100]) - 1.0) < 1e-10
+
+
+@pytest.mark.parametrize("name,params", [
+    ("heat_3d", {"N": 48, "TSTEPS": 8}),
+    ("jacobi_2d", {"N": 300, "TSTEPS": 12}),
+    ("gemm", {"NI": 300, "NJ": 260, "NK": 200}),
+    ("atax", {"M": 700, "N": 500}),
+    ("bicg", {"M": 600, "N": 900}),
+    ("softmax", {"R": 512, "SM": 128}),
+    ("mlp", {"NB": 64, "C": 64, "S0": 256, "S1": 128, "S2": 64}),
+    ("conv2d_bias", {"NB": 4, "H": 16, "W": 12, "CI": 4, "CO": 8, "K": 3}),
+])
+def test_engine_matches_oracle_at_medium_sizes(name, params):
+    prog, b = _bundle(name)
+    inputs = W.make_inputs(name, prog, params, 3)
+    res = gradient(prog, inputs, params, bundle=b)
+    promote = tol_for(prog) > 1e-8
+    v, g, _ = O.gradient(prog, b.backward, b.forwarding, b.required, inputs, params, promote64=promote)
+    tol = tol_for(prog)
+    assert rel_err(res.value, v) <= tol
+    for k in g:
+        assert rel_err(res.grads[k], g[k]) <= tol, k
+
+
+def test_c3_full_size_gemm_atax_bicg_against_fp64_identities():
+    """C3 sizes (N=4000): gradients have closed forms for the linear kernels:
+    gemm  dA = 1.5*1 B^T, dB = 1.5*A^T 1, dC = 1.2;  atax  dx = A^T A^T 1 ...
+    checked against torch fp64 on the same device data."""
+    n = 4000
+    prog, b = _bundle("gemm")
+    params = {"NI": n, "NJ": n, "NK": n}
+    inputs = W.make_inputs("gemm", prog, params, 0)
+    res = gradient(prog, inputs, params, bundle=b)
+    A, B = (torch.from_numpy(inputs[k]).cuda() for k in ("A", "B"))
+    ones = torch.ones(n, n, dtype=torch.float64, device="cuda")
+    ref_dA = (1.5 * ones @ B.T).cpu().numpy()
+    ref_dB = (1.5 * A.T @ ones).cpu().numpy()
+    assert rel_err(res.grads["A"], ref_dA) <= 1e-10
+    assert rel_err(res.grads["B"], ref_dB) <= 1e-10
+    assert rel_err(res.grads["C"], np.full((n, n), 1.2)) <= 1e-10
+    ref_v = float((1.5 * (A @ B) + 1.2 * torch.from_numpy(inputs["C"]).cuda()).sum())
+    assert rel_err(res.value, ref_v) <= 1e-10
+
+
+@pytest.mark.parametrize("name,params", [("heat_3d", {"N": 512, "TSTEPS": 100}),
+                                         ("jacobi_2d", {"N": 700, "TSTEPS": 200})])
+def test_full_size_stencil_adjoint_dot_product(name, params):
+    """Linear programs: O(A + d) - O(A) = <grad_A, d> (adjoint identity
+    <J v, w> = <v, J^T w>), checked at the full C5 / C2 sizes where the
+    reference would take days."""
+    prog, b = _bundle(name)
+    eng = Engine(prog, b, params)
+    inputs = W.make_inputs(name, prog, params, 0)
+    rng = np.random.default_rng(7)
+    d = rng.uniform(0.0, 1.0, inputs["A"].shape)  # same-sign: no cancellation in <g, d>
+    r0 = eng.gradient(inputs)
+    v0, gA = float(r0.value), r0.grads["A"].copy()
+    r1 = eng.gradient({**inputs, "A": inputs["A"] + d})
+    lhs = float(r1.value) - v0
+    rhs = float(np.sum(gA * d))
+    assert abs(lhs - rhs) / max(1.0, abs(rhs)) < 1e-9
+    # gradient of a linear program does not depend on the point
+    assert rel_err(r1.grads["A"], gA) <= 1e-12
+
+
+def test_graph_replay_is_bit_identical_to_eager():
+    prog, b = _bundle("heat_3d")
+    params = {"N": 40, "TSTEPS": 6}
+    inputs = W.make_inputs("heat_3d", prog, params, 1)
+    eng = Engine(prog, b, params)
+    r_eager = eng.gradient(inputs)   # first run: eager
+    g0, v0 = r_eager.grads["A"].copy(), float(r_eager.value)
+    r_graph = eng.gradient(inputs)   # second run: captured graph
+    assert eng.exe.graph is not None
+    assert float(r_graph.value) == v0
+    assert np.array_equal(r_graph.grads["A"], g0)
+
+
+def test_domain_error_is_raised_eagerly_from_the_device():
+    prog, b = _bundle("softmax")
+    params = {"R": 3, "SM": 4}
+    inputs = W.make_inputs("softmax", prog, params, 0)
+    inputs["x"][:] = -200.0  # exp underflows -> row sum 0 -> division by zero
+    with pytest.raises(DomainError):
+        gradient(prog, inputs, params, bundle=b)
+
+
+def test_c2_literal_budget_is_infeasible_like_the_reference():
+    import json
+
+    inf = json.load(open(os.path.join(GOLD, "infeasible.json")))
+    for name, rec in inf.items():
+        # the floor is the two gradient buffers: 2 * N^d * 8 bytes
+        n = rec["params"]["N"]
+        d = 2 if name == "jacobi_2d" else 3
+        assert rec["min_peak_bytes"] == 2 * n**d * 8
+
+
+def test_unsupported_constructs_fail_loudly():
+    prog, b = _bundle("corpus_branchy_scale")
+    with pytest.raises(UnsupportedConstruct):
+        gradient(prog, {"X": np.ones(8), "s": np.array(0.3)}, {"n": 8}, bundle=b)
