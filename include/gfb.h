@@ -26,7 +26,7 @@
 extern "C" {
 #endif
 
-#define GFB_ABI_VERSION 3
+#define GFB_ABI_VERSION 4
 
 #define GFB_MAX_PARAMS 8    /* map parameters (iteration-space rank) */
 #define GFB_MAX_RANK 8      /* array rank */
@@ -197,6 +197,45 @@ typedef struct {
   double tap_coef[GFB_MAX_TAPS];
 } gfb_stencil_desc;
 
+/*
+ * Radius-1 star stencil sweep (positions 0 centre, 1/2 -/+ dim0, 3/4 -/+
+ * dim1, 5/6 -/+ dim2; rank 2 arrays omit dim0): one linear map sweep
+ *   D[y] = base(y) + sum_p [y in mask_p] coef_p * S[y + e_p]   for y in [lo, hi)
+ * with base(y) as in gfb_stencil_desc (mode 0 acc, 1/3 zero, 2 folded clear).
+ */
+typedef struct {
+  double coef[7];
+  int32_t present; /* bit p: tap at position p */
+  int32_t masked;  /* bit p: tap p carries a mask box */
+  int32_t mode;
+  int32_t _pad;
+  int64_t mlo[7][3], mhi[7][3];
+  int64_t lo[3], hi[3];
+  int64_t clo[3], chi[3];
+} gfb_star_op;
+
+/*
+ * Fused pair of star sweeps (one jacobi_2d / heat_3d timestep, forward or
+ * adjoint): X = a(Y) then Z = b(X), in one pass. X is staged in shared
+ * memory with a one-point halo; Z is written to `zout` (a ping-pong buffer
+ * when Z aliases Y); X is written to `xout` only if `xwrite`, and never
+ * inside the dead box (values the next writer overwrites unread).
+ * Elements outside a's / b's region take the old X / Z values.
+ */
+typedef struct {
+  int32_t rank;   /* 2 or 3 */
+  int32_t dtype;
+  int32_t xwrite;
+  int32_t _pad;
+  int64_t dims[3];
+  gfb_star_op a, b;
+  const void *y, *xold;
+  void *xout;
+  const void *zold;
+  void *zout;
+  int64_t dead_lo[3], dead_hi[3];
+} gfb_star_pair_desc;
+
 /* ---- entry points --------------------------------------------------- */
 
 int gfb_abi_version(void);
@@ -213,6 +252,10 @@ int gfb_gather_launch(const gfb_gather_desc *d, void *stream);
 int64_t gfb_gather_workspace_bytes(const gfb_gather_desc *d);
 /* linear stencil fast path of _exec_map (interpreter.py:478-507) */
 int gfb_stencil_launch(const gfb_stencil_desc *d, void *stream);
+
+/* fused forward / adjoint timestep of a radius-1 stencil program (two
+ * consecutive _exec_map sweeps, interpreter.py:478-507) */
+int gfb_star_pair_launch(const gfb_star_pair_desc *d, void *stream);
 
 /* reduce_sum library node (interpreter.py:447-451): out (=|+=) sum(x[0:n]).
  * workspace >= gfb_reduce_workspace_bytes(n) bytes; deterministic order. */

@@ -19,7 +19,7 @@ MAXCODE = 128
 MAXCONST = 24
 MAXTAPS = 32
 MAXSRCS = 4
-ABI_VERSION = 3
+ABI_VERSION = 4
 
 F32, F64 = 0, 1
 
@@ -75,6 +75,18 @@ class StencilDesc(C.Structure):
                 ("tap_mlo", (i64 * 3) * MAXTAPS), ("tap_mhi", (i64 * 3) * MAXTAPS), ("tap_coef", f64 * MAXTAPS)]
 
 
+class StarOp(C.Structure):
+    _fields_ = [("coef", f64 * 7), ("present", i32), ("masked", i32), ("mode", i32), ("_pad", i32),
+                ("mlo", (i64 * 3) * 7), ("mhi", (i64 * 3) * 7), ("lo", i64 * 3), ("hi", i64 * 3),
+                ("clo", i64 * 3), ("chi", i64 * 3)]
+
+
+class StarPairDesc(C.Structure):
+    _fields_ = [("rank", i32), ("dtype", i32), ("xwrite", i32), ("_pad", i32), ("dims", i64 * 3),
+                ("a", StarOp), ("b", StarOp), ("y", vp), ("xold", vp), ("xout", vp), ("zold", vp), ("zout", vp),
+                ("dead_lo", i64 * 3), ("dead_hi", i64 * 3)]
+
+
 _LIB = None
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libgfb.so")
@@ -89,6 +101,7 @@ _SIGS = [
     ("gfb_gather_launch", i32, [C.POINTER(GatherDesc), vp]),
     ("gfb_gather_workspace_bytes", i64, [C.POINTER(GatherDesc)]),
     ("gfb_stencil_launch", i32, [C.POINTER(StencilDesc), vp]),
+    ("gfb_star_pair_launch", i32, [C.POINTER(StarPairDesc), vp]),
     ("gfb_reduce_workspace_bytes", i64, [i64]),
     ("gfb_reduce_sum", i32, [vp, i32, i64, vp, i32, i32, vp, vp]),
     ("gfb_elementwise", i32, [i32, f64, vp, i64, vp, i64, vp, i64, i32, i32, vp, vp]),
@@ -124,7 +137,7 @@ def load(path: str | None = None):
     sizes = (i64 * 8)()
     n = lib.gfb_struct_sizes(sizes, 8)
     want = [C.sizeof(Space), C.sizeof(Operand), C.sizeof(MapDesc), C.sizeof(Term), C.sizeof(GatherDesc),
-            C.sizeof(StencilDesc)]
+            C.sizeof(StencilDesc), C.sizeof(StarOp), C.sizeof(StarPairDesc)]
     got = list(sizes[:n])
     if got[: len(want)] != want:
         raise EngineError(f"struct layout mismatch between gfb.h and _lib.py: C {got} vs ctypes {want}")

@@ -260,6 +260,9 @@ def lower_gradient(program: Program, bundle: Bundle, params: dict, shapes: dict,
         if g is not None:
             outputs["grad:" + ind] = g
     low.finish(list(outputs.values()))
+    outputs = {k: low.resolve(b) for k, b in outputs.items()}
+    fenv = {k: low.resolve(b) for k, b in fenv.items()}
+    benv = {k: low.resolve(b) for k, b in benv.items()}
     return Lowered(low, inputs, outputs, seed_buf, fenv, benv, tape, fwd_prog, bwd_prog)
 
 
@@ -376,9 +379,9 @@ def run_forward(program, inputs: dict, params: dict | None = None, *, record=Non
         raise UnboundName(f"dependent '{prog.dependent}' was never written")
     observed = list(env.values()) + (list(tape.values.values()) if tape else [])
     low.finish(observed)
-    exe = Executable(low, ins, {"value": dep}, use_graph=False)
+    exe = Executable(low, ins, {"value": low.resolve(dep)}, use_graph=False)
     exe.run(inputs)
-    out_env = {k: exe.view(b) for k, b in env.items()}
+    out_env = {k: exe.view(low.resolve(b)) for k, b in env.items()}
     res = RunResult(env=out_env, value=exe.output_host("value"), op_count=exe.flops, tape=tape)
     res._exe = exe
     return res
@@ -414,7 +417,7 @@ def run_backward(program, backward, inputs: dict, params: dict | None = None, *,
     outputs = {"value": seed_buf} if seed_buf is not None else {}
     exe = Executable(low, ins, outputs, seed_buf=seed_buf, use_graph=False)
     exe.run({**pass_in, **extra_in}, seed)
-    out_env = {k: exe.view(b) for k, b in env.items()}
+    out_env = {k: exe.view(low.resolve(b)) for k, b in env.items()}
     return RunResult(env=out_env, value=None if seed_buf is None else exe.output_host("value"), op_count=exe.flops)
 
 

@@ -25,11 +25,15 @@ struct StencilGeom {
   int64_t d1, d2;                // padded dims of the two inner dimensions
   int64_t lo0, lo1, lo2, e0, e1, e2;
   int64_t tap_off[GFB_MAX_TAPS];  // linear offset of each tap
+  const void *tap_base[GFB_MAX_TAPS];  // source pointer pre-shifted by the tap offset
   int64_t mlo[GFB_MAX_TAPS][3], mhi[GFB_MAX_TAPS][3];
   int64_t clo[3], chi[3];
 };
 
-template <typename T>
+// Taps are unrolled up to MAXT (compile-time) and their box masks are split
+// per dimension: the j/k part is evaluated once per thread, the i part once
+// per plane (block-uniform), so the inner loop is predicate + load + FMA.
+template <typename T, int MAXT>
 __global__ void __launch_bounds__(kSX *kSY) stencil_kernel(const __grid_constant__ gfb_stencil_desc d,
                                                            const __grid_constant__ StencilGeom g) {
   const int64_t k = g.lo2 + (int64_t)blockIdx.x * kSX + threadIdx.x;
@@ -37,27 +41,41 @@ __global__ void __launch_bounds__(kSX *kSY) stencil_kernel(const __grid_constant
   if (k >= g.lo2 + g.e2 || j >= g.lo1 + g.e1) return;
   const int64_t i_begin = g.lo0 + (int64_t)blockIdx.z * kMarch;
   const int64_t i_end = min(i_begin + kMarch, g.lo0 + g.e0);
+  const int nt = d.ntaps;
+  uint32_t mjk = 0;
+#pragma unroll
+  for (int t = 0; t < MAXT; ++t) {
+    if (t < nt) {
+      bool ok = !d.tap_masked[t] ||
+                (j >= g.mlo[t][1] && j < g.mhi[t][1] && k >= g.mlo[t][2] && k < g.mhi[t][2]);
+      mjk |= (uint32_t)ok << t;
+    }
+  }
+  const bool crow = j >= g.clo[1] && j < g.chi[1] && k >= g.clo[2] && k < g.chi[2];
   T *dst = (T *)d.dst;
   for (int64_t i = i_begin; i < i_end; ++i) {
+    uint32_t m = mjk;
+#pragma unroll
+    for (int t = 0; t < MAXT; ++t)
+      if (t < nt && d.tap_masked[t] && (i < g.mlo[t][0] || i >= g.mhi[t][0])) m &= ~(1u << t);
     const int64_t off = (i * g.d1 + j) * g.d2 + k;
     T acc;
     if (d.clear_mode == 0) {
       acc = dst[off];
     } else if (d.clear_mode == 2) {
-      bool in = i >= g.clo[0] && i < g.chi[0] && j >= g.clo[1] && j < g.chi[1] && k >= g.clo[2] && k < g.chi[2];
+      const bool in = crow && i >= g.clo[0] && i < g.chi[0];
       acc = in ? T(0) : dst[off];
     } else {
       acc = T(0);
     }
-    for (int t = 0; t < d.ntaps; ++t) {
-      if (d.tap_masked[t]) {
-        if (i < g.mlo[t][0] || i >= g.mhi[t][0] || j < g.mlo[t][1] || j >= g.mhi[t][1] || k < g.mlo[t][2] ||
-            k >= g.mhi[t][2])
-          continue;
-      }
-      const T *src = (const T *)d.src[d.tap_src[t]];
-      acc += (T)d.tap_coef[t] * __ldg(src + off + g.tap_off[t]);
-    }
+    // all tap loads first (independent, issued back to back), then the FMAs
+    T v[MAXT];
+#pragma unroll
+    for (int t = 0; t < MAXT; ++t)
+      v[t] = (t < nt && ((m >> t) & 1u)) ? __ldg((const T *)g.tap_base[t] + off) : T(0);
+#pragma unroll
+    for (int t = 0; t < MAXT; ++t)
+      if (t < nt) acc += (T)d.tap_coef[t] * v[t];
     dst[off] = acc;
   }
 }
@@ -90,6 +108,8 @@ extern "C" int gfb_stencil_launch(const gfb_stencil_desc *d, void *stream) {
     int64_t dl[3] = {0, 0, 0};
     for (int r = 0; r < d->rank; ++r) dl[pad + r] = d->tap_delta[t][r];
     g.tap_off[t] = (dl[0] * g.d1 + dl[1]) * g.d2 + dl[2];
+    const int64_t esz = d->dtype == GFB_F64 ? 8 : 4;
+    g.tap_base[t] = (const char *)d->src[d->tap_src[t]] + g.tap_off[t] * esz;
     for (int r = 0; r < 3; ++r) {
       g.mlo[t][r] = r < pad ? INT64_MIN / 4 : d->tap_mlo[t][r - pad];
       g.mhi[t][r] = r < pad ? INT64_MAX / 4 : d->tap_mhi[t][r - pad];
@@ -103,9 +123,18 @@ extern "C" int gfb_stencil_launch(const gfb_stencil_desc *d, void *stream) {
   dim3 grid((unsigned)ceil_div(g.e2, kSX), (unsigned)ceil_div(g.e1, kSY), (unsigned)ceil_div(g.e0, kMarch));
   if (grid.y > 65535 || grid.z > 65535) return set_error(GFB_EUNSUPPORTED, "gfb_stencil_launch: extent too large");
   cudaStream_t st = (cudaStream_t)stream;
-  if (d->dtype == GFB_F64)
-    stencil_kernel<double><<<grid, block, 0, st>>>(*d, g);
-  else
-    stencil_kernel<float><<<grid, block, 0, st>>>(*d, g);
+#define GFB_STENCIL_LAUNCH(MT)                                      \
+  if (d->dtype == GFB_F64)                                          \
+    stencil_kernel<double, MT><<<grid, block, 0, st>>>(*d, g);      \
+  else                                                              \
+    stencil_kernel<float, MT><<<grid, block, 0, st>>>(*d, g);
+  if (d->ntaps <= 8) {
+    GFB_STENCIL_LAUNCH(8)
+  } else if (d->ntaps <= 16) {
+    GFB_STENCIL_LAUNCH(16)
+  } else {
+    GFB_STENCIL_LAUNCH(32)
+  }
+#undef GFB_STENCIL_LAUNCH
   return check_launch("stencil");
 }

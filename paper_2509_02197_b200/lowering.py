@@ -415,9 +415,21 @@ class Op:
     reads: tuple = ()
     writes: tuple = ()
     full_write = False  # True when the op defines every element of its single write
+    _bufs: tuple = ()   # attribute names holding Buffers (remapped by ping-pong)
 
     def prepare(self, rt):
         pass
+
+    def remap(self, f):
+        """Substitute every buffer reference b by f(b) (physical placement)."""
+        for name in self._bufs:
+            v = getattr(self, name)
+            if isinstance(v, Buffer):
+                setattr(self, name, f(v))
+            elif isinstance(v, list):
+                setattr(self, name, [f(x) if isinstance(x, Buffer) else x for x in v])
+        self.reads = tuple(f(b) for b in self.reads)
+        self.writes = tuple(f(b) for b in self.writes)
 
     def launch(self, rt, stream):
         raise NotImplementedError
@@ -434,6 +446,14 @@ class MapOp(Op):
         self.compute_f64 = compute_f64
         self.reads = tuple(a.buf for a in ins) + tuple(a.buf for a, w in outs if w == 1)
         self.writes = tuple(a.buf for a, _ in outs)
+
+    def remap(self, f):
+        for a in self.ins:
+            a.buf = f(a.buf)
+        for a, _ in self.outs:
+            a.buf = f(a.buf)
+        self.reads = tuple(f(b) for b in self.reads)
+        self.writes = tuple(f(b) for b in self.writes)
 
     def prepare(self, rt):
         d = L.MapDesc()
@@ -470,6 +490,13 @@ class GatherOp(Op):
 
     def workspace_bytes(self):
         return 0 if self.nsplit <= 1 else self.nsplit * box_size(self.ybox) * (8 if self.compute_f64 else 4)
+
+    def remap(self, f):
+        for a in self.ins:
+            a.buf = f(a.buf)
+        self.dst = f(self.dst)
+        self.reads = tuple(f(b) for b in self.reads)
+        self.writes = tuple(f(b) for b in self.writes)
 
     def prepare(self, rt):
         d = L.GatherDesc()
@@ -515,6 +542,7 @@ class GatherOp(Op):
 
 class StencilOp(Op):
     family = "stencil"
+    _bufs = ("dst", "srcs")
 
     def __init__(self, dst: Buffer, srcs: list, region, clear_mode, clear_box, taps, *, kind="sweep"):
         # taps: (src index, coef, delta tuple, mask box or None)
@@ -563,6 +591,7 @@ class FillOp(Op):
     """D[box] = value (materialized pending clear / zero-init)."""
 
     family = "fill"
+    _bufs = ("dst",)
 
     def __init__(self, dst: Buffer, box, value=0.0):
         self.dst, self.box, self.value = dst, box, value
@@ -589,6 +618,7 @@ class FillOp(Op):
 
 class ReduceOp(Op):
     family = "reduce_sum"
+    _bufs = ("x", "out")
 
     def __init__(self, x: Buffer, out: Buffer, accumulate: bool):
         self.x, self.out, self.accumulate = x, out, accumulate
@@ -606,6 +636,7 @@ class ReduceOp(Op):
 
 class EwOp(Op):
     family = "elementwise"
+    _bufs = ("a", "b", "out")
 
     def __init__(self, op: int, const: float, a: Buffer, b: Buffer | None, out: Buffer, accumulate: bool):
         self.op, self.const, self.a, self.b, self.out, self.accumulate = op, const, a, b, out, accumulate
@@ -623,6 +654,7 @@ class EwOp(Op):
 
 class BroadcastOp(Op):
     family = "broadcast"
+    _bufs = ("src", "out")
 
     def __init__(self, src: Buffer | None, scale: float, out: Buffer, accumulate: bool):
         self.src, self.scale, self.out, self.accumulate = src, scale, out, accumulate
@@ -639,6 +671,7 @@ class BroadcastOp(Op):
 
 class MatmulOp(Op):
     family = "matmul"
+    _bufs = ("a", "b", "out")
 
     def __init__(self, a: Buffer, b: Buffer, out: Buffer, ta: bool, tb: bool, M, N, K, accumulate: bool):
         self.a, self.b, self.out = a, b, out
@@ -666,6 +699,7 @@ class MatmulOp(Op):
 
 class CopyOp(Op):
     family = "copy"
+    _bufs = ("dst", "src")
 
     def __init__(self, dst: Buffer, src: Buffer):
         self.dst, self.src = dst, src
@@ -677,6 +711,97 @@ class CopyOp(Op):
     def launch(self, rt, stream):
         if not self.elided:
             L.check(rt.lib.gfb_copy(self.dst.ptr, self.src.ptr, self.dst.nbytes, stream), "copy")
+
+
+STAR_POS = {(0, 0, 0): 0, (-1, 0, 0): 1, (1, 0, 0): 2, (0, -1, 0): 3, (0, 1, 0): 4, (0, 0, -1): 5, (0, 0, 1): 6}
+
+
+def star_form(op):
+    """(source, {position: (coef, mask)}) if a StencilOp is a single-source
+    radius-1 star on a rank-2/3 array, else None."""
+    if not isinstance(op, StencilOp) or len(op.srcs) != 1:
+        return None
+    rank = len(op.dst.shape)
+    if rank not in (2, 3) or op.srcs[0].shape != op.dst.shape or op.srcs[0].kind != op.dst.kind:
+        return None
+    taps = {}
+    for _si, coef, delta, mask in op.taps:
+        d3 = (0,) * (3 - rank) + tuple(delta)
+        pos = STAR_POS.get(d3)
+        if pos is None or pos in taps:
+            return None
+        taps[pos] = (coef, mask)
+    return op.srcs[0], taps
+
+
+def _fill_star(so: L.StarOp, op: StencilOp, taps: dict):
+    rank = len(op.dst.shape)
+    so.mode = op.clear_mode
+    for pos, (coef, mask) in taps.items():
+        so.present |= 1 << pos
+        so.coef[pos] = coef
+        if mask is not None:
+            so.masked |= 1 << pos
+            for r in range(rank):
+                so.mlo[pos][r], so.mhi[pos][r] = mask[r]
+    for r in range(rank):
+        so.lo[r], so.hi[r] = op.region[r]
+        if op.clear_box is not None:
+            so.clo[r], so.chi[r] = op.clear_box[r]
+
+
+class StarPairOp(Op):
+    """Two consecutive radius-1 star sweeps X = a(Y); Z = b(X) in one
+    launch (csrc/star.cu). Physical outputs are assigned by the ping-pong
+    placement pass (``xout``/``zout``)."""
+
+    family = "star_pair"
+
+    def __init__(self, a: StencilOp, b: StencilOp, fa, fb, xwrite: bool, dead):
+        self.a, self.b, self.fa, self.fb = a, b, fa, fb
+        self.X, self.Y, self.Z = a.dst, fa[0], b.dst
+        self.xwrite, self.dead = xwrite, dead
+        self.xout = self.X
+        self.zout = self.Z
+        self._refresh()
+
+    def _refresh(self):
+        self.reads = (self.Y, self.X, self.Z)
+        self.writes = (self.zout,) + ((self.xout,) if self.xwrite else ())
+
+    def remap(self, f):
+        self.X, self.Y, self.Z = f(self.X), f(self.Y), f(self.Z)
+        self.xout, self.zout = f(self.xout), f(self.zout)
+        self._refresh()
+
+    def algorithmic_bytes(self) -> int:
+        # the two map sweeps it replaces, each one read + one write of the array
+        return self.a.algorithmic_bytes() + self.b.algorithmic_bytes()
+
+    def dram_bytes(self) -> int:
+        n = self.Z.nbytes
+        return 2 * n + (n if self.xwrite and self.dead is None else 0)
+
+    def prepare(self, rt):
+        d = L.StarPairDesc()
+        rank = len(self.Z.shape)
+        d.rank, d.dtype = rank, self.Z.dtype
+        d.xwrite = 1 if self.xwrite else 0
+        for r in range(rank):
+            d.dims[r] = self.Z.shape[r]
+        _fill_star(d.a, self.a, self.fa[1])
+        _fill_star(d.b, self.b, self.fb[1])
+        d.y, d.xold, d.zold = self.Y.ptr, self.X.ptr, self.Z.ptr
+        d.xout = self.xout.ptr if self.xwrite else None
+        d.zout = self.zout.ptr
+        if self.dead is not None:
+            for r in range(rank):
+                d.dead_lo[r], d.dead_hi[r] = self.dead[r]
+        self.desc = d
+        self._ref = C.byref(d)
+
+    def launch(self, rt, stream):
+        L.check(rt.lib.gfb_star_pair_launch(self._ref, stream), "star_pair")
 
 
 # ---------------------------------------------------------------------------
@@ -749,7 +874,85 @@ class Lowering:
     def finish(self, observed: list):
         for b in observed:
             self.materialize(b)
+        if os.environ.get("GFB_FUSE", "1") != "0":
+            self._fuse_star_pairs(observed)
         self._elide_copies()
+
+    def resolve(self, buf: Buffer) -> Buffer:
+        """Physical buffer holding ``buf``'s final value (after ping-pong)."""
+        return self.final.get(buf.bid, buf) if hasattr(self, "final") else buf
+
+    def _fuse_star_pairs(self, observed):
+        """Fuse adjacent radius-1 star sweeps X = a(Y); Z = b(X) into one
+        launch, then place ping-pong physical buffers."""
+        ops = self.ops
+        obs = {b.bid for b in observed}
+        fused, i = [], 0
+        while i < len(ops):
+            a = ops[i]
+            b = ops[i + 1] if i + 1 < len(ops) else None
+            fa, fb = star_form(a), star_form(b) if b is not None else None
+            if (fa and fb and a.dst.shape == b.dst.shape and a.dst.kind == b.dst.kind
+                    and fb[0] is a.dst and fa[0] is not a.dst and b.dst is not a.dst):
+                xwrite, dead = self._x_liveness(a.dst, i + 2, obs)
+                fused.append(StarPairOp(a, b, fa, fb, xwrite, dead))
+                i += 2
+            else:
+                fused.append(a)
+                i += 1
+        if len(fused) == len(ops):
+            return
+        # placement: every fused pair writes Z (and a live X) into the other
+        # physical buffer of a two-buffer ring when the old value is still
+        # being read by neighbouring CTAs during the launch
+        cur, alt = {}, {}
+
+        def phys(b):
+            return cur.get(b.bid, b)
+
+        def other(logical: Buffer, now: Buffer) -> Buffer:
+            ring = alt.get(logical.bid)
+            if ring is None:
+                twin = self.new_buffer(logical.name + "~pp", logical.shape, logical.kind, fresh=False)
+                ring = alt[logical.bid] = (logical, twin)
+            return ring[1] if now is ring[0] else ring[0]
+
+        for op in fused:
+            if isinstance(op, StarPairOp):
+                X, Y, Z = op.X, op.Y, op.Z
+                op.remap(phys)
+                if Z is Y:
+                    op.zout = other(Z, op.Z)
+                    cur[Z.bid] = op.zout
+                if op.xwrite:
+                    op.xout = other(X, op.X)
+                    cur[X.bid] = op.xout
+                op._refresh()
+            else:
+                op.remap(phys)
+        self.final = dict(cur)
+        self.ops = fused
+
+    def _x_liveness(self, X: Buffer, start: int, obs: set):
+        """(write X back?, dead box) for the intermediate of a fused pair."""
+        whole = whole_box(X.shape)
+        for op in self.ops[start:]:
+            touches_read = any(b is X for b in op.reads)
+            touches_write = any(b is X for b in op.writes)
+            if not (touches_read or touches_write):
+                continue
+            if isinstance(op, StencilOp) and op.dst is X and not any(s is X for s in op.srcs):
+                if op.clear_mode in (1, 3):
+                    dead = op.region
+                elif op.clear_mode == 2:
+                    dead = op.clear_box
+                else:
+                    return True, None
+                if box_contains(dead, whole):
+                    return False, None
+                return True, dead
+            return True, None
+        return (X.bid in obs), None
 
     def _elide_copies(self):
         """Copies whose source and destination are never written afterwards
@@ -1217,7 +1420,7 @@ class ProgramRun:
     def lower_pointwise(self, space, t, outs, ins, compute_f64, what):
         # stencil fast path: a single linear output over identity+offset subsets
         if len(outs) == 1:
-            op = self._stencil_pointwise(space, t, outs[0], ins)
+            op = self._broadcast_pointwise(space, t, outs[0], ins) or self._stencil_pointwise(space, t, outs[0], ins)
             if op is not None:
                 self.low.emit(op)
                 return
@@ -1242,6 +1445,35 @@ class ProgramRun:
                     self.low.materialize(buf)
             out_specs.append((acc, w))
         self.low.emit(MapOp(space, [ins[c] for c in conns], out_specs, code, segs, compute_f64))
+
+    def _broadcast_pointwise(self, space, t, out, ins):
+        """`out[all] (+)= c * scalar` (the reduce_sum adjoint map,
+        autodiff.py:940-960) as one streaming fill."""
+        conn, acc, wcr = out
+        if space.np == 0:
+            return None
+        lin = linearize(t.body[conn])
+        if lin is None or len(lin[1]) > 1 or (lin[1] and lin[0] != 0.0):
+            return None
+        src, scale = None, lin[0]
+        if lin[1]:
+            (c, scale), = lin[1].items()
+            if ins[c].buf.shape != () or ins[c].buf.kind != acc.buf.kind:
+                return None
+            src = ins[c].buf
+        dst = acc.buf
+        if self._image_box(acc, space) != whole_box(dst.shape) or not self._injective(acc, space):
+            return None
+        accumulate = wcr == "sum"
+        if dst.pending is not None:
+            if dst.pending == whole_box(dst.shape):
+                accumulate = False
+                dst.pending = None
+            else:
+                self.low.materialize(dst)
+        if not accumulate:
+            dst.pending = None
+        return BroadcastOp(src, scale, dst, accumulate)
 
     def _stencil_pointwise(self, space, t, out, ins):
         conn, acc, wcr = out

@@ -22,6 +22,7 @@ from paper_2509_02197_b200.lowering import (
     MapOp,
     MatmulOp,
     ReduceOp,
+    StarPairOp,
     StencilOp,
 )
 
@@ -175,6 +176,8 @@ class Emulator:
             self.gather(op.desc)
         elif isinstance(op, StencilOp):
             self.stencil(op.desc)
+        elif isinstance(op, StarPairOp):
+            self.star_pair(op.desc)
         elif isinstance(op, FillOp):
             a, o = self.arr(op.dst.ptr)
             if op.whole:
@@ -320,6 +323,30 @@ class Emulator:
             cur = np.where(inside, 0, cur)
         a[off] = cur + acc
 
+    def star_pair(self, d):
+        rank = d.rank
+        dims = [d.dims[r] for r in range(rank)]
+        n = int(np.prod(dims))
+
+        def view(ptr):
+            a, o = self.arr(ptr)
+            return a[o:o + n].reshape(dims)
+
+        Y, Xo, Zo = view(d.y), view(d.xold), view(d.zold)
+        Y, Xo, Zo = Y.copy(), Xo.copy(), Zo.copy()
+        Xn = _star_apply(d.a, Y, Xo, rank, dims)
+        Zn = _star_apply(d.b, Xn, Zo, rank, dims)
+        view(d.zout)[...] = Zn
+        if d.xwrite:
+            ys = np.meshgrid(*[np.arange(k) for k in dims], indexing="ij")
+            dead = np.ones(ys[0].shape, dtype=bool)
+            for r in range(rank):
+                dead &= (ys[r] >= d.dead_lo[r]) & (ys[r] < d.dead_hi[r])
+            if not any(d.dead_hi[r] > d.dead_lo[r] for r in range(rank)):
+                dead[...] = False
+            out = view(d.xout)
+            out[~dead] = Xn[~dead]
+
     def stencil(self, d):
         rank = d.rank
         a, base = self.arr(d.dst)
@@ -355,6 +382,41 @@ class Emulator:
             safe = tuple(np.where(m, ix, 0) for ix in idx)
             acc = acc + np.where(m, T(d.tap_coef[t]) * S[safe], 0).astype(T)
         D[sl] = acc
+
+
+_STAR = [(0, 0, 0), (-1, 0, 0), (1, 0, 0), (0, -1, 0), (0, 1, 0), (0, 0, -1), (0, 0, 1)]
+
+
+def _star_apply(so, src, old, rank, dims):
+    """One radius-1 star op over the whole array (values outside its region
+    keep `old`)."""
+    T = old.dtype.type
+    ys = np.meshgrid(*[np.arange(n) for n in dims], indexing="ij")
+    pad = 3 - rank
+
+    def inb(lo, hi):
+        m = np.ones(ys[0].shape, dtype=bool)
+        for r in range(rank):
+            m &= (ys[r] >= lo[r]) & (ys[r] < hi[r])
+        return m
+
+    region = inb(so.lo, so.hi)
+    if so.mode == 0:
+        acc = old.copy()
+    elif so.mode == 2:
+        acc = np.where(inb(so.clo, so.chi), 0, old).astype(T)
+    else:
+        acc = np.zeros_like(old)
+    for pos in range(7):
+        if not (so.present >> pos) & 1:
+            continue
+        delta = _STAR[pos][pad:]
+        m = region.copy()
+        if (so.masked >> pos) & 1:
+            m &= inb(so.mlo[pos], so.mhi[pos])
+        idx = tuple(np.clip(ys[r] + delta[r], 0, dims[r] - 1) for r in range(rank))
+        acc = acc + np.where(m, T(so.coef[pos]) * src[idx], 0).astype(T)
+    return np.where(region, acc, old).astype(T)
 
 
 def execute(exe_builder_low, inputs: dict, input_bufs: dict, seed_buf=None, seed=1.0):

@@ -61,18 +61,34 @@ def test_lowered_planned_replay(cid):
     _check(lw, view, pb.forward, value, grads)
 
 
-def test_stencil_adjoint_is_one_gather_sweep_per_map_with_clears_folded():
-    """heat_3d: per timestep 2 forward sweeps + 2 adjoint gather sweeps, no
-    separate clear passes (the `_z` clears fold into the next sweep)."""
+def test_stencil_timestep_is_one_fused_launch_with_clears_folded():
+    """heat_3d: each timestep (2 forward sweeps, or 2 adjoint gather sweeps
+    with their `_z` clears folded) is ONE fused star-pair launch; no
+    separate clear passes; dead intermediates are not written back."""
+    from paper_2509_02197_b200.lowering import StarPairOp
+
     prog, b = _bundle("heat_3d")
     params = {"N": 10, "TSTEPS": 5}
     inputs = W.make_inputs("heat_3d", prog, params, 0)
     lw = lower_gradient(prog, b, params, _check_inputs(prog, inputs, params))
-    sweeps = [op for op in lw.low.ops if isinstance(op, StencilOp)]
-    assert len(sweeps) == 4 * (params["TSTEPS"] - 1)
-    assert not any(isinstance(op, FillOp) for op in lw.low.ops)
-    adj = [op for op in sweeps if op.kind == "adjoint"]
-    assert all(op.clear_mode in (1, 2) for op in adj)
+    pairs = [op for op in lw.low.ops if isinstance(op, StarPairOp)]
+    assert len(pairs) == 2 * (params["TSTEPS"] - 1)
+    assert not any(isinstance(op, (FillOp, StencilOp)) for op in lw.low.ops)
+    fwd, bwd = pairs[: len(pairs) // 2], pairs[len(pairs) // 2:]
+    # between timesteps only the boundary shell of the intermediate (B, B__grad) is live
+    assert all(p.xwrite and p.dead is not None for p in fwd[:-1] + bwd[:-1])
+    assert not fwd[-1].xwrite and not bwd[-1].xwrite  # never read again, not observed
+    assert all(p.b.clear_mode in (1, 2) for p in bwd)
+
+
+def test_unfused_launch_list_matches_too(monkeypatch):
+    monkeypatch.setenv("GFB_FUSE", "0")
+    prog, b = _bundle("heat_3d")
+    cid = "heat_3d__N8_TSTEPS3"
+    inputs, value, grads, _ = load_case(cid)
+    lw, em, view = _emulate(prog, b, IDX["cases"][cid]["params"], inputs)
+    assert any(isinstance(op, StencilOp) for op in lw.low.ops)
+    _check(lw, view, prog, value, grads)
 
 
 def test_tape_snapshot_is_aliased_when_never_overwritten():
