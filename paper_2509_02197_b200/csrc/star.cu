@@ -18,7 +18,7 @@
 
 namespace gfb {
 
-constexpr int kPX = 32, kPY = 8, kPM = 16;  // tile (k, j) and planes per CTA
+constexpr int kPX = 32, kPY = 16, kPM = 16;  // tile (k, j), planes per CTA; 512 threads
 
 struct StarOpDev {
   double coef[7];
@@ -34,7 +34,7 @@ struct StarOpDev {
 struct StarPairDev {
   int32_t d0, d1, d2;
   int32_t xwrite;  // write X back (outside the dead box)
-  int64_t ps, rs;  // plane / row strides
+  int32_t ps, rs;  // plane / row strides (arrays < 2^31 elements)
   StarOpDev a, b;
   const void *y;      // source of a
   const void *xold;   // old X (base of a, value outside a's region)
@@ -44,66 +44,81 @@ struct StarPairDev {
   int32_t dlo[3], dhi[3];  // dead box of X (not written back)
 };
 
-__device__ __forceinline__ bool in_box(const int32_t *lo, const int32_t *hi, int i, int j, int k) {
-  return i >= lo[0] && i < hi[0] && j >= lo[1] && j < hi[1] && k >= lo[2] && k < hi[2];
-}
+// Per-coordinate predicate bits. For a point (i, j, k) the predicate word is
+// M0[i] & M1[j] & M2[k]: bits 0..6 = tap p's mask box admits the point,
+// bit 7 = inside the op's region, bit 8 = inside its clear box, bit 9 = in
+// the dead box (op a only), bit 10 = inside the array.
+enum : uint32_t { kRegion = 1u << 7, kClear = 1u << 8, kDead = 1u << 9, kArray = 1u << 10 };
 
-template <typename T>
-__device__ __forceinline__ T star_base(const StarOpDev &o, const T *__restrict__ old, int64_t off, int i, int j,
-                                       int k) {
-  if (o.mode == 0) return old[off];
-  if (o.mode == 2) return in_box(o.clo, o.chi, i, j, k) ? T(0) : old[off];
-  return T(0);
-}
-
-// op a at one point from global memory (tap sources read through L1)
-template <typename T>
-__device__ __forceinline__ T star_eval_global(const StarOpDev &o, const T *__restrict__ src,
-                                              const T *__restrict__ old, int64_t off, int64_t ps, int64_t rs, int i,
-                                              int j, int k) {
-  T acc = star_base<T>(o, old, off, i, j, k);
-  const int64_t doff[7] = {0, -ps, ps, -rs, rs, -1, 1};
-  T v[7];
+__device__ __forceinline__ uint32_t coord_bits(const StarOpDev &o, int dim, int c, int extent, const int32_t *dlo,
+                                               const int32_t *dhi) {
+  uint32_t b = 0;
 #pragma unroll
   for (int p = 0; p < 7; ++p) {
-    bool on = (o.present >> p) & 1;
-    if (on && ((o.masked >> p) & 1)) on = in_box(o.mlo[p], o.mhi[p], i, j, k);
-    v[p] = on ? __ldg(src + off + doff[p]) : T(0);
+    bool ok = !((o.masked >> p) & 1) || (c >= o.mlo[p][dim] && c < o.mhi[p][dim]);
+    b |= (uint32_t)ok << p;
   }
-#pragma unroll
-  for (int p = 0; p < 7; ++p)
-    if ((o.present >> p) & 1) acc += (T)o.coef[p] * v[p];
-  return acc;
+  if (c >= o.lo[dim] && c < o.hi[dim]) b |= kRegion;
+  if (c >= o.clo[dim] && c < o.chi[dim]) b |= kClear;
+  if (dlo && c >= dlo[dim] && c < dhi[dim]) b |= kDead;
+  if (c >= 0 && c < extent) b |= kArray;
+  return b;
 }
 
 template <typename T>
 __global__ void __launch_bounds__(kPX *kPY) star_pair_kernel(const __grid_constant__ StarPairDev d) {
   __shared__ T xs[3][kPY + 2][kPX + 2];
+  __shared__ uint32_t aj[kPY + 2], ak[kPX + 2], bj[kPY], bk[kPX];
   const int tx = threadIdx.x, ty = threadIdx.y, tid = ty * kPX + tx;
   const int k0 = blockIdx.x * kPX, j0 = blockIdx.y * kPY;
   const int i0 = blockIdx.z * kPM, i1 = min(i0 + kPM, d.d0);
+  if (tid < kPY + 2) aj[tid] = coord_bits(d.a, 1, j0 - 1 + tid, d.d1, d.dlo, d.dhi);
+  if (tid >= 32 && tid < 32 + kPX + 2) ak[tid - 32] = coord_bits(d.a, 2, k0 - 1 + (tid - 32), d.d2, d.dlo, d.dhi);
+  if (tid >= 96 && tid < 96 + kPY) bj[tid - 96] = coord_bits(d.b, 1, j0 + (tid - 96), d.d1, nullptr, nullptr);
+  if (tid >= 128 && tid < 128 + kPX) bk[tid - 128] = coord_bits(d.b, 2, k0 + (tid - 128), d.d2, nullptr, nullptr);
+  __syncthreads();
   const T *__restrict__ Y = (const T *)d.y;
   const T *__restrict__ Xo = (const T *)d.xold;
   const T *__restrict__ Zo = (const T *)d.zold;
   T *Xn = (T *)d.xout;
   T *Zn = (T *)d.zout;
+  const int ps = d.ps, rs = d.rs;
+  T ca[7], cb[7];
+#pragma unroll
+  for (int p = 0; p < 7; ++p) {
+    ca[p] = (T)d.a.coef[p];
+    cb[p] = (T)d.b.coef[p];
+  }
+  const uint32_t apres = d.a.present, bpres = d.b.present;
   constexpr int HW = (kPY + 2) * (kPX + 2);
   for (int q = i0 - 1; q <= i1; ++q) {
     const int slot = (q + 3) % 3;
     if (q >= 0 && q < d.d0) {
+      const uint32_t mi = coord_bits(d.a, 0, q, d.d0, d.dlo, d.dhi);
+      const bool own = q >= i0 && q < i1;
       for (int p = tid; p < HW; p += kPX * kPY) {
         const int hj = p / (kPX + 2), hk = p - hj * (kPX + 2);
-        const int j = j0 - 1 + hj, k = k0 - 1 + hk;
+        const uint32_t m = mi & aj[hj] & ak[hk];
         T v = T(0);
-        if (j >= 0 && j < d.d1 && k >= 0 && k < d.d2) {
-          const int64_t off = (int64_t)q * d.ps + (int64_t)j * d.rs + k;
-          if (in_box(d.a.lo, d.a.hi, q, j, k))
-            v = star_eval_global<T>(d.a, Y, Xo, off, d.ps, d.rs, q, j, k);
-          else
+        if (m & kArray) {
+          const int off = q * ps + (j0 - 1 + hj) * rs + (k0 - 1 + hk);
+          if (m & kRegion) {
+            T acc;
+            if (d.a.mode == 0 || (d.a.mode == 2 && !(m & kClear)))
+              acc = Xo[off];
+            else
+              acc = T(0);
+            const int doff[7] = {0, -ps, ps, -rs, rs, -1, 1};
+            T t[7];
+#pragma unroll
+            for (int e = 0; e < 7; ++e) t[e] = (((apres & m) >> e) & 1) ? __ldg(Y + off + doff[e]) : T(0);
+#pragma unroll
+            for (int e = 0; e < 7; ++e) acc += ca[e] * t[e];
+            v = acc;
+          } else {
             v = Xo[off];
-          if (d.xwrite && q >= i0 && q < i1 && hj >= 1 && hj <= kPY && hk >= 1 && hk <= kPX &&
-              !in_box(d.dlo, d.dhi, q, j, k))
-            Xn[off] = v;
+          }
+          if (d.xwrite && own && hj >= 1 && hj <= kPY && hk >= 1 && hk <= kPX && !(m & kDead)) Xn[off] = v;
         }
         xs[slot][hj][hk] = v;
       }
@@ -111,27 +126,28 @@ __global__ void __launch_bounds__(kPX *kPY) star_pair_kernel(const __grid_consta
     __syncthreads();
     const int i = q - 1;
     if (i >= i0 && i < i1) {
-      const int j = j0 + ty, k = k0 + tx;
-      if (j < d.d1 && k < d.d2) {
-        const int64_t off = (int64_t)i * d.ps + (int64_t)j * d.rs + k;
+      const uint32_t m = coord_bits(d.b, 0, i, d.d0, nullptr, nullptr) & bj[ty] & bk[tx];
+      if (m & kArray) {
+        const int off = i * ps + (j0 + ty) * rs + (k0 + tx);
         T w;
-        if (in_box(d.b.lo, d.b.hi, i, j, k)) {
-          w = star_base<T>(d.b, Zo, off, i, j, k);
+        if (m & kRegion) {
+          if (d.b.mode == 0 || (d.b.mode == 2 && !(m & kClear)))
+            w = Zo[off];
+          else
+            w = T(0);
           const int sc = (i + 3) % 3, sm = (i + 2) % 3, sp = (i + 4) % 3;
-          T v[7];
-          v[0] = xs[sc][ty + 1][tx + 1];
-          v[1] = xs[sm][ty + 1][tx + 1];
-          v[2] = xs[sp][ty + 1][tx + 1];
-          v[3] = xs[sc][ty][tx + 1];
-          v[4] = xs[sc][ty + 2][tx + 1];
-          v[5] = xs[sc][ty + 1][tx];
-          v[6] = xs[sc][ty + 1][tx + 2];
+          T t[7];
+          t[0] = xs[sc][ty + 1][tx + 1];
+          t[1] = xs[sm][ty + 1][tx + 1];
+          t[2] = xs[sp][ty + 1][tx + 1];
+          t[3] = xs[sc][ty][tx + 1];
+          t[4] = xs[sc][ty + 2][tx + 1];
+          t[5] = xs[sc][ty + 1][tx];
+          t[6] = xs[sc][ty + 1][tx + 2];
+          const uint32_t on = bpres & m;
 #pragma unroll
-          for (int p = 0; p < 7; ++p) {
-            bool on = (d.b.present >> p) & 1;
-            if (on && ((d.b.masked >> p) & 1)) on = in_box(d.b.mlo[p], d.b.mhi[p], i, j, k);
-            if (on) w += (T)d.b.coef[p] * v[p];
-          }
+          for (int e = 0; e < 7; ++e)
+            if ((on >> e) & 1) w += cb[e] * t[e];
         } else {
           w = Zo[off];
         }
@@ -180,8 +196,8 @@ extern "C" int gfb_star_pair_launch(const gfb_star_pair_desc *s, void *stream) {
   d.d0 = (int32_t)dims[0];
   d.d1 = (int32_t)dims[1];
   d.d2 = (int32_t)dims[2];
-  d.ps = dims[1] * dims[2];
-  d.rs = dims[2];
+  d.ps = (int32_t)(dims[1] * dims[2]);
+  d.rs = (int32_t)dims[2];
   d.xwrite = s->xwrite;
   fill_star_op(d.a, s->a, pad);
   fill_star_op(d.b, s->b, pad);
