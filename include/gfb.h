@@ -26,7 +26,7 @@
 extern "C" {
 #endif
 
-#define GFB_ABI_VERSION 4
+#define GFB_ABI_VERSION 5
 
 #define GFB_MAX_PARAMS 8    /* map parameters (iteration-space rank) */
 #define GFB_MAX_RANK 8      /* array rank */
@@ -234,6 +234,11 @@ typedef struct {
   const void *zold;
   void *zout;
   int64_t dead_lo[3], dead_hi[3];
+  /* slab decomposition along the outermost dimension (rank 3 only): the
+   * arrays hold global planes [plane0, plane0 + dims[0]); Z (and X) are
+   * produced for local planes [zlo, zhi). Single device: 0, 0, dims[0]. */
+  int64_t plane0, zlo, zhi;
+  int64_t global_d0;
 } gfb_star_pair_desc;
 
 /* ---- entry points --------------------------------------------------- */

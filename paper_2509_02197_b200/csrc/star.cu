@@ -32,7 +32,9 @@ struct StarOpDev {
 };
 
 struct StarPairDev {
-  int32_t d0, d1, d2;
+  int32_t d0, d1, d2;   // local extents
+  int32_t p0, gd0;      // global index of local plane 0, global extent of dim 0
+  int32_t zlo, zhi;     // local planes to produce
   int32_t xwrite;  // write X back (outside the dead box)
   int32_t ps, rs;  // plane / row strides (arrays < 2^31 elements)
   StarOpDev a, b;
@@ -66,16 +68,59 @@ __device__ __forceinline__ uint32_t coord_bits(const StarOpDev &o, int dim, int 
 }
 
 template <typename T>
+__device__ __forceinline__ T star_x_point(const StarPairDev &d, const T *__restrict__ Y, const T *__restrict__ Xo,
+                                          const T (&ca)[7], uint32_t apres, uint32_t m, int off, int ps, int rs) {
+  if (!(m & kRegion)) return Xo[off];
+  T acc = (d.a.mode == 0 || (d.a.mode == 2 && !(m & kClear))) ? Xo[off] : T(0);
+  const int doff[7] = {0, -ps, ps, -rs, rs, -1, 1};
+  T t[7];
+#pragma unroll
+  for (int e = 0; e < 7; ++e) t[e] = (((apres & m) >> e) & 1) ? __ldg(Y + off + doff[e]) : T(0);
+#pragma unroll
+  for (int e = 0; e < 7; ++e) acc += ca[e] * t[e];
+  return acc;
+}
+
+template <typename T>
 __global__ void __launch_bounds__(kPX *kPY) star_pair_kernel(const __grid_constant__ StarPairDev d) {
-  __shared__ T xs[3][kPY + 2][kPX + 2];
-  __shared__ uint32_t aj[kPY + 2], ak[kPX + 2], bj[kPY], bk[kPX];
+  constexpr int HX = kPX + 2, HW = (kPY + 2) * HX, NT = kPX * kPY;
+  __shared__ T xs[3][kPY + 2][HX];
+  __shared__ uint32_t aj[kPY + 2], ak[HX], bj[kPY], bk[kPX], ai[kPM + 2], bi[kPM];
   const int tx = threadIdx.x, ty = threadIdx.y, tid = ty * kPX + tx;
   const int k0 = blockIdx.x * kPX, j0 = blockIdx.y * kPY;
-  const int i0 = blockIdx.z * kPM, i1 = min(i0 + kPM, d.d0);
+  const int i0 = d.zlo + blockIdx.z * kPM, i1 = min(i0 + kPM, d.zhi);
+  // per-coordinate predicate words, once per CTA
   if (tid < kPY + 2) aj[tid] = coord_bits(d.a, 1, j0 - 1 + tid, d.d1, d.dlo, d.dhi);
-  if (tid >= 32 && tid < 32 + kPX + 2) ak[tid - 32] = coord_bits(d.a, 2, k0 - 1 + (tid - 32), d.d2, d.dlo, d.dhi);
+  if (tid >= 32 && tid < 32 + HX) ak[tid - 32] = coord_bits(d.a, 2, k0 - 1 + (tid - 32), d.d2, d.dlo, d.dhi);
   if (tid >= 96 && tid < 96 + kPY) bj[tid - 96] = coord_bits(d.b, 1, j0 + (tid - 96), d.d1, nullptr, nullptr);
   if (tid >= 128 && tid < 128 + kPX) bk[tid - 128] = coord_bits(d.b, 2, k0 + (tid - 128), d.d2, nullptr, nullptr);
+  if (tid >= 192 && tid < 192 + kPM + 2)
+    ai[tid - 192] = coord_bits(d.a, 0, i0 - 1 + (tid - 192) + d.p0, d.gd0, d.dlo, d.dhi);
+  if (tid >= 224 && tid < 224 + kPM) bi[tid - 224] = coord_bits(d.b, 0, i0 + (tid - 224) + d.p0, d.gd0, nullptr, nullptr);
+  __shared__ uint32_t s_and_a, s_or_a, s_and_b, s_or_b;
+  if (tid == 0) {
+    s_and_a = s_and_b = 0xffffffffu;
+    s_or_a = s_or_b = 0u;
+  }
+  __syncthreads();
+  // block-uniform summary: AND / OR of the predicate words over the CTA's
+  // window (a: halo window of X, b: core of Z) -> interior fast path
+  {
+    const int na = min(i1 + 1, d.d0) - max(i0 - 1, 0);
+    uint32_t wa = 0xffffffffu, oa = 0u, wb = 0xffffffffu, ob = 0u;
+    if (tid < kPY + 2) { wa &= aj[tid]; oa |= aj[tid]; }
+    if (tid < HX) { wa &= ak[tid]; oa |= ak[tid]; }
+    if (tid < na) { const uint32_t v = ai[max(i0 - 1, 0) - (i0 - 1) + tid]; wa &= v; oa |= v; }
+    if (tid < kPY) { wb &= bj[tid]; ob |= bj[tid]; }
+    if (tid < kPX) { wb &= bk[tid]; ob |= bk[tid]; }
+    if (tid < i1 - i0) { wb &= bi[tid]; ob |= bi[tid]; }
+    if (tid < 64) {
+      atomicAnd(&s_and_a, wa);
+      atomicOr(&s_or_a, oa);
+      atomicAnd(&s_and_b, wb);
+      atomicOr(&s_or_b, ob);
+    }
+  }
   __syncthreads();
   const T *__restrict__ Y = (const T *)d.y;
   const T *__restrict__ Xo = (const T *)d.xold;
@@ -90,51 +135,103 @@ __global__ void __launch_bounds__(kPX *kPY) star_pair_kernel(const __grid_consta
     cb[p] = (T)d.b.coef[p];
   }
   const uint32_t apres = d.a.present, bpres = d.b.present;
-  constexpr int HW = (kPY + 2) * (kPX + 2);
+  // the (at most two) halo-window points this thread computes per plane
+  const int hj0 = tid / HX, hk0 = tid - hj0 * HX;
+  const int p1 = tid + NT;
+  const bool has1 = p1 < HW;
+  const int hj1 = p1 / HX, hk1 = p1 - hj1 * HX;
+  const uint32_t mjk0 = aj[hj0] & ak[hk0];
+  const uint32_t mjk1 = has1 ? (aj[hj1] & ak[hk1]) : 0u;
+  const bool core0 = hj0 >= 1 && hj0 <= kPY && hk0 >= 1 && hk0 <= kPX;
+  const bool core1 = has1 && hj1 >= 1 && hj1 <= kPY && hk1 >= 1 && hk1 <= kPX;
+  const int rel0 = (j0 - 1 + hj0) * rs + (k0 - 1 + hk0);
+  const int rel1 = (j0 - 1 + hj1) * rs + (k0 - 1 + hk1);
+  const uint32_t mzjk = bj[ty] & bk[tx];
+  const int zrel = (j0 + ty) * rs + (k0 + tx);
+  {
+    // interior fast path: every window point inside the array and both
+    // regions, every present tap admitted, clear / dead predicates uniform
+    const uint32_t fa = apres | kRegion | kArray, fb = bpres | kRegion | kArray;
+    const uint32_t aA = s_and_a, oA = s_or_a, aB = s_and_b, oB = s_or_b;
+    const bool fast = (aA & fa) == fa && (aB & fb) == fb && ((aA ^ oA) & (kClear | kDead)) == 0 &&
+                      ((aB ^ oB) & kClear) == 0 && i0 >= 1 && i1 + 1 <= d.d0;
+    if (fast) {
+      const bool xbase = d.a.mode == 0 || (d.a.mode == 2 && !(aA & kClear));
+      const bool zbase = d.b.mode == 0 || (d.b.mode == 2 && !(aB & kClear));
+      const bool xw = d.xwrite && !(aA & kDead);
+      const int doff[7] = {0, -ps, ps, -rs, rs, -1, 1};
+      for (int q = i0 - 1; q <= i1; ++q) {
+        const int slot = (q + 3) % 3;
+        const bool own = xw && q >= i0 && q < i1;
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          if (h == 1 && !has1) break;
+          const int off = q * ps + (h ? rel1 : rel0);
+          T acc = xbase ? Xo[off] : T(0);
+#pragma unroll
+          for (int e = 0; e < 7; ++e)
+            if ((apres >> e) & 1) acc += ca[e] * __ldg(Y + off + doff[e]);
+          if (own && (h ? core1 : core0)) Xn[off] = acc;
+          if (h)
+            xs[slot][hj1][hk1] = acc;
+          else
+            xs[slot][hj0][hk0] = acc;
+        }
+        __syncthreads();
+        const int i = q - 1;
+        if (i >= i0 && i < i1) {
+          const int off = i * ps + zrel;
+          T w = zbase ? Zo[off] : T(0);
+          const int sc = (i + 3) % 3, sm = (i + 2) % 3, sp = (i + 4) % 3;
+          if (bpres & 1) w += cb[0] * xs[sc][ty + 1][tx + 1];
+          if (bpres & 2) w += cb[1] * xs[sm][ty + 1][tx + 1];
+          if (bpres & 4) w += cb[2] * xs[sp][ty + 1][tx + 1];
+          if (bpres & 8) w += cb[3] * xs[sc][ty][tx + 1];
+          if (bpres & 16) w += cb[4] * xs[sc][ty + 2][tx + 1];
+          if (bpres & 32) w += cb[5] * xs[sc][ty + 1][tx];
+          if (bpres & 64) w += cb[6] * xs[sc][ty + 1][tx + 2];
+          Zn[off] = w;
+        }
+        __syncthreads();
+      }
+      return;
+    }
+  }
   for (int q = i0 - 1; q <= i1; ++q) {
     const int slot = (q + 3) % 3;
     if (q >= 0 && q < d.d0) {
-      const uint32_t mi = coord_bits(d.a, 0, q, d.d0, d.dlo, d.dhi);
-      const bool own = q >= i0 && q < i1;
-      for (int p = tid; p < HW; p += kPX * kPY) {
-        const int hj = p / (kPX + 2), hk = p - hj * (kPX + 2);
-        const uint32_t m = mi & aj[hj] & ak[hk];
+      const uint32_t mi = ai[q - i0 + 1];
+      const bool own = q >= i0 && q < i1 && d.xwrite;
+      {
+        const uint32_t m = mi & mjk0;
         T v = T(0);
         if (m & kArray) {
-          const int off = q * ps + (j0 - 1 + hj) * rs + (k0 - 1 + hk);
-          if (m & kRegion) {
-            T acc;
-            if (d.a.mode == 0 || (d.a.mode == 2 && !(m & kClear)))
-              acc = Xo[off];
-            else
-              acc = T(0);
-            const int doff[7] = {0, -ps, ps, -rs, rs, -1, 1};
-            T t[7];
-#pragma unroll
-            for (int e = 0; e < 7; ++e) t[e] = (((apres & m) >> e) & 1) ? __ldg(Y + off + doff[e]) : T(0);
-#pragma unroll
-            for (int e = 0; e < 7; ++e) acc += ca[e] * t[e];
-            v = acc;
-          } else {
-            v = Xo[off];
-          }
-          if (d.xwrite && own && hj >= 1 && hj <= kPY && hk >= 1 && hk <= kPX && !(m & kDead)) Xn[off] = v;
+          const int off = q * ps + rel0;
+          v = star_x_point<T>(d, Y, Xo, ca, apres, m, off, ps, rs);
+          if (own && core0 && !(m & kDead)) Xn[off] = v;
         }
-        xs[slot][hj][hk] = v;
+        xs[slot][hj0][hk0] = v;
+      }
+      if (has1) {
+        const uint32_t m = mi & mjk1;
+        T v = T(0);
+        if (m & kArray) {
+          const int off = q * ps + rel1;
+          v = star_x_point<T>(d, Y, Xo, ca, apres, m, off, ps, rs);
+          if (own && core1 && !(m & kDead)) Xn[off] = v;
+        }
+        xs[slot][hj1][hk1] = v;
       }
     }
     __syncthreads();
     const int i = q - 1;
     if (i >= i0 && i < i1) {
-      const uint32_t m = coord_bits(d.b, 0, i, d.d0, nullptr, nullptr) & bj[ty] & bk[tx];
+      const uint32_t m = bi[i - i0] & mzjk;
       if (m & kArray) {
-        const int off = i * ps + (j0 + ty) * rs + (k0 + tx);
+        const int off = i * ps + zrel;
         T w;
         if (m & kRegion) {
-          if (d.b.mode == 0 || (d.b.mode == 2 && !(m & kClear)))
-            w = Zo[off];
-          else
-            w = T(0);
+          w = (d.b.mode == 0 || (d.b.mode == 2 && !(m & kClear))) ? Zo[off] : T(0);
           const int sc = (i + 3) % 3, sm = (i + 2) % 3, sp = (i + 4) % 3;
           T t[7];
           t[0] = xs[sc][ty + 1][tx + 1];
@@ -199,6 +296,18 @@ extern "C" int gfb_star_pair_launch(const gfb_star_pair_desc *s, void *stream) {
   d.ps = (int32_t)(dims[1] * dims[2]);
   d.rs = (int32_t)dims[2];
   d.xwrite = s->xwrite;
+  if (s->rank == 3) {
+    d.p0 = (int32_t)s->plane0;
+    d.gd0 = (int32_t)(s->global_d0 > 0 ? s->global_d0 : dims[0]);
+    d.zlo = (int32_t)s->zlo;
+    d.zhi = (int32_t)(s->zhi > s->zlo ? s->zhi : dims[0]);
+  } else {
+    d.p0 = 0;
+    d.gd0 = 1;
+    d.zlo = 0;
+    d.zhi = 1;
+  }
+  if (d.zlo < 0 || d.zhi > d.d0 || d.zlo >= d.zhi) return set_error(GFB_EINVAL, "gfb_star_pair_launch: bad plane range");
   fill_star_op(d.a, s->a, pad);
   fill_star_op(d.b, s->b, pad);
   d.y = s->y;
@@ -212,7 +321,7 @@ extern "C" int gfb_star_pair_launch(const gfb_star_pair_desc *s, void *stream) {
     d.dhi[r] = padded ? (1 << 30) : (int32_t)s->dead_hi[r - pad];
   }
   dim3 block(kPX, kPY);
-  dim3 grid((unsigned)ceil_div(d.d2, kPX), (unsigned)ceil_div(d.d1, kPY), (unsigned)ceil_div(d.d0, kPM));
+  dim3 grid((unsigned)ceil_div(d.d2, kPX), (unsigned)ceil_div(d.d1, kPY), (unsigned)ceil_div(d.zhi - d.zlo, kPM));
   cudaStream_t st = (cudaStream_t)stream;
   if (s->dtype == GFB_F64)
     star_pair_kernel<double><<<grid, block, 0, st>>>(d);

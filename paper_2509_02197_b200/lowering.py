@@ -128,6 +128,7 @@ class Buffer:
         # deferred gradient clear); None = contents are materialized
         self.pending = whole_box(self.shape) if fresh else None
         self.alias_of: Buffer | None = None
+        self.offset = 0  # element offset into alias_of (slab views)
         self.tensor = None
         self.strides = tuple(int(np.prod(self.shape[d + 1:], dtype=np.int64)) for d in range(len(self.shape)))
 
@@ -137,12 +138,19 @@ class Buffer:
             b = b.alias_of
         return b
 
+    def root_offset(self) -> int:
+        b, off = self, 0
+        while b.alias_of is not None:
+            off += b.offset
+            b = b.alias_of
+        return off
+
     @property
     def ptr(self) -> int:
         t = self.root().tensor
         if t is None:
             raise RuntimeError(f"buffer '{self.name}' not allocated")
-        return t.data_ptr()
+        return t.data_ptr() + self.root_offset() * self.itemsize
 
     def __repr__(self):
         return f"Buffer({self.name}, {self.shape}, {self.kind})"
@@ -763,6 +771,9 @@ class StarPairOp(Op):
         self.xwrite, self.dead = xwrite, dead
         self.xout = self.X
         self.zout = self.Z
+        # slab placement (decomp.py): global plane of local plane 0, local
+        # planes produced, global extent of dim 0; single device: whole array
+        self.plane0, self.zrange, self.global_d0 = 0, None, None
         self._refresh()
 
     def _refresh(self):
@@ -797,6 +808,9 @@ class StarPairOp(Op):
         if self.dead is not None:
             for r in range(rank):
                 d.dead_lo[r], d.dead_hi[r] = self.dead[r]
+        d.plane0 = self.plane0
+        d.zlo, d.zhi = self.zrange if self.zrange is not None else (0, self.Z.shape[0])
+        d.global_d0 = self.global_d0 if self.global_d0 is not None else self.Z.shape[0]
         self.desc = d
         self._ref = C.byref(d)
 

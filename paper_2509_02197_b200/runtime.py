@@ -70,7 +70,8 @@ class Executable:
 
     def view(self, b: Buffer) -> torch.Tensor:
         t = b.root().tensor
-        return t[: b.numel].view(b.shape) if b.shape else t[:1].view(())
+        o = b.root_offset()
+        return t[o: o + b.numel].view(b.shape) if b.shape else t[o:o + 1].view(())
 
     # -- execution -----------------------------------------------------------------
 
@@ -79,9 +80,10 @@ class Executable:
             v = values[name]
             dst = self.view(buf)
             if isinstance(v, torch.Tensor):
-                src = v.to(device=self.device, dtype=dst.dtype)
+                src = v if v.dtype == dst.dtype else v.to(dst.dtype)
                 if tuple(src.shape) != tuple(dst.shape):
                     src = src.reshape(dst.shape)
+                # device tensors: one D2D copy; pinned host tensors: async DMA
                 dst.copy_(src, non_blocking=True)
             else:
                 arr = np.ascontiguousarray(np.asarray(v, dtype=NP_DTYPE[buf.kind])).reshape(buf.shape)
@@ -127,7 +129,12 @@ class Executable:
         return self.view(self.outputs[key])
 
     def output_host(self, key) -> np.ndarray:
-        return self.output(key).detach().cpu().numpy().copy()
+        """Fresh host array (owned by the caller) via a pinned staging copy."""
+        t = self.output(key)
+        h = torch.empty(t.shape, dtype=t.dtype, pin_memory=True)
+        h.copy_(t, non_blocking=True)
+        torch.cuda.current_stream(self.device).synchronize()
+        return h.numpy()
 
     # -- profiling helpers ----------------------------------------------------------
 

@@ -334,18 +334,25 @@ class Emulator:
 
         Y, Xo, Zo = view(d.y), view(d.xold), view(d.zold)
         Y, Xo, Zo = Y.copy(), Xo.copy(), Zo.copy()
-        Xn = _star_apply(d.a, Y, Xo, rank, dims)
-        Zn = _star_apply(d.b, Xn, Zo, rank, dims)
-        view(d.zout)[...] = Zn
+        p0 = d.plane0 if rank == 3 else 0
+        zlo, zhi = (d.zlo, d.zhi) if rank == 3 else (0, dims[0])
+        Xn = _star_apply(d.a, Y, Xo, rank, dims, p0)
+        Zn = _star_apply(d.b, Xn, Zo, rank, dims, p0)
+        zv = view(d.zout)
+        zv[zlo:zhi] = Zn[zlo:zhi]
         if d.xwrite:
-            ys = np.meshgrid(*[np.arange(k) for k in dims], indexing="ij")
+            ys = list(np.meshgrid(*[np.arange(k) for k in dims], indexing="ij"))
+            ys[0] = ys[0] + p0
             dead = np.ones(ys[0].shape, dtype=bool)
             for r in range(rank):
                 dead &= (ys[r] >= d.dead_lo[r]) & (ys[r] < d.dead_hi[r])
             if not any(d.dead_hi[r] > d.dead_lo[r] for r in range(rank)):
                 dead[...] = False
+            own = np.zeros(ys[0].shape, dtype=bool)
+            own[zlo:zhi] = True
             out = view(d.xout)
-            out[~dead] = Xn[~dead]
+            sel = ~dead & own
+            out[sel] = Xn[sel]
 
     def stencil(self, d):
         rank = d.rank
@@ -387,11 +394,13 @@ class Emulator:
 _STAR = [(0, 0, 0), (-1, 0, 0), (1, 0, 0), (0, -1, 0), (0, 1, 0), (0, 0, -1), (0, 0, 1)]
 
 
-def _star_apply(so, src, old, rank, dims):
-    """One radius-1 star op over the whole array (values outside its region
-    keep `old`)."""
+def _star_apply(so, src, old, rank, dims, p0=0):
+    """One radius-1 star op over the whole (local) array (values outside its
+    region keep `old`); p0 = global index of local plane 0."""
     T = old.dtype.type
-    ys = np.meshgrid(*[np.arange(n) for n in dims], indexing="ij")
+    ys = list(np.meshgrid(*[np.arange(n) for n in dims], indexing="ij"))
+    ys[0] = ys[0] + p0
+    loc0 = ys[0] - p0
     pad = 3 - rank
 
     def inb(lo, hi):
@@ -414,7 +423,7 @@ def _star_apply(so, src, old, rank, dims):
         m = region.copy()
         if (so.masked >> pos) & 1:
             m &= inb(so.mlo[pos], so.mhi[pos])
-        idx = tuple(np.clip(ys[r] + delta[r], 0, dims[r] - 1) for r in range(rank))
+        idx = tuple(np.clip((loc0 if r == 0 else ys[r]) + delta[r], 0, dims[r] - 1) for r in range(rank))
         acc = acc + np.where(m, T(so.coef[pos]) * src[idx], 0).astype(T)
     return np.where(region, acc, old).astype(T)
 
@@ -449,6 +458,7 @@ def execute(exe_builder_low, inputs: dict, input_bufs: dict, seed_buf=None, seed
 
     def view(b):
         t = b.root().tensor.arr
-        return t[:b.numel].reshape(b.shape) if b.shape else t[:1].reshape(())
+        o = b.root_offset()
+        return t[o:o + b.numel].reshape(b.shape) if b.shape else t[o:o + 1].reshape(())
 
     return em, view
