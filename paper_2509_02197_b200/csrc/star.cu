@@ -81,6 +81,92 @@ __device__ __forceinline__ T star_x_point(const StarPairDev &d, const T *__restr
   return acc;
 }
 
+// Interior fast path of one CTA: compile-time full stars, no predicates.
+// HAS_I: rank-3 arrays (taps along dim 0); rank-2 arrays have one plane.
+template <typename T, bool HAS_I>
+__device__ __forceinline__ void star_pair_fast(const StarPairDev &d, T (*xs)[kPY + 2][kPX + 2], uint32_t aA,
+                                               uint32_t aB, int i0, int i1, int tid, int hj0, int hk0, int hj1,
+                                               int hk1, bool has1, bool core0, bool core1, int rel0, int rel1,
+                                               int zrel, const T (&ca)[7], const T (&cb)[7]) {
+  const T *__restrict__ Y = (const T *)d.y;
+  const T *__restrict__ Xo = (const T *)d.xold;
+  const T *__restrict__ Zo = (const T *)d.zold;
+  T *__restrict__ Xn = (T *)d.xout;
+  T *__restrict__ Zn = (T *)d.zout;
+  const int ps = d.ps, rs = d.rs;
+  const int tx = threadIdx.x, ty = threadIdx.y;
+  const bool xbase = d.a.mode == 0 || (d.a.mode == 2 && !(aA & kClear));
+  const bool zbase = d.b.mode == 0 || (d.b.mode == 2 && !(aB & kClear));
+  const bool xw = d.xwrite && !(aA & kDead);
+  const bool xw0 = xw && core0, xw1 = xw && core1;
+  int s_m = (i0 + 2) % 3, s_c = (i0 + 3) % 3, s_p = (i0 + 4) % 3;  // slots of planes i-1, i, i+1 for i = i0
+  int slot = (i0 + 2) % 3;                                          // slot of plane q = i0 - 1
+  const int qbeg = HAS_I ? i0 - 1 : 0, qend = HAS_I ? i1 : 0;
+  if (!HAS_I) {
+    s_c = 0;
+    slot = 0;
+  }
+  for (int q = qbeg; q <= qend; ++q) {
+    const bool own = q >= i0 && q < i1;
+    {
+      const T *y = Y + (q * ps + rel0);
+      T acc = xbase ? Xo[q * ps + rel0] : T(0);
+      T t0 = __ldg(y), t3 = __ldg(y - rs), t4 = __ldg(y + rs), t5 = __ldg(y - 1), t6 = __ldg(y + 1);
+      T t1 = HAS_I ? __ldg(y - ps) : T(0), t2 = HAS_I ? __ldg(y + ps) : T(0);
+      acc += ca[0] * t0;
+      if (HAS_I) {
+        acc += ca[1] * t1;
+        acc += ca[2] * t2;
+      }
+      acc += ca[3] * t3;
+      acc += ca[4] * t4;
+      acc += ca[5] * t5;
+      acc += ca[6] * t6;
+      if (own && xw0) Xn[q * ps + rel0] = acc;
+      xs[slot][hj0][hk0] = acc;
+    }
+    if (has1) {
+      const T *y = Y + (q * ps + rel1);
+      T acc = xbase ? Xo[q * ps + rel1] : T(0);
+      T t0 = __ldg(y), t3 = __ldg(y - rs), t4 = __ldg(y + rs), t5 = __ldg(y - 1), t6 = __ldg(y + 1);
+      T t1 = HAS_I ? __ldg(y - ps) : T(0), t2 = HAS_I ? __ldg(y + ps) : T(0);
+      acc += ca[0] * t0;
+      if (HAS_I) {
+        acc += ca[1] * t1;
+        acc += ca[2] * t2;
+      }
+      acc += ca[3] * t3;
+      acc += ca[4] * t4;
+      acc += ca[5] * t5;
+      acc += ca[6] * t6;
+      if (own && xw1) Xn[q * ps + rel1] = acc;
+      xs[slot][hj1][hk1] = acc;
+    }
+    __syncthreads();
+    const int i = HAS_I ? q - 1 : q;
+    if (i >= i0) {
+      const int off = i * ps + zrel;
+      T w = zbase ? Zo[off] : T(0);
+      w += cb[0] * xs[s_c][ty + 1][tx + 1];
+      if (HAS_I) {
+        w += cb[1] * xs[s_m][ty + 1][tx + 1];
+        w += cb[2] * xs[s_p][ty + 1][tx + 1];
+      }
+      w += cb[3] * xs[s_c][ty][tx + 1];
+      w += cb[4] * xs[s_c][ty + 2][tx + 1];
+      w += cb[5] * xs[s_c][ty + 1][tx];
+      w += cb[6] * xs[s_c][ty + 1][tx + 2];
+      Zn[off] = w;
+      const int t = s_m;
+      s_m = s_c;
+      s_c = s_p;
+      s_p = t;
+    }
+    slot = slot == 2 ? 0 : slot + 1;
+    __syncthreads();
+  }
+}
+
 template <typename T>
 __global__ void __launch_bounds__(kPX *kPY) star_pair_kernel(const __grid_constant__ StarPairDev d) {
   constexpr int HX = kPX + 2, HW = (kPY + 2) * HX, NT = kPX * kPY;
@@ -150,50 +236,21 @@ __global__ void __launch_bounds__(kPX *kPY) star_pair_kernel(const __grid_consta
   const int zrel = (j0 + ty) * rs + (k0 + tx);
   {
     // interior fast path: every window point inside the array and both
-    // regions, every present tap admitted, clear / dead predicates uniform
-    const uint32_t fa = apres | kRegion | kArray, fb = bpres | kRegion | kArray;
+    // regions, every tap admitted, clear / dead predicates uniform, and both
+    // ops full stars (all positions of the array's rank present)
+    const uint32_t full = d.d0 > 1 ? 0x7fu : 0x79u;
+    const uint32_t fa = full | kRegion | kArray, fb = full | kRegion | kArray;
     const uint32_t aA = s_and_a, oA = s_or_a, aB = s_and_b, oB = s_or_b;
-    const bool fast = (aA & fa) == fa && (aB & fb) == fb && ((aA ^ oA) & (kClear | kDead)) == 0 &&
-                      ((aB ^ oB) & kClear) == 0 && i0 >= 1 && i1 + 1 <= d.d0;
+    const bool fast = apres == full && bpres == full && (aA & fa) == fa && (aB & fb) == fb &&
+                      ((aA ^ oA) & (kClear | kDead)) == 0 && ((aB ^ oB) & kClear) == 0 &&
+                      (d.d0 == 1 || (i0 >= 1 && i1 + 1 <= d.d0));
     if (fast) {
-      const bool xbase = d.a.mode == 0 || (d.a.mode == 2 && !(aA & kClear));
-      const bool zbase = d.b.mode == 0 || (d.b.mode == 2 && !(aB & kClear));
-      const bool xw = d.xwrite && !(aA & kDead);
-      const int doff[7] = {0, -ps, ps, -rs, rs, -1, 1};
-      for (int q = i0 - 1; q <= i1; ++q) {
-        const int slot = (q + 3) % 3;
-        const bool own = xw && q >= i0 && q < i1;
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          if (h == 1 && !has1) break;
-          const int off = q * ps + (h ? rel1 : rel0);
-          T acc = xbase ? Xo[off] : T(0);
-#pragma unroll
-          for (int e = 0; e < 7; ++e)
-            if ((apres >> e) & 1) acc += ca[e] * __ldg(Y + off + doff[e]);
-          if (own && (h ? core1 : core0)) Xn[off] = acc;
-          if (h)
-            xs[slot][hj1][hk1] = acc;
-          else
-            xs[slot][hj0][hk0] = acc;
-        }
-        __syncthreads();
-        const int i = q - 1;
-        if (i >= i0 && i < i1) {
-          const int off = i * ps + zrel;
-          T w = zbase ? Zo[off] : T(0);
-          const int sc = (i + 3) % 3, sm = (i + 2) % 3, sp = (i + 4) % 3;
-          if (bpres & 1) w += cb[0] * xs[sc][ty + 1][tx + 1];
-          if (bpres & 2) w += cb[1] * xs[sm][ty + 1][tx + 1];
-          if (bpres & 4) w += cb[2] * xs[sp][ty + 1][tx + 1];
-          if (bpres & 8) w += cb[3] * xs[sc][ty][tx + 1];
-          if (bpres & 16) w += cb[4] * xs[sc][ty + 2][tx + 1];
-          if (bpres & 32) w += cb[5] * xs[sc][ty + 1][tx];
-          if (bpres & 64) w += cb[6] * xs[sc][ty + 1][tx + 2];
-          Zn[off] = w;
-        }
-        __syncthreads();
-      }
+      if (d.d0 > 1)
+        star_pair_fast<T, true>(d, xs, aA, aB, i0, i1, tid, hj0, hk0, hj1, hk1, has1, core0, core1, rel0, rel1,
+                                zrel, ca, cb);
+      else
+        star_pair_fast<T, false>(d, xs, aA, aB, i0, i1, tid, hj0, hk0, hj1, hk1, has1, core0, core1, rel0, rel1,
+                                 zrel, ca, cb);
       return;
     }
   }
