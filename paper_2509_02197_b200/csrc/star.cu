@@ -83,6 +83,38 @@ __device__ __forceinline__ T star_x_point(const StarPairDev &d, const T *__restr
 
 // Interior fast path of one CTA: compile-time full stars, no predicates.
 // HAS_I: rank-3 arrays (taps along dim 0); rank-2 arrays have one plane.
+// X planes live in a 4-slot ring, so one barrier per plane suffices (the
+// slot written for plane q+1 was last read by Z(q-3+1) before the previous
+// barrier), and the global loads of the next plane are issued before the
+// barrier so they overlap it and the Z stage.
+template <typename T, bool HAS_I>
+struct StarTaps {
+  T v[7];
+  __device__ __forceinline__ void load(const T *__restrict__ y, int ps, int rs) {
+    v[0] = __ldg(y);
+    v[3] = __ldg(y - rs);
+    v[4] = __ldg(y + rs);
+    v[5] = __ldg(y - 1);
+    v[6] = __ldg(y + 1);
+    if (HAS_I) {
+      v[1] = __ldg(y - ps);
+      v[2] = __ldg(y + ps);
+    }
+  }
+  __device__ __forceinline__ T dot(const T (&c)[7], T acc) const {
+    acc += c[0] * v[0];
+    if (HAS_I) {
+      acc += c[1] * v[1];
+      acc += c[2] * v[2];
+    }
+    acc += c[3] * v[3];
+    acc += c[4] * v[4];
+    acc += c[5] * v[5];
+    acc += c[6] * v[6];
+    return acc;
+  }
+};
+
 template <typename T, bool HAS_I>
 __device__ __forceinline__ void star_pair_fast(const StarPairDev &d, T (*xs)[kPY + 2][kPX + 2], uint32_t aA,
                                                uint32_t aB, int i0, int i1, int tid, int hj0, int hk0, int hj1,
@@ -99,78 +131,53 @@ __device__ __forceinline__ void star_pair_fast(const StarPairDev &d, T (*xs)[kPY
   const bool zbase = d.b.mode == 0 || (d.b.mode == 2 && !(aB & kClear));
   const bool xw = d.xwrite && !(aA & kDead);
   const bool xw0 = xw && core0, xw1 = xw && core1;
-  int s_m = (i0 + 2) % 3, s_c = (i0 + 3) % 3, s_p = (i0 + 4) % 3;  // slots of planes i-1, i, i+1 for i = i0
-  int slot = (i0 + 2) % 3;                                          // slot of plane q = i0 - 1
   const int qbeg = HAS_I ? i0 - 1 : 0, qend = HAS_I ? i1 : 0;
-  if (!HAS_I) {
-    s_c = 0;
-    slot = 0;
-  }
+  StarTaps<T, HAS_I> r0, r1;
+  r0.load(Y + (qbeg * ps + rel0), ps, rs);
+  if (has1) r1.load(Y + (qbeg * ps + rel1), ps, rs);
   for (int q = qbeg; q <= qend; ++q) {
+    const int slot = q & 3;
     const bool own = q >= i0 && q < i1;
     {
-      const T *y = Y + (q * ps + rel0);
-      T acc = xbase ? Xo[q * ps + rel0] : T(0);
-      T t0 = __ldg(y), t3 = __ldg(y - rs), t4 = __ldg(y + rs), t5 = __ldg(y - 1), t6 = __ldg(y + 1);
-      T t1 = HAS_I ? __ldg(y - ps) : T(0), t2 = HAS_I ? __ldg(y + ps) : T(0);
-      acc += ca[0] * t0;
-      if (HAS_I) {
-        acc += ca[1] * t1;
-        acc += ca[2] * t2;
-      }
-      acc += ca[3] * t3;
-      acc += ca[4] * t4;
-      acc += ca[5] * t5;
-      acc += ca[6] * t6;
-      if (own && xw0) Xn[q * ps + rel0] = acc;
+      const int off = q * ps + rel0;
+      const T acc = r0.dot(ca, xbase ? Xo[off] : T(0));
+      if (own && xw0) Xn[off] = acc;
       xs[slot][hj0][hk0] = acc;
     }
     if (has1) {
-      const T *y = Y + (q * ps + rel1);
-      T acc = xbase ? Xo[q * ps + rel1] : T(0);
-      T t0 = __ldg(y), t3 = __ldg(y - rs), t4 = __ldg(y + rs), t5 = __ldg(y - 1), t6 = __ldg(y + 1);
-      T t1 = HAS_I ? __ldg(y - ps) : T(0), t2 = HAS_I ? __ldg(y + ps) : T(0);
-      acc += ca[0] * t0;
-      if (HAS_I) {
-        acc += ca[1] * t1;
-        acc += ca[2] * t2;
-      }
-      acc += ca[3] * t3;
-      acc += ca[4] * t4;
-      acc += ca[5] * t5;
-      acc += ca[6] * t6;
-      if (own && xw1) Xn[q * ps + rel1] = acc;
+      const int off = q * ps + rel1;
+      const T acc = r1.dot(ca, xbase ? Xo[off] : T(0));
+      if (own && xw1) Xn[off] = acc;
       xs[slot][hj1][hk1] = acc;
+    }
+    if (q < qend) {  // prefetch the next plane across the barrier
+      r0.load(Y + ((q + 1) * ps + rel0), ps, rs);
+      if (has1) r1.load(Y + ((q + 1) * ps + rel1), ps, rs);
     }
     __syncthreads();
     const int i = HAS_I ? q - 1 : q;
     if (i >= i0) {
       const int off = i * ps + zrel;
+      const int sc = i & 3, sm = (i - 1) & 3, sp = (i + 1) & 3;
       T w = zbase ? Zo[off] : T(0);
-      w += cb[0] * xs[s_c][ty + 1][tx + 1];
+      w += cb[0] * xs[sc][ty + 1][tx + 1];
       if (HAS_I) {
-        w += cb[1] * xs[s_m][ty + 1][tx + 1];
-        w += cb[2] * xs[s_p][ty + 1][tx + 1];
+        w += cb[1] * xs[sm][ty + 1][tx + 1];
+        w += cb[2] * xs[sp][ty + 1][tx + 1];
       }
-      w += cb[3] * xs[s_c][ty][tx + 1];
-      w += cb[4] * xs[s_c][ty + 2][tx + 1];
-      w += cb[5] * xs[s_c][ty + 1][tx];
-      w += cb[6] * xs[s_c][ty + 1][tx + 2];
+      w += cb[3] * xs[sc][ty][tx + 1];
+      w += cb[4] * xs[sc][ty + 2][tx + 1];
+      w += cb[5] * xs[sc][ty + 1][tx];
+      w += cb[6] * xs[sc][ty + 1][tx + 2];
       Zn[off] = w;
-      const int t = s_m;
-      s_m = s_c;
-      s_c = s_p;
-      s_p = t;
     }
-    slot = slot == 2 ? 0 : slot + 1;
-    __syncthreads();
   }
 }
 
 template <typename T>
-__global__ void __launch_bounds__(kPX *kPY) star_pair_kernel(const __grid_constant__ StarPairDev d) {
+__global__ void __launch_bounds__(kPX *kPY, 2) star_pair_kernel(const __grid_constant__ StarPairDev d) {
   constexpr int HX = kPX + 2, HW = (kPY + 2) * HX, NT = kPX * kPY;
-  __shared__ T xs[3][kPY + 2][HX];
+  __shared__ T xs[4][kPY + 2][HX];
   __shared__ uint32_t aj[kPY + 2], ak[HX], bj[kPY], bk[kPX], ai[kPM + 2], bi[kPM];
   const int tx = threadIdx.x, ty = threadIdx.y, tid = ty * kPX + tx;
   const int k0 = blockIdx.x * kPX, j0 = blockIdx.y * kPY;
