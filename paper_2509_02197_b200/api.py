@@ -305,8 +305,11 @@ def _result(exe: Executable, program: Program, inputs: dict, bundle) -> Gradient
         else:
             ref = np.asarray(inputs[ind])
             grads[ind] = np.zeros(ref.shape, dtype=NP_DTYPE[program.descriptors[ind].element_kind])
-    fenv = {k: exe.view(b) for k, b in exe.forward_env.items()}
-    benv = {k: exe.view(b) for k, b in exe.backward_env.items()}
+    # env entries whose HBM was recycled by the liveness arena are omitted
+    # (inputs, the dependent and the gradients always remain)
+    kept = getattr(exe, "keep_bids", None)
+    fenv = {k: exe.view(b) for k, b in exe.forward_env.items() if kept is None or b.root().bid in kept}
+    benv = {k: exe.view(b) for k, b in exe.backward_env.items() if kept is None or b.root().bid in kept}
     fwd = RunResult(env=fenv, value=value, op_count=exe.flops, tape=exe.tape)
     bwd = RunResult(env=benv, value=None, op_count=exe.flops)
     return GradientResult(value=value, grads=grads, forward=fwd, backward=bwd, bundle=bundle)
@@ -379,7 +382,8 @@ def run_forward(program, inputs: dict, params: dict | None = None, *, record=Non
         raise UnboundName(f"dependent '{prog.dependent}' was never written")
     observed = list(env.values()) + (list(tape.values.values()) if tape else [])
     low.finish(observed)
-    exe = Executable(low, ins, {"value": low.resolve(dep)}, use_graph=False)
+    exe = Executable(low, ins, {"value": low.resolve(dep)}, use_graph=False,
+                     pinned=[low.resolve(b) for b in observed])
     exe.run(inputs)
     out_env = {k: exe.view(low.resolve(b)) for k, b in env.items()}
     res = RunResult(env=out_env, value=exe.output_host("value"), op_count=exe.flops, tape=tape)
@@ -415,7 +419,8 @@ def run_backward(program, backward, inputs: dict, params: dict | None = None, *,
     ProgramRun(low, bwd, params, env, src_tape=tape, forwarding=fw).run()
     low.finish(list(env.values()))
     outputs = {"value": seed_buf} if seed_buf is not None else {}
-    exe = Executable(low, ins, outputs, seed_buf=seed_buf, use_graph=False)
+    exe = Executable(low, ins, outputs, seed_buf=seed_buf, use_graph=False,
+                     pinned=[low.resolve(b) for b in env.values()])
     exe.run({**pass_in, **extra_in}, seed)
     out_env = {k: exe.view(low.resolve(b)) for k, b in env.items()}
     return RunResult(env=out_env, value=None if seed_buf is None else exe.output_host("value"), op_count=exe.flops)

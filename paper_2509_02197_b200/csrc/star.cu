@@ -101,6 +101,19 @@ struct StarTaps {
       v[2] = __ldg(y + ps);
     }
   }
+  // predicated load: tap e only if bit e of `m` is set (out-of-array taps
+  // are never admitted by the predicate words, so no load goes out of bounds)
+  __device__ __forceinline__ void load_masked(const T *__restrict__ y, int ps, int rs, uint32_t m) {
+    v[0] = (m & 1u) ? __ldg(y) : T(0);
+    v[3] = (m & 8u) ? __ldg(y - rs) : T(0);
+    v[4] = (m & 16u) ? __ldg(y + rs) : T(0);
+    v[5] = (m & 32u) ? __ldg(y - 1) : T(0);
+    v[6] = (m & 64u) ? __ldg(y + 1) : T(0);
+    if (HAS_I) {
+      v[1] = (m & 2u) ? __ldg(y - ps) : T(0);
+      v[2] = (m & 4u) ? __ldg(y + ps) : T(0);
+    }
+  }
   __device__ __forceinline__ T dot(const T (&c)[7], T acc) const {
     acc += c[0] * v[0];
     if (HAS_I) {
@@ -174,6 +187,92 @@ __device__ __forceinline__ void star_pair_fast(const StarPairDev &d, T (*xs)[kPY
   }
 }
 
+// Boundary CTAs: the same pipelined loop with per-point predicate words
+// (array / region / clear / dead bits and per-tap mask bits), all branch-free
+// selects around predicated loads.
+template <typename T, bool HAS_I>
+__device__ __forceinline__ void star_pair_checked(const StarPairDev &d, T (*xs)[kPY + 2][kPX + 2],
+                                                  const uint32_t *ai, const uint32_t *bi, int i0, int i1,
+                                                  uint32_t mjk0, uint32_t mjk1, uint32_t mzjk, int hj0, int hk0,
+                                                  int hj1, int hk1, bool has1, bool core0, bool core1, int rel0,
+                                                  int rel1, int zrel, const T (&ca)[7], const T (&cb)[7]) {
+  const T *__restrict__ Y = (const T *)d.y;
+  const T *__restrict__ Xo = (const T *)d.xold;
+  const T *__restrict__ Zo = (const T *)d.zold;
+  T *__restrict__ Xn = (T *)d.xout;
+  T *__restrict__ Zn = (T *)d.zout;
+  const int ps = d.ps, rs = d.rs;
+  const int tx = threadIdx.x, ty = threadIdx.y;
+  const uint32_t apres = d.a.present, bpres = d.b.present;
+  const int amode = d.a.mode, bmode = d.b.mode;
+  const int qbeg = HAS_I ? max(i0 - 1, 0) : 0, qend = HAS_I ? i1 : 0;
+  StarTaps<T, HAS_I> r0, r1;
+  auto xmask = [&](int q, uint32_t mjk) { return ai[q - i0 + 1] & mjk; };
+  auto prefetch = [&](int q) {
+    const uint32_t m0 = xmask(q, mjk0);
+    if ((m0 & (kArray | kRegion)) == (kArray | kRegion)) r0.load_masked(Y + (q * ps + rel0), ps, rs, m0 & apres);
+    if (has1) {
+      const uint32_t m1 = xmask(q, mjk1);
+      if ((m1 & (kArray | kRegion)) == (kArray | kRegion)) r1.load_masked(Y + (q * ps + rel1), ps, rs, m1 & apres);
+    }
+  };
+  auto xpoint = [&](const StarTaps<T, HAS_I> &r, uint32_t m, int off, bool own, bool core) -> T {
+    if (!(m & kArray)) return T(0);
+    T v;
+    if (m & kRegion) {
+      const bool base = amode == 0 || (amode == 2 && !(m & kClear));
+      v = r.dot(ca, base ? Xo[off] : T(0));
+    } else {
+      v = Xo[off];
+    }
+    if (own && core && d.xwrite && !(m & kDead)) Xn[off] = v;
+    return v;
+  };
+  prefetch(qbeg);
+  for (int q = qbeg; q <= qend; ++q) {
+    // X(q) exists only inside the local array; the Z plane that would read
+    // X(d0) at the array end has that tap masked off by b's predicates
+    if (q < d.d0) {
+      const int slot = q & 3;
+      const bool own = q >= i0 && q < i1;
+      const T v0 = xpoint(r0, xmask(q, mjk0), q * ps + rel0, own, core0);
+      xs[slot][hj0][hk0] = v0;
+      if (has1) {
+        const T v1 = xpoint(r1, xmask(q, mjk1), q * ps + rel1, own, core1);
+        xs[slot][hj1][hk1] = v1;
+      }
+      if (q < qend && q + 1 < d.d0) prefetch(q + 1);
+    }
+    __syncthreads();
+    const int i = HAS_I ? q - 1 : q;
+    if (i >= i0 && i < i1) {
+      const uint32_t m = bi[i - i0] & mzjk;
+      if (m & kArray) {
+        const int off = i * ps + zrel;
+        T w;
+        if (m & kRegion) {
+          const bool base = bmode == 0 || (bmode == 2 && !(m & kClear));
+          w = base ? Zo[off] : T(0);
+          const uint32_t on = bpres & m;
+          const int sc = i & 3, sm = (i - 1) & 3, sp = (i + 1) & 3;
+          w += (on & 1u) ? cb[0] * xs[sc][ty + 1][tx + 1] : T(0);
+          if (HAS_I) {
+            w += (on & 2u) ? cb[1] * xs[sm][ty + 1][tx + 1] : T(0);
+            w += (on & 4u) ? cb[2] * xs[sp][ty + 1][tx + 1] : T(0);
+          }
+          w += (on & 8u) ? cb[3] * xs[sc][ty][tx + 1] : T(0);
+          w += (on & 16u) ? cb[4] * xs[sc][ty + 2][tx + 1] : T(0);
+          w += (on & 32u) ? cb[5] * xs[sc][ty + 1][tx] : T(0);
+          w += (on & 64u) ? cb[6] * xs[sc][ty + 1][tx + 2] : T(0);
+        } else {
+          w = Zo[off];
+        }
+        Zn[off] = w;
+      }
+    }
+  }
+}
+
 template <typename T>
 __global__ void __launch_bounds__(kPX *kPY, 2) star_pair_kernel(const __grid_constant__ StarPairDev d) {
   constexpr int HX = kPX + 2, HW = (kPY + 2) * HX, NT = kPX * kPY;
@@ -215,12 +314,7 @@ __global__ void __launch_bounds__(kPX *kPY, 2) star_pair_kernel(const __grid_con
     }
   }
   __syncthreads();
-  const T *__restrict__ Y = (const T *)d.y;
-  const T *__restrict__ Xo = (const T *)d.xold;
-  const T *__restrict__ Zo = (const T *)d.zold;
-  T *Xn = (T *)d.xout;
-  T *Zn = (T *)d.zout;
-  const int ps = d.ps, rs = d.rs;
+  const int rs = d.rs;
   T ca[7], cb[7];
 #pragma unroll
   for (int p = 0; p < 7; ++p) {
@@ -261,62 +355,12 @@ __global__ void __launch_bounds__(kPX *kPY, 2) star_pair_kernel(const __grid_con
       return;
     }
   }
-  for (int q = i0 - 1; q <= i1; ++q) {
-    const int slot = (q + 3) % 3;
-    if (q >= 0 && q < d.d0) {
-      const uint32_t mi = ai[q - i0 + 1];
-      const bool own = q >= i0 && q < i1 && d.xwrite;
-      {
-        const uint32_t m = mi & mjk0;
-        T v = T(0);
-        if (m & kArray) {
-          const int off = q * ps + rel0;
-          v = star_x_point<T>(d, Y, Xo, ca, apres, m, off, ps, rs);
-          if (own && core0 && !(m & kDead)) Xn[off] = v;
-        }
-        xs[slot][hj0][hk0] = v;
-      }
-      if (has1) {
-        const uint32_t m = mi & mjk1;
-        T v = T(0);
-        if (m & kArray) {
-          const int off = q * ps + rel1;
-          v = star_x_point<T>(d, Y, Xo, ca, apres, m, off, ps, rs);
-          if (own && core1 && !(m & kDead)) Xn[off] = v;
-        }
-        xs[slot][hj1][hk1] = v;
-      }
-    }
-    __syncthreads();
-    const int i = q - 1;
-    if (i >= i0 && i < i1) {
-      const uint32_t m = bi[i - i0] & mzjk;
-      if (m & kArray) {
-        const int off = i * ps + zrel;
-        T w;
-        if (m & kRegion) {
-          w = (d.b.mode == 0 || (d.b.mode == 2 && !(m & kClear))) ? Zo[off] : T(0);
-          const int sc = (i + 3) % 3, sm = (i + 2) % 3, sp = (i + 4) % 3;
-          T t[7];
-          t[0] = xs[sc][ty + 1][tx + 1];
-          t[1] = xs[sm][ty + 1][tx + 1];
-          t[2] = xs[sp][ty + 1][tx + 1];
-          t[3] = xs[sc][ty][tx + 1];
-          t[4] = xs[sc][ty + 2][tx + 1];
-          t[5] = xs[sc][ty + 1][tx];
-          t[6] = xs[sc][ty + 1][tx + 2];
-          const uint32_t on = bpres & m;
-#pragma unroll
-          for (int e = 0; e < 7; ++e)
-            if ((on >> e) & 1) w += cb[e] * t[e];
-        } else {
-          w = Zo[off];
-        }
-        Zn[off] = w;
-      }
-    }
-    __syncthreads();
-  }
+  if (d.d0 > 1)
+    star_pair_checked<T, true>(d, xs, ai, bi, i0, i1, mjk0, mjk1, mzjk, hj0, hk0, hj1, hk1, has1, core0, core1, rel0,
+                               rel1, zrel, ca, cb);
+  else
+    star_pair_checked<T, false>(d, xs, ai, bi, i0, i1, mjk0, mjk1, mzjk, hj0, hk0, hj1, hk1, has1, core0, core1,
+                                rel0, rel1, zrel, ca, cb);
 }
 
 static int fill_star_op(StarOpDev &o, const gfb_star_op &s, int pad) {

@@ -30,7 +30,7 @@ def require_cuda():
 
 class Executable:
     def __init__(self, low: Lowering, inputs: dict, outputs: dict, *, seed_buf: Buffer | None = None,
-                 device=None, use_graph: bool | None = None):
+                 device=None, use_graph: bool | None = None, pinned=(), reuse: bool | None = None):
         require_cuda()
         self.lib = L.load()
         self.low = low
@@ -44,6 +44,8 @@ class Executable:
         self.use_graph = env_graph if use_graph is None else use_graph
         self.graph = None
         self.runs = 0
+        self.pinned = list(pinned)
+        self.reuse = (os.environ.get("GFB_ARENA", "1") != "0") if reuse is None else reuse
         self._allocate()
         for op in self.ops:
             op.prepare(self)
@@ -51,12 +53,57 @@ class Executable:
     # -- memory ------------------------------------------------------------------
 
     def _allocate(self):
+        """Place every root buffer. With reuse (default), buffers that are not
+        live at the same time share one liveness-planned HBM arena (first-fit
+        over [first use, last use] intervals of the launch list); inputs,
+        outputs, the seed and explicitly pinned buffers live for the whole
+        run. ``payload_peak`` is the arena size: the device-side counterpart
+        of the planner's peak (checkpointing.py:10-17 counts intermediates,
+        gradients and kept values, not inputs or the dependent)."""
+        roots = [b for b in self.low.buffers if b.alias_of is None and b.tensor is None]
+        keep = {b.root().bid for b in list(self.inputs.values()) + list(self.outputs.values()) + self.pinned}
+        if self.seed_buf is not None:
+            keep.add(self.seed_buf.root().bid)
+        first, last = {}, {}
+        for i, op in enumerate(self.ops):
+            for b in tuple(op.reads) + tuple(op.writes):
+                r = b.root().bid
+                first.setdefault(r, i)
+                last[r] = i
         total = 0
-        for b in self.low.buffers:
-            if b.alias_of is not None or b.tensor is not None:
-                continue
-            b.tensor = torch.empty(max(b.numel, 1), dtype=TORCH_DTYPE[b.kind], device=self.device)
-            total += b.tensor.numel() * b.tensor.element_size()
+        placed = []
+        for b in roots:
+            if not self.reuse or b.bid in keep or b.bid not in first:
+                b.tensor = torch.empty(max(b.numel, 1), dtype=TORCH_DTYPE[b.kind], device=self.device)
+                total += b.tensor.numel() * b.tensor.element_size()
+            else:
+                placed.append(b)
+        # first-fit interval placement, largest first within equal start
+        placed.sort(key=lambda b: (first[b.bid], -b.nbytes))
+        live = []  # (offset, size, last)
+        arena = 0
+        offsets = {}
+        for b in placed:
+            align = 256 if b.nbytes >= 4096 else 16
+            size = (max(b.nbytes, 1) + align - 1) // align * align
+            live = [x for x in live if x[2] >= first[b.bid]]
+            live.sort()
+            off = 0
+            for o, sz, _ in live:
+                if off + size <= o:
+                    break
+                off = max(off, o + sz)
+            offsets[b.bid] = off
+            live.append((off, size, last[b.bid]))
+            arena = max(arena, off + size)
+        self.arena = torch.empty(max(arena, 256), dtype=torch.uint8, device=self.device)
+        self.keep_bids = keep
+        for b in placed:
+            o = offsets[b.bid]
+            b.tensor = self.arena[o:o + max(b.nbytes, 1) + (-max(b.nbytes, 1)) % b.itemsize].view(TORCH_DTYPE[b.kind])
+        self.payload_peak = arena
+        self.keep_bids = keep | {b.bid for b in roots if b.tensor is not None and b.bid not in offsets}
+        total += arena
         ws = 0
         for op in self.ops:
             f = getattr(op, "workspace_bytes", None)
