@@ -137,10 +137,26 @@ def roofline(exe, inputs, peak, peak_kind):
     avg_bytes = fam_b[dom] / fam_n[dom]
     achieved = avg_bytes / (avg_ms * 1e-3) / 1e9
     shares = {k: round(v / total, 4) for k, v in sorted(fam_t.items(), key=lambda kv: -kv[1])}
+    traffic, dram_frac = None, None
+    ncu = ncu_traffic().get(dom)
+    if ncu is not None:
+        # DRAM bytes per launch from the committed ncu --set full capture
+        traffic = ncu["dram_bytes_per_launch"]
+        dram_frac = round(traffic / (avg_ms * 1e-3) / 1e9 / peak, 4)
     return {"bound": "hbm", "kernel": dom, "achieved": round(achieved, 1), "peak": peak, "peak_kind": peak_kind,
-            "unit": "GB/s", "frac": round(achieved / peak, 4), "traffic": None,
+            "unit": "GB/s", "frac": round(achieved / peak, 4), "traffic": traffic, "dram_frac": dram_frac,
             "bytes_per_launch": int(avg_bytes), "avg_launch_ms": round(avg_ms, 5), "launches_per_step": fam_n[dom],
-            "step_share": shares}
+            "step_share": shares,
+            "note": "bytes_per_launch = SURVEY 8(d) algorithmic bytes of the sweeps one launch performs "
+                    "(a fused star_pair launch performs two sweeps); traffic = measured DRAM bytes per launch"}
+
+
+def ncu_traffic():
+    path = os.path.join(REPO, "profiles", "ncu_traffic.json")
+    if os.path.exists(path):
+        with open(path) as f:
+            return json.load(f)
+    return {}
 
 
 def cpu_baseline_stencil(name, params):

@@ -28,6 +28,43 @@ def require_cuda():
         raise EngineError("the B200 engine needs a CUDA device; none is visible (no CPU fallback)")
 
 
+def plan_arena(ops, roots, keep, to_end=frozenset()):
+    """Liveness-planned placement of the non-pinned root buffers in one arena:
+    live interval = [first, last] launch index touching the buffer (aliases
+    and views count for their root); greedy first-fit by interval start.
+    Returns ({bid: byte offset}, arena bytes)."""
+    first, last = {}, {}
+    for i, op in enumerate(ops):
+        for b in tuple(op.reads) + tuple(op.writes):
+            r = b.root().bid
+            first.setdefault(r, i)
+            last[r] = i
+    for r in to_end:  # results: live from first write until read back after the run
+        if r in first:
+            last[r] = len(ops)
+    # scalars stay outside (the planner counts them as free, checkpointing.py:10-17)
+    placed = [b for b in roots if b.bid not in keep and b.bid in first and b.shape != ()]
+    # largest first, each at the lowest offset free over its whole interval
+    placed.sort(key=lambda b: (-b.nbytes, first[b.bid]))
+    done = []  # (offset, size, first, last)
+    arena = 0
+    offsets = {}
+    for b in placed:
+        align = 256 if b.nbytes >= 4096 else 16
+        size = (max(b.nbytes, 1) + align - 1) // align * align
+        f, l = first[b.bid], last[b.bid]
+        busy = sorted((o, sz) for o, sz, bf, bl in done if bf <= l and f <= bl)
+        off = 0
+        for o, sz in busy:
+            if off + size <= o:
+                break
+            off = max(off, (o + sz + align - 1) // align * align)
+        offsets[b.bid] = off
+        done.append((off, size, f, l))
+        arena = max(arena, off + size)
+    return offsets, arena
+
+
 class Executable:
     def __init__(self, low: Lowering, inputs: dict, outputs: dict, *, seed_buf: Buffer | None = None,
                  device=None, use_graph: bool | None = None, pinned=(), reuse: bool | None = None):
@@ -61,48 +98,24 @@ class Executable:
         of the planner's peak (checkpointing.py:10-17 counts intermediates,
         gradients and kept values, not inputs or the dependent)."""
         roots = [b for b in self.low.buffers if b.alias_of is None and b.tensor is None]
-        keep = {b.root().bid for b in list(self.inputs.values()) + list(self.outputs.values()) + self.pinned}
+        keep = {b.root().bid for b in list(self.inputs.values()) + self.pinned}
         if self.seed_buf is not None:
             keep.add(self.seed_buf.root().bid)
-        first, last = {}, {}
-        for i, op in enumerate(self.ops):
-            for b in tuple(op.reads) + tuple(op.writes):
-                r = b.root().bid
-                first.setdefault(r, i)
-                last[r] = i
+        outs = {b.root().bid for b in self.outputs.values()}
+        offsets, arena = plan_arena(self.ops, roots, keep, outs) if self.reuse else ({}, 0)
         total = 0
-        placed = []
+        placed = [b for b in roots if b.bid in offsets]
         for b in roots:
-            if not self.reuse or b.bid in keep or b.bid not in first:
+            if b.bid not in offsets:
                 b.tensor = torch.empty(max(b.numel, 1), dtype=TORCH_DTYPE[b.kind], device=self.device)
                 total += b.tensor.numel() * b.tensor.element_size()
-            else:
-                placed.append(b)
-        # first-fit interval placement, largest first within equal start
-        placed.sort(key=lambda b: (first[b.bid], -b.nbytes))
-        live = []  # (offset, size, last)
-        arena = 0
-        offsets = {}
-        for b in placed:
-            align = 256 if b.nbytes >= 4096 else 16
-            size = (max(b.nbytes, 1) + align - 1) // align * align
-            live = [x for x in live if x[2] >= first[b.bid]]
-            live.sort()
-            off = 0
-            for o, sz, _ in live:
-                if off + size <= o:
-                    break
-                off = max(off, o + sz)
-            offsets[b.bid] = off
-            live.append((off, size, last[b.bid]))
-            arena = max(arena, off + size)
         self.arena = torch.empty(max(arena, 256), dtype=torch.uint8, device=self.device)
         self.keep_bids = keep
         for b in placed:
             o = offsets[b.bid]
             b.tensor = self.arena[o:o + max(b.nbytes, 1) + (-max(b.nbytes, 1)) % b.itemsize].view(TORCH_DTYPE[b.kind])
         self.payload_peak = arena
-        self.keep_bids = keep | {b.bid for b in roots if b.tensor is not None and b.bid not in offsets}
+        self.keep_bids = keep | outs | {b.bid for b in roots if b.tensor is not None and b.bid not in offsets}
         total += arena
         ws = 0
         for op in self.ops:

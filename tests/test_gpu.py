@@ -248,8 +248,8 @@ def test_slab_decomposition_kernels_in_lockstep(world):
 @pytest.mark.parametrize("cid", sorted(c for c in IDX["plans"] if "tight" in c or "floor" in c))
 def test_planned_device_payload_respects_the_budget(cid):
     """Device memory of a planned run: the liveness arena (intermediates,
-    gradients, kept values; the planner's accounting excludes inputs and the
-    dependent, checkpointing.py:10-17) plus the gradient outputs stays within
+    gradients including the results, kept values; the planner's accounting
+    excludes inputs and the dependent, checkpointing.py:10-17) stays within
     the plan's modelled peak t* <= budget."""
     from paper_2509_02197_b200 import api
 
@@ -259,7 +259,8 @@ def test_planned_device_payload_respects_the_budget(cid):
     api.clear_cache()
     run_planned(pb, inputs, meta["params"])
     exe = next(iter(api._CACHE.values()))
-    grad_bytes = sum(exe.outputs[k].nbytes for k in exe.outputs if k.startswith("grad:"))
     limit = pb.report["limit_bytes"]
-    used = exe.payload_peak + grad_bytes
-    assert used <= meta["t_star"] * 1.05 + 4096, (used, meta["t_star"], limit)
+    used = exe.payload_peak  # arena holds intermediates, gradients (incl. results), kept values
+    assert used <= meta["t_star"], (used, meta["t_star"], limit)
+    if limit is not None:
+        assert used <= limit
