@@ -13,80 +13,11 @@
 // Positions: 0 centre, 1 (-1,0,0), 2 (+1,0,0), 3 (0,-1,0), 4 (0,+1,0),
 // 5 (0,0,-1), 6 (0,0,+1) on a row-major [d0][d1][d2] array (rank 2 arrays
 // are padded with d0 = 1).
-#include "gfb_common.cuh"
 #include "gfb_internal.h"
+#include "star_common.cuh"
 
 namespace gfb {
 
-constexpr int kPX = 32, kPY = 16, kPM = 16;  // tile (k, j), planes per CTA; 512 threads
-
-struct StarOpDev {
-  double coef[7];
-  int32_t present;  // bit p: a tap at position p
-  int32_t masked;   // bit p: the tap has a mask box
-  int32_t mode;     // base: 0 old[y], 1/3 zero, 2 zero inside clear box else old[y]
-  int32_t _pad;
-  int32_t mlo[7][3], mhi[7][3];
-  int32_t lo[3], hi[3];
-  int32_t clo[3], chi[3];
-};
-
-struct StarPairDev {
-  int32_t d0, d1, d2;   // local extents
-  int32_t p0, gd0;      // global index of local plane 0, global extent of dim 0
-  int32_t zlo, zhi;     // local planes to produce
-  int32_t xwrite;  // write X back (outside the dead box)
-  int32_t ps, rs;  // plane / row strides (arrays < 2^31 elements)
-  StarOpDev a, b;
-  const void *y;      // source of a
-  const void *xold;   // old X (base of a, value outside a's region)
-  void *xout;         // X write-back target (ping-pong)
-  const void *zold;   // old Z (base of b, value outside b's region)
-  void *zout;         // Z target
-  int32_t dlo[3], dhi[3];  // dead box of X (not written back)
-};
-
-// Per-coordinate predicate bits. For a point (i, j, k) the predicate word is
-// M0[i] & M1[j] & M2[k]: bits 0..6 = tap p's mask box admits the point,
-// bit 7 = inside the op's region, bit 8 = inside its clear box, bit 9 = in
-// the dead box (op a only), bit 10 = inside the array.
-enum : uint32_t { kRegion = 1u << 7, kClear = 1u << 8, kDead = 1u << 9, kArray = 1u << 10 };
-
-__device__ __forceinline__ uint32_t coord_bits(const StarOpDev &o, int dim, int c, int extent, const int32_t *dlo,
-                                               const int32_t *dhi) {
-  uint32_t b = 0;
-#pragma unroll
-  for (int p = 0; p < 7; ++p) {
-    bool ok = !((o.masked >> p) & 1) || (c >= o.mlo[p][dim] && c < o.mhi[p][dim]);
-    b |= (uint32_t)ok << p;
-  }
-  if (c >= o.lo[dim] && c < o.hi[dim]) b |= kRegion;
-  if (c >= o.clo[dim] && c < o.chi[dim]) b |= kClear;
-  if (dlo && c >= dlo[dim] && c < dhi[dim]) b |= kDead;
-  if (c >= 0 && c < extent) b |= kArray;
-  return b;
-}
-
-template <typename T>
-__device__ __forceinline__ T star_x_point(const StarPairDev &d, const T *__restrict__ Y, const T *__restrict__ Xo,
-                                          const T (&ca)[7], uint32_t apres, uint32_t m, int off, int ps, int rs) {
-  if (!(m & kRegion)) return Xo[off];
-  T acc = (d.a.mode == 0 || (d.a.mode == 2 && !(m & kClear))) ? Xo[off] : T(0);
-  const int doff[7] = {0, -ps, ps, -rs, rs, -1, 1};
-  T t[7];
-#pragma unroll
-  for (int e = 0; e < 7; ++e) t[e] = (((apres & m) >> e) & 1) ? __ldg(Y + off + doff[e]) : T(0);
-#pragma unroll
-  for (int e = 0; e < 7; ++e) acc += ca[e] * t[e];
-  return acc;
-}
-
-// Interior fast path of one CTA: compile-time full stars, no predicates.
-// HAS_I: rank-3 arrays (taps along dim 0); rank-2 arrays have one plane.
-// X planes live in a 4-slot ring, so one barrier per plane suffices (the
-// slot written for plane q+1 was last read by Z(q-3+1) before the previous
-// barrier), and the global loads of the next plane are issued before the
-// barrier so they overlap it and the Z stage.
 template <typename T, bool HAS_I>
 struct StarTaps {
   T v[7];
@@ -278,42 +209,11 @@ __global__ void __launch_bounds__(kPX *kPY, 2) star_pair_kernel(const __grid_con
   constexpr int HX = kPX + 2, HW = (kPY + 2) * HX, NT = kPX * kPY;
   __shared__ T xs[4][kPY + 2][HX];
   __shared__ uint32_t aj[kPY + 2], ak[HX], bj[kPY], bk[kPX], ai[kPM + 2], bi[kPM];
+  __shared__ uint32_t s_and_a, s_or_a, s_and_b, s_or_b;
   const int tx = threadIdx.x, ty = threadIdx.y, tid = ty * kPX + tx;
   const int k0 = blockIdx.x * kPX, j0 = blockIdx.y * kPY;
   const int i0 = d.zlo + blockIdx.z * kPM, i1 = min(i0 + kPM, d.zhi);
-  // per-coordinate predicate words, once per CTA
-  if (tid < kPY + 2) aj[tid] = coord_bits(d.a, 1, j0 - 1 + tid, d.d1, d.dlo, d.dhi);
-  if (tid >= 32 && tid < 32 + HX) ak[tid - 32] = coord_bits(d.a, 2, k0 - 1 + (tid - 32), d.d2, d.dlo, d.dhi);
-  if (tid >= 96 && tid < 96 + kPY) bj[tid - 96] = coord_bits(d.b, 1, j0 + (tid - 96), d.d1, nullptr, nullptr);
-  if (tid >= 128 && tid < 128 + kPX) bk[tid - 128] = coord_bits(d.b, 2, k0 + (tid - 128), d.d2, nullptr, nullptr);
-  if (tid >= 192 && tid < 192 + kPM + 2)
-    ai[tid - 192] = coord_bits(d.a, 0, i0 - 1 + (tid - 192) + d.p0, d.gd0, d.dlo, d.dhi);
-  if (tid >= 224 && tid < 224 + kPM) bi[tid - 224] = coord_bits(d.b, 0, i0 + (tid - 224) + d.p0, d.gd0, nullptr, nullptr);
-  __shared__ uint32_t s_and_a, s_or_a, s_and_b, s_or_b;
-  if (tid == 0) {
-    s_and_a = s_and_b = 0xffffffffu;
-    s_or_a = s_or_b = 0u;
-  }
-  __syncthreads();
-  // block-uniform summary: AND / OR of the predicate words over the CTA's
-  // window (a: halo window of X, b: core of Z) -> interior fast path
-  {
-    const int na = min(i1 + 1, d.d0) - max(i0 - 1, 0);
-    uint32_t wa = 0xffffffffu, oa = 0u, wb = 0xffffffffu, ob = 0u;
-    if (tid < kPY + 2) { wa &= aj[tid]; oa |= aj[tid]; }
-    if (tid < HX) { wa &= ak[tid]; oa |= ak[tid]; }
-    if (tid < na) { const uint32_t v = ai[max(i0 - 1, 0) - (i0 - 1) + tid]; wa &= v; oa |= v; }
-    if (tid < kPY) { wb &= bj[tid]; ob |= bj[tid]; }
-    if (tid < kPX) { wb &= bk[tid]; ob |= bk[tid]; }
-    if (tid < i1 - i0) { wb &= bi[tid]; ob |= bi[tid]; }
-    if (tid < 64) {
-      atomicAnd(&s_and_a, wa);
-      atomicOr(&s_or_a, oa);
-      atomicAnd(&s_and_b, wb);
-      atomicOr(&s_or_b, ob);
-    }
-  }
-  __syncthreads();
+  star_prologue(d, i0, i1, tid, aj, ak, bj, bk, ai, bi, s_and_a, s_or_a, s_and_b, s_or_b);
   const int rs = d.rs;
   T ca[7], cb[7];
 #pragma unroll
@@ -362,6 +262,9 @@ __global__ void __launch_bounds__(kPX *kPY, 2) star_pair_kernel(const __grid_con
     star_pair_checked<T, false>(d, xs, ai, bi, i0, i1, mjk0, mjk1, mzjk, hj0, hk0, hj1, hk1, has1, core0, core1,
                                 rel0, rel1, zrel, ca, cb);
 }
+
+bool star_tma_usable(const StarPairDev &d, int dtype);
+int launch_star_pair_tma(const StarPairDev &d, int dtype, dim3 grid, cudaStream_t st);
 
 static int fill_star_op(StarOpDev &o, const gfb_star_op &s, int pad) {
   o.present = s.present;
@@ -431,6 +334,7 @@ extern "C" int gfb_star_pair_launch(const gfb_star_pair_desc *s, void *stream) {
   dim3 block(kPX, kPY);
   dim3 grid((unsigned)ceil_div(d.d2, kPX), (unsigned)ceil_div(d.d1, kPY), (unsigned)ceil_div(d.zhi - d.zlo, kPM));
   cudaStream_t st = (cudaStream_t)stream;
+  if (star_tma_usable(d, s->dtype)) return launch_star_pair_tma(d, s->dtype, grid, st);
   if (s->dtype == GFB_F64)
     star_pair_kernel<double><<<grid, block, 0, st>>>(d);
   else
