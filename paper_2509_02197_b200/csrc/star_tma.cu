@@ -16,8 +16,9 @@
 namespace gfb {
 
 constexpr int YK = kPX + 4, YJ = kPY + 4;  // Y window: halo 2 in (j, k)
-constexpr int kDist = 4;                    // planes in flight ahead of use
-constexpr int NSY = kDist + 3;              // Y ring slots
+constexpr int kDist = 5;                    // planes in flight ahead of use
+constexpr int NSY = kDist + 3;              // Y ring slots (8: index by mask)
+static_assert((NSY & (NSY - 1)) == 0, "Y ring must be a power of two");
 
 __device__ __forceinline__ uint32_t smem_u32(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
 
@@ -84,13 +85,13 @@ __device__ __forceinline__ void star_tma_body(const CUtensorMap *ymap, const Sta
   const int yhi = HAS_I ? min(min(qend, d.d0 - 1) + 1, d.d0 - 1) : 0;
   constexpr uint32_t kTx = (uint32_t)(YJ * YK * sizeof(T));
   auto issue = [&](int p) {
-    const int r = p - ylo, slot = r % NSY;
+    const int r = p - ylo, slot = r & (NSY - 1);
     mbar_expect_tx(&mbar[slot], kTx);
     tma_load_3d(&ys[slot][0][0], ymap, &mbar[slot], k0 - 2, j0 - 2, p);
   };
   auto wait_plane = [&](int p) {
     const int r = p - ylo;
-    mbar_wait(&mbar[r % NSY], (uint32_t)((r / NSY) & 1));
+    mbar_wait(&mbar[r & (NSY - 1)], (uint32_t)((r / NSY) & 1));
   };
   if (tid == 0) {
     for (int s = 0; s < NSY; ++s) mbar_init(&mbar[s], 1);
@@ -163,6 +164,74 @@ __device__ __forceinline__ void star_tma_body(const CUtensorMap *ymap, const Sta
     return v;
   };
 
+  if (fast && !xbase_f && !zbase_f && !xw_f) {
+    // Interior CTA of a timestep whose bases vanish and whose intermediate is
+    // not written back here (both jacobi / heat timesteps away from the
+    // array boundary): the whole plane loop is shared-memory arithmetic plus
+    // one coalesced store per output point.
+    constexpr int YS = YJ * YK, XS = (kPY + 2) * (kPX + 2);
+    const T *ysf = &ys[0][0][0];
+    T *xsf = &xs[0][0][0];
+    const int yo0 = (hj0 + 1) * YK + hk0 + 1, yo1 = (hj1 + 1) * YK + hk1 + 1;
+    const int xo0 = hj0 * HX + hk0, xo1 = hj1 * HX + hk1;
+    const int zo = (ty + 1) * HX + tx + 1;
+    const T a0 = ca[0], a1 = ca[1], a2 = ca[2], a3 = ca[3], a4 = ca[4], a5 = ca[5], a6 = ca[6];
+    const T b0 = cb[0], b1 = cb[1], b2 = cb[2], b3 = cb[3], b4 = cb[4], b5 = cb[5], b6 = cb[6];
+    T *zp = Zn + (int64_t)(qbeg - 1) * ps + zrel;
+    for (int q = qbeg; q <= qend; ++q) {
+      if (tid == 0) {
+        const int pn = q + 1 + kDist;
+        if (pn > pre_hi && pn <= yhi) {
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+          issue(pn);
+        }
+      }
+      if (HAS_I && q + 1 <= yhi && q + 1 > qbeg) wait_plane(q + 1);
+      const int r = q - ylo;
+      const T *yc = ysf + (r & (NSY - 1)) * YS;
+      const T *ym = ysf + ((r - 1) & (NSY - 1)) * YS;
+      const T *yp = ysf + ((r + 1) & (NSY - 1)) * YS;
+      T *xw = xsf + (q & 3) * XS;
+      {
+        const T *c = yc + yo0;
+        T acc = a0 * c[0];
+        if (HAS_I) acc = fma(a1, ym[yo0], fma(a2, yp[yo0], acc));
+        acc = fma(a3, c[-YK], acc);
+        acc = fma(a4, c[YK], acc);
+        acc = fma(a5, c[-1], acc);
+        acc = fma(a6, c[1], acc);
+        xw[xo0] = acc;
+      }
+      if (has1) {
+        const T *c = yc + yo1;
+        T acc = a0 * c[0];
+        if (HAS_I) acc = fma(a1, ym[yo1], fma(a2, yp[yo1], acc));
+        acc = fma(a3, c[-YK], acc);
+        acc = fma(a4, c[YK], acc);
+        acc = fma(a5, c[-1], acc);
+        acc = fma(a6, c[1], acc);
+        xw[xo1] = acc;
+      }
+      __syncthreads();
+      if (!HAS_I || q >= i0 + 1) {  // Z(i) for i = q - 1 in [i0, i1)
+        const int i = HAS_I ? q - 1 : q;
+        const T *xc = xsf + (i & 3) * XS + zo;
+        T w = b0 * xc[0];
+        if (HAS_I) {
+          const T *xm = xsf + ((i - 1) & 3) * XS + zo;
+          const T *xp = xsf + ((i + 1) & 3) * XS + zo;
+          w = fma(b1, xm[0], fma(b2, xp[0], w));
+        }
+        w = fma(b3, xc[-HX], w);
+        w = fma(b4, xc[HX], w);
+        w = fma(b5, xc[-1], w);
+        w = fma(b6, xc[1], w);
+        zp[HAS_I ? 0 : ps] = w;
+      }
+      zp += ps;
+    }
+    return;
+  }
   for (int q = qbeg; q <= qend; ++q) {
     if (q < d.d0) {
       if (tid == 0) {

@@ -196,6 +196,12 @@ def decompose(lw, plan: SlabPlan, comm) -> DistLowered:
     return DistLowered(low, inputs, outputs, seed, plan)
 
 
+def torch_empty_pinned(t):
+    import torch
+
+    return torch.empty(t.shape, dtype=t.dtype, pin_memory=True)
+
+
 class SlabEngine:
     """One rank of a slab-decomposed gradient (bench.py under torchrun)."""
 
@@ -230,6 +236,27 @@ class SlabEngine:
 
     def check(self):
         self.exe.check()
+
+    def gradient(self, host_local_inputs: dict, seed=1.0):
+        """End-to-end call on this rank: H2D of the local slabs, the run,
+        D2H of the value and of the owned planes of every gradient."""
+        from .api import GradientResult
+
+        self.exe.run(host_local_inputs, seed)
+        value = self.exe.output_host("value")
+        lo, hi = self.plan.own_local
+        grads = {}
+        for key in self.exe.outputs:
+            if key.startswith("grad:"):
+                t = self.exe.output(key)[lo:hi]
+                h = torch_empty_pinned(t)
+                h.copy_(t, non_blocking=True)
+                grads[key[5:]] = h
+        import torch
+
+        torch.cuda.current_stream(self.device).synchronize()
+        return GradientResult(value=value, grads={k: v.numpy() for k, v in grads.items()}, forward=None,
+                              backward=None, bundle=None)
 
     def own_grad(self, name: str):
         g = self.exe.output("grad:" + name)
