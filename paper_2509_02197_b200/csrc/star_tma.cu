@@ -57,6 +57,9 @@ __host__ __device__ constexpr size_t star_tma_smem_bytes() {
   return (size_t)NSY * YJ * YK * sizeof(T) + (size_t)4 * (kPY + 2) * (kPX + 2) * sizeof(T) + NSY * sizeof(uint64_t);
 }
 
+constexpr int kTT = kPX * kPY / 2;  // 256 threads: each owns two Z rows (ty, ty + 8)
+constexpr int kXP = 3;              // halo-window X points per thread per plane (612 over 256)
+
 template <typename T, bool HAS_I>
 __device__ __forceinline__ void star_tma_body(const CUtensorMap *ymap, const StarPairDev &d, T (*ys)[YJ][YK],
                                               T (*xs)[kPY + 2][kPX + 2], uint64_t *mbar, const uint32_t *aj,
@@ -65,7 +68,8 @@ __device__ __forceinline__ void star_tma_body(const CUtensorMap *ymap, const Sta
                                               uint32_t aB, int i0, int i1) {
   const int tx = threadIdx.x, ty = threadIdx.y, tid = ty * kPX + tx;
   const int k0 = blockIdx.x * kPX, j0 = blockIdx.y * kPY;
-  constexpr int HX = kPX + 2, HW = (kPY + 2) * HX, NT = kPX * kPY;
+  constexpr int HX = kPX + 2, HW = (kPY + 2) * HX;
+  constexpr int YS = YJ * YK, XS = (kPY + 2) * HX;
   const T *__restrict__ Xo = (const T *)d.xold;
   const T *__restrict__ Zo = (const T *)d.zold;
   T *__restrict__ Xn = (T *)d.xout;
@@ -101,84 +105,92 @@ __device__ __forceinline__ void star_tma_body(const CUtensorMap *ymap, const Sta
   const int pre_hi = min(ylo + kDist + 1, yhi);
   if (tid == 0)
     for (int p = ylo; p <= pre_hi; ++p) issue(p);
-  // thread -> halo-window points (at most two per plane)
-  const int hj0 = tid / HX, hk0 = tid - hj0 * HX;
-  const int p1 = tid + NT;
-  const bool has1 = p1 < HW;
-  const int hj1 = p1 / HX, hk1 = p1 - hj1 * HX;
-  const uint32_t mjk0 = aj[hj0] & ak[hk0];
-  const uint32_t mjk1 = has1 ? (aj[hj1] & ak[hk1]) : 0u;
-  const bool core0 = hj0 >= 1 && hj0 <= kPY && hk0 >= 1 && hk0 <= kPX;
-  const bool core1 = has1 && hj1 >= 1 && hj1 <= kPY && hk1 >= 1 && hk1 <= kPX;
-  const int rel0 = (j0 - 1 + hj0) * rs + (k0 - 1 + hk0);
-  const int rel1 = (j0 - 1 + hj1) * rs + (k0 - 1 + hk1);
-  const uint32_t mzjk = bj[ty] & bk[tx];
-  const int zrel = (j0 + ty) * rs + (k0 + tx);
+  // thread -> halo-window X points p = tid + m * kTT (m < kXP, p < HW)
+  int hj[kXP], hk[kXP], yo[kXP], xo[kXP], rel[kXP];
+  bool has[kXP], core[kXP];
+  uint32_t mjk[kXP];
+#pragma unroll
+  for (int m = 0; m < kXP; ++m) {
+    const int p = tid + m * kTT;
+    has[m] = p < HW;
+    hj[m] = has[m] ? p / HX : 0;
+    hk[m] = has[m] ? p - hj[m] * HX : 0;
+    yo[m] = (hj[m] + 1) * YK + hk[m] + 1;
+    xo[m] = hj[m] * HX + hk[m];
+    rel[m] = (j0 - 1 + hj[m]) * rs + (k0 - 1 + hk[m]);
+    core[m] = has[m] && hj[m] >= 1 && hj[m] <= kPY && hk[m] >= 1 && hk[m] <= kPX;
+    mjk[m] = has[m] ? (aj[hj[m]] & ak[hk[m]]) : 0u;
+  }
+  // Z rows ty and ty + 8
+  const int zrel0 = (j0 + ty) * rs + (k0 + tx), zrel1 = zrel0 + 8 * rs;
+  const int zo0 = (ty + 1) * HX + tx + 1, zo1 = zo0 + 8 * HX;
+  const uint32_t mz0 = bj[ty] & bk[tx], mz1 = bj[ty + 8] & bk[tx];
   const bool xbase_f = amode == 0 || (amode == 2 && !(aA & kClear));
   const bool zbase_f = bmode == 0 || (bmode == 2 && !(aB & kClear));
   const bool xw_f = d.xwrite && !(aA & kDead);
   for (int p = ylo; p <= min(qbeg, yhi); ++p) wait_plane(p);
-
-  // one X point from the Y ring
-  auto xpoint = [&](int q, int hj, int hk, uint32_t m, int rel, bool core, bool own) -> T {
-    const int off = q * ps + rel;
-    const int sc = (q - ylo) % NSY;
-    const T *yc = &ys[sc][hj + 1][hk + 1];
-    if (fast) {
-      T acc = xbase_f ? Xo[off] : T(0);
-      acc += ca[0] * yc[0];
-      if (HAS_I) {
-        const int sm = (q - 1 - ylo) % NSY, sp = (q + 1 - ylo) % NSY;
-        acc += ca[1] * ys[sm][hj + 1][hk + 1];
-        acc += ca[2] * ys[sp][hj + 1][hk + 1];
-      }
-      acc += ca[3] * yc[-YK];
-      acc += ca[4] * yc[YK];
-      acc += ca[5] * yc[-1];
-      acc += ca[6] * yc[1];
-      if (own && core && xw_f) Xn[off] = acc;
-      return acc;
-    }
-    if (!(m & kArray)) return T(0);
-    T v;
-    if (m & kRegion) {
-      const bool base = amode == 0 || (amode == 2 && !(m & kClear));
-      T acc = base ? Xo[off] : T(0);
-      const uint32_t on = apres & m;
-      acc += (on & 1u) ? ca[0] * yc[0] : T(0);
-      if (HAS_I) {
-        // planes outside [ylo, yhi] are never filled: their taps are masked
-        const int sm = (q - 1 - ylo + NSY) % NSY, sp = (q + 1 - ylo) % NSY;
-        acc += (on & 2u) ? ca[1] * ys[sm][hj + 1][hk + 1] : T(0);
-        acc += (on & 4u) ? ca[2] * ys[sp][hj + 1][hk + 1] : T(0);
-      }
-      acc += (on & 8u) ? ca[3] * yc[-YK] : T(0);
-      acc += (on & 16u) ? ca[4] * yc[YK] : T(0);
-      acc += (on & 32u) ? ca[5] * yc[-1] : T(0);
-      acc += (on & 64u) ? ca[6] * yc[1] : T(0);
-      v = acc;
-    } else {
-      v = Xo[off];
-    }
-    if (own && core && d.xwrite && !(m & kDead)) Xn[off] = v;
-    return v;
-  };
+  const T *ysf = &ys[0][0][0];
+  T *xsf = &xs[0][0][0];
 
   if (fast && !xbase_f && !zbase_f && !xw_f) {
-    // Interior CTA of a timestep whose bases vanish and whose intermediate is
-    // not written back here (both jacobi / heat timesteps away from the
-    // array boundary): the whole plane loop is shared-memory arithmetic plus
-    // one coalesced store per output point.
-    constexpr int YS = YJ * YK, XS = (kPY + 2) * (kPX + 2);
-    const T *ysf = &ys[0][0][0];
-    T *xsf = &xs[0][0][0];
-    const int yo0 = (hj0 + 1) * YK + hk0 + 1, yo1 = (hj1 + 1) * YK + hk1 + 1;
-    const int xo0 = hj0 * HX + hk0, xo1 = hj1 * HX + hk1;
-    const int zo = (ty + 1) * HX + tx + 1;
+    // Interior CTA: every tap admitted, bases vanish, no X write-back. The
+    // plane loop is shared-memory arithmetic plus coalesced Z stores.
     const T a0 = ca[0], a1 = ca[1], a2 = ca[2], a3 = ca[3], a4 = ca[4], a5 = ca[5], a6 = ca[6];
     const T b0 = cb[0], b1 = cb[1], b2 = cb[2], b3 = cb[3], b4 = cb[4], b5 = cb[5], b6 = cb[6];
-    T *zp = Zn + (int64_t)(qbeg - 1) * ps + zrel;
-    for (int q = qbeg; q <= qend; ++q) {
+    T *zp = Zn + (int64_t)(qbeg - 1) * ps;
+    int r = qbeg - ylo;
+    for (int q = qbeg; q <= qend; ++q, ++r, zp += ps) {
+      if (tid == 0) {
+        const int pn = q + 1 + kDist;
+        if (pn > pre_hi && pn <= yhi) {
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+          issue(pn);
+        }
+      }
+      if (HAS_I && q + 1 <= yhi && q + 1 > qbeg) wait_plane(q + 1);
+      const T *yc = ysf + (r & (NSY - 1)) * YS;
+      const T *ym = ysf + ((r - 1) & (NSY - 1)) * YS;
+      const T *yp = ysf + ((r + 1) & (NSY - 1)) * YS;
+      T *xw = xsf + (q & 3) * XS;
+#pragma unroll
+      for (int m = 0; m < kXP; ++m) {
+        if (m == kXP - 1 && !has[m]) break;
+        const T *c = yc + yo[m];
+        T acc = a0 * c[0];
+        if (HAS_I) acc = fma(a1, ym[yo[m]], fma(a2, yp[yo[m]], acc));
+        acc = fma(a3, c[-YK], acc);
+        acc = fma(a4, c[YK], acc);
+        acc = fma(a5, c[-1], acc);
+        acc = fma(a6, c[1], acc);
+        xw[xo[m]] = acc;
+      }
+      __syncthreads();
+      if (!HAS_I || q >= i0 + 1) {  // Z(i) for i = q - 1 in [i0, i1)
+        const int i = HAS_I ? q - 1 : q;
+        const T *xc = xsf + (i & 3) * XS;
+        const T *xm = xsf + ((i - 1) & 3) * XS;
+        const T *xp = xsf + ((i + 1) & 3) * XS;
+        T *zrow = HAS_I ? zp : zp + ps;
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int zo = h ? zo1 : zo0;
+          const T *c = xc + zo;
+          T w = b0 * c[0];
+          if (HAS_I) w = fma(b1, xm[zo], fma(b2, xp[zo], w));
+          w = fma(b3, c[-HX], w);
+          w = fma(b4, c[HX], w);
+          w = fma(b5, c[-1], w);
+          w = fma(b6, c[1], w);
+          zrow[h ? zrel1 : zrel0] = w;
+        }
+      }
+    }
+    return;
+  }
+
+  // boundary / general CTA: per-point predicate words, branch-free selects
+  for (int q = qbeg; q <= qend; ++q) {
+    if (q < d.d0) {
       if (tid == 0) {
         const int pn = q + 1 + kDist;
         if (pn > pre_hi && pn <= yhi) {
@@ -189,113 +201,80 @@ __device__ __forceinline__ void star_tma_body(const CUtensorMap *ymap, const Sta
       if (HAS_I && q + 1 <= yhi && q + 1 > qbeg) wait_plane(q + 1);
       const int r = q - ylo;
       const T *yc = ysf + (r & (NSY - 1)) * YS;
-      const T *ym = ysf + ((r - 1) & (NSY - 1)) * YS;
+      const T *ym = ysf + ((r - 1) & (NSY - 1)) * YS;  // never filled: taps masked
       const T *yp = ysf + ((r + 1) & (NSY - 1)) * YS;
       T *xw = xsf + (q & 3) * XS;
-      {
-        const T *c = yc + yo0;
-        T acc = a0 * c[0];
-        if (HAS_I) acc = fma(a1, ym[yo0], fma(a2, yp[yo0], acc));
-        acc = fma(a3, c[-YK], acc);
-        acc = fma(a4, c[YK], acc);
-        acc = fma(a5, c[-1], acc);
-        acc = fma(a6, c[1], acc);
-        xw[xo0] = acc;
-      }
-      if (has1) {
-        const T *c = yc + yo1;
-        T acc = a0 * c[0];
-        if (HAS_I) acc = fma(a1, ym[yo1], fma(a2, yp[yo1], acc));
-        acc = fma(a3, c[-YK], acc);
-        acc = fma(a4, c[YK], acc);
-        acc = fma(a5, c[-1], acc);
-        acc = fma(a6, c[1], acc);
-        xw[xo1] = acc;
-      }
-      __syncthreads();
-      if (!HAS_I || q >= i0 + 1) {  // Z(i) for i = q - 1 in [i0, i1)
-        const int i = HAS_I ? q - 1 : q;
-        const T *xc = xsf + (i & 3) * XS + zo;
-        T w = b0 * xc[0];
-        if (HAS_I) {
-          const T *xm = xsf + ((i - 1) & 3) * XS + zo;
-          const T *xp = xsf + ((i + 1) & 3) * XS + zo;
-          w = fma(b1, xm[0], fma(b2, xp[0], w));
-        }
-        w = fma(b3, xc[-HX], w);
-        w = fma(b4, xc[HX], w);
-        w = fma(b5, xc[-1], w);
-        w = fma(b6, xc[1], w);
-        zp[HAS_I ? 0 : ps] = w;
-      }
-      zp += ps;
-    }
-    return;
-  }
-  for (int q = qbeg; q <= qend; ++q) {
-    if (q < d.d0) {
-      if (tid == 0) {
-        const int pn = q + 1 + kDist;
-        if (pn > pre_hi && pn <= yhi) {
-          // the slot being refilled was last read (generic proxy) before
-          // the previous barrier; order those reads before the async write
-          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-          issue(pn);
-        }
-      }
-      if (HAS_I && q + 1 <= yhi && q + 1 > qbeg) wait_plane(q + 1);
-      const int slot = q & 3;
       const bool own = q >= i0 && q < i1;
       const uint32_t mi = ai[q - i0 + 1];
-      xs[slot][hj0][hk0] = xpoint(q, hj0, hk0, mi & mjk0, rel0, core0, own);
-      if (has1) xs[slot][hj1][hk1] = xpoint(q, hj1, hk1, mi & mjk1, rel1, core1, own);
+#pragma unroll
+      for (int m = 0; m < kXP; ++m) {
+        if (!has[m]) continue;
+        const uint32_t mm = mi & mjk[m];
+        T v = T(0);
+        if (mm & kArray) {
+          const int off = q * ps + rel[m];
+          if (mm & kRegion) {
+            const bool base = amode == 0 || (amode == 2 && !(mm & kClear));
+            T acc = base ? Xo[off] : T(0);
+            const uint32_t on = apres & mm;
+            const T *c = yc + yo[m];
+            acc += (on & 1u) ? ca[0] * c[0] : T(0);
+            if (HAS_I) {
+              acc += (on & 2u) ? ca[1] * ym[yo[m]] : T(0);
+              acc += (on & 4u) ? ca[2] * yp[yo[m]] : T(0);
+            }
+            acc += (on & 8u) ? ca[3] * c[-YK] : T(0);
+            acc += (on & 16u) ? ca[4] * c[YK] : T(0);
+            acc += (on & 32u) ? ca[5] * c[-1] : T(0);
+            acc += (on & 64u) ? ca[6] * c[1] : T(0);
+            v = acc;
+          } else {
+            v = Xo[off];
+          }
+          if (own && core[m] && d.xwrite && !(mm & kDead)) Xn[off] = v;
+        }
+        xw[xo[m]] = v;
+      }
     }
     __syncthreads();
     const int i = HAS_I ? q - 1 : q;
     if (i >= i0 && i < i1) {
-      const int off = i * ps + zrel;
-      const int sc = i & 3, sm = (i - 1) & 3, sp = (i + 1) & 3;
-      if (fast) {
-        T w = zbase_f ? Zo[off] : T(0);
-        w += cb[0] * xs[sc][ty + 1][tx + 1];
-        if (HAS_I) {
-          w += cb[1] * xs[sm][ty + 1][tx + 1];
-          w += cb[2] * xs[sp][ty + 1][tx + 1];
-        }
-        w += cb[3] * xs[sc][ty][tx + 1];
-        w += cb[4] * xs[sc][ty + 2][tx + 1];
-        w += cb[5] * xs[sc][ty + 1][tx];
-        w += cb[6] * xs[sc][ty + 1][tx + 2];
-        Zn[off] = w;
-      } else {
-        const uint32_t m = bi[i - i0] & mzjk;
-        if (m & kArray) {
-          T w;
-          if (m & kRegion) {
-            const bool base = bmode == 0 || (bmode == 2 && !(m & kClear));
-            w = base ? Zo[off] : T(0);
-            const uint32_t on = bpres & m;
-            w += (on & 1u) ? cb[0] * xs[sc][ty + 1][tx + 1] : T(0);
-            if (HAS_I) {
-              w += (on & 2u) ? cb[1] * xs[sm][ty + 1][tx + 1] : T(0);
-              w += (on & 4u) ? cb[2] * xs[sp][ty + 1][tx + 1] : T(0);
-            }
-            w += (on & 8u) ? cb[3] * xs[sc][ty][tx + 1] : T(0);
-            w += (on & 16u) ? cb[4] * xs[sc][ty + 2][tx + 1] : T(0);
-            w += (on & 32u) ? cb[5] * xs[sc][ty + 1][tx] : T(0);
-            w += (on & 64u) ? cb[6] * xs[sc][ty + 1][tx + 2] : T(0);
-          } else {
-            w = Zo[off];
+      const T *xc = xsf + (i & 3) * XS;
+      const T *xm = xsf + ((i - 1) & 3) * XS;
+      const T *xp = xsf + ((i + 1) & 3) * XS;
+      const uint32_t mi = bi[i - i0];
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const uint32_t m = mi & (h ? mz1 : mz0);
+        if (!(m & kArray)) continue;
+        const int off = i * ps + (h ? zrel1 : zrel0);
+        T w;
+        if (m & kRegion) {
+          const bool base = bmode == 0 || (bmode == 2 && !(m & kClear));
+          w = base ? Zo[off] : T(0);
+          const uint32_t on = bpres & m;
+          const int zo = h ? zo1 : zo0;
+          const T *c = xc + zo;
+          w += (on & 1u) ? cb[0] * c[0] : T(0);
+          if (HAS_I) {
+            w += (on & 2u) ? cb[1] * xm[zo] : T(0);
+            w += (on & 4u) ? cb[2] * xp[zo] : T(0);
           }
-          Zn[off] = w;
+          w += (on & 8u) ? cb[3] * c[-HX] : T(0);
+          w += (on & 16u) ? cb[4] * c[HX] : T(0);
+          w += (on & 32u) ? cb[5] * c[-1] : T(0);
+          w += (on & 64u) ? cb[6] * c[1] : T(0);
+        } else {
+          w = Zo[off];
         }
+        Zn[off] = w;
       }
     }
   }
 }
 
 template <typename T>
-__global__ void __launch_bounds__(kPX *kPY, 2)
+__global__ void __launch_bounds__(kTT, 3)
     star_pair_tma_kernel(const __grid_constant__ CUtensorMap ymap, const __grid_constant__ StarPairDev d) {
   extern __shared__ __align__(128) unsigned char smem[];
   T(*ys)[YJ][YK] = reinterpret_cast<T(*)[YJ][YK]>(smem);
@@ -350,7 +329,7 @@ int launch_star_pair_tma(const StarPairDev &d, int dtype, dim3 grid, cudaStream_
                            CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return set_error(GFB_ECUDA, "cuTensorMapEncodeTiled failed for the star-pair source");
-  dim3 block(kPX, kPY);
+  dim3 block(kPX, kPY / 2);
   if (dtype == GFB_F64) {
     static bool attr = false;
     const size_t sm = star_tma_smem_bytes<double>();
