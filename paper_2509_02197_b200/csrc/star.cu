@@ -272,12 +272,40 @@ static int fill_star_op(StarOpDev &o, const gfb_star_op &s, int pad) {
   o.mode = s.mode;
   for (int p = 0; p < 7; ++p) {
     o.coef[p] = s.coef[p];
+    o.fcoef[p] = (float)s.coef[p];
     for (int r = 0; r < 3; ++r) {
       bool padded = r < pad;
       o.mlo[p][r] = padded ? -(1 << 30) : (int32_t)s.mlo[p][r - pad];
       o.mhi[p][r] = padded ? (1 << 30) : (int32_t)s.mhi[p][r - pad];
     }
   }
+  // detect the source-mask form of the tap masks (host side, once per launch)
+  static const int kDelta[7][3] = {{0, 0, 0}, {-1, 0, 0}, {1, 0, 0}, {0, -1, 0}, {0, 1, 0}, {0, 0, -1}, {0, 0, 1}};
+  o.srcmask = s.masked == 0 ? 0 : 1;
+  bool first = true;
+  for (int p = 0; p < 7 && o.srcmask == 1; ++p) {
+    if (!((s.present >> p) & 1)) continue;
+    if (!((s.masked >> p) & 1)) {
+      o.srcmask = -1;
+      break;
+    }
+    for (int r = 0; r < 3; ++r) {
+      const int32_t lo = o.mlo[p][r] + (r < pad ? 0 : kDelta[p][r]);
+      const int32_t hi = o.mhi[p][r] + (r < pad ? 0 : kDelta[p][r]);
+      if (first) {
+        o.smlo[r] = lo;
+        o.smhi[r] = hi;
+      } else if (o.smlo[r] != lo || o.smhi[r] != hi) {
+        o.srcmask = -1;
+      }
+    }
+    first = false;
+  }
+  if (o.srcmask != 1)
+    for (int r = 0; r < 3; ++r) {
+      o.smlo[r] = -(1 << 30);
+      o.smhi[r] = 1 << 30;
+    }
   for (int r = 0; r < 3; ++r) {
     bool padded = r < pad;
     o.lo[r] = padded ? 0 : (int32_t)s.lo[r - pad];
@@ -334,7 +362,9 @@ extern "C" int gfb_star_pair_launch(const gfb_star_pair_desc *s, void *stream) {
   dim3 block(kPX, kPY);
   dim3 grid((unsigned)ceil_div(d.d2, kPX), (unsigned)ceil_div(d.d1, kPY), (unsigned)ceil_div(d.zhi - d.zlo, kPM));
   cudaStream_t st = (cudaStream_t)stream;
-  if (star_tma_usable(d, s->dtype)) return launch_star_pair_tma(d, s->dtype, grid, st);
+  // the TMA kernel runs masks as data (source-mask form); general masks use the L1 kernel
+  if (d.a.srcmask >= 0 && d.b.srcmask >= 0 && star_tma_usable(d, s->dtype))
+    return launch_star_pair_tma(d, s->dtype, grid, st);
   if (s->dtype == GFB_F64)
     star_pair_kernel<double><<<grid, block, 0, st>>>(d);
   else

@@ -16,6 +16,11 @@ struct StarOpDev {
   int32_t mlo[7][3], mhi[7][3];
   int32_t lo[3], hi[3];
   int32_t clo[3], chi[3];
+  // source mask: every masked tap p admits y iff y + e_p lies in [smlo, smhi)
+  // (the form the adjoint gather produces: "source point inside the map box")
+  int32_t srcmask;  // 0: taps unmasked, 1: source-mask form, -1: general masks
+  int32_t smlo[3], smhi[3];
+  float fcoef[7];   // coef rounded to fp32 (fp32 kernels)
 };
 
 struct StarPairDev {
@@ -37,7 +42,7 @@ struct StarPairDev {
 // M0[i] & M1[j] & M2[k]: bits 0..6 = tap p's mask box admits the point,
 // bit 7 = inside the op's region, bit 8 = inside its clear box, bit 9 = in
 // the dead box (op a only), bit 10 = inside the array.
-enum : uint32_t { kRegion = 1u << 7, kClear = 1u << 8, kDead = 1u << 9, kArray = 1u << 10 };
+enum : uint32_t { kRegion = 1u << 7, kClear = 1u << 8, kDead = 1u << 9, kArray = 1u << 10, kSrcB = 1u << 11 };
 
 __device__ __forceinline__ uint32_t coord_bits(const StarOpDev &o, int dim, int c, int extent, const int32_t *dlo,
                                                const int32_t *dhi) {
@@ -85,12 +90,16 @@ __device__ __forceinline__ void star_prologue(const StarPairDev &d, int i0, int 
   constexpr int HX = kPX + 2;
   const int k0 = blockIdx.x * kPX, j0 = blockIdx.y * kPY;
   // per-coordinate predicate words, once per CTA
-  if (tid < kPY + 2) aj[tid] = coord_bits(d.a, 1, j0 - 1 + tid, d.d1, d.dlo, d.dhi);
-  if (tid >= 32 && tid < 32 + HX) ak[tid - 32] = coord_bits(d.a, 2, k0 - 1 + (tid - 32), d.d2, d.dlo, d.dhi);
+  // op-a words carry kSrcB: the X point lies in op b's source mask
+  auto srcb = [&](int dim, int c) { return (c >= d.b.smlo[dim] && c < d.b.smhi[dim]) ? kSrcB : 0u; };
+  if (tid < kPY + 2) aj[tid] = coord_bits(d.a, 1, j0 - 1 + tid, d.d1, d.dlo, d.dhi) | srcb(1, j0 - 1 + tid);
+  if (tid >= 32 && tid < 32 + HX)
+    ak[tid - 32] = coord_bits(d.a, 2, k0 - 1 + (tid - 32), d.d2, d.dlo, d.dhi) | srcb(2, k0 - 1 + (tid - 32));
   if (tid >= 96 && tid < 96 + kPY) bj[tid - 96] = coord_bits(d.b, 1, j0 + (tid - 96), d.d1, nullptr, nullptr);
   if (tid >= 128 && tid < 128 + kPX) bk[tid - 128] = coord_bits(d.b, 2, k0 + (tid - 128), d.d2, nullptr, nullptr);
   if (tid >= 192 && tid < 192 + kPM + 2)
-    ai[tid - 192] = coord_bits(d.a, 0, i0 - 1 + (tid - 192) + d.p0, d.gd0, d.dlo, d.dhi);
+    ai[tid - 192] = coord_bits(d.a, 0, i0 - 1 + (tid - 192) + d.p0, d.gd0, d.dlo, d.dhi) |
+                    srcb(0, i0 - 1 + (tid - 192) + d.p0);
   if (tid >= 224 && tid < 224 + kPM) bi[tid - 224] = coord_bits(d.b, 0, i0 + (tid - 224) + d.p0, d.gd0, nullptr, nullptr);
   if (tid == 0) {
     s_and_a = s_and_b = 0xffffffffu;

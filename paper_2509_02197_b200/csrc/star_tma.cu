@@ -10,15 +10,27 @@
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
+#include <type_traits>
+
 #include "gfb_internal.h"
 #include "star_common.cuh"
 
 namespace gfb {
 
-constexpr int YK = kPX + 4, YJ = kPY + 4;  // Y window: halo 2 in (j, k)
-constexpr int kDist = 5;                    // planes in flight ahead of use
-constexpr int NSY = kDist + 3;              // Y ring slots (8: index by mask)
+// Y window: halo 2 in (j, k). The row pitch is padded so that a column of
+// the window (the edge X points) spreads over more shared-memory banks; the
+// TMA box inner extent must stay a multiple of 16 bytes.
+constexpr int YJ = kPY + 4;
+template <typename T>
+__host__ __device__ constexpr int ypitch() {
+  return sizeof(T) == 8 ? kPX + 6 : kPX + 4;
+}
+constexpr int kDist = 5;        // planes in flight ahead of use
+constexpr int NSY = kDist + 3;  // Y ring slots (8: index by mask)
 static_assert((NSY & (NSY - 1)) == 0, "Y ring must be a power of two");
+constexpr int HX = kPX + 2;           // X~ window pitch (halo 1)
+constexpr int XS = (kPY + 2) * HX;    // X~ window plane
+constexpr int kTT = kPX * kPY / 2;    // 256 threads: each owns two adjacent Z rows
 
 __device__ __forceinline__ uint32_t smem_u32(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
 
@@ -52,46 +64,67 @@ __device__ __forceinline__ void tma_load_3d(void *dst, const CUtensorMap *map, u
       : "memory");
 }
 
+// ring slot stride (elements): TMA destinations must be 128-byte aligned
+template <typename T>
+__host__ __device__ constexpr int yslot() {
+  return (int)(((size_t)YJ * ypitch<T>() * sizeof(T) + 127) / 128 * 128 / sizeof(T));
+}
 template <typename T>
 __host__ __device__ constexpr size_t star_tma_smem_bytes() {
-  return (size_t)NSY * YJ * YK * sizeof(T) + (size_t)4 * (kPY + 2) * (kPX + 2) * sizeof(T) + NSY * sizeof(uint64_t);
+  return (size_t)NSY * yslot<T>() * sizeof(T) + (size_t)4 * XS * sizeof(T) + NSY * sizeof(uint64_t);
 }
 
-constexpr int kTT = kPX * kPY / 2;  // 256 threads: each owns two Z rows (ty, ty + 8)
-constexpr int kXP = 3;              // halo-window X points per thread per plane (612 over 256)
+template <typename T>
+__device__ __forceinline__ T coef(const StarOpDev &o, int p);
+template <>
+__device__ __forceinline__ double coef<double>(const StarOpDev &o, int p) {
+  return o.coef[p];
+}
+template <>
+__device__ __forceinline__ float coef<float>(const StarOpDev &o, int p) {
+  return o.fcoef[p];
+}
 
+// One CTA: a (kPY x kPX) column of Z over planes [i0, i1), marching along
+// dim 0. Per plane q: X(q) = a(Y) on the CTA's halo window, then Z(q - 1) =
+// b(X). Thread (tx, ty) owns the Z points (2ty, tx), (2ty + 1, tx) and the X
+// points at the same positions, so the dim-0 taps of both sweeps and the
+// shared j-neighbour come from registers rolled along the march; only the
+// remaining in-plane neighbours are shared-memory loads. Warps 0..3 also
+// compute one point each of the X halo ring (rows 0 / kPY + 1, columns
+// 0 / kPX + 1). Shared-memory wavefronts, not HBM, bound this kernel, so
+// every load removed here is time.
+//
+// Masks are data: op a's taps are in source-mask form (every masked tap
+// reads "source inside M_a"), so values outside M_a are zeroed in the Y ring
+// once per plane and every tap runs unmasked; op b's source mask is applied
+// when X is stored (X~ = X inside M_b, else 0). Points whose region / base /
+// write-back status differs from the CTA's common case take a fix-up branch.
 template <typename T, bool HAS_I>
-__device__ __forceinline__ void star_tma_body(const CUtensorMap *ymap, const StarPairDev &d, T (*ys)[YJ][YK],
-                                              T (*xs)[kPY + 2][kPX + 2], uint64_t *mbar, const uint32_t *aj,
-                                              const uint32_t *ak, const uint32_t *bj, const uint32_t *bk,
-                                              const uint32_t *ai, const uint32_t *bi, bool fast, uint32_t aA,
-                                              uint32_t aB, int i0, int i1) {
+__device__ __forceinline__ void star_tma_body(const CUtensorMap *ymap, const StarPairDev &d, T *ys, T *xs,
+                                              uint64_t *mbar, const uint32_t *aj, const uint32_t *ak,
+                                              const uint32_t *bj, const uint32_t *bk, const uint32_t *ai,
+                                              const uint32_t *bi, int i0, int i1) {
+  constexpr int YK = ypitch<T>();
+  constexpr int YS = YJ * YK, YSS = yslot<T>();
   const int tx = threadIdx.x, ty = threadIdx.y, tid = ty * kPX + tx;
   const int k0 = blockIdx.x * kPX, j0 = blockIdx.y * kPY;
-  constexpr int HX = kPX + 2, HW = (kPY + 2) * HX;
-  constexpr int YS = YJ * YK, XS = (kPY + 2) * HX;
   const T *__restrict__ Xo = (const T *)d.xold;
   const T *__restrict__ Zo = (const T *)d.zold;
   T *__restrict__ Xn = (T *)d.xout;
   T *__restrict__ Zn = (T *)d.zout;
   const int ps = d.ps, rs = d.rs;
-  T ca[7], cb[7];
-#pragma unroll
-  for (int p = 0; p < 7; ++p) {
-    ca[p] = (T)d.a.coef[p];
-    cb[p] = (T)d.b.coef[p];
-  }
-  const uint32_t apres = d.a.present, bpres = d.b.present;
   const int amode = d.a.mode, bmode = d.b.mode;
   // planes: X(q) for q in [qbeg, min(qend, d0 - 1)], Y needed on [ylo, yhi]
   const int qbeg = HAS_I ? max(i0 - 1, 0) : 0, qend = HAS_I ? i1 : 0;
   const int ylo = HAS_I ? max(qbeg - 1, 0) : 0;
   const int yhi = HAS_I ? min(min(qend, d.d0 - 1) + 1, d.d0 - 1) : 0;
-  constexpr uint32_t kTx = (uint32_t)(YJ * YK * sizeof(T));
+  constexpr uint32_t kTx = (uint32_t)(YS * sizeof(T));
+  auto slot_of = [&](int p) { return ys + ((p - ylo) & (NSY - 1)) * YSS; };
   auto issue = [&](int p) {
-    const int r = p - ylo, slot = r & (NSY - 1);
-    mbar_expect_tx(&mbar[slot], kTx);
-    tma_load_3d(&ys[slot][0][0], ymap, &mbar[slot], k0 - 2, j0 - 2, p);
+    const int sl = (p - ylo) & (NSY - 1);
+    mbar_expect_tx(&mbar[sl], kTx);
+    tma_load_3d(ys + sl * YSS, ymap, &mbar[sl], k0 - 2, j0 - 2, p);
   };
   auto wait_plane = [&](int p) {
     const int r = p - ylo;
@@ -105,91 +138,128 @@ __device__ __forceinline__ void star_tma_body(const CUtensorMap *ymap, const Sta
   const int pre_hi = min(ylo + kDist + 1, yhi);
   if (tid == 0)
     for (int p = ylo; p <= pre_hi; ++p) issue(p);
-  // thread -> halo-window X points p = tid + m * kTT (m < kXP, p < HW)
-  int hj[kXP], hk[kXP], yo[kXP], xo[kXP], rel[kXP];
-  bool has[kXP], core[kXP];
-  uint32_t mjk[kXP];
-#pragma unroll
-  for (int m = 0; m < kXP; ++m) {
-    const int p = tid + m * kTT;
-    has[m] = p < HW;
-    hj[m] = has[m] ? p / HX : 0;
-    hk[m] = has[m] ? p - hj[m] * HX : 0;
-    yo[m] = (hj[m] + 1) * YK + hk[m] + 1;
-    xo[m] = hj[m] * HX + hk[m];
-    rel[m] = (j0 - 1 + hj[m]) * rs + (k0 - 1 + hk[m]);
-    core[m] = has[m] && hj[m] >= 1 && hj[m] <= kPY && hk[m] >= 1 && hk[m] <= kPX;
-    mjk[m] = has[m] ? (aj[hj[m]] & ak[hk[m]]) : 0u;
-  }
-  // Z rows ty and ty + 8
-  const int zrel0 = (j0 + ty) * rs + (k0 + tx), zrel1 = zrel0 + 8 * rs;
-  const int zo0 = (ty + 1) * HX + tx + 1, zo1 = zo0 + 8 * HX;
-  const uint32_t mz0 = bj[ty] & bk[tx], mz1 = bj[ty + 8] & bk[tx];
-  const bool xbase_f = amode == 0 || (amode == 2 && !(aA & kClear));
-  const bool zbase_f = bmode == 0 || (bmode == 2 && !(aB & kClear));
-  const bool xw_f = d.xwrite && !(aA & kDead);
-  for (int p = ylo; p <= min(qbeg, yhi); ++p) wait_plane(p);
-  const T *ysf = &ys[0][0][0];
-  T *xsf = &xs[0][0][0];
 
-  if (fast && !xbase_f && !zbase_f && !xw_f) {
-    // Interior CTA: every tap admitted, bases vanish, no X write-back. The
-    // plane loop is shared-memory arithmetic plus coalesced Z stores.
-    const T a0 = ca[0], a1 = ca[1], a2 = ca[2], a3 = ca[3], a4 = ca[4], a5 = ca[5], a6 = ca[6];
-    const T b0 = cb[0], b1 = cb[1], b2 = cb[2], b3 = cb[3], b4 = cb[4], b5 = cb[5], b6 = cb[6];
-    T *zp = Zn + (int64_t)(qbeg - 1) * ps;
-    int r = qbeg - ylo;
-    for (int q = qbeg; q <= qend; ++q, ++r, zp += ps) {
-      if (tid == 0) {
-        const int pn = q + 1 + kDist;
-        if (pn > pre_hi && pn <= yhi) {
-          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-          issue(pn);
-        }
-      }
-      if (HAS_I && q + 1 <= yhi && q + 1 > qbeg) wait_plane(q + 1);
-      const T *yc = ysf + (r & (NSY - 1)) * YS;
-      const T *ym = ysf + ((r - 1) & (NSY - 1)) * YS;
-      const T *yp = ysf + ((r + 1) & (NSY - 1)) * YS;
-      T *xw = xsf + (q & 3) * XS;
-#pragma unroll
-      for (int m = 0; m < kXP; ++m) {
-        if (m == kXP - 1 && !has[m]) break;
-        const T *c = yc + yo[m];
-        T acc = a0 * c[0];
-        if (HAS_I) acc = fma(a1, ym[yo[m]], fma(a2, yp[yo[m]], acc));
-        acc = fma(a3, c[-YK], acc);
-        acc = fma(a4, c[YK], acc);
-        acc = fma(a5, c[-1], acc);
-        acc = fma(a6, c[1], acc);
-        xw[xo[m]] = acc;
-      }
-      __syncthreads();
-      if (!HAS_I || q >= i0 + 1) {  // Z(i) for i = q - 1 in [i0, i1)
-        const int i = HAS_I ? q - 1 : q;
-        const T *xc = xsf + (i & 3) * XS;
-        const T *xm = xsf + ((i - 1) & 3) * XS;
-        const T *xp = xsf + ((i + 1) & 3) * XS;
-        T *zrow = HAS_I ? zp : zp + ps;
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          const int zo = h ? zo1 : zo0;
-          const T *c = xc + zo;
-          T w = b0 * c[0];
-          if (HAS_I) w = fma(b1, xm[zo], fma(b2, xp[zo], w));
-          w = fma(b3, c[-HX], w);
-          w = fma(b4, c[HX], w);
-          w = fma(b5, c[-1], w);
-          w = fma(b6, c[1], w);
-          zrow[h ? zrel1 : zrel0] = w;
-        }
+  // this thread's points (window coordinates: X~ halo 1, Y halo 2)
+  const int hj0 = 2 * ty + 1, hk = tx + 1;
+  int rj = -1, rk = 0;  // halo-ring X point
+  if (ty == 0) {
+    rj = 0;
+    rk = hk;
+  } else if (ty == 1) {
+    rj = kPY + 1;
+    rk = hk;
+  } else if (ty == 2 && tx < kPY + 2) {
+    rj = tx;
+    rk = 0;
+  } else if (ty == 3 && tx < kPY + 2) {
+    rj = tx;
+    rk = kPX + 1;
+  }
+  const bool ring = rj >= 0;
+  const int yo0 = (hj0 + 1) * YK + hk + 1, yo1 = yo0 + YK;
+  const int yor = ring ? (rj + 1) * YK + rk + 1 : yo0;
+  const int xo0 = hj0 * HX + hk, xo1 = xo0 + HX;
+  const int xor_ = ring ? rj * HX + rk : xo0;
+  const int rel0 = (j0 + 2 * ty) * rs + (k0 + tx), rel1 = rel0 + rs;
+  const int relr = (j0 - 1 + rj) * rs + (k0 - 1 + rk);
+  const uint32_t mx0 = aj[hj0] & ak[hk], mx1 = aj[hj0 + 1] & ak[hk];
+  const uint32_t mxr = ring ? (aj[rj] & ak[rk]) : 0u;
+  const uint32_t mz0 = bj[2 * ty] & bk[tx], mz1 = bj[2 * ty + 1] & bk[tx];
+
+  const bool ysrc = d.a.srcmask == 1;
+  const bool yj_in = j0 - 2 >= d.a.smlo[1] && j0 + kPY + 2 <= d.a.smhi[1];
+  const bool yk_in = k0 - 2 >= d.a.smlo[2] && k0 + kPX + 2 <= d.a.smhi[2];
+  auto prepare_plane = [&](int p) {
+    // zero what the taps must not see: planes never loaded (outside the
+    // local array) and, in source-mask form, values outside M_a
+    T *slot = slot_of(p);
+    const int pg = p + d.p0;
+    const bool outside = p < 0 || p >= d.d0 || (ysrc && (pg < d.a.smlo[0] || pg >= d.a.smhi[0]));
+    if (outside) {
+      for (int e = tid; e < YS; e += kTT) slot[e] = T(0);
+    } else if (ysrc && !(yj_in && yk_in)) {
+      for (int e = tid; e < YS; e += kTT) {
+        const int jj = e / YK, kk = e - jj * YK;
+        const int j = j0 - 2 + jj, k = k0 - 2 + kk;
+        if (j < d.a.smlo[1] || j >= d.a.smhi[1] || k < d.a.smlo[2] || k >= d.a.smhi[2]) slot[e] = T(0);
       }
     }
-    return;
+  };
+  // common-case predicate patterns (block-uniform)
+  const uint32_t xmask = kArray | kRegion | (amode == 2 ? kClear : 0u) | (d.xwrite ? kDead : 0u);
+  const uint32_t xval = amode == 0 ? 0xffffffffu : xmask;  // mode 0: base always added -> fix-up
+  const uint32_t zmask = kArray | kRegion | (bmode == 2 ? kClear : 0u);
+  const uint32_t zval = bmode == 0 ? 0xffffffffu : zmask;
+  // X~ of one point from its tap sum; abnormal points take the fix-up
+  auto x_tilde = [&](T acc, uint32_t w, int rel, bool wb, int q) -> T {
+    if ((w & xmask) != xval) {
+      if (!(w & kArray)) {
+        acc = T(0);
+      } else {
+        const int off = q * ps + rel;
+        if (!(w & kRegion))
+          acc = Xo[off];
+        else if (amode == 0 || (amode == 2 && !(w & kClear)))
+          acc += Xo[off];
+        if (wb && d.xwrite && !(w & kDead)) Xn[off] = acc;
+      }
+    }
+    return (w & kSrcB) ? acc : T(0);
+  };
+  const T a0 = coef<T>(d.a, 0), a1 = coef<T>(d.a, 1), a2 = coef<T>(d.a, 2), a3 = coef<T>(d.a, 3),
+          a4 = coef<T>(d.a, 4), a5 = coef<T>(d.a, 5), a6 = coef<T>(d.a, 6);
+  const T b0 = coef<T>(d.b, 0), b1 = coef<T>(d.b, 1), b2 = coef<T>(d.b, 2), b3 = coef<T>(d.b, 3),
+          b4 = coef<T>(d.b, 4), b5 = coef<T>(d.b, 5), b6 = coef<T>(d.b, 6);
+
+  // CTA-uniform "every point normal" tests: AND of the (j, k) predicate
+  // words over the X window / Z tile; per plane the dim-0 word completes it
+  __shared__ uint32_t s_jk[2];
+  if (ty == 0) {
+    uint32_t va = ak[tx] & (tx < kPY + 2 ? aj[tx] : ~0u) & (tx + 32 < HX ? ak[tx + 32] : ~0u);
+    uint32_t vb = bk[tx] & (tx < kPY ? bj[tx] : ~0u);
+    va = __reduce_and_sync(0xffffffffu, va);
+    vb = __reduce_and_sync(0xffffffffu, vb);
+    if (tx == 0) {
+      s_jk[0] = va;
+      s_jk[1] = vb;
+    }
+  }
+  const uint32_t xfast_m = xmask | kSrcB;
+
+  for (int p = ylo; p <= min(qbeg + 1, yhi); ++p) wait_plane(p);
+  if (HAS_I) {
+    for (int p = qbeg - 1; p <= qbeg + 1; ++p) prepare_plane(p);
+  } else {
+    prepare_plane(0);
+  }
+  __syncthreads();
+  const uint32_t jka = (amode == 0) ? 0u : s_jk[0], jkb = (bmode == 0) ? 0u : s_jk[1];
+
+  // Registers rolled along the march, rotated by index (three live planes):
+  // y*[.] = Y centre values at the own (0, 1) and ring (r) X points,
+  // x*[.] = X~ at the own Z points. Step s of the unrolled loop finds
+  // Y(q - 1), Y(q) in slots s, s + 1 and loads Y(q + 1) into slot s + 2
+  // (mod 3); X~(q - 2), X~(q - 1) likewise and X~(q) goes to slot s + 2.
+  T y0[3], y1[3], yr[3], x0[3], x1[3];
+#pragma unroll
+  for (int u = 0; u < 3; ++u) y0[u] = y1[u] = yr[u] = x0[u] = x1[u] = T(0);
+  {
+    const T *yq = slot_of(qbeg);
+    y0[1] = yq[yo0];
+    y1[1] = yq[yo1];
+    yr[1] = yq[yor];
+    if (HAS_I) {
+      const T *yqm = slot_of(qbeg - 1);
+      y0[0] = yqm[yo0];
+      y1[0] = yqm[yo1];
+      yr[0] = yqm[yor];
+    }
   }
 
-  // boundary / general CTA: per-point predicate words, branch-free selects
-  for (int q = qbeg; q <= qend; ++q) {
+  auto step = [&](auto S, int q) {
+    constexpr int M = decltype(S)::value, C = (M + 1) % 3, P = (M + 2) % 3;
+    x0[P] = T(0);
+    x1[P] = T(0);
     if (q < d.d0) {
       if (tid == 0) {
         const int pn = q + 1 + kDist;
@@ -198,78 +268,113 @@ __device__ __forceinline__ void star_tma_body(const CUtensorMap *ymap, const Sta
           issue(pn);
         }
       }
-      if (HAS_I && q + 1 <= yhi && q + 1 > qbeg) wait_plane(q + 1);
-      const int r = q - ylo;
-      const T *yc = ysf + (r & (NSY - 1)) * YS;
-      const T *ym = ysf + ((r - 1) & (NSY - 1)) * YS;  // never filled: taps masked
-      const T *yp = ysf + ((r + 1) & (NSY - 1)) * YS;
-      T *xw = xsf + (q & 3) * XS;
-      const bool own = q >= i0 && q < i1;
+      if (HAS_I) {
+        // plane q + 2 is needed by X(q + 1): land it and mask it now; the
+        // barrier below orders this before any read of it
+        const int pn = q + 2;
+        if (pn <= yhi && pn > qbeg + 1) wait_plane(pn);
+        if (pn <= qend + 1 && pn > qbeg + 1) prepare_plane(pn);
+      }
+      const T *yc = slot_of(q);
+      const T *yp = slot_of(q + 1);
+      T *xw = xs + (q & 3) * XS;
       const uint32_t mi = ai[q - i0 + 1];
-#pragma unroll
-      for (int m = 0; m < kXP; ++m) {
-        if (!has[m]) continue;
-        const uint32_t mm = mi & mjk[m];
-        T v = T(0);
-        if (mm & kArray) {
-          const int off = q * ps + rel[m];
-          if (mm & kRegion) {
-            const bool base = amode == 0 || (amode == 2 && !(mm & kClear));
-            T acc = base ? Xo[off] : T(0);
-            const uint32_t on = apres & mm;
-            const T *c = yc + yo[m];
-            acc += (on & 1u) ? ca[0] * c[0] : T(0);
-            if (HAS_I) {
-              acc += (on & 2u) ? ca[1] * ym[yo[m]] : T(0);
-              acc += (on & 4u) ? ca[2] * yp[yo[m]] : T(0);
-            }
-            acc += (on & 8u) ? ca[3] * c[-YK] : T(0);
-            acc += (on & 16u) ? ca[4] * c[YK] : T(0);
-            acc += (on & 32u) ? ca[5] * c[-1] : T(0);
-            acc += (on & 64u) ? ca[6] * c[1] : T(0);
-            v = acc;
-          } else {
-            v = Xo[off];
-          }
-          if (own && core[m] && d.xwrite && !(mm & kDead)) Xn[off] = v;
-        }
-        xw[xo[m]] = v;
+      if (HAS_I) {
+        y0[P] = yp[yo0];
+        y1[P] = yp[yo1];
+      }
+      // short dependency chains: four partial sums per point
+      T p0 = a0 * y0[C], p1 = a0 * y1[C];
+      if (HAS_I) {
+        p0 = fma(a1, y0[M], p0);
+        p1 = fma(a1, y1[M], p1);
+      }
+      T q0 = a4 * y1[C], q1 = a3 * y0[C];
+      if (HAS_I) {
+        q0 = fma(a2, y0[P], q0);
+        q1 = fma(a2, y1[P], q1);
+      }
+      const T r0 = fma(a5, yc[yo0 - 1], a3 * yc[yo0 - YK]);
+      const T r1 = fma(a5, yc[yo1 - 1], a4 * yc[yo1 + YK]);
+      p0 = fma(a6, yc[yo0 + 1], p0);
+      p1 = fma(a6, yc[yo1 + 1], p1);
+      T acc0 = (p0 + q0) + r0, acc1 = (p1 + q1) + r1;
+      const bool fast = ((mi & jka) & xfast_m) == xfast_m;
+      if (!fast) {
+        const bool own = q >= i0 && q < i1;
+        acc0 = x_tilde(acc0, mi & mx0, rel0, own, q);
+        acc1 = x_tilde(acc1, mi & mx1, rel1, own, q);
+      }
+      x0[P] = acc0;
+      x1[P] = acc1;
+      xw[xo0] = acc0;
+      xw[xo1] = acc1;
+      if (ring) {
+        const T yrp = HAS_I ? yp[yor] : T(0);
+        T pr = a0 * yr[C];
+        if (HAS_I) pr = fma(a1, yr[M], fma(a2, yrp, pr));
+        const T qr = fma(a3, yc[yor - YK], a4 * yc[yor + YK]);
+        const T rr = fma(a5, yc[yor - 1], a6 * yc[yor + 1]);
+        T acc = (pr + qr) + rr;
+        if (!fast) acc = x_tilde(acc, mi & mxr, relr, false, q);
+        xw[xor_] = acc;
+        yr[P] = yrp;
       }
     }
     __syncthreads();
     const int i = HAS_I ? q - 1 : q;
     if (i >= i0 && i < i1) {
-      const T *xc = xsf + (i & 3) * XS;
-      const T *xm = xsf + ((i - 1) & 3) * XS;
-      const T *xp = xsf + ((i + 1) & 3) * XS;
+      const T *xc = xs + (i & 3) * XS;
+      // centre values: X~(i) and, along dim 0, X~(i -/+ 1) from registers
+      const T c0 = HAS_I ? x0[C] : x0[P], c1 = HAS_I ? x1[C] : x1[P];
+      T p0 = b0 * c0, p1 = b0 * c1;
+      if (HAS_I) {
+        p0 = fma(b1, x0[M], p0);
+        p1 = fma(b1, x1[M], p1);
+      }
+      T q0 = b4 * c1, q1 = b3 * c0;
+      if (HAS_I) {
+        q0 = fma(b2, x0[P], q0);
+        q1 = fma(b2, x1[P], q1);
+      }
+      const T r0 = fma(b5, xc[xo0 - 1], b3 * xc[xo0 - HX]);
+      const T r1 = fma(b5, xc[xo1 - 1], b4 * xc[xo1 + HX]);
+      p0 = fma(b6, xc[xo0 + 1], p0);
+      p1 = fma(b6, xc[xo1 + 1], p1);
+      T z0 = (p0 + q0) + r0, z1 = (p1 + q1) + r1;
+      T *zrow = Zn + (size_t)i * ps + rel0;
       const uint32_t mi = bi[i - i0];
+      if (((mi & jkb) & zmask) == zmask) {
+        zrow[0] = z0;
+        zrow[rs] = z1;
+      } else {
+        const T *zold = Zo + (size_t)i * ps + rel0;
 #pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const uint32_t m = mi & (h ? mz1 : mz0);
-        if (!(m & kArray)) continue;
-        const int off = i * ps + (h ? zrel1 : zrel0);
-        T w;
-        if (m & kRegion) {
-          const bool base = bmode == 0 || (bmode == 2 && !(m & kClear));
-          w = base ? Zo[off] : T(0);
-          const uint32_t on = bpres & m;
-          const int zo = h ? zo1 : zo0;
-          const T *c = xc + zo;
-          w += (on & 1u) ? cb[0] * c[0] : T(0);
-          if (HAS_I) {
-            w += (on & 2u) ? cb[1] * xm[zo] : T(0);
-            w += (on & 4u) ? cb[2] * xp[zo] : T(0);
+        for (int h = 0; h < 2; ++h) {
+          const uint32_t w = mi & (h ? mz1 : mz0);
+          T z = h ? z1 : z0;
+          const int o = h ? rs : 0;
+          if ((w & zmask) != zval) {
+            if (!(w & kArray)) continue;
+            if (!(w & kRegion))
+              z = zold[o];
+            else if (bmode == 0 || (bmode == 2 && !(w & kClear)))
+              z += zold[o];
           }
-          w += (on & 8u) ? cb[3] * c[-HX] : T(0);
-          w += (on & 16u) ? cb[4] * c[HX] : T(0);
-          w += (on & 32u) ? cb[5] * c[-1] : T(0);
-          w += (on & 64u) ? cb[6] * c[1] : T(0);
-        } else {
-          w = Zo[off];
+          zrow[o] = z;
         }
-        Zn[off] = w;
       }
     }
+  };
+  using I0 = std::integral_constant<int, 0>;
+  using I1 = std::integral_constant<int, 1>;
+  using I2 = std::integral_constant<int, 2>;
+  for (int q = qbeg; q <= qend; q += 3) {
+    step(I0{}, q);
+    if (q + 1 > qend) break;
+    step(I1{}, q + 1);
+    if (q + 2 > qend) break;
+    step(I2{}, q + 2);
   }
 }
 
@@ -277,26 +382,19 @@ template <typename T>
 __global__ void __launch_bounds__(kTT, 3)
     star_pair_tma_kernel(const __grid_constant__ CUtensorMap ymap, const __grid_constant__ StarPairDev d) {
   extern __shared__ __align__(128) unsigned char smem[];
-  T(*ys)[YJ][YK] = reinterpret_cast<T(*)[YJ][YK]>(smem);
-  T(*xs)[kPY + 2][kPX + 2] = reinterpret_cast<T(*)[kPY + 2][kPX + 2]>(smem + (size_t)NSY * YJ * YK * sizeof(T));
-  uint64_t *mbar = reinterpret_cast<uint64_t *>(smem + (size_t)NSY * YJ * YK * sizeof(T) +
-                                                (size_t)4 * (kPY + 2) * (kPX + 2) * sizeof(T));
+  constexpr size_t ybytes = (size_t)NSY * yslot<T>() * sizeof(T);
+  T *ys = reinterpret_cast<T *>(smem);
+  T *xs = reinterpret_cast<T *>(smem + ybytes);
+  uint64_t *mbar = reinterpret_cast<uint64_t *>(smem + ybytes + (size_t)4 * XS * sizeof(T));
   __shared__ uint32_t aj[kPY + 2], ak[kPX + 2], bj[kPY], bk[kPX], ai[kPM + 2], bi[kPM];
   __shared__ uint32_t s_and_a, s_or_a, s_and_b, s_or_b;
   const int tid = threadIdx.y * kPX + threadIdx.x;
   const int i0 = d.zlo + blockIdx.z * kPM, i1 = min(i0 + kPM, d.zhi);
   star_prologue(d, i0, i1, tid, aj, ak, bj, bk, ai, bi, s_and_a, s_or_a, s_and_b, s_or_b);
-  const uint32_t apres = d.a.present, bpres = d.b.present;
-  const uint32_t full = d.d0 > 1 ? 0x7fu : 0x79u;
-  const uint32_t fa = full | kRegion | kArray, fb = full | kRegion | kArray;
-  const uint32_t aA = s_and_a, oA = s_or_a, aB = s_and_b, oB = s_or_b;
-  const bool fast = apres == full && bpres == full && (aA & fa) == fa && (aB & fb) == fb &&
-                    ((aA ^ oA) & (kClear | kDead)) == 0 && ((aB ^ oB) & kClear) == 0 &&
-                    (d.d0 == 1 || (i0 >= 2 && i1 <= d.d0 - 2));
   if (d.d0 > 1)
-    star_tma_body<T, true>(&ymap, d, ys, xs, mbar, aj, ak, bj, bk, ai, bi, fast, aA, aB, i0, i1);
+    star_tma_body<T, true>(&ymap, d, ys, xs, mbar, aj, ak, bj, bk, ai, bi, i0, i1);
   else
-    star_tma_body<T, false>(&ymap, d, ys, xs, mbar, aj, ak, bj, bk, ai, bi, fast, aA, aB, i0, i1);
+    star_tma_body<T, false>(&ymap, d, ys, xs, mbar, aj, ak, bj, bk, ai, bi, i0, i1);
 }
 
 static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
@@ -322,7 +420,7 @@ int launch_star_pair_tma(const StarPairDev &d, int dtype, dim3 grid, cudaStream_
   CUtensorMap map;
   cuuint64_t dims[3] = {(cuuint64_t)d.d2, (cuuint64_t)d.d1, (cuuint64_t)d.d0};
   cuuint64_t strides[2] = {(cuuint64_t)(d.d2 * es), (cuuint64_t)((int64_t)d.d1 * d.d2 * es)};
-  cuuint32_t box[3] = {(cuuint32_t)YK, (cuuint32_t)YJ, 1};
+  cuuint32_t box[3] = {(cuuint32_t)(dtype == GFB_F64 ? ypitch<double>() : ypitch<float>()), (cuuint32_t)YJ, 1};
   cuuint32_t estr[3] = {1, 1, 1};
   CUresult r = encode_fn()(&map, dtype == GFB_F64 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32,
                            3, const_cast<void *>(d.y), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
