@@ -26,7 +26,7 @@
 extern "C" {
 #endif
 
-#define GFB_ABI_VERSION 5
+#define GFB_ABI_VERSION 6
 
 #define GFB_MAX_PARAMS 8    /* map parameters (iteration-space rank) */
 #define GFB_MAX_RANK 8      /* array rank */
@@ -241,13 +241,50 @@ typedef struct {
   int64_t global_d0;
 } gfb_star_pair_desc;
 
+/*
+ * Affine product contraction (implicit GEMM; fast path of the gather pass
+ * for wcr="sum" maps whose tasklet is a scaled product of two reads with
+ * affine subsets, e.g. convolution forward / input / weight adjoints):
+ *     D[m, n] = base(m, n) + scale * sum_k A[ta(m) + ta(k)] * B[tb(n) + tb(k)]
+ * over the flattened output coordinates split into m (those A depends on)
+ * and n (those only B depends on) and the flattened free parameters k.
+ * A product is counted only when every constraint holds:
+ *     lo[c] <= cm[c](m) + ck[c](k) < hi[c]   for c < ncm   (A side)
+ *     lo[c] <= cn[c](n) + ck[c](k) < hi[c]   for ncm <= c < ncm + ncn
+ * (pivot parameters of the reparameterised scatter staying in their box).
+ * Index tables are int32 device arrays, one entry per m / n / k:
+ *   mtab[m] = {A offset, D offset, inside clear box, cm[0..ncm)}
+ *   ntab[n] = {B offset, D offset, inside clear box, cn[0..ncn)}
+ *   ktab[k] = {A offset, B offset, ck[0..ncm+ncn)}
+ * base follows gfb_gather_desc.clear_mode (a clear-box point needs both its
+ * m and n bits). nsplit > 1 splits k; fp64 partials go to the workspace
+ * (nsplit * M * N doubles) and a second pass adds them in a fixed order.
+ */
+typedef struct {
+  int32_t dtype;
+  int32_t clear_mode;
+  int32_t ncm, ncn;
+  int32_t a_kfast;   /* A contiguous along k (else along m): load layout */
+  int32_t b_nfast;   /* B contiguous along n (else along k) */
+  int32_t nsplit;
+  int32_t mstride, nstride, kstride;  /* int32 words per table entry */
+  int64_t M, N, K;
+  double scale;
+  const void *a, *b;
+  void *d;
+  const int32_t *mtab, *ntab, *ktab;
+  int32_t lo[4], hi[4];
+  void *workspace;
+} gfb_contract_desc;
+
 /* ---- entry points --------------------------------------------------- */
 
 int gfb_abi_version(void);
 const char *gfb_last_error(void);
 int gfb_device_sm_count(void);
 /* sizes of gfb_space, gfb_operand, gfb_map_desc, gfb_term, gfb_gather_desc,
- * gfb_stencil_desc (binding layout check); returns the count written */
+ * gfb_stencil_desc, gfb_star_op, gfb_star_pair_desc, gfb_contract_desc
+ * (binding layout check); returns the count written */
 int gfb_struct_sizes(int64_t *out, int32_t cap);
 
 /* replaces Executor._exec_map / _exec_tasklet (interpreter.py:478-507, 405-426) */
@@ -257,6 +294,9 @@ int gfb_gather_launch(const gfb_gather_desc *d, void *stream);
 int64_t gfb_gather_workspace_bytes(const gfb_gather_desc *d);
 /* linear stencil fast path of _exec_map (interpreter.py:478-507) */
 int gfb_stencil_launch(const gfb_stencil_desc *d, void *stream);
+/* product-contraction fast path of the wcr="sum" scatter (interpreter.py:
+ * 422-423, 478-507): implicit GEMM over index tables */
+int gfb_contract_launch(const gfb_contract_desc *d, void *stream);
 
 /* fused forward / adjoint timestep of a radius-1 stencil program (two
  * consecutive _exec_map sweeps, interpreter.py:478-507) */

@@ -19,7 +19,7 @@ MAXCODE = 128
 MAXCONST = 24
 MAXTAPS = 32
 MAXSRCS = 4
-ABI_VERSION = 5
+ABI_VERSION = 6
 
 F32, F64 = 0, 1
 
@@ -88,6 +88,13 @@ class StarPairDesc(C.Structure):
                 ("global_d0", i64)]
 
 
+class ContractDesc(C.Structure):
+    _fields_ = [("dtype", i32), ("clear_mode", i32), ("ncm", i32), ("ncn", i32), ("a_kfast", i32),
+                ("b_nfast", i32), ("nsplit", i32), ("mstride", i32), ("nstride", i32), ("kstride", i32),
+                ("M", i64), ("N", i64), ("K", i64), ("scale", f64), ("a", vp), ("b", vp), ("d", vp),
+                ("mtab", vp), ("ntab", vp), ("ktab", vp), ("lo", i32 * 4), ("hi", i32 * 4), ("workspace", vp)]
+
+
 _LIB = None
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libgfb.so")
@@ -103,6 +110,7 @@ _SIGS = [
     ("gfb_gather_workspace_bytes", i64, [C.POINTER(GatherDesc)]),
     ("gfb_stencil_launch", i32, [C.POINTER(StencilDesc), vp]),
     ("gfb_star_pair_launch", i32, [C.POINTER(StarPairDesc), vp]),
+    ("gfb_contract_launch", i32, [C.POINTER(ContractDesc), vp]),
     ("gfb_reduce_workspace_bytes", i64, [i64]),
     ("gfb_reduce_sum", i32, [vp, i32, i64, vp, i32, i32, vp, vp]),
     ("gfb_elementwise", i32, [i32, f64, vp, i64, vp, i64, vp, i64, i32, i32, vp, vp]),
@@ -135,10 +143,10 @@ def load(path: str | None = None):
         fn.argtypes = args
     if lib.gfb_abi_version() != ABI_VERSION:
         raise EngineError(f"libgfb ABI {lib.gfb_abi_version()} != expected {ABI_VERSION}; rebuild")
-    sizes = (i64 * 8)()
-    n = lib.gfb_struct_sizes(sizes, 8)
+    sizes = (i64 * 9)()
+    n = lib.gfb_struct_sizes(sizes, 9)
     want = [C.sizeof(Space), C.sizeof(Operand), C.sizeof(MapDesc), C.sizeof(Term), C.sizeof(GatherDesc),
-            C.sizeof(StencilDesc), C.sizeof(StarOp), C.sizeof(StarPairDesc)]
+            C.sizeof(StencilDesc), C.sizeof(StarOp), C.sizeof(StarPairDesc), C.sizeof(ContractDesc)]
     got = list(sizes[:n])
     if got[: len(want)] != want:
         raise EngineError(f"struct layout mismatch between gfb.h and _lib.py: C {got} vs ctypes {want}")

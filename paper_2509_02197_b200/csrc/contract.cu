@@ -1,0 +1,226 @@
+// Affine product contraction: implicit GEMM over index tables (gfb.h,
+// gfb_contract_desc).
+//
+// Replaces the per-target free-loop of the generic gather pass (map.cu) for
+// wcr="sum" maps whose tasklet is `scale * a * b` with affine subsets — the
+// reference's convolution forward sum and the two adjoint scatters
+// (autodiff.py:962-1081 emits them; interpreter.py:422-423 accumulates them
+// point by point). Output coordinates split into m (those A depends on) and
+// n (those only B depends on); the free parameters flatten into k. Every
+// element address is a table lookup plus an add, so one CTA stages a
+// (BM x BK) slab of A and a (BK x BN) slab of B in shared memory and runs a
+// register-blocked outer product, exactly like a GEMM whose operand rows are
+// gathered. Constraints (pivot parameters of a reparameterised scatter that
+// must stay in their box) zero the staged element.
+#include <algorithm>
+
+#include "gfb_common.cuh"
+#include "gfb_internal.h"
+
+namespace gfb {
+
+template <typename T, int BM, int BN, int BK, int TM, int TN>
+__global__ void __launch_bounds__((BM / TM) * (BN / TN))
+    contract_kernel(const __grid_constant__ gfb_contract_desc d) {
+  constexpr int NX = BN / TN, NY = BM / TM, NT = NX * NY;
+  constexpr int AP = BM + 16 / (int)sizeof(T), BP = BN + 16 / (int)sizeof(T);  // 16-byte aligned rows
+  static_assert((BM * BK) % NT == 0 && (BN * BK) % NT == 0, "tile / thread mismatch");
+  __shared__ __align__(16) T As[BK][AP];
+  __shared__ __align__(16) T Bs[BK][BP];
+  __shared__ int32_t sma[BM], smc[2][BM];
+  __shared__ int32_t snb[BN], snc[2][BN];
+  __shared__ int32_t ska[BK], skb[BK], skc[4][BK];
+  const int tid = threadIdx.x;
+  const int64_t m0 = (int64_t)blockIdx.x * BM, n0 = (int64_t)blockIdx.y * BN;
+  const int ncm = d.ncm, ncn = d.ncn;
+  const int64_t M = d.M, N = d.N, K = d.K;
+  const int s = blockIdx.z;
+  const int64_t kb = K * s / d.nsplit, ke = K * (s + 1) / d.nsplit;
+  const T *__restrict__ Ag = (const T *)d.a;
+  const T *__restrict__ Bg = (const T *)d.b;
+
+  for (int i = tid; i < BM; i += NT) {
+    const int64_t m = m0 + i;
+    if (m < M) {
+      const int32_t *e = d.mtab + m * d.mstride;
+      sma[i] = e[0];
+      smc[0][i] = ncm > 0 ? e[3] : 0;
+      smc[1][i] = ncm > 1 ? e[4] : 0;
+    }
+  }
+  for (int i = tid; i < BN; i += NT) {
+    const int64_t n = n0 + i;
+    if (n < N) {
+      const int32_t *e = d.ntab + n * d.nstride;
+      snb[i] = e[0];
+      snc[0][i] = ncn > 0 ? e[3] : 0;
+      snc[1][i] = ncn > 1 ? e[4] : 0;
+    }
+  }
+
+  T acc[TM][TN];
+#pragma unroll
+  for (int i = 0; i < TM; ++i)
+#pragma unroll
+    for (int j = 0; j < TN; ++j) acc[i][j] = T(0);
+  const int tx = tid % NX, ty = tid / NX;
+
+  for (int64_t k0 = kb; k0 < ke; k0 += BK) {
+    __syncthreads();  // previous tile consumed (and the m / n tables written)
+    for (int i = tid; i < BK; i += NT) {
+      const int64_t k = k0 + i;
+      if (k < ke) {
+        const int32_t *e = d.ktab + k * d.kstride;
+        ska[i] = e[0];
+        skb[i] = e[1];
+        for (int c = 0; c < ncm + ncn; ++c) skc[c][i] = e[2 + c];
+      }
+    }
+    __syncthreads();
+    // A slab: As[kk][mm] = A(m, k) or 0
+    auto a_elem = [&](int mm, int kk) -> T {
+      const int64_t m = m0 + mm, k = k0 + kk;
+      if (m >= M || k >= ke) return T(0);
+      bool ok = true;
+      for (int c = 0; c < ncm; ++c) {
+        const int32_t v = smc[c][mm] + skc[c][kk];
+        ok &= v >= d.lo[c] && v < d.hi[c];
+      }
+      return ok ? Ag[(int64_t)sma[mm] + ska[kk]] : T(0);
+    };
+    auto b_elem = [&](int nn, int kk) -> T {
+      const int64_t n = n0 + nn, k = k0 + kk;
+      if (n >= N || k >= ke) return T(0);
+      bool ok = true;
+      for (int c = 0; c < ncn; ++c) {
+        const int32_t v = snc[c][nn] + skc[ncm + c][kk];
+        ok &= v >= d.lo[ncm + c] && v < d.hi[ncm + c];
+      }
+      return ok ? Bg[(int64_t)snb[nn] + skb[kk]] : T(0);
+    };
+    if (d.a_kfast) {
+#pragma unroll
+      for (int r = 0; r < BM * BK / NT; ++r) {
+        const int e = tid + r * NT, kk = e % BK, mm = e / BK;
+        As[kk][mm] = a_elem(mm, kk);
+      }
+    } else {
+#pragma unroll
+      for (int r = 0; r < BM * BK / NT; ++r) {
+        const int e = tid + r * NT, mm = e % BM, kk = e / BM;
+        As[kk][mm] = a_elem(mm, kk);
+      }
+    }
+    if (d.b_nfast) {
+#pragma unroll
+      for (int r = 0; r < BN * BK / NT; ++r) {
+        const int e = tid + r * NT, nn = e % BN, kk = e / BN;
+        Bs[kk][nn] = b_elem(nn, kk);
+      }
+    } else {
+#pragma unroll
+      for (int r = 0; r < BN * BK / NT; ++r) {
+        const int e = tid + r * NT, kk = e % BK, nn = e / BK;
+        Bs[kk][nn] = b_elem(nn, kk);
+      }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int kk = 0; kk < BK; ++kk) {
+      T a[TM], b[TN];
+#pragma unroll
+      for (int i = 0; i < TM; ++i) a[i] = As[kk][ty * TM + i];
+#pragma unroll
+      for (int j = 0; j < TN; ++j) b[j] = Bs[kk][tx * TN + j];
+#pragma unroll
+      for (int i = 0; i < TM; ++i)
+#pragma unroll
+        for (int j = 0; j < TN; ++j) acc[i][j] = fma(a[i], b[j], acc[i][j]);
+    }
+  }
+
+  // epilogue
+  T *__restrict__ Dg = (T *)d.d;
+#pragma unroll
+  for (int i = 0; i < TM; ++i) {
+    const int64_t m = m0 + ty * TM + i;
+    if (m >= M) continue;
+    const int32_t *me = d.mtab + m * d.mstride;
+    const int32_t dm = me[1], mclr = me[2];
+#pragma unroll
+    for (int j = 0; j < TN; ++j) {
+      const int64_t n = n0 + tx * TN + j;
+      if (n >= N) continue;
+      if (d.nsplit > 1) {
+        ((double *)d.workspace)[((int64_t)s * M + m) * N + n] = (double)acc[i][j];
+        continue;
+      }
+      const int32_t *ne = d.ntab + n * d.nstride;
+      const int64_t off = (int64_t)dm + ne[1];
+      const T v = (T)d.scale * acc[i][j];
+      T base = T(0);
+      if (d.clear_mode == 0 || (d.clear_mode == 2 && !(mclr && ne[2]))) base = Dg[off];
+      Dg[off] = base + v;
+    }
+  }
+}
+
+// split-k: fixed-order fp64 sum of the partials, then the base as above
+template <typename T>
+__global__ void contract_finish_kernel(const __grid_constant__ gfb_contract_desc d) {
+  const int64_t M = d.M, N = d.N, MN = M * N;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < MN; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t m = e / N, n = e - m * N;
+    double sum = 0.0;
+    for (int s = 0; s < d.nsplit; ++s) sum += ((const double *)d.workspace)[(int64_t)s * MN + e];
+    const int32_t *me = d.mtab + m * d.mstride, *ne = d.ntab + n * d.nstride;
+    const int64_t off = (int64_t)me[1] + ne[1];
+    T *Dg = (T *)d.d;
+    T base = T(0);
+    if (d.clear_mode == 0 || (d.clear_mode == 2 && !(me[2] && ne[2]))) base = Dg[off];
+    Dg[off] = base + (T)(d.scale * sum);
+  }
+}
+
+template <typename T, int BM, int BN, int TM, int TN>
+static void launch_contract(const gfb_contract_desc &d, cudaStream_t st) {
+  constexpr int BK = 16;
+  dim3 grid((unsigned)ceil_div(d.M, BM), (unsigned)ceil_div(d.N, BN), (unsigned)d.nsplit);
+  contract_kernel<T, BM, BN, BK, TM, TN><<<grid, (BM / TM) * (BN / TN), 0, st>>>(d);
+}
+
+template <typename T>
+static void launch_contract_t(const gfb_contract_desc &d, cudaStream_t st) {
+  // variant choice mirrored by lowering.contract_tile
+  if (d.N <= 16)
+    launch_contract<T, 128, 16, 4, 2>(d, st);
+  else if (d.N <= 32)
+    launch_contract<T, 128, 32, 4, 4>(d, st);
+  else
+    launch_contract<T, 64, 64, 4, 4>(d, st);
+  if (d.nsplit > 1) {
+    const int64_t MN = d.M * d.N;
+    const unsigned blocks = (unsigned)std::min<int64_t>(ceil_div(MN, 256), 148 * 16);
+    contract_finish_kernel<T><<<blocks, 256, 0, st>>>(d);
+  }
+}
+
+}  // namespace gfb
+
+using namespace gfb;
+
+extern "C" int gfb_contract_launch(const gfb_contract_desc *d, void *stream) {
+  if (!d || !d->a || !d->b || !d->d || !d->mtab || !d->ntab || !d->ktab || d->M <= 0 || d->N <= 0 || d->K <= 0 ||
+      d->nsplit < 1 || d->ncm < 0 || d->ncm > 2 || d->ncn < 0 || d->ncn > 2 || d->mstride < 3 + d->ncm ||
+      d->nstride < 3 + d->ncn || d->kstride < 2 + d->ncm + d->ncn)
+    return set_error(GFB_EINVAL, "gfb_contract_launch: bad descriptor");
+  if (d->nsplit > 1 && !d->workspace) return set_error(GFB_EINVAL, "gfb_contract_launch: split-k needs a workspace");
+  if (d->M > ((int64_t)1 << 40) || d->N > 65535 * 64 || d->nsplit > 65535)
+    return set_error(GFB_EINVAL, "gfb_contract_launch: extents out of range");
+  cudaStream_t st = (cudaStream_t)stream;
+  if (d->dtype == GFB_F64)
+    launch_contract_t<double>(*d, st);
+  else
+    launch_contract_t<float>(*d, st);
+  return check_launch("contract");
+}

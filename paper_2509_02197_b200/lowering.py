@@ -721,6 +721,255 @@ class CopyOp(Op):
             L.check(rt.lib.gfb_copy(self.dst.ptr, self.src.ptr, self.dst.nbytes, stream), "copy")
 
 
+def contract_tile(N: int):
+    """(BM, BN) of the contraction kernel variant gfb_contract_launch picks."""
+    if N <= 16:
+        return 128, 16
+    if N <= 32:
+        return 128, 32
+    return 64, 64
+
+
+class ContractOp(Op):
+    """Product-contraction gather as an implicit GEMM over index tables
+    (csrc/contract.cu): D[m, n] = base + scale * sum_k A[.] B[.], see gfb.h."""
+
+    family = "contract"
+    _bufs = ("a", "b", "dst")
+
+    def __init__(self, dst, a, b, scale, clear_mode, M, N, K, mtab, ntab, ktab, ncm, ncn, lo, hi, a_kfast,
+                 b_nfast, nsplit):
+        self.dst, self.a, self.b, self.scale, self.clear_mode = dst, a, b, scale, clear_mode
+        self.M, self.N, self.K = M, N, K
+        self.mtab, self.ntab, self.ktab = mtab, ntab, ktab
+        self.ncm, self.ncn, self.lo, self.hi = ncm, ncn, lo, hi
+        self.a_kfast, self.b_nfast, self.nsplit = a_kfast, b_nfast, nsplit
+        self.reads = (a, b) + ((dst,) if clear_mode in (0, 2) else ())
+        self.writes = (dst,)
+
+    def workspace_bytes(self):
+        return 0 if self.nsplit <= 1 else self.nsplit * self.M * self.N * 8
+
+    def flops(self):
+        return 2 * self.M * self.N * self.K
+
+    def prepare(self, rt):
+        d = L.ContractDesc()
+        d.dtype = self.dst.dtype
+        d.clear_mode = self.clear_mode
+        d.ncm, d.ncn = self.ncm, self.ncn
+        d.a_kfast, d.b_nfast, d.nsplit = self.a_kfast, self.b_nfast, self.nsplit
+        d.mstride, d.nstride, d.kstride = self.mtab.shape[1], self.ntab.shape[1], self.ktab.shape[1]
+        d.M, d.N, d.K = self.M, self.N, self.K
+        d.scale = self.scale
+        d.a, d.b, d.d = self.a.ptr, self.b.ptr, self.dst.ptr
+        d.mtab, d.ntab, d.ktab = rt.upload(self.mtab), rt.upload(self.ntab), rt.upload(self.ktab)
+        for c in range(self.ncm + self.ncn):
+            d.lo[c], d.hi[c] = self.lo[c], self.hi[c]
+        d.workspace = rt.workspace_ptr if self.nsplit > 1 else None
+        self.desc = d
+        self._ref = C.byref(d)
+
+    def launch(self, rt, stream):
+        L.check(rt.lib.gfb_contract_launch(self._ref, stream), "contract")
+
+
+def product_form(expr):
+    """(scale, [connectors]) if expr is a constant times a product of
+    connector reads, else None."""
+    t = type(expr)
+    if t is Const:
+        return float(expr.value), []
+    if t is Name:
+        return 1.0, [expr.id]
+    if t is Unary and expr.op == "neg":
+        r = product_form(expr.x)
+        return None if r is None else (-r[0], r[1])
+    if t is Binary and expr.op in ("mul", "div"):
+        a, b = product_form(expr.x), product_form(expr.y)
+        if a is None or b is None:
+            return None
+        if expr.op == "mul":
+            return a[0] * b[0], a[1] + b[1]
+        if b[1] or b[0] == 0:
+            return None
+        return a[0] / b[0], a[1]
+    return None
+
+
+def pivot_rows(Cm, np_):
+    """Solve the output subset for parameters: per output row one pivot
+    parameter with coefficient +-1 (preferring one no later row uses); the
+    other parameters of a pivot row become free. Returns (row_of, order)."""
+    row_of = [-1] * np_
+    forced_free = set()
+    order = []
+    for r in range(len(Cm)):
+        cands = [p for p in range(np_) if abs(Cm[r][p]) == 1 and row_of[p] < 0 and p not in forced_free]
+        if not cands:
+            continue
+        later = [p for p in cands if not any(Cm[rr][p] for rr in range(r + 1, len(Cm)))]
+        p = (later or cands)[0]
+        row_of[p] = r
+        order.append(p)
+        for q in range(np_):
+            if q != p and Cm[r][q] != 0 and row_of[q] < 0:
+                forced_free.add(q)
+    return row_of, order
+
+
+def _grid(exts):
+    """Row-major coordinates (n_points, len(exts)) of a box of extents."""
+    if not exts:
+        return np.zeros((1, 0), dtype=np.int64)
+    g = np.indices(exts, dtype=np.int64).reshape(len(exts), -1)
+    return g.T
+
+
+INT32_MAX = 2**31 - 1
+
+
+def _i32(a):
+    a = np.asarray(a, dtype=np.int64)
+    if a.size and (a.min() < -INT32_MAX or a.max() > INT32_MAX):
+        return None
+    return np.ascontiguousarray(a.astype(np.int32))
+
+
+def contract_form(space, body, acc, ins, dst, ybox, clear_mode, cbox):
+    """Build the ContractOp of a single-term gather whose body is a scaled
+    product of two reads, or None when the pass does not have that shape
+    (the generic gather then runs it)."""
+    if space.triangular or space.np == 0 or any(s != 1 for s in space.step) or space.empty:
+        return None
+    if os.environ.get("GFB_CONTRACT", "1") == "0":
+        return None
+    pf = product_form(body)
+    if pf is None or len(pf[1]) != 2 or pf[1][0] == pf[1][1]:
+        return None
+    scale, (ca, cb) = pf
+    A, B = ins[ca], ins[cb]
+    if A.buf.kind != dst.kind or B.buf.kind != dst.kind:
+        return None
+    np_ = space.np
+    Cm, off = acc.matrix(np_)
+    rank = len(Cm)
+    if rank == 0:
+        return None
+    row_of, order = pivot_rows(Cm, np_)
+    if sorted(row_of[p] for p in order) != list(range(rank)):
+        return None  # an output row without a pivot: generic gather checks it
+    free = [p for p in range(np_) if row_of[p] < 0]
+    nv = rank + len(free) + 1
+    form = {}
+    for i, p in enumerate(free):
+        v = np.zeros(nv, dtype=np.int64)
+        v[rank + i] = 1
+        form[p] = v
+    for p in order:
+        r = row_of[p]
+        v = np.zeros(nv, dtype=np.int64)
+        v[r] = 1
+        v[-1] = -off[r]
+        for q in range(np_):
+            if q != p and Cm[r][q] != 0:
+                if q not in form:
+                    return None
+                v = v - Cm[r][q] * form[q]
+        form[p] = v * Cm[r][p]
+
+    def addr(a):
+        c0, st = a.flat(np_)
+        v = np.zeros(nv, dtype=np.int64)
+        v[-1] = c0
+        for p in range(np_):
+            v = v + st[p] * form[p]
+        return v
+
+    fa, fb = addr(A), addr(B)
+    ext = [hi - lo for lo, hi in ybox]
+    ya = {r for r in range(rank) if fa[r] != 0}
+    yb = {r for r in range(rank) if fb[r] != 0}
+    if ya & yb:
+        return None  # a batch dimension: no operand reuse, the generic gather is as good
+    if int(np.prod([ext[r] for r in yb], dtype=np.int64)) > int(np.prod([ext[r] for r in ya], dtype=np.int64)):
+        A, B, fa, fb, ya, yb = B, A, fb, fa, yb, ya
+    ndims = sorted(yb)
+    mdims = [r for r in range(rank) if r not in yb]
+    # pivot-range constraints not implied by the boxes
+    yl = [lo for lo, _ in ybox]
+    yh = [hi - 1 for _, hi in ybox]
+    cons_m, cons_n = [], []
+    for p in order:
+        v = form[p]
+        vmin = vmax = int(v[-1])
+        for r in range(rank):
+            a, b = int(v[r]) * yl[r], int(v[r]) * yh[r]
+            vmin, vmax = vmin + min(a, b), vmax + max(a, b)
+        for i, q in enumerate(free):
+            a, b = int(v[rank + i]) * space.first[q], int(v[rank + i]) * space.last[q]
+            vmin, vmax = vmin + min(a, b), vmax + max(a, b)
+        lo_p, hi_p = space.first[p], space.last[p] + 1
+        if vmin >= lo_p and vmax < hi_p:
+            continue
+        dep = {r for r in range(rank) if v[r] != 0}
+        if dep <= set(mdims):
+            cons_m.append((v, lo_p, hi_p))
+        elif dep <= set(ndims):
+            cons_n.append((v, lo_p, hi_p))
+        else:
+            return None
+    if len(cons_m) > 2 or len(cons_n) > 2:
+        return None
+    # k order: free parameters by decreasing |A stride| (innermost contiguous)
+    kperm = sorted(range(len(free)), key=lambda i: -abs(int(fa[rank + i])))
+    kdims = [free[i] for i in kperm]
+    M = int(np.prod([ext[r] for r in mdims], dtype=np.int64))
+    N = int(np.prod([ext[r] for r in ndims], dtype=np.int64))
+    K = int(np.prod([space.ext[q] for q in kdims], dtype=np.int64))
+    if M == 0 or N == 0 or K == 0:
+        return None
+
+    def side(dims, f, cons):
+        g = _grid([ext[r] for r in dims]) + np.array([yl[r] for r in dims], dtype=np.int64)
+        cols = [g @ np.array([f[r] for r in dims], dtype=np.int64),
+                g @ np.array([dst.strides[r] for r in dims], dtype=np.int64)]
+        if cbox is not None:
+            inside = np.ones(g.shape[0], dtype=bool)
+            for j, r in enumerate(dims):
+                inside &= (g[:, j] >= cbox[r][0]) & (g[:, j] < cbox[r][1])
+            cols.append(inside.astype(np.int64))
+        else:
+            cols.append(np.ones(g.shape[0], dtype=np.int64))
+        for v, _, _ in cons:
+            cols.append(g @ np.array([v[r] for r in dims], dtype=np.int64))
+        return _i32(np.stack(cols, axis=1))
+
+    mtab = side(mdims, fa, cons_m)
+    ntab = side(ndims, fb, cons_n)
+    gk = _grid([space.ext[q] for q in kdims]) + np.array([space.first[q] for q in kdims], dtype=np.int64)
+    fi = [free.index(q) for q in kdims]
+    kcols = [gk @ np.array([fa[rank + i] for i in fi], dtype=np.int64) + fa[-1],
+             gk @ np.array([fb[rank + i] for i in fi], dtype=np.int64) + fb[-1]]
+    for v, _, _ in cons_m + cons_n:
+        kcols.append(gk @ np.array([v[rank + i] for i in fi], dtype=np.int64) + v[-1])
+    ktab = _i32(np.stack(kcols, axis=1))
+    if mtab is None or ntab is None or ktab is None:
+        return None
+    bounds = [(lo, hi) for _, lo, hi in cons_m + cons_n]
+    if any(abs(b) > INT32_MAX for lh in bounds for b in lh):
+        return None
+    a_kfast = 1 if kdims and abs(int(fa[rank + free.index(kdims[-1])])) == 1 else 0
+    b_nfast = 1 if ndims and abs(int(fb[ndims[-1]])) == 1 else 0
+    BM, BN = contract_tile(N)
+    tiles = -(-M // BM) * -(-N // BN)
+    nsplit = 1
+    if tiles < 2 * 148 and K >= 64 * 16:
+        nsplit = int(min(-(-2 * 148 // tiles), K // (32 * 16), 1024))
+    return ContractOp(dst, A.buf, B.buf, scale, clear_mode, M, N, K, mtab, ntab, ktab, len(cons_m), len(cons_n),
+                      [lo for lo, _ in bounds], [hi for _, hi in bounds], a_kfast, b_nfast, max(nsplit, 1))
+
+
 STAR_POS = {(0, 0, 0): 0, (-1, 0, 0): 1, (1, 0, 0): 2, (0, -1, 0): 3, (0, 1, 0): 4, (0, 0, -1): 5, (0, 0, 1): 6}
 
 
@@ -1544,6 +1793,8 @@ class ProgramRun:
             clear_mode = 1 if cbox == ybox else 2
             dst.pending = None
         op = self._stencil_gather(space, t, group, ins, dst, ybox, clear_mode, cbox)
+        if op is None and len(group) == 1:
+            op = contract_form(space, t.body[group[0][0]], group[0][1], ins, dst, ybox, clear_mode, cbox)
         if op is not None:
             self.low.emit(op)
             return
@@ -1567,20 +1818,7 @@ class ProgramRun:
         for conn, acc, _ in group:
             seg = code.compile(t.body[conn], ci)
             Cm, off = acc.matrix(np_)
-            row_of = [-1] * np_
-            forced_free = set()
-            order = []
-            for r in range(len(Cm)):
-                cands = [p for p in range(np_) if abs(Cm[r][p]) == 1 and row_of[p] < 0 and p not in forced_free]
-                if not cands:
-                    continue
-                later = [p for p in cands if not any(Cm[rr][p] for rr in range(r + 1, len(Cm)))]
-                p = (later or cands)[0]
-                row_of[p] = r
-                order.append(p)
-                for q in range(np_):
-                    if q != p and Cm[r][q] != 0 and row_of[q] < 0:
-                        forced_free.add(q)
+            row_of, order = pivot_rows(Cm, np_)
             terms.append((row_of, order, Cm, off, seg))
         # work shape: free iterations per target
         F = max(int(np.prod([space.ext[p] for p in range(np_) if rof[p] < 0], dtype=np.int64))

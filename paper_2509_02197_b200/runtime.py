@@ -126,7 +126,16 @@ class Executable:
         self.workspace_ptr = self.workspace.data_ptr()
         self.err = torch.zeros(1, dtype=torch.int32, device=self.device)
         self.err_ptr = self.err.data_ptr()
+        self.aux = []  # static per-launch tables (index tables of contractions)
         self.device_bytes = total + self.workspace.numel()
+
+    def upload(self, arr: np.ndarray) -> int:
+        """Copy a static host table to device memory owned by this executable;
+        returns its device pointer."""
+        t = torch.from_numpy(np.ascontiguousarray(arr)).to(self.device)
+        self.aux.append(t)
+        self.device_bytes += t.numel() * t.element_size()
+        return t.data_ptr()
 
     def view(self, b: Buffer) -> torch.Tensor:
         t = b.root().tensor

@@ -15,6 +15,7 @@ import numpy as np
 from paper_2509_02197_b200 import _lib as L
 from paper_2509_02197_b200.lowering import (
     BroadcastOp,
+    ContractOp,
     CopyOp,
     EwOp,
     FillOp,
@@ -178,6 +179,8 @@ class Emulator:
             self.stencil(op.desc)
         elif isinstance(op, StarPairOp):
             self.star_pair(op.desc)
+        elif isinstance(op, ContractOp):
+            self.contract(op.desc)
         elif isinstance(op, FillOp):
             a, o = self.arr(op.dst.ptr)
             if op.whole:
@@ -236,6 +239,41 @@ class Emulator:
                 da[do:do + op.dst.numel] = sa[so:so + op.src.numel]
         else:
             raise NotImplementedError(type(op))
+
+    def table(self, ptr, n, stride):
+        a, o = self.arr(ptr)
+        return a[o:o + n * stride * 4].view(np.int32).reshape(n, stride) if a.dtype == np.uint8 else \
+            a[o:o + n * stride].reshape(n, stride)
+
+    def contract(self, d):
+        T = NPT[d.dtype]
+        M, N, K = d.M, d.N, d.K
+        mt, nt, kt = self.table(d.mtab, M, d.mstride), self.table(d.ntab, N, d.nstride), self.table(d.ktab, K, d.kstride)
+        aa, ao = self.arr(d.a)
+        ba, bo = self.arr(d.b)
+        ia = ao + mt[:, 0].astype(np.int64)[:, None] + kt[:, 0].astype(np.int64)[None, :]
+        ok = np.ones((M, K), dtype=bool)
+        for c in range(d.ncm):
+            v = mt[:, 3 + c].astype(np.int64)[:, None] + kt[:, 2 + c].astype(np.int64)[None, :]
+            ok &= (v >= d.lo[c]) & (v < d.hi[c])
+        Am = np.where(ok, aa[np.where(ok, ia, ao)], 0).astype(T)
+        ib = bo + kt[:, 1].astype(np.int64)[:, None] + nt[:, 0].astype(np.int64)[None, :]
+        okb = np.ones((K, N), dtype=bool)
+        for c in range(d.ncn):
+            v = nt[:, 3 + c].astype(np.int64)[None, :] + kt[:, 2 + d.ncm + c].astype(np.int64)[:, None]
+            okb &= (v >= d.lo[d.ncm + c]) & (v < d.hi[d.ncm + c])
+        Bm = np.where(okb, ba[np.where(okb, ib, bo)], 0).astype(T)
+        acc = (Am.astype(np.float64) @ Bm.astype(np.float64)) * d.scale
+        da, do = self.arr(d.d)
+        off = do + mt[:, 1].astype(np.int64)[:, None] + nt[:, 1].astype(np.int64)[None, :]
+        if d.clear_mode in (1, 3):
+            base = 0
+        elif d.clear_mode == 2:
+            inside = (mt[:, 2][:, None] != 0) & (nt[:, 2][None, :] != 0)
+            base = np.where(inside, 0, da[off])
+        else:
+            base = da[off]
+        da[off] = (base + acc).astype(da.dtype)
 
     def map(self, d):
         T = np.float64 if d.compute_f64 else np.float32
@@ -441,6 +479,13 @@ def execute(exe_builder_low, inputs: dict, input_bufs: dict, seed_buf=None, seed
         pass
 
     rt = RT()
+
+    def upload(arr):
+        a = mem.alloc(arr.size, arr.dtype)
+        a[:] = arr.reshape(-1)
+        return a.ctypes.data
+
+    rt.upload = upload
     ws = mem.alloc(1 << 16, np.uint8)
     rt.workspace_ptr = ws.ctypes.data
     em = Emulator(mem)
