@@ -26,7 +26,7 @@
 extern "C" {
 #endif
 
-#define GFB_ABI_VERSION 6
+#define GFB_ABI_VERSION 7
 
 #define GFB_MAX_PARAMS 8    /* map parameters (iteration-space rank) */
 #define GFB_MAX_RANK 8      /* array rank */
@@ -277,14 +277,61 @@ typedef struct {
   void *workspace;
 } gfb_contract_desc;
 
+/*
+ * Vectorised map (pointwise and single-dimension reductions). The host folds
+ * the iteration box into `ndim` loop dimensions (innermost last, adjacent
+ * dimensions merged when every operand's strides allow) with zero-based loop
+ * coordinates k: element offset = c0 + sum_d s[d] * k_d. Each warp owns a row
+ * (all but the innermost coordinate, decomposed once) and 32 * vec points of
+ * the innermost one; the tasklet bytecode runs on a register stack of static
+ * depth (code[pc] = op | depth_before << 6 | arg << 10), vec points per lane.
+ *   mode 0: pointwise; out[o] (wcr 0 store, 1 add) per point
+ *   mode 1: out[0] = base + sum over the innermost dimension (warp per row)
+ *   mode 2: ndim == 2; out[0] = base + sum over dimension 0 (columns along
+ *           dimension 1; nsplit row ranges, fp64 partials in the workspace)
+ * base follows gfb_gather_desc.clear_mode with the clear box in loop
+ * coordinates of the kept dimensions.
+ */
+#define GFB_M2_DIMS 8
+#define GFB_M2_OUTS 4
+#define GFB_M2_DEPTH 6
+typedef struct {
+  const void *base;
+  int32_t dtype;
+  int32_t _pad;
+  int64_t c0;
+  int64_t s[GFB_M2_DIMS];
+} gfb_m2_operand;
+
+typedef struct {
+  int32_t mode;
+  int32_t compute_f64;
+  int32_t ndim;
+  int32_t vec;
+  int32_t n_in, n_out;
+  int32_t clear_mode;
+  int32_t nsplit;
+  int64_t ext[GFB_M2_DIMS];
+  gfb_m2_operand in[GFB_MAX_INPUTS];
+  gfb_m2_operand out[GFB_M2_OUTS];
+  int32_t wcr[GFB_M2_OUTS];
+  int32_t code_start[GFB_M2_OUTS];
+  int32_t code_len[GFB_M2_OUTS];
+  uint32_t code[GFB_MAX_CODE];
+  double consts[GFB_MAX_CONSTS];
+  int64_t clear_lo[GFB_M2_DIMS], clear_hi[GFB_M2_DIMS];
+  void *workspace;
+  uint32_t *err;
+} gfb_map2_desc;
+
 /* ---- entry points --------------------------------------------------- */
 
 int gfb_abi_version(void);
 const char *gfb_last_error(void);
 int gfb_device_sm_count(void);
 /* sizes of gfb_space, gfb_operand, gfb_map_desc, gfb_term, gfb_gather_desc,
- * gfb_stencil_desc, gfb_star_op, gfb_star_pair_desc, gfb_contract_desc
- * (binding layout check); returns the count written */
+ * gfb_stencil_desc, gfb_star_op, gfb_star_pair_desc, gfb_contract_desc,
+ * gfb_map2_desc (binding layout check); returns the count written */
 int gfb_struct_sizes(int64_t *out, int32_t cap);
 
 /* replaces Executor._exec_map / _exec_tasklet (interpreter.py:478-507, 405-426) */
@@ -297,6 +344,10 @@ int gfb_stencil_launch(const gfb_stencil_desc *d, void *stream);
 /* product-contraction fast path of the wcr="sum" scatter (interpreter.py:
  * 422-423, 478-507): implicit GEMM over index tables */
 int gfb_contract_launch(const gfb_contract_desc *d, void *stream);
+/* vectorised pointwise map / one-dimensional reduction (see gfb_map2_desc);
+ * replaces _exec_map / _exec_tasklet (interpreter.py:478-507, 405-426) */
+int gfb_map2_launch(const gfb_map2_desc *d, void *stream);
+int64_t gfb_map2_workspace_bytes(const gfb_map2_desc *d);
 
 /* fused forward / adjoint timestep of a radius-1 stencil program (two
  * consecutive _exec_map sweeps, interpreter.py:478-507) */

@@ -19,7 +19,7 @@ MAXCODE = 128
 MAXCONST = 24
 MAXTAPS = 32
 MAXSRCS = 4
-ABI_VERSION = 6
+ABI_VERSION = 7
 
 F32, F64 = 0, 1
 
@@ -95,6 +95,21 @@ class ContractDesc(C.Structure):
                 ("mtab", vp), ("ntab", vp), ("ktab", vp), ("lo", i32 * 4), ("hi", i32 * 4), ("workspace", vp)]
 
 
+M2DIMS, M2OUTS, M2DEPTH = 8, 4, 6
+
+
+class M2Operand(C.Structure):
+    _fields_ = [("base", vp), ("dtype", i32), ("_pad", i32), ("c0", i64), ("s", i64 * M2DIMS)]
+
+
+class Map2Desc(C.Structure):
+    _fields_ = [("mode", i32), ("compute_f64", i32), ("ndim", i32), ("vec", i32), ("n_in", i32), ("n_out", i32),
+                ("clear_mode", i32), ("nsplit", i32), ("ext", i64 * M2DIMS), ("in_", M2Operand * MAXIN),
+                ("out", M2Operand * M2OUTS), ("wcr", i32 * M2OUTS), ("code_start", i32 * M2OUTS),
+                ("code_len", i32 * M2OUTS), ("code", C.c_uint32 * MAXCODE), ("consts", f64 * MAXCONST),
+                ("clear_lo", i64 * M2DIMS), ("clear_hi", i64 * M2DIMS), ("workspace", vp), ("err", vp)]
+
+
 _LIB = None
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libgfb.so")
@@ -111,6 +126,8 @@ _SIGS = [
     ("gfb_stencil_launch", i32, [C.POINTER(StencilDesc), vp]),
     ("gfb_star_pair_launch", i32, [C.POINTER(StarPairDesc), vp]),
     ("gfb_contract_launch", i32, [C.POINTER(ContractDesc), vp]),
+    ("gfb_map2_launch", i32, [C.POINTER(Map2Desc), vp]),
+    ("gfb_map2_workspace_bytes", i64, [C.POINTER(Map2Desc)]),
     ("gfb_reduce_workspace_bytes", i64, [i64]),
     ("gfb_reduce_sum", i32, [vp, i32, i64, vp, i32, i32, vp, vp]),
     ("gfb_elementwise", i32, [i32, f64, vp, i64, vp, i64, vp, i64, i32, i32, vp, vp]),
@@ -143,10 +160,11 @@ def load(path: str | None = None):
         fn.argtypes = args
     if lib.gfb_abi_version() != ABI_VERSION:
         raise EngineError(f"libgfb ABI {lib.gfb_abi_version()} != expected {ABI_VERSION}; rebuild")
-    sizes = (i64 * 9)()
-    n = lib.gfb_struct_sizes(sizes, 9)
+    sizes = (i64 * 10)()
+    n = lib.gfb_struct_sizes(sizes, 10)
     want = [C.sizeof(Space), C.sizeof(Operand), C.sizeof(MapDesc), C.sizeof(Term), C.sizeof(GatherDesc),
-            C.sizeof(StencilDesc), C.sizeof(StarOp), C.sizeof(StarPairDesc), C.sizeof(ContractDesc)]
+            C.sizeof(StencilDesc), C.sizeof(StarOp), C.sizeof(StarPairDesc), C.sizeof(ContractDesc),
+            C.sizeof(Map2Desc)]
     got = list(sizes[:n])
     if got[: len(want)] != want:
         raise EngineError(f"struct layout mismatch between gfb.h and _lib.py: C {got} vs ctypes {want}")

@@ -6,93 +6,170 @@
 //   K == 1            rank-1 update (outer-product adjoints of matvecs), HBM
 //   N == 1 / M == 1   matrix-vector products (atax / bicg), HBM-bound
 //   otherwise         tiled GEMM: fp64 on the DMMA tensor path
-//                     (mma.sync.m8n8k4.f64 -> DMMA), fp32 on FFMA
+//                     (mma.sync.m8n8k4.f64 -> DMMA), fp32 on FFMA (split-K
+//                     when the tile grid does not cover the SMs)
 #include "gfb_common.cuh"
 #include "gfb_internal.h"
 
 namespace gfb {
 
 // ---------------------------------------------------------------------------
-// generic SIMT tile GEMM (fp32; also the fp64 fallback for odd shapes)
+// fp32 FFMA GEMM: 64 x 128 CTA tile, BK = 16, 256 threads each owning a
+// 4 x 8 register block (a: one 16-byte shared load, b: two), next tile
+// prefetched into registers while the current one is consumed. Skinny
+// problems (the mlp layers: M = batch = 64) split K over blockIdx.z so the
+// grid covers the SMs; fp32 partials are reduced in a fixed order.
 
-constexpr int kBM = 64, kBN = 64, kBK = 16, kTM = 4, kTN = 4;
+constexpr int kSM = 64, kSN = 128, kSK = 16;
+constexpr int kSAP = kSM + 4, kSBP = kSN + 4;
 
-template <typename T>
-__global__ void __launch_bounds__(256) gemm_simt_kernel(int ta, int tb, int64_t M, int64_t N, int64_t K,
-                                                        const T *__restrict__ A, int64_t lda,
-                                                        const T *__restrict__ B, int64_t ldb, T *C, int64_t ldc,
-                                                        int accumulate) {
-  __shared__ T As[kBK][kBM + 1];
-  __shared__ T Bs[kBK][kBN + 1];
+template <bool TA, bool TB>
+__global__ void __launch_bounds__(256, 2) sgemm_kernel(int64_t M, int64_t N, int64_t K, const float *__restrict__ A,
+                                                    int64_t lda, const float *__restrict__ B, int64_t ldb,
+                                                    float *C, int64_t ldc, int accumulate, float *partial,
+                                                    int64_t kchunk) {
+  __shared__ __align__(16) float As[kSK][kSAP];
+  __shared__ __align__(16) float Bs[kSK][kSBP];
   const int tid = threadIdx.x;
   const int tx = tid % 16, ty = tid / 16;
-  const int64_t m0 = (int64_t)blockIdx.y * kBM, n0 = (int64_t)blockIdx.x * kBN;
-  T acc[kTM][kTN];
+  const int64_t m0 = (int64_t)blockIdx.y * kSM, n0 = (int64_t)blockIdx.x * kSN;
+  const int64_t kb = (int64_t)blockIdx.z * kchunk, ke = min(kb + kchunk, K);
+  // element (mm, kk) / (kk, nn) owned by this thread in the load of a tile
+  auto a_at = [&](int r, int &mm, int &kk) {
+    const int e = tid + r * 256;
+    if (TA) {
+      mm = e % kSM;
+      kk = e / kSM;
+    } else {
+      kk = e % kSK;
+      mm = e / kSK;
+    }
+  };
+  auto b_at = [&](int r, int &kk, int &nn) {
+    const int e = tid + r * 256;
+    if (TB) {
+      kk = e % kSK;
+      nn = e / kSK;
+    } else {
+      nn = e % kSN;
+      kk = e / kSN;
+    }
+  };
+  float ra[kSM * kSK / 256], rb[kSN * kSK / 256];
+  auto load = [&](int64_t k0) {
 #pragma unroll
-  for (int a = 0; a < kTM; ++a)
-#pragma unroll
-    for (int b = 0; b < kTN; ++b) acc[a][b] = T(0);
-  for (int64_t k0 = 0; k0 < K; k0 += kBK) {
-    // A tile: kBM x kBK elements, 256 threads -> 4 each
-#pragma unroll
-    for (int r = 0; r < (kBM * kBK) / 256; ++r) {
-      int e = tid + r * 256;
+    for (int r = 0; r < kSM * kSK / 256; ++r) {
       int mm, kk;
-      if (ta) {  // A stored [K, M]: walk m fastest for coalescing
-        mm = e % kBM;
-        kk = e / kBM;
-      } else {
-        kk = e % kBK;
-        mm = e / kBK;
-      }
-      int64_t gm = m0 + mm, gk = k0 + kk;
-      T v = T(0);
-      if (gm < M && gk < K) v = ta ? A[gk * lda + gm] : A[gm * lda + gk];
-      As[kk][mm] = v;
+      a_at(r, mm, kk);
+      const int64_t gm = m0 + mm, gk = k0 + kk;
+      ra[r] = (gm < M && gk < ke) ? (TA ? A[gk * lda + gm] : A[gm * lda + gk]) : 0.f;
     }
 #pragma unroll
-    for (int r = 0; r < (kBN * kBK) / 256; ++r) {
-      int e = tid + r * 256;
-      int nn, kk;
-      if (tb) {  // B stored [N, K]
-        kk = e % kBK;
-        nn = e / kBK;
-      } else {
-        nn = e % kBN;
-        kk = e / kBN;
-      }
-      int64_t gn = n0 + nn, gk = k0 + kk;
-      T v = T(0);
-      if (gn < N && gk < K) v = tb ? B[gn * ldb + gk] : B[gk * ldb + gn];
-      Bs[kk][nn] = v;
+    for (int r = 0; r < kSN * kSK / 256; ++r) {
+      int kk, nn;
+      b_at(r, kk, nn);
+      const int64_t gn = n0 + nn, gk = k0 + kk;
+      rb[r] = (gn < N && gk < ke) ? (TB ? B[gn * ldb + gk] : B[gk * ldb + gn]) : 0.f;
     }
+  };
+  auto stash = [&]() {
+#pragma unroll
+    for (int r = 0; r < kSM * kSK / 256; ++r) {
+      int mm, kk;
+      a_at(r, mm, kk);
+      As[kk][mm] = ra[r];
+    }
+#pragma unroll
+    for (int r = 0; r < kSN * kSK / 256; ++r) {
+      int kk, nn;
+      b_at(r, kk, nn);
+      Bs[kk][nn] = rb[r];
+    }
+  };
+  float acc[4][8];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 8; ++j) acc[i][j] = 0.f;
+  if (kb < ke) load(kb);
+  for (int64_t k0 = kb; k0 < ke; k0 += kSK) {
     __syncthreads();
-#pragma unroll
-    for (int kk = 0; kk < kBK; ++kk) {
-      T a[kTM], b[kTN];
-#pragma unroll
-      for (int q = 0; q < kTM; ++q) a[q] = As[kk][ty + 16 * q];
-#pragma unroll
-      for (int q = 0; q < kTN; ++q) b[q] = Bs[kk][tx + 16 * q];
-#pragma unroll
-      for (int p = 0; p < kTM; ++p)
-#pragma unroll
-        for (int q = 0; q < kTN; ++q) acc[p][q] = fma(a[p], b[q], acc[p][q]);
-    }
+    stash();
     __syncthreads();
+    if (k0 + kSK < ke) load(k0 + kSK);
+#pragma unroll
+    for (int kk = 0; kk < kSK; ++kk) {
+      const float4 a = *reinterpret_cast<const float4 *>(&As[kk][ty * 4]);
+      const float4 b0 = *reinterpret_cast<const float4 *>(&Bs[kk][tx * 4]);
+      const float4 b1 = *reinterpret_cast<const float4 *>(&Bs[kk][64 + tx * 4]);
+      const float av[4] = {a.x, a.y, a.z, a.w};
+      const float bv[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 8; ++j) acc[i][j] = fmaf(av[i], bv[j], acc[i][j]);
+    }
   }
 #pragma unroll
-  for (int p = 0; p < kTM; ++p) {
-    int64_t gm = m0 + ty + 16 * p;
+  for (int i = 0; i < 4; ++i) {
+    const int64_t gm = m0 + ty * 4 + i;
     if (gm >= M) continue;
 #pragma unroll
-    for (int q = 0; q < kTN; ++q) {
-      int64_t gn = n0 + tx + 16 * q;
+    for (int j = 0; j < 8; ++j) {
+      const int64_t gn = n0 + (j < 4 ? tx * 4 + j : 64 + tx * 4 + (j - 4));
       if (gn >= N) continue;
-      T *c = C + gm * ldc + gn;
-      *c = accumulate ? (T)(*c + acc[p][q]) : acc[p][q];
+      if (partial) {
+        partial[((int64_t)blockIdx.z * M + gm) * N + gn] = acc[i][j];
+      } else {
+        float *c = C + gm * ldc + gn;
+        *c = accumulate ? *c + acc[i][j] : acc[i][j];
+      }
     }
   }
+}
+
+__global__ void sgemm_splits_finish(int64_t M, int64_t N, int64_t ns, const float *__restrict__ partial, float *C,
+                                    int64_t ldc, int accumulate) {
+  const int64_t MN = M * N;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < MN; e += (int64_t)gridDim.x * blockDim.x) {
+    float s = 0.f;
+    for (int64_t q = 0; q < ns; ++q) s += partial[q * MN + e];
+    const int64_t m = e / N, n = e - m * N;
+    float *c = C + m * ldc + n;
+    *c = accumulate ? *c + s : s;
+  }
+}
+
+static int64_t sgemm_splits(int64_t M, int64_t N, int64_t K) {
+  const int64_t tiles = ceil_div(M, kSM) * ceil_div(N, kSN);
+  const int64_t target = 2 * (int64_t)sm_count();
+  if (tiles >= target) return 1;
+  int64_t ns = ceil_div(target, tiles);
+  const int64_t maxs = K / (4 * kSK);
+  if (ns > maxs) ns = maxs;
+  return ns < 1 ? 1 : ns;
+}
+
+static int sgemm(int ta, int tb, int64_t M, int64_t N, int64_t K, const float *A, int64_t lda, const float *B,
+                 int64_t ldb, float *C, int64_t ldc, int accumulate, void *ws, cudaStream_t st) {
+  const int64_t ns = sgemm_splits(M, N, K);
+  const int64_t chunk = ceil_div(ceil_div(K, ns), kSK) * kSK;
+  const int64_t nz = ceil_div(K, chunk);
+  float *partial = nz > 1 ? (float *)ws : nullptr;
+  dim3 grid((unsigned)ceil_div(N, kSN), (unsigned)ceil_div(M, kSM), (unsigned)nz);
+  if (ta && tb)
+    sgemm_kernel<true, true><<<grid, 256, 0, st>>>(M, N, K, A, lda, B, ldb, C, ldc, accumulate, partial, chunk);
+  else if (ta)
+    sgemm_kernel<true, false><<<grid, 256, 0, st>>>(M, N, K, A, lda, B, ldb, C, ldc, accumulate, partial, chunk);
+  else if (tb)
+    sgemm_kernel<false, true><<<grid, 256, 0, st>>>(M, N, K, A, lda, B, ldb, C, ldc, accumulate, partial, chunk);
+  else
+    sgemm_kernel<false, false><<<grid, 256, 0, st>>>(M, N, K, A, lda, B, ldb, C, ldc, accumulate, partial, chunk);
+  if (nz > 1) {
+    const unsigned blocks = (unsigned)min(ceil_div(M * N, 256), (int64_t)sm_count() * 8);
+    sgemm_splits_finish<<<blocks, 256, 0, st>>>(M, N, nz, partial, C, ldc, accumulate);
+  }
+  return check_launch("sgemm");
 }
 
 // ---------------------------------------------------------------------------
@@ -201,8 +278,17 @@ __global__ void __launch_bounds__(256) gemv_rowdot_kernel(int64_t M, int64_t K, 
   const int lane = threadIdx.x & 31;
   if (row >= M) return;
   const T *a = A + row * lda;
-  T acc = T(0);
-  for (int64_t k = lane; k < K; k += 32) acc = fma(a[k], x[k * incx], acc);
+  // eight independent partial sums keep eight loads per lane in flight
+  T part[8];
+#pragma unroll
+  for (int u = 0; u < 8; ++u) part[u] = T(0);
+  int64_t k = lane;
+  for (; k + 7 * 32 < K; k += 8 * 32) {
+#pragma unroll
+    for (int u = 0; u < 8; ++u) part[u] = fma(a[k + u * 32], x[(k + u * 32) * incx], part[u]);
+  }
+  for (; k < K; k += 32) part[0] = fma(a[k], x[k * incx], part[0]);
+  T acc = ((part[0] + part[1]) + (part[2] + part[3])) + ((part[4] + part[5]) + (part[6] + part[7]));
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) acc += __shfl_down_sync(0xffffffffu, acc, o);
   if (lane == 0) {
@@ -222,10 +308,16 @@ __global__ void __launch_bounds__(256) gemv_colsum_kernel(int64_t M, int64_t K, 
   const int g = threadIdx.x >> 5;
   const int64_t kb = (int64_t)blockIdx.y * kchunk;
   const int64_t ke = min(kb + kchunk, K);
-  T acc = T(0);
-  if (i < M)
-    for (int64_t k = kb + g; k < ke; k += 8) acc = fma(S[k * lds + i], x[k * incx], acc);
-  red[g][threadIdx.x & 31] = acc;
+  T part[4] = {T(0), T(0), T(0), T(0)};
+  if (i < M) {
+    int64_t k = kb + g;
+    for (; k + 24 < ke; k += 32) {
+#pragma unroll
+      for (int u = 0; u < 4; ++u) part[u] = fma(S[(k + 8 * u) * lds + i], x[(k + 8 * u) * incx], part[u]);
+    }
+    for (; k < ke; k += 8) part[0] = fma(S[k * lds + i], x[k * incx], part[0]);
+  }
+  red[g][threadIdx.x & 31] = (part[0] + part[1]) + (part[2] + part[3]);
   __syncthreads();
   if (g == 0 && i < M) {
     T s = T(0);
@@ -251,13 +343,13 @@ template <typename T>
 __global__ void __launch_bounds__(256) rank1_kernel(int64_t M, int64_t N, const T *__restrict__ u, int64_t incu,
                                                     const T *__restrict__ v, int64_t incv, T *C, int64_t ldc,
                                                     int accumulate) {
-  const int64_t total = M * N;
-  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t f = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; f < total; f += stride) {
-    int64_t i = f / N, j = f % N;
-    T r = u[i * incu] * v[j * incv];
-    T *c = C + i * ldc + j;
-    *c = accumulate ? (T)(*c + r) : r;
+  for (int64_t i = blockIdx.y; i < M; i += gridDim.y) {
+    const T ui = u[i * incu];
+    T *row = C + i * ldc;
+    for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < N; j += (int64_t)gridDim.x * blockDim.x) {
+      const T r = ui * v[j * incv];
+      row[j] = accumulate ? (T)(row[j] + r) : r;
+    }
   }
 }
 
@@ -295,9 +387,8 @@ static int matmul_t(int ta, int tb, int64_t M, int64_t N, int64_t K, const T *A,
     // op(A) column 0: element i at A[i*lda] (no ta) or A[i] (ta: A stored [1, M])
     int64_t incu = ta ? 1 : lda;
     int64_t incv = tb ? ldb : 1;  // op(B) row 0: B[j] (no tb) or B[j*ldb] (tb: stored [N,1])
-    int64_t total = M * N;
-    unsigned blocks = (unsigned)min(ceil_div(total, 256 * 4), (int64_t)sm_count() * 8);
-    rank1_kernel<T><<<blocks, 256, 0, st>>>(M, N, A, incu, B, incv, C, ldc, accumulate);
+    dim3 grid((unsigned)min(ceil_div(N, 256), (int64_t)8), (unsigned)min(M, (int64_t)65535));
+    rank1_kernel<T><<<grid, 256, 0, st>>>(M, N, A, incu, B, incv, C, ldc, accumulate);
     return check_launch("rank1");
   }
   if (N == 1) {
@@ -330,6 +421,14 @@ extern "C" int64_t gfb_matmul_workspace_bytes(int32_t dtype, int32_t ta, int32_t
   int64_t es = dtype == GFB_F64 ? 8 : 4;
   if (K > 1 && N == 1 && ta) return colsum_splits(M, K) * M * es;
   if (K > 1 && M == 1 && !tb && N > 1) return colsum_splits(N, K) * N * es;
+  if (dtype != GFB_F64 && K > 1 && M > 1 && N > 1) {
+    const int64_t ns = sgemm_splits(M, N, K);
+    if (ns > 1) {
+      const int64_t chunk = ceil_div(ceil_div(K, ns), kSK) * kSK;
+      const int64_t nz = ceil_div(K, chunk);
+      if (nz > 1) return nz * M * N * 4;
+    }
+  }
   return 0;
 }
 
@@ -352,8 +451,6 @@ extern "C" int gfb_matmul(int32_t dtype, int32_t ta, int32_t tb, int64_t M, int6
   rc = matmul_t<float>(ta, tb, M, N, K, (const float *)A, lda, (const float *)B, ldb, (float *)C, ldc, accumulate,
                        workspace, st);
   if (rc >= 0) return rc;
-  dim3 grid((unsigned)ceil_div(N, kBN), (unsigned)ceil_div(M, kBM));
-  gemm_simt_kernel<float><<<grid, 256, 0, st>>>(ta, tb, M, N, K, (const float *)A, lda, (const float *)B, ldb,
-                                                (float *)C, ldc, accumulate);
-  return check_launch("sgemm_simt");
+  return sgemm(ta, tb, M, N, K, (const float *)A, lda, (const float *)B, ldb, (float *)C, ldc, accumulate, workspace,
+               st);
 }

@@ -1,0 +1,467 @@
+// Vectorised map kernels (gfb.h, gfb_map2_desc): device templates shared by
+// the bytecode instantiation (map2.cu) and the ahead-of-time compiled tasklet
+// bodies (gen_tasklets.cu).
+//
+// Replaces the per-point interpretation of MapNode bodies (Executor.
+// _exec_map / _exec_tasklet, interpreter.py:478-507, :405-426) for
+// rectangular spaces:
+//  * the host folds the box into loop dimensions and merges adjacent ones,
+//    so a warp decomposes its row index once and walks the innermost
+//    dimension with plain int32 strides;
+//  * the bytecode carries its static stack depth, so the evaluation stack
+//    lives in registers: every instruction is one uniform two-level switch
+//    (depth, opcode) whose cases touch compile-time register slots, applied
+//    to V points per lane; generated bodies skip the dispatch entirely;
+//  * warp-coalesced operands: lane l of a warp owns points l + 32 v.
+#pragma once
+
+#include <algorithm>
+
+#include "gfb_common.cuh"
+#include "gfb_internal.h"
+
+namespace gfb {
+
+constexpr int kM2Depth = GFB_M2_DEPTH;
+constexpr int kM2Warps = 8;  // 256-thread CTAs
+constexpr int kM2Bases = GFB_MAX_INPUTS + GFB_M2_OUTS;
+
+template <typename T, int V>
+__device__ __forceinline__ void m2_unary(int op, T (&x)[V], uint32_t vm, uint32_t &bad) {
+  switch (op) {
+    case GFB_OP_NEG:
+#pragma unroll
+      for (int v = 0; v < V; ++v) x[v] = -x[v];
+      break;
+    case GFB_OP_SIN:
+#pragma unroll
+      for (int v = 0; v < V; ++v) x[v] = t_sin(x[v]);
+      break;
+    case GFB_OP_COS:
+#pragma unroll
+      for (int v = 0; v < V; ++v) x[v] = t_cos(x[v]);
+      break;
+    case GFB_OP_EXP:
+#pragma unroll
+      for (int v = 0; v < V; ++v) x[v] = t_exp(x[v]);
+      break;
+    case GFB_OP_LOG:
+#pragma unroll
+      for (int v = 0; v < V; ++v) {
+        if (((vm >> v) & 1) && !(x[v] > T(0))) bad |= GFB_EBIT_LOG;
+        x[v] = t_log(x[v]);
+      }
+      break;
+    case GFB_OP_SQRT:
+#pragma unroll
+      for (int v = 0; v < V; ++v) {
+        if (((vm >> v) & 1) && x[v] < T(0)) bad |= GFB_EBIT_SQRT;
+        x[v] = sqrt(x[v]);
+      }
+      break;
+    case GFB_OP_TANH:
+#pragma unroll
+      for (int v = 0; v < V; ++v) x[v] = t_tanh(x[v]);
+      break;
+    case GFB_OP_ABS:
+#pragma unroll
+      for (int v = 0; v < V; ++v) x[v] = fabs(x[v]);
+      break;
+    case GFB_OP_SIGN:
+#pragma unroll
+      for (int v = 0; v < V; ++v)
+        x[v] = x[v] > T(0) ? T(1) : (x[v] < T(0) ? T(-1) : (x[v] == T(0) ? T(0) : x[v]));
+      break;
+    default:
+      break;
+  }
+}
+
+template <typename T, int V>
+__device__ __forceinline__ void m2_binary(int op, T (&a)[V], const T (&b)[V], uint32_t vm, uint32_t &bad) {
+  switch (op) {
+    case GFB_OP_ADD:
+#pragma unroll
+      for (int v = 0; v < V; ++v) a[v] = a[v] + b[v];
+      break;
+    case GFB_OP_SUB:
+#pragma unroll
+      for (int v = 0; v < V; ++v) a[v] = a[v] - b[v];
+      break;
+    case GFB_OP_MUL:
+#pragma unroll
+      for (int v = 0; v < V; ++v) a[v] = a[v] * b[v];
+      break;
+    case GFB_OP_DIV:
+#pragma unroll
+      for (int v = 0; v < V; ++v) {
+        if (((vm >> v) & 1) && b[v] == T(0)) bad |= GFB_EBIT_DIV0;
+        a[v] = a[v] / b[v];
+      }
+      break;
+    case GFB_OP_IDIV:
+#pragma unroll
+      for (int v = 0; v < V; ++v) {
+        if (((vm >> v) & 1) && b[v] == T(0)) bad |= GFB_EBIT_IDIV0;
+        a[v] = np_floordiv(a[v], b[v]);
+      }
+      break;
+    case GFB_OP_MOD:
+#pragma unroll
+      for (int v = 0; v < V; ++v) {
+        if (((vm >> v) & 1) && b[v] == T(0)) bad |= GFB_EBIT_MOD0;
+        a[v] = np_mod(a[v], b[v]);
+      }
+      break;
+    case GFB_OP_MIN:
+#pragma unroll
+      for (int v = 0; v < V; ++v) a[v] = b[v] < a[v] ? b[v] : a[v];
+      break;
+    case GFB_OP_MAX:
+#pragma unroll
+      for (int v = 0; v < V; ++v) a[v] = b[v] > a[v] ? b[v] : a[v];
+      break;
+    case GFB_OP_POW:
+#pragma unroll
+      for (int v = 0; v < V; ++v) {
+        if ((vm >> v) & 1) {
+          if (a[v] == T(0) && b[v] < T(0)) bad |= GFB_EBIT_POW;
+          if (a[v] < T(0) && b[v] != floor(b[v])) bad |= GFB_EBIT_POW;
+        }
+        a[v] = t_pow(a[v], b[v]);
+      }
+      break;
+    default:
+      break;
+  }
+}
+
+// error bits are collected for valid points only (masked-off lanes evaluate
+// on placeholder values) and raised once per evaluation
+
+template <typename T, int V, int D, typename F>
+__device__ __forceinline__ void m2_step(int op, int arg, T (&s)[kM2Depth][V], const double *consts, F &fetch,
+                                        uint32_t vm, uint32_t &bad) {
+  if (op == GFB_OP_IN) {
+    if constexpr (D < kM2Depth) fetch(arg, s[D]);
+  } else if (op == GFB_OP_CONST) {
+    if constexpr (D < kM2Depth) {
+      const T c = (T)consts[arg];
+#pragma unroll
+      for (int v = 0; v < V; ++v) s[D][v] = c;
+    }
+  } else if (op >= GFB_OP_NEG) {
+    if constexpr (D >= 1 && D <= kM2Depth) m2_unary<T, V>(op, s[D - 1], vm, bad);
+  } else {
+    if constexpr (D >= 2 && D <= kM2Depth) m2_binary<T, V>(op, s[D - 2], s[D - 1], vm, bad);
+  }
+}
+
+template <typename T, int V, typename F>
+__device__ __forceinline__ void m2_eval(const gfb_map2_desc &d, int start, int len, F &fetch, uint32_t vm,
+                                        T (&res)[V]) {
+  T s[kM2Depth][V];
+  uint32_t bad = 0;
+  for (int pc = start; pc < start + len; ++pc) {
+    const uint32_t ins = d.code[pc];
+    const int op = (int)(ins & 63u), dep = (int)((ins >> 6) & 15u), arg = (int)(ins >> 10);
+    switch (dep) {
+      case 0: m2_step<T, V, 0>(op, arg, s, d.consts, fetch, vm, bad); break;
+      case 1: m2_step<T, V, 1>(op, arg, s, d.consts, fetch, vm, bad); break;
+      case 2: m2_step<T, V, 2>(op, arg, s, d.consts, fetch, vm, bad); break;
+      case 3: m2_step<T, V, 3>(op, arg, s, d.consts, fetch, vm, bad); break;
+      case 4: m2_step<T, V, 4>(op, arg, s, d.consts, fetch, vm, bad); break;
+      case 5: m2_step<T, V, 5>(op, arg, s, d.consts, fetch, vm, bad); break;
+      default: m2_step<T, V, 6>(op, arg, s, d.consts, fetch, vm, bad); break;
+    }
+  }
+  if (bad) raise_bits(d.err, bad);
+#pragma unroll
+  for (int v = 0; v < V; ++v) res[v] = s[0][v];
+}
+
+// Loads of input k at the item's points on demand (the body's IN); masked-
+// off points read 1. at(k, v): int32 element offset of operand k at point v
+// (the host only routes spaces whose offsets fit in int32 here).
+template <typename T, int V, typename At>
+struct M2Fetch {
+  const gfb_map2_desc &d;
+  At &at;
+  uint32_t vm;
+  __device__ __forceinline__ void operator()(int k, T (&dst)[V]) const {
+    const gfb_m2_operand &o = d.in[k];
+    if (o.dtype == GFB_F64) {
+      const double *p = (const double *)o.base;
+#pragma unroll
+      for (int v = 0; v < V; ++v) dst[v] = ((vm >> v) & 1) ? (T)p[at(k, v)] : T(1);
+    } else {
+      const float *p = (const float *)o.base;
+#pragma unroll
+      for (int v = 0; v < V; ++v) dst[v] = ((vm >> v) & 1) ? (T)p[at(k, v)] : T(1);
+    }
+  }
+};
+
+// Per-warp row bases (nd > 2): lane k < n_in + n_out computes operand k's
+// offset of the row (all coordinates but the innermost), then the warp syncs.
+__device__ __forceinline__ void m2_row_bases(const gfb_map2_desc &d, int32_t row, int lane, int32_t *sb) {
+  __syncwarp();
+  if (lane < d.n_in + d.n_out) {
+    const gfb_m2_operand &o = lane < d.n_in ? d.in[lane] : d.out[lane - d.n_in];
+    int32_t rem = row, off = (int32_t)o.c0;
+    for (int dd = d.ndim - 2; dd >= 0; --dd) {
+      const int32_t e = (int32_t)d.ext[dd];
+      const int32_t k = rem % e;
+      rem /= e;
+      off += (int32_t)o.s[dd] * k;
+    }
+    sb[lane] = off;
+  }
+  __syncwarp();
+}
+
+__device__ __forceinline__ bool m2_row_in_clear(const gfb_map2_desc &d, int32_t row) {
+  int32_t rem = row;
+  bool in = true;
+  for (int dd = d.ndim - 2; dd >= 0; --dd) {
+    const int32_t e = (int32_t)d.ext[dd];
+    const int32_t k = rem % e;
+    rem /= e;
+    in &= k >= d.clear_lo[dd] && k < d.clear_hi[dd];
+  }
+  return in;
+}
+
+template <typename T>
+__device__ __forceinline__ T m2_base(const gfb_map2_desc &d, bool inside, int32_t off) {
+  if (d.clear_mode == 1 || d.clear_mode == 3 || (d.clear_mode == 2 && inside)) return T(0);
+  return load_as<T>(const_cast<void *>(d.out[0].base), d.out[0].dtype, off);
+}
+
+__device__ __forceinline__ const gfb_m2_operand &m2_op(const gfb_map2_desc &d, int k) {
+  return k < d.n_in ? d.in[k] : d.out[k - d.n_in];
+}
+
+// Body policies: VmBody interprets the bytecode; generated bodies
+// (gen_tasklets.cu) are the same tasklets compiled ahead of time.
+struct VmBody {
+  template <typename T, int V, typename F>
+  static __device__ __forceinline__ void eval(const gfb_map2_desc &d, int o, F &fetch, uint32_t vm, T (&r)[V]) {
+    m2_eval<T, V>(d, d.code_start[o], d.code_len[o], fetch, vm, r);
+  }
+};
+
+// evaluate every output at the item's points and store them
+template <typename T, int V, typename Body, typename At>
+__device__ __forceinline__ void m2_points(const gfb_map2_desc &d, At &at, uint32_t vm) {
+  M2Fetch<T, V, At> fetch{d, at, vm};
+  for (int o = 0; o < d.n_out; ++o) {
+    T r[V];
+    Body::template eval<T, V>(d, o, fetch, vm, r);
+    const gfb_m2_operand &wo = d.out[o];
+    const int k = d.n_in + o;
+    if (wo.dtype == GFB_F64) {
+      double *p = (double *)wo.base;
+#pragma unroll
+      for (int v = 0; v < V; ++v)
+        if ((vm >> v) & 1) p[at(k, v)] = d.wcr[o] ? p[at(k, v)] + (double)r[v] : (double)r[v];
+    } else {
+      float *p = (float *)wo.base;
+#pragma unroll
+      for (int v = 0; v < V; ++v)
+        if ((vm >> v) & 1) p[at(k, v)] = d.wcr[o] ? p[at(k, v)] + (float)r[v] : (float)r[v];
+    }
+  }
+}
+
+// LAYOUT 0: ndim == 2, warp item = (row, 32*V points of the row)
+// LAYOUT 1: ndim == 2 with a short row: warp item = 32*V consecutive points
+//           of the flattened space, row = point / E by a multiply-shift
+// LAYOUT 2: ndim > 2, row bases staged per warp in shared memory
+template <typename T, int V, int LAYOUT, typename Body>
+__global__ void __launch_bounds__(256) map2_pointwise_kernel(const __grid_constant__ gfb_map2_desc d, int32_t rows,
+                                                             int32_t cpr, uint64_t magic) {
+  __shared__ int32_t sbase[kM2Warps][kM2Bases];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int nd = d.ndim;
+  const int32_t E = (int32_t)d.ext[nd - 1];
+  const int32_t total = rows * E;
+  const int32_t items = LAYOUT == 1 ? (int32_t)ceil_div(total, 32 * V) : rows * cpr;
+  int32_t *sb = sbase[w];
+  for (int32_t it = blockIdx.x * kM2Warps + w; it < items; it += gridDim.x * kM2Warps) {
+    if (LAYOUT == 1) {
+      int32_t rw[V], cl[V];
+      uint32_t vm = 0;
+#pragma unroll
+      for (int v = 0; v < V; ++v) {
+        const int32_t f = it * 32 * V + lane + 32 * v;
+        vm |= (uint32_t)(f < total) << v;
+        rw[v] = (int32_t)(((uint64_t)(uint32_t)f * magic) >> 40);
+        cl[v] = f - rw[v] * E;
+      }
+      auto at = [&](int k, int v) -> int32_t {
+        const gfb_m2_operand &o = m2_op(d, k);
+        return (int32_t)o.c0 + (int32_t)o.s[0] * rw[v] + (int32_t)o.s[1] * cl[v];
+      };
+      m2_points<T, V, Body>(d, at, vm);
+    } else {
+      const int32_t row = cpr == 1 ? it : it / cpr, chunk = it - row * cpr;
+      if (LAYOUT == 2) m2_row_bases(d, row, lane, sb);
+      const int32_t i0 = chunk * 32 * V + lane;
+      uint32_t vm = 0;
+#pragma unroll
+      for (int v = 0; v < V; ++v) vm |= (uint32_t)(i0 + 32 * v < E) << v;
+      auto at = [&](int k, int v) -> int32_t {
+        const gfb_m2_operand &o = m2_op(d, k);
+        const int32_t si = (int32_t)o.s[LAYOUT == 0 ? 1 : nd - 1];
+        const int32_t rb = LAYOUT == 0 ? (int32_t)o.c0 + (int32_t)o.s[0] * row : sb[k];
+        return rb + si * i0 + v * (32 * si);
+      };
+      m2_points<T, V, Body>(d, at, vm);
+    }
+  }
+}
+
+template <typename T, int V, bool ROW1, typename Body>
+__global__ void __launch_bounds__(256) map2_reduce_inner_kernel(const __grid_constant__ gfb_map2_desc d,
+                                                                int32_t rows) {
+  __shared__ int32_t sbase[kM2Warps][kM2Bases];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int nd = d.ndim;
+  const int32_t E = (int32_t)d.ext[nd - 1];
+  int32_t *sb = sbase[w];
+  for (int32_t row = blockIdx.x * kM2Warps + w; row < rows; row += gridDim.x * kM2Warps) {
+    if (!ROW1) m2_row_bases(d, row, lane, sb);
+    auto rowbase = [&](int k) -> int32_t {
+      const gfb_m2_operand &o = m2_op(d, k);
+      return ROW1 ? (int32_t)o.c0 + (int32_t)o.s[0] * row : sb[k];
+    };
+    T acc = T(0);
+    for (int32_t c0 = 0; c0 < E; c0 += 32 * V) {
+      const int32_t i0 = c0 + lane;
+      uint32_t vm = 0;
+#pragma unroll
+      for (int v = 0; v < V; ++v) vm |= (uint32_t)(i0 + 32 * v < E) << v;
+      auto at = [&](int k, int v) -> int32_t {
+        const int32_t si = (int32_t)m2_op(d, k).s[ROW1 ? 1 : nd - 1];
+        return rowbase(k) + si * i0 + v * (32 * si);
+      };
+      M2Fetch<T, V, decltype(at)> fetch{d, at, vm};
+      T r[V];
+      Body::template eval<T, V>(d, 0, fetch, vm, r);
+#pragma unroll
+      for (int v = 0; v < V; ++v)
+        if ((vm >> v) & 1) acc += r[v];
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_down_sync(0xffffffffu, acc, o);
+    if (lane == 0) {
+      const int32_t off = rowbase(d.n_in);
+      const bool inside = d.clear_mode == 2 ? m2_row_in_clear(d, row) : true;
+      store_as<T>(const_cast<void *>(d.out[0].base), d.out[0].dtype, off, m2_base<T>(d, inside, off) + acc);
+    }
+  }
+}
+
+// column sums: lane = column, V rows per warp iteration (V loads in flight)
+template <typename T, int V, typename Body>
+__global__ void __launch_bounds__(256) map2_reduce_outer_kernel(const __grid_constant__ gfb_map2_desc d) {
+  __shared__ T red[kM2Warps][32];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int32_t R = (int32_t)d.ext[0], E = (int32_t)d.ext[1];
+  const int s = blockIdx.y, ns = d.nsplit;
+  const int32_t rb = (int32_t)((int64_t)R * s / ns), re = (int32_t)((int64_t)R * (s + 1) / ns);
+  const int32_t i = blockIdx.x * 32 + lane;
+  T acc = T(0);
+  for (int32_t r = rb + w * V; r < re; r += kM2Warps * V) {
+    uint32_t vm = 0;
+#pragma unroll
+    for (int v = 0; v < V; ++v) vm |= (uint32_t)(i < E && r + v < re) << v;
+    auto at = [&](int k, int v) -> int32_t {
+      const gfb_m2_operand &o = m2_op(d, k);
+      return (int32_t)o.c0 + (int32_t)o.s[0] * (r + v) + (int32_t)o.s[1] * i;
+    };
+    M2Fetch<T, V, decltype(at)> fetch{d, at, vm};
+    T x[V];
+    Body::template eval<T, V>(d, 0, fetch, vm, x);
+#pragma unroll
+    for (int v = 0; v < V; ++v)
+      if ((vm >> v) & 1) acc += x[v];
+  }
+  red[w][lane] = acc;
+  __syncthreads();
+  if (w != 0 || i >= E) return;
+  T sum = T(0);
+  for (int ww = 0; ww < kM2Warps; ++ww) sum += red[ww][lane];
+  if (ns > 1) {
+    ((double *)d.workspace)[(int64_t)s * E + i] = (double)sum;
+  } else {
+    const gfb_m2_operand &wo = d.out[0];
+    const int32_t off = (int32_t)wo.c0 + (int32_t)wo.s[1] * i;
+    const bool inside = i >= d.clear_lo[1] && i < d.clear_hi[1];
+    store_as<T>(const_cast<void *>(wo.base), wo.dtype, off, m2_base<T>(d, inside, off) + sum);
+  }
+}
+
+template <typename T>
+__global__ void map2_finish_kernel(const __grid_constant__ gfb_map2_desc d) {
+  const int32_t E = (int32_t)d.ext[1];
+  for (int32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < E; i += gridDim.x * blockDim.x) {
+    double sum = 0.0;
+    for (int s = 0; s < d.nsplit; ++s) sum += ((const double *)d.workspace)[(int64_t)s * E + i];
+    const gfb_m2_operand &wo = d.out[0];
+    const int32_t off = (int32_t)wo.c0 + (int32_t)wo.s[1] * i;
+    const bool inside = i >= d.clear_lo[1] && i < d.clear_hi[1];
+    store_as<T>(const_cast<void *>(wo.base), wo.dtype, off, m2_base<T>(d, inside, off) + (T)sum);
+  }
+}
+
+// MODE: the one mode a generated body is used with, or -1 (every mode)
+template <typename T, int V, typename Body, int MODE = -1>
+inline int launch_map2(const gfb_map2_desc &d, cudaStream_t st) {
+  const int nd = d.ndim;
+  const int64_t E = d.ext[nd - 1];
+  int64_t rows = 1;
+  for (int dd = 0; dd < nd - 1; ++dd) rows *= d.ext[dd];
+  const int64_t cap = (int64_t)sm_count() * 8;  // resident CTAs of 256 threads
+  if (d.mode != MODE && MODE != -1) return set_error(GFB_EINVAL, "gfb_map2_launch: generated body used in another mode");
+  if constexpr (MODE == -1 || MODE == 0) {
+    if (d.mode == 0) {
+      const int64_t cpr = ceil_div(E, 32 * V);
+      if (nd == 2 && E < 32 * V && E < 512) {
+        const uint64_t magic = (((uint64_t)1 << 40) + (uint64_t)E - 1) / (uint64_t)E;
+        const int64_t blocks =
+            std::max<int64_t>(std::min<int64_t>(ceil_div(rows * E, 32 * V * kM2Warps), cap * 4), 1);
+        map2_pointwise_kernel<T, V, 1, Body><<<(unsigned)blocks, 256, 0, st>>>(d, (int32_t)rows, (int32_t)cpr, magic);
+      } else {
+        const int64_t blocks = std::max<int64_t>(std::min<int64_t>(ceil_div(rows * cpr, kM2Warps), cap * 4), 1);
+        if (nd == 2)
+          map2_pointwise_kernel<T, V, 0, Body><<<(unsigned)blocks, 256, 0, st>>>(d, (int32_t)rows, (int32_t)cpr, 0);
+        else
+          map2_pointwise_kernel<T, V, 2, Body><<<(unsigned)blocks, 256, 0, st>>>(d, (int32_t)rows, (int32_t)cpr, 0);
+      }
+    }
+  }
+  if constexpr (MODE == -1 || MODE == 1) {
+    if (d.mode == 1) {
+      const int64_t blocks = std::max<int64_t>(std::min<int64_t>(ceil_div(rows, kM2Warps), cap * 4), 1);
+      if (nd == 2)
+        map2_reduce_inner_kernel<T, V, true, Body><<<(unsigned)blocks, 256, 0, st>>>(d, (int32_t)rows);
+      else
+        map2_reduce_inner_kernel<T, V, false, Body><<<(unsigned)blocks, 256, 0, st>>>(d, (int32_t)rows);
+    }
+  }
+  if constexpr (MODE == -1 || MODE == 2) {
+    if (d.mode == 2) {
+      dim3 grid((unsigned)ceil_div(E, 32), (unsigned)d.nsplit);
+      map2_reduce_outer_kernel<T, V, Body><<<grid, 256, 0, st>>>(d);
+      if (d.nsplit > 1) {
+        const unsigned blocks = (unsigned)std::min<int64_t>(ceil_div(E, 256), cap);
+        map2_finish_kernel<T><<<blocks, 256, 0, st>>>(d);
+      }
+    }
+  }
+  return check_launch("map2");
+}
+
+}  // namespace gfb

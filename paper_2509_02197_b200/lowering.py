@@ -721,6 +721,259 @@ class CopyOp(Op):
             L.check(rt.lib.gfb_copy(self.dst.ptr, self.src.ptr, self.dst.nbytes, stream), "copy")
 
 
+def packed_code(code: "Code", segs) -> list | None:
+    """Bytecode for gfb_map2: op | depth_before << 6 | arg << 10 per
+    instruction, or None if a segment needs more than GFB_M2_DEPTH slots."""
+    out = [0] * len(code.code)
+    for start, n in segs:
+        depth = 0
+        for pc in range(start, start + n):
+            op, arg = code.code[pc], code.arg[pc]
+            out[pc] = op | (depth << 6) | (arg << 10)
+            if op in (L.OP_IN, L.OP_CONST):
+                depth += 1
+                if depth > L.M2DEPTH:
+                    return None
+            elif op < L.OP_NEG:
+                depth -= 1
+    return out
+
+
+def fold_loops(space, flats, labels):
+    """Loop dimensions of a rectangular space for gfb_map2: parameters in
+    the given order (labels[p] groups them; only same-label neighbours
+    merge), zero-based coordinates with first/step folded into each
+    operand's (c0, strides), extent-1 dimensions dropped, and adjacent
+    dimensions merged when every operand's strides allow.
+    flats: per operand (c0, [stride per parameter]); labels: per parameter in
+    loop order, list of (param, label). Returns (ext, [(c0, strides)], dim labels)."""
+    dims = [(p, lab) for p, lab in labels if space.ext[p] > 1]
+    ops = []
+    for c0, st in flats:
+        c0f = c0 + sum(st[p] * space.first[p] for p in range(space.np))
+        ops.append([c0f, [st[p] * space.step[p] for p, _ in dims]])
+    ext = [space.ext[p] for p, _ in dims]
+    labs = [lab for _, lab in dims]
+    i = len(ext) - 2
+    while i >= 0:
+        if labs[i] == labs[i + 1] and all(o[1][i] == ext[i + 1] * o[1][i + 1] for o in ops):
+            ext[i] *= ext[i + 1]
+            for o in ops:
+                o[1][i] = o[1][i + 1]
+                del o[1][i + 1]
+            del ext[i + 1]
+            del labs[i + 1]
+        i -= 1
+    return ext, ops, labs
+
+
+def _fits_i32(ext, ops) -> bool:
+    """gfb_map2 indexes in int32: point count and every operand offset."""
+    if int(np.prod(ext, dtype=np.int64)) >= 2**31 - 4096:
+        return False
+    for c0, st in ops:
+        lo = hi = c0
+        for e, v in zip(ext, st):
+            a = v * (e - 1)
+            lo, hi = lo + min(a, 0), hi + max(a, 0)
+        if lo < 0 or hi >= 2**31:
+            return False
+    return True
+
+
+class Map2Op(Op):
+    """Vectorised pointwise map or one-dimensional reduction (csrc/map2.cu)."""
+
+    def __init__(self, mode, ext, ins, outs, code, segs, compute_f64, *, clear_mode=1, clear_box=None, nsplit=1,
+                 family="map_pointwise"):
+        # ins: [(Buffer, c0, strides)]; outs: [(Buffer, c0, strides, wcr)]
+        self.mode, self.ext, self.ins, self.outs = mode, ext, ins, outs
+        self.code, self.segs, self.compute_f64 = code, segs, compute_f64
+        self.clear_mode, self.clear_box, self.nsplit = clear_mode, clear_box, nsplit
+        self.family = family
+        self.vec = 4  # informational: the kernel picks 4 (fp32) / 2 (fp64) points per lane
+        self._refresh()
+
+    def _refresh(self):
+        self.reads = tuple(b for b, _, _ in self.ins) + tuple(
+            b for b, _, _, w in self.outs if w == 1 or (self.mode != 0 and self.clear_mode in (0, 2)))
+        self.writes = tuple(b for b, _, _, _ in self.outs)
+
+    def remap(self, f):
+        self.ins = [(f(b), c0, st) for b, c0, st in self.ins]
+        self.outs = [(f(b), c0, st, w) for b, c0, st, w in self.outs]
+        self._refresh()
+
+    def workspace_bytes(self):
+        return self.nsplit * self.ext[1] * 8 if self.mode == 2 and self.nsplit > 1 else 0
+
+    def prepare(self, rt):
+        d = L.Map2Desc()
+        d.mode, d.compute_f64, d.ndim, d.vec = self.mode, 1 if self.compute_f64 else 0, len(self.ext), self.vec
+        d.n_in, d.n_out = len(self.ins), len(self.outs)
+        d.clear_mode, d.nsplit = self.clear_mode, self.nsplit
+        for i, e in enumerate(self.ext):
+            d.ext[i] = e
+            d.clear_lo[i], d.clear_hi[i] = (self.clear_box[i] if self.clear_box else (0, e))
+        for k, (b, c0, st) in enumerate(self.ins):
+            o = d.in_[k]
+            o.base, o.dtype, o.c0 = b.ptr, b.dtype, c0
+            for i, v in enumerate(st):
+                o.s[i] = v
+        for k, (b, c0, st, w) in enumerate(self.outs):
+            o = d.out[k]
+            o.base, o.dtype, o.c0 = b.ptr, b.dtype, c0
+            for i, v in enumerate(st):
+                o.s[i] = v
+            d.wcr[k] = w
+            d.code_start[k], d.code_len[k] = self.segs[k]
+        for i, v in enumerate(self.code_words):
+            d.code[i] = v
+        for i, v in enumerate(self.code.consts):
+            d.consts[i] = v
+        d.workspace = rt.workspace_ptr if self.workspace_bytes() else None
+        d.err = rt.err_ptr
+        self.desc = d
+        self._ref = C.byref(d)
+
+    def launch(self, rt, stream):
+        L.check(rt.lib.gfb_map2_launch(self._ref, stream), "map2")
+
+
+def map2_pointwise(space, ins, outs, code, segs, compute_f64):
+    """Map2Op for a rectangular pointwise map, or None (generic evaluator).
+    ins: [Access]; outs: [(Access, wcr)]."""
+    if space.triangular or space.empty or len(outs) > L.M2OUTS or os.environ.get("GFB_MAP2", "1") == "0":
+        return None
+    if any(w not in (0, 1) for _, w in outs):
+        return None
+    words = packed_code(code, segs)
+    if words is None:
+        return None
+    np_ = space.np
+    in_roots = [a.buf.root().bid for a in ins]
+    out_roots = [a.buf.root().bid for a, _ in outs]
+    if len(outs) > 1 and (len(set(out_roots)) != len(out_roots) or set(out_roots) & set(in_roots)):
+        return None  # read-all-then-write across outputs needs the generic evaluator
+    if len(outs) == 1 and out_roots[0] in in_roots:
+        fo = outs[0][0].flat(np_)
+        if any(a.buf.root().bid == out_roots[0] and (a.flat(np_) != fo or a.buf.root_offset() !=
+                                                      outs[0][0].buf.root_offset()) for a in ins):
+            return None
+    flats = [a.flat(np_) for a in ins] + [a.flat(np_) for a, _ in outs]
+    # innermost loop dimension: the parameter with the smallest output stride
+    o0 = flats[len(ins)][1]
+    order = list(range(np_))
+    cand = [p for p in order if o0[p] != 0 and space.ext[p] > 1]
+    if cand:
+        best = min(cand, key=lambda p: (abs(o0[p]), -p))
+        order.remove(best)
+        order.append(best)
+    ext, ops, _ = fold_loops(space, flats, [(p, 0) for p in order])
+    while len(ext) < 2:  # the kernels walk (row, innermost) pairs
+        ext = [1] + ext
+        ops = [[c0, [0] + st] for c0, st in ops]
+    if len(ext) > L.M2DIMS or not _fits_i32(ext, ops):
+        return None
+    op = Map2Op(0, ext, [(a.buf, c0, st) for a, (c0, st) in zip(ins, ops[:len(ins)])],
+                [(a.buf, c0, st, w) for (a, w), (c0, st) in zip(outs, ops[len(ins):])], code, segs, compute_f64)
+    op.code_words = words
+    return op
+
+
+def map2_reduce(space, acc, ins, dst, ybox, clear_mode, cbox, code, seg, compute_f64):
+    """Map2Op for a single-term gather whose output subset selects
+    parameters one-to-one (every other parameter is summed over), when the
+    summed parameters fold into one loop dimension; else None."""
+    if space.triangular or space.empty or os.environ.get("GFB_MAP2", "1") == "0":
+        return None
+    np_ = space.np
+    Cm, off = acc.matrix(np_)
+    kept = {}
+    for r, row in enumerate(Cm):
+        nz = [p for p, c in enumerate(row) if c != 0]
+        if len(nz) != 1 or row[nz[0]] != 1 or nz[0] in kept.values():
+            return None
+        kept[r] = nz[0]
+    # the targets must be exactly the image of the space (no extra clears)
+    for r, p in kept.items():
+        lo = space.first[p] + off[r]
+        if space.step[p] != 1 or ybox[r] != (lo, lo + space.ext[p]):
+            return None
+    kp = set(kept.values())
+    red = [p for p in range(np_) if p not in kp and space.ext[p] > 1]
+    if not red:
+        return None
+    words = packed_code(code, [seg])
+    if words is None:
+        return None
+    flats = [a.flat(np_) for a in ins] + [acc.flat(np_)]
+    # innermost contiguous parameter of the reads decides the layout
+    smallest = None
+    for c0, st in flats[:-1]:
+        for p in range(np_):
+            if st[p] != 0 and space.ext[p] > 1 and (smallest is None or abs(st[p]) < smallest[0]):
+                smallest = (abs(st[p]), p)
+    inner_reduced = smallest is None or smallest[1] not in kp
+    keptp = [p for p in range(np_) if p in kp]
+    labels = ([(p, 0) for p in keptp] + [(p, 1) for p in red]) if inner_reduced else \
+        ([(p, 1) for p in red] + [(p, 0) for p in keptp])
+    ext, ops, labs = fold_loops(space, flats, labels)
+    if labs.count(1) != 1:
+        return None
+    # clear box in loop coordinates of the kept dimensions
+    cl = None
+    if clear_mode == 2:
+        kept_dims = [p for p, _ in labels if space.ext[p] > 1 and p in kp]
+        if len(kept_dims) != labs.count(0):
+            return None  # kept dimensions merged: clear box not expressible per dimension
+        cl = []
+        r_of = {p: r for r, p in kept.items()}
+        kd = iter(kept_dims)
+        for lab in labs:
+            if lab == 1:
+                cl.append((0, 0))
+                continue
+            p = next(kd)
+            r = r_of[p]
+            base = space.first[p] + off[r]
+            cl.append((cbox[r][0] - base, cbox[r][1] - base))
+        # kept params of extent 1 must lie inside the clear box
+        for r, p in kept.items():
+            if space.ext[p] == 1 and not (cbox[r][0] <= space.first[p] + off[r] < cbox[r][1]):
+                return None
+    if inner_reduced:
+        mode = 1
+        if labs[-1] != 1:
+            return None
+        if not ext[:-1]:
+            ext = [1] + ext
+            ops = [[c0, [0] + st] for c0, st in ops]
+            if cl is not None:
+                cl = [(0, 1)] + cl
+    else:
+        mode = 2
+        if labs == [1]:
+            ext, ops = ext + [1], [[c0, st + [0]] for c0, st in ops]
+            if cl is not None:
+                cl = cl + [(0, 1)]
+            labs = [1, 0]
+        if labs != [1, 0]:
+            return None
+    if len(ext) > L.M2DIMS or not _fits_i32(ext, ops):
+        return None
+    nsplit = 1
+    if mode == 2:
+        chunks = -(-ext[1] // 32)
+        nsplit = int(max(1, min(-(-2 * 148 // chunks), ext[0] // 64, 4096)))
+    n_in = len(ins)
+    op = Map2Op(mode, ext, [(a.buf, c0, st) for a, (c0, st) in zip(ins, ops[:n_in])],
+                [(dst, ops[n_in][0], ops[n_in][1], 0)], code, [seg], compute_f64, clear_mode=clear_mode,
+                clear_box=cl, nsplit=nsplit, family="map_reduce")
+    op.code_words = words
+    return op
+
+
 def contract_tile(N: int):
     """(BM, BN) of the contraction kernel variant gfb_contract_launch picks."""
     if N <= 16:
@@ -1707,7 +1960,8 @@ class ProgramRun:
                 else:
                     self.low.materialize(buf)
             out_specs.append((acc, w))
-        self.low.emit(MapOp(space, [ins[c] for c in conns], out_specs, code, segs, compute_f64))
+        op = map2_pointwise(space, [ins[c] for c in conns], out_specs, code, segs, compute_f64)
+        self.low.emit(op or MapOp(space, [ins[c] for c in conns], out_specs, code, segs, compute_f64))
 
     def _broadcast_pointwise(self, space, t, out, ins):
         """`out[all] (+)= c * scalar` (the reduce_sum adjoint map,
@@ -1820,6 +2074,12 @@ class ProgramRun:
             Cm, off = acc.matrix(np_)
             row_of, order = pivot_rows(Cm, np_)
             terms.append((row_of, order, Cm, off, seg))
+        if len(group) == 1:
+            op = map2_reduce(space, group[0][1], [ins[c] for c in used], dst, ybox, clear_mode, cbox, code,
+                             terms[0][4], compute_f64)
+            if op is not None:
+                self.low.emit(op)
+                return
         # work shape: free iterations per target
         F = max(int(np.prod([space.ext[p] for p in range(np_) if rof[p] < 0], dtype=np.int64))
                 for rof, *_ in terms)

@@ -16,6 +16,7 @@ from paper_2509_02197_b200 import _lib as L
 from paper_2509_02197_b200.lowering import (
     BroadcastOp,
     ContractOp,
+    Map2Op,
     CopyOp,
     EwOp,
     FillOp,
@@ -181,6 +182,8 @@ class Emulator:
             self.star_pair(op.desc)
         elif isinstance(op, ContractOp):
             self.contract(op.desc)
+        elif isinstance(op, Map2Op):
+            self.map2(op.desc)
         elif isinstance(op, FillOp):
             a, o = self.arr(op.dst.ptr)
             if op.whole:
@@ -274,6 +277,55 @@ class Emulator:
         else:
             base = da[off]
         da[off] = (base + acc).astype(da.dtype)
+
+    def map2(self, d):
+        T = np.float64 if d.compute_f64 else np.float32
+        nd = d.ndim
+        ext = [d.ext[i] for i in range(nd)]
+        k = np.indices(ext, dtype=np.int64).reshape(nd, -1)
+
+        def offs(o):
+            return o.c0 + sum(o.s[i] * k[i] for i in range(nd))
+
+        def fetch(j):
+            o = d.in_[j]
+            a, base = self.arr(o.base)
+            return a[base + offs(o)].astype(T)
+
+        words = list(d.code)
+        code = [w & 63 for w in words]
+        arg = [w >> 10 for w in words]
+        consts = list(d.consts)
+        vals = [np.broadcast_to(np.asarray(_vm(code, arg, d.code_start[o], d.code_len[o], consts, fetch, T, self.err),
+                                           dtype=T), k.shape[1:]) for o in range(d.n_out)]
+        if d.mode == 0:
+            for o in range(d.n_out):
+                w = d.out[o]
+                a, base = self.arr(w.base)
+                idx = base + offs(w)
+                a[idx] = vals[o] if d.wcr[o] == 0 else a[idx] + vals[o]
+            return
+        w = d.out[0]
+        a, base = self.arr(w.base)
+        idx = (base + offs(w)).reshape(ext)
+        v = vals[0].reshape(ext)
+        if d.mode == 1:
+            acc, tgt = v.sum(axis=-1, dtype=T), idx[..., 0]
+            kk = k.reshape([nd] + ext)[:-1, ..., 0]
+            inside = np.ones(tgt.shape, dtype=bool)
+            for i in range(nd - 1):
+                inside &= (kk[i] >= d.clear_lo[i]) & (kk[i] < d.clear_hi[i])
+        else:
+            acc, tgt = v.sum(axis=0, dtype=T), idx[0]
+            kk = np.arange(ext[1])
+            inside = (kk >= d.clear_lo[1]) & (kk < d.clear_hi[1])
+        if d.clear_mode in (1, 3):
+            base_v = 0
+        elif d.clear_mode == 2:
+            base_v = np.where(inside, 0, a[tgt])
+        else:
+            base_v = a[tgt]
+        a[tgt] = base_v + acc
 
     def map(self, d):
         T = np.float64 if d.compute_f64 else np.float32
