@@ -26,7 +26,7 @@
 extern "C" {
 #endif
 
-#define GFB_ABI_VERSION 7
+#define GFB_ABI_VERSION 8
 
 #define GFB_MAX_PARAMS 8    /* map parameters (iteration-space rank) */
 #define GFB_MAX_RANK 8      /* array rank */
@@ -222,11 +222,17 @@ typedef struct {
  * inside the dead box (values the next writer overwrites unread).
  * Elements outside a's / b's region take the old X / Z values.
  */
+/* gfb_star_pair_desc.flags: outside the op's region Z (X) is a copy of its
+ * old value; when the host knows the target twin already holds equal values
+ * there (ping-pong buffers after both were initialised), the copy is skipped */
+#define GFB_STAR_SKIP_ZCOPY 1
+#define GFB_STAR_SKIP_XCOPY 2
+
 typedef struct {
   int32_t rank;   /* 2 or 3 */
   int32_t dtype;
   int32_t xwrite;
-  int32_t _pad;
+  int32_t flags;  /* GFB_STAR_SKIP_* */
   int64_t dims[3];
   gfb_star_op a, b;
   const void *y, *xold;

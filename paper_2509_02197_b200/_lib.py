@@ -19,9 +19,10 @@ MAXCODE = 128
 MAXCONST = 24
 MAXTAPS = 32
 MAXSRCS = 4
-ABI_VERSION = 7
+ABI_VERSION = 8
 
 F32, F64 = 0, 1
+STAR_SKIP_ZCOPY, STAR_SKIP_XCOPY = 1, 2
 
 # bytecode opcodes (enum gfb_op)
 OP_IN, OP_CONST, OP_ADD, OP_SUB, OP_MUL, OP_DIV, OP_IDIV, OP_MOD, OP_MIN, OP_MAX, OP_POW = range(11)
@@ -82,7 +83,7 @@ class StarOp(C.Structure):
 
 
 class StarPairDesc(C.Structure):
-    _fields_ = [("rank", i32), ("dtype", i32), ("xwrite", i32), ("_pad", i32), ("dims", i64 * 3),
+    _fields_ = [("rank", i32), ("dtype", i32), ("xwrite", i32), ("flags", i32), ("dims", i64 * 3),
                 ("a", StarOp), ("b", StarOp), ("y", vp), ("xold", vp), ("xout", vp), ("zold", vp), ("zout", vp),
                 ("dead_lo", i64 * 3), ("dead_hi", i64 * 3), ("plane0", i64), ("zlo", i64), ("zhi", i64),
                 ("global_d0", i64)]

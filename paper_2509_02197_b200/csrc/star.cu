@@ -156,7 +156,7 @@ __device__ __forceinline__ void star_pair_checked(const StarPairDev &d, T (*xs)[
     } else {
       v = Xo[off];
     }
-    if (own && core && d.xwrite && !(m & kDead)) Xn[off] = v;
+    if (own && core && d.xwrite && !(m & kDead) && !(d.skipx && !(m & kRegion))) Xn[off] = v;
     return v;
   };
   prefetch(qbeg);
@@ -196,6 +196,7 @@ __device__ __forceinline__ void star_pair_checked(const StarPairDev &d, T (*xs)[
           w += (on & 32u) ? cb[5] * xs[sc][ty + 1][tx] : T(0);
           w += (on & 64u) ? cb[6] * xs[sc][ty + 1][tx + 2] : T(0);
         } else {
+          if (d.skipz) continue;
           w = Zo[off];
         }
         Zn[off] = w;
@@ -335,6 +336,8 @@ extern "C" int gfb_star_pair_launch(const gfb_star_pair_desc *s, void *stream) {
   d.ps = (int32_t)(dims[1] * dims[2]);
   d.rs = (int32_t)dims[2];
   d.xwrite = s->xwrite;
+  d.skipz = (s->flags & GFB_STAR_SKIP_ZCOPY) ? 1 : 0;
+  d.skipx = (s->flags & GFB_STAR_SKIP_XCOPY) ? 1 : 0;
   if (s->rank == 3) {
     d.p0 = (int32_t)s->plane0;
     d.gd0 = (int32_t)(s->global_d0 > 0 ? s->global_d0 : dims[0]);

@@ -1,12 +1,28 @@
 // TMA-fed variant of the fused star-pair kernel (see star.cu for the
-// algorithm). The source planes Y(q) are moved into a shared-memory ring by
-// the Tensor Memory Accelerator (cp.async.bulk.tensor, one elected thread,
-// mbarrier transaction counts), kDist planes ahead of use, with the one-
-// point halo window [j0-2, j0+kPY+2) x [k0-2, k0+kPX+2) per plane; TMA
-// zero-fills the parts that fall outside the array. Every tap of the first
-// sweep is then one shared-memory load at an immediate offset, the global
-// traffic is bulk and asynchronous, and the SMs spend their issue slots on
-// the arithmetic.
+// algorithm: X = a(Y); Z = b(X), two radius-1 star sweeps in one launch).
+//
+// One CTA owns a (tPY x tPX) = 32 x 32 column of Z over tPM planes and
+// marches along dim 0. The source planes Y(q), with a two-point halo in
+// (j, k), are moved into a shared-memory ring by the Tensor Memory
+// Accelerator (cp.async.bulk.tensor, one elected thread, mbarrier
+// transaction counts) kDist planes ahead of use; TMA zero-fills whatever
+// falls outside the array. Per plane q the CTA computes X(q) on its one-point
+// halo window (kept as X~ in a 3-slot shared ring), then Z(q - 1).
+//
+// Thread (tx, ty) owns the four Z points (4ty + u, tx), u < 4, and the X
+// points at the same positions. The dim-0 taps of both sweeps and the
+// j-neighbours inside the thread's four rows come from registers rolled
+// along the march, so per point only the +-k neighbours (and one j-neighbour
+// per four rows) are shared-memory loads. Warps 0..4 also compute one point
+// each of the X halo ring. The CTA-uniform overhead of a plane (ring
+// issue, barrier, predicates) is spread over 1024 points.
+//
+// Masks are data: op a's taps are in source-mask form (every masked tap
+// reads "source inside M_a"), so values outside M_a are zeroed in the Y ring
+// once per plane and every tap runs unmasked; op b's source mask is applied
+// when X is stored (X~ = X inside M_b, else 0). Points whose region / base /
+// write-back status differs from the plane's common case take a fix-up
+// branch; a plane whose whole window is common takes none.
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
@@ -17,20 +33,35 @@
 
 namespace gfb {
 
-// Y window: halo 2 in (j, k). The row pitch is padded so that a column of
-// the window (the edge X points) spreads over more shared-memory banks; the
-// TMA box inner extent must stay a multiple of 16 bytes.
-constexpr int YJ = kPY + 4;
+#ifndef GFB_STAR_TPY
+#define GFB_STAR_TPY 32
+#endif
+#ifndef GFB_STAR_KR
+#define GFB_STAR_KR 4
+#endif
+#ifndef GFB_STAR_TPM
+#define GFB_STAR_TPM 32
+#endif
+#ifndef GFB_STAR_UNROLL
+#define GFB_STAR_UNROLL 1
+#endif
+constexpr int tPX = 32, tPY = GFB_STAR_TPY, tPM = GFB_STAR_TPM;  // CTA tile (k, j) and planes
+constexpr int kR = GFB_STAR_KR;                                   // Z rows per thread
+constexpr int tThreads = tPX * (tPY / kR);
+static_assert(tPY % kR == 0 && tThreads % 32 == 0 && tThreads <= 512, "tile / thread mismatch");
+static_assert(2 * (tPY + 2) <= tThreads - 64, "halo-ring columns need warps 2..");
+constexpr int YJ = tPY + 4;                  // Y window rows (halo 2)
+// Y window pitch: halo 2 in k; padded so an edge column spreads over more
+// shared-memory banks (the TMA box inner extent stays a multiple of 16 B)
 template <typename T>
 __host__ __device__ constexpr int ypitch() {
-  return sizeof(T) == 8 ? kPX + 6 : kPX + 4;
+  return sizeof(T) == 8 ? tPX + 6 : tPX + 4;
 }
-constexpr int kDist = 5;        // planes in flight ahead of use
-constexpr int NSY = kDist + 3;  // Y ring slots (8: index by mask)
-static_assert((NSY & (NSY - 1)) == 0, "Y ring must be a power of two");
-constexpr int HX = kPX + 2;           // X~ window pitch (halo 1)
-constexpr int XS = (kPY + 2) * HX;    // X~ window plane
-constexpr int kTT = kPX * kPY / 2;    // 256 threads: each owns two adjacent Z rows
+constexpr int NSY = 6;         // Y ring slots
+constexpr int kDist = NSY - 2; // planes issued ahead (slot of Y(q-1) is free at step q)
+constexpr int HX = tPX + 2;    // X~ window pitch (halo 1)
+constexpr int XS = (tPY + 2) * HX;
+constexpr int NXS = 3;         // X~ ring slots
 
 __device__ __forceinline__ uint32_t smem_u32(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
 
@@ -64,6 +95,19 @@ __device__ __forceinline__ void tma_load_3d(void *dst, const CUtensorMap *map, u
       : "memory");
 }
 
+// Ampere-style asynchronous copy of one element into shared memory: the
+// old-value loads of fix-up points are issued one plane ahead, so their
+// DRAM latency overlaps a whole march step instead of stalling it.
+template <typename T>
+__device__ __forceinline__ void cp_async_elem(T *dst, const T *src) {
+  if constexpr (sizeof(T) == 8)
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+  else
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
+
 // ring slot stride (elements): TMA destinations must be 128-byte aligned
 template <typename T>
 __host__ __device__ constexpr int yslot() {
@@ -71,7 +115,7 @@ __host__ __device__ constexpr int yslot() {
 }
 template <typename T>
 __host__ __device__ constexpr size_t star_tma_smem_bytes() {
-  return (size_t)NSY * yslot<T>() * sizeof(T) + (size_t)4 * XS * sizeof(T) + NSY * sizeof(uint64_t);
+  return (size_t)NSY * yslot<T>() * sizeof(T) + (size_t)NXS * XS * sizeof(T) + NSY * sizeof(uint64_t);
 }
 
 template <typename T>
@@ -85,30 +129,57 @@ __device__ __forceinline__ float coef<float>(const StarOpDev &o, int p) {
   return o.fcoef[p];
 }
 
-// One CTA: a (kPY x kPX) column of Z over planes [i0, i1), marching along
-// dim 0. Per plane q: X(q) = a(Y) on the CTA's halo window, then Z(q - 1) =
-// b(X). Thread (tx, ty) owns the Z points (2ty, tx), (2ty + 1, tx) and the X
-// points at the same positions, so the dim-0 taps of both sweeps and the
-// shared j-neighbour come from registers rolled along the march; only the
-// remaining in-plane neighbours are shared-memory loads. Warps 0..3 also
-// compute one point each of the X halo ring (rows 0 / kPY + 1, columns
-// 0 / kPX + 1). Shared-memory wavefronts, not HBM, bound this kernel, so
-// every load removed here is time.
-//
-// Masks are data: op a's taps are in source-mask form (every masked tap
-// reads "source inside M_a"), so values outside M_a are zeroed in the Y ring
-// once per plane and every tap runs unmasked; op b's source mask is applied
-// when X is stored (X~ = X inside M_b, else 0). Points whose region / base /
-// write-back status differs from the CTA's common case take a fix-up branch.
+// Per-coordinate predicate words of the CTA (star_common.cuh coord_bits;
+// op-a words also carry kSrcB = "inside op b's source mask").
+struct TmaWords {
+  uint32_t aj[tPY + 2], ak[tPX + 2], bj[tPY], bk[tPX], ai[tPM + 2], bi[tPM];
+  uint32_t jk[2];  // AND over the X window / Z tile of the (j, k) words
+};
+
+__device__ __forceinline__ void tma_prologue(const StarPairDev &d, int i0, int j0, int k0, int tid, TmaWords &w) {
+  auto srcb = [&](int dim, int c) { return (c >= d.b.smlo[dim] && c < d.b.smhi[dim]) ? kSrcB : 0u; };
+  constexpr int nA = tPY + 2, nB = nA + tPX + 2, nC = nB + tPY, nD = nC + tPX, nE = nD + tPM + 2, nF = nE + tPM;
+  for (int e = tid; e < nF; e += tThreads) {
+    if (e < nA) {
+      w.aj[e] = coord_bits(d.a, 1, j0 - 1 + e, d.d1, d.dlo, d.dhi) | srcb(1, j0 - 1 + e);
+    } else if (e < nB) {
+      const int c = k0 - 1 + (e - nA);
+      w.ak[e - nA] = coord_bits(d.a, 2, c, d.d2, d.dlo, d.dhi) | srcb(2, c);
+    } else if (e < nC) {
+      w.bj[e - nB] = coord_bits(d.b, 1, j0 + (e - nB), d.d1, nullptr, nullptr);
+    } else if (e < nD) {
+      w.bk[e - nC] = coord_bits(d.b, 2, k0 + (e - nC), d.d2, nullptr, nullptr);
+    } else if (e < nE) {
+      const int c = i0 - 1 + (e - nD) + d.p0;
+      w.ai[e - nD] = coord_bits(d.a, 0, c, d.gd0, d.dlo, d.dhi) | srcb(0, c);
+    } else {
+      w.bi[e - nE] = coord_bits(d.b, 0, i0 + (e - nE) + d.p0, d.gd0, nullptr, nullptr);
+    }
+  }
+  __syncthreads();
+  if (tid < 32) {
+    uint32_t va = ~0u, vb = ~0u;
+    for (int e = tid; e < tPY + 2; e += 32) va &= w.aj[e];
+    for (int e = tid; e < tPX + 2; e += 32) va &= w.ak[e];
+    for (int e = tid; e < tPY; e += 32) vb &= w.bj[e];
+    for (int e = tid; e < tPX; e += 32) vb &= w.bk[e];
+    va = __reduce_and_sync(0xffffffffu, va);
+    vb = __reduce_and_sync(0xffffffffu, vb);
+    if (tid == 0) {
+      w.jk[0] = va;
+      w.jk[1] = vb;
+    }
+  }
+}
+
 template <typename T, bool HAS_I>
 __device__ __forceinline__ void star_tma_body(const CUtensorMap *ymap, const StarPairDev &d, T *ys, T *xs,
-                                              uint64_t *mbar, const uint32_t *aj, const uint32_t *ak,
-                                              const uint32_t *bj, const uint32_t *bk, const uint32_t *ai,
-                                              const uint32_t *bi, int i0, int i1) {
+                                              uint64_t *mbar, const TmaWords &W, T (*xst)[kR + 1][tThreads],
+                                              int i0, int i1) {
   constexpr int YK = ypitch<T>();
   constexpr int YS = YJ * YK, YSS = yslot<T>();
-  const int tx = threadIdx.x, ty = threadIdx.y, tid = ty * kPX + tx;
-  const int k0 = blockIdx.x * kPX, j0 = blockIdx.y * kPY;
+  const int tx = threadIdx.x, ty = threadIdx.y, tid = ty * tPX + tx;
+  const int k0 = blockIdx.x * tPX, j0 = blockIdx.y * tPY;
   const T *__restrict__ Xo = (const T *)d.xold;
   const T *__restrict__ Zo = (const T *)d.zold;
   T *__restrict__ Xn = (T *)d.xout;
@@ -120,55 +191,62 @@ __device__ __forceinline__ void star_tma_body(const CUtensorMap *ymap, const Sta
   const int ylo = HAS_I ? max(qbeg - 1, 0) : 0;
   const int yhi = HAS_I ? min(min(qend, d.d0 - 1) + 1, d.d0 - 1) : 0;
   constexpr uint32_t kTx = (uint32_t)(YS * sizeof(T));
-  auto slot_of = [&](int p) { return ys + ((p - ylo) & (NSY - 1)) * YSS; };
+  auto slot_of = [&](int p) { return ys + ((p - ylo + NSY) % NSY) * YSS; };
   auto issue = [&](int p) {
-    const int sl = (p - ylo) & (NSY - 1);
+    const int sl = (p - ylo) % NSY;
     mbar_expect_tx(&mbar[sl], kTx);
     tma_load_3d(ys + sl * YSS, ymap, &mbar[sl], k0 - 2, j0 - 2, p);
   };
   auto wait_plane = [&](int p) {
     const int r = p - ylo;
-    mbar_wait(&mbar[r & (NSY - 1)], (uint32_t)((r / NSY) & 1));
+    mbar_wait(&mbar[r % NSY], (uint32_t)((r / NSY) & 1));
   };
   if (tid == 0) {
     for (int s = 0; s < NSY; ++s) mbar_init(&mbar[s], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
-  const int pre_hi = min(ylo + kDist + 1, yhi);
+  // planes issued before the march: the loop issues q + 1 + kDist from
+  // q = qbeg on; when the march starts at plane 0 the slot of plane -1 (a
+  // zero plane) must stay free, hence qbeg + kDist rather than a full ring
+  const int pre_hi = min(qbeg + kDist, yhi);
   if (tid == 0)
     for (int p = ylo; p <= pre_hi; ++p) issue(p);
 
   // this thread's points (window coordinates: X~ halo 1, Y halo 2)
-  const int hj0 = 2 * ty + 1, hk = tx + 1;
-  int rj = -1, rk = 0;  // halo-ring X point
+  const int hj0 = kR * ty + 1, hk = tx + 1;
+  int rj = -1, rk = 0;  // halo-ring X point: warps 0, 1 the end rows, then the end columns
   if (ty == 0) {
     rj = 0;
     rk = hk;
   } else if (ty == 1) {
-    rj = kPY + 1;
+    rj = tPY + 1;
     rk = hk;
-  } else if (ty == 2 && tx < kPY + 2) {
-    rj = tx;
-    rk = 0;
-  } else if (ty == 3 && tx < kPY + 2) {
-    rj = tx;
-    rk = kPX + 1;
+  } else {
+    const int g = (ty - 2) * 32 + tx;
+    if (g < 2 * (tPY + 2)) {
+      rj = g % (tPY + 2);
+      rk = g < tPY + 2 ? 0 : tPX + 1;
+    }
   }
   const bool ring = rj >= 0;
-  const int yo0 = (hj0 + 1) * YK + hk + 1, yo1 = yo0 + YK;
+  const int yo0 = (hj0 + 1) * YK + hk + 1;  // Y offset of row u: yo0 + u * YK
   const int yor = ring ? (rj + 1) * YK + rk + 1 : yo0;
-  const int xo0 = hj0 * HX + hk, xo1 = xo0 + HX;
+  const int xo0 = hj0 * HX + hk;  // X~ offset of row u: xo0 + u * HX
   const int xor_ = ring ? rj * HX + rk : xo0;
-  const int rel0 = (j0 + 2 * ty) * rs + (k0 + tx), rel1 = rel0 + rs;
+  const int rel0 = (j0 + kR * ty) * rs + (k0 + tx);  // global offset of row u: rel0 + u * rs
   const int relr = (j0 - 1 + rj) * rs + (k0 - 1 + rk);
-  const uint32_t mx0 = aj[hj0] & ak[hk], mx1 = aj[hj0 + 1] & ak[hk];
-  const uint32_t mxr = ring ? (aj[rj] & ak[rk]) : 0u;
-  const uint32_t mz0 = bj[2 * ty] & bk[tx], mz1 = bj[2 * ty + 1] & bk[tx];
+  uint32_t mx[kR], mz[kR];
+#pragma unroll
+  for (int u = 0; u < kR; ++u) {
+    mx[u] = W.aj[hj0 + u] & W.ak[hk];
+    mz[u] = W.bj[kR * ty + u] & W.bk[tx];
+  }
+  const uint32_t mxr = ring ? (W.aj[rj] & W.ak[rk]) : 0u;
 
   const bool ysrc = d.a.srcmask == 1;
-  const bool yj_in = j0 - 2 >= d.a.smlo[1] && j0 + kPY + 2 <= d.a.smhi[1];
-  const bool yk_in = k0 - 2 >= d.a.smlo[2] && k0 + kPX + 2 <= d.a.smhi[2];
+  const bool yj_in = j0 - 2 >= d.a.smlo[1] && j0 + tPY + 2 <= d.a.smhi[1];
+  const bool yk_in = k0 - 2 >= d.a.smlo[2] && k0 + tPX + 2 <= d.a.smhi[2];
   auto prepare_plane = [&](int p) {
     // zero what the taps must not see: planes never loaded (outside the
     // local array) and, in source-mask form, values outside M_a
@@ -176,32 +254,50 @@ __device__ __forceinline__ void star_tma_body(const CUtensorMap *ymap, const Sta
     const int pg = p + d.p0;
     const bool outside = p < 0 || p >= d.d0 || (ysrc && (pg < d.a.smlo[0] || pg >= d.a.smhi[0]));
     if (outside) {
-      for (int e = tid; e < YS; e += kTT) slot[e] = T(0);
+      for (int e = tid; e < YS; e += tThreads) slot[e] = T(0);
     } else if (ysrc && !(yj_in && yk_in)) {
-      for (int e = tid; e < YS; e += kTT) {
+      for (int e = tid; e < YS; e += tThreads) {
         const int jj = e / YK, kk = e - jj * YK;
         const int j = j0 - 2 + jj, k = k0 - 2 + kk;
         if (j < d.a.smlo[1] || j >= d.a.smhi[1] || k < d.a.smlo[2] || k >= d.a.smhi[2]) slot[e] = T(0);
       }
     }
   };
-  // common-case predicate patterns (block-uniform)
+  // common-case predicate patterns
   const uint32_t xmask = kArray | kRegion | (amode == 2 ? kClear : 0u) | (d.xwrite ? kDead : 0u);
   const uint32_t xval = amode == 0 ? 0xffffffffu : xmask;  // mode 0: base always added -> fix-up
   const uint32_t zmask = kArray | kRegion | (bmode == 2 ? kClear : 0u);
   const uint32_t zval = bmode == 0 ? 0xffffffffu : zmask;
+  const uint32_t xfast_m = xmask | kSrcB;
+  // old X values a point's fix-up needs: outside op a's region (copy) or
+  // where the base is added (mode 0, mode 2 outside the clear box)
+  auto needs_xo = [&](uint32_t w) {
+    return (w & kArray) && (!(w & kRegion) || amode == 0 || (amode == 2 && !(w & kClear)));
+  };
+  // stage plane q's old values of this thread's fix-up points (slot u < kR:
+  // own rows, kR: ring point) into xst[q & 1]; nothing for a common plane
+  auto prefetch_xo = [&](int q) {
+    if (q > min(qend, d.d0 - 1)) return;
+    const uint32_t mi = W.ai[q - i0 + 1];
+    if (((mi & W.jk[0]) & xfast_m) == xfast_m && amode != 0) return;
+    const T *src = Xo + (size_t)q * ps;
+#pragma unroll
+    for (int u = 0; u < kR; ++u)
+      if (needs_xo(mi & mx[u])) cp_async_elem(&xst[q & 1][u][tid], src + rel0 + u * rs);
+    if (ring && needs_xo(mi & mxr)) cp_async_elem(&xst[q & 1][kR][tid], src + relr);
+    cp_async_commit();
+  };
   // X~ of one point from its tap sum; abnormal points take the fix-up
-  auto x_tilde = [&](T acc, uint32_t w, int rel, bool wb, int q) -> T {
+  auto x_tilde = [&](T acc, uint32_t w, int slot, int rel, bool wb, int q) -> T {
     if ((w & xmask) != xval) {
       if (!(w & kArray)) {
         acc = T(0);
       } else {
-        const int off = q * ps + rel;
         if (!(w & kRegion))
-          acc = Xo[off];
+          acc = xst[q & 1][slot][tid];
         else if (amode == 0 || (amode == 2 && !(w & kClear)))
-          acc += Xo[off];
-        if (wb && d.xwrite && !(w & kDead)) Xn[off] = acc;
+          acc += xst[q & 1][slot][tid];
+        if (wb && d.xwrite && !(w & kDead) && !(d.skipx && !(w & kRegion))) Xn[(size_t)q * ps + rel] = acc;
       }
     }
     return (w & kSrcB) ? acc : T(0);
@@ -211,21 +307,7 @@ __device__ __forceinline__ void star_tma_body(const CUtensorMap *ymap, const Sta
   const T b0 = coef<T>(d.b, 0), b1 = coef<T>(d.b, 1), b2 = coef<T>(d.b, 2), b3 = coef<T>(d.b, 3),
           b4 = coef<T>(d.b, 4), b5 = coef<T>(d.b, 5), b6 = coef<T>(d.b, 6);
 
-  // CTA-uniform "every point normal" tests: AND of the (j, k) predicate
-  // words over the X window / Z tile; per plane the dim-0 word completes it
-  __shared__ uint32_t s_jk[2];
-  if (ty == 0) {
-    uint32_t va = ak[tx] & (tx < kPY + 2 ? aj[tx] : ~0u) & (tx + 32 < HX ? ak[tx + 32] : ~0u);
-    uint32_t vb = bk[tx] & (tx < kPY ? bj[tx] : ~0u);
-    va = __reduce_and_sync(0xffffffffu, va);
-    vb = __reduce_and_sync(0xffffffffu, vb);
-    if (tx == 0) {
-      s_jk[0] = va;
-      s_jk[1] = vb;
-    }
-  }
-  const uint32_t xfast_m = xmask | kSrcB;
-
+  prefetch_xo(qbeg);
   for (int p = ylo; p <= min(qbeg + 1, yhi); ++p) wait_plane(p);
   if (HAS_I) {
     for (int p = qbeg - 1; p <= qbeg + 1; ++p) prepare_plane(p);
@@ -233,33 +315,37 @@ __device__ __forceinline__ void star_tma_body(const CUtensorMap *ymap, const Sta
     prepare_plane(0);
   }
   __syncthreads();
-  const uint32_t jka = (amode == 0) ? 0u : s_jk[0], jkb = (bmode == 0) ? 0u : s_jk[1];
+  const uint32_t jka = (amode == 0) ? 0u : W.jk[0], jkb = (bmode == 0) ? 0u : W.jk[1];
 
   // Registers rolled along the march, rotated by index (three live planes):
-  // y*[.] = Y centre values at the own (0, 1) and ring (r) X points,
-  // x*[.] = X~ at the own Z points. Step s of the unrolled loop finds
-  // Y(q - 1), Y(q) in slots s, s + 1 and loads Y(q + 1) into slot s + 2
-  // (mod 3); X~(q - 2), X~(q - 1) likewise and X~(q) goes to slot s + 2.
-  T y0[3], y1[3], yr[3], x0[3], x1[3];
+  // yv[u][.] = Y centre values at the own X points (row u), yr[.] at the
+  // ring point, xv[u][.] = X~ at the own Z points. Step S of the unrolled
+  // march finds Y(q - 1), Y(q) in slots S, S + 1 and loads Y(q + 1) into
+  // slot S + 2 (mod 3); X~(q - 2), X~(q - 1) likewise, X~(q) goes to S + 2.
+  T yv[kR][3], yr[3], xv[kR][3];
 #pragma unroll
-  for (int u = 0; u < 3; ++u) y0[u] = y1[u] = yr[u] = x0[u] = x1[u] = T(0);
+  for (int s = 0; s < 3; ++s) {
+    yr[s] = T(0);
+#pragma unroll
+    for (int u = 0; u < kR; ++u) yv[u][s] = xv[u][s] = T(0);
+  }
   {
     const T *yq = slot_of(qbeg);
-    y0[1] = yq[yo0];
-    y1[1] = yq[yo1];
+#pragma unroll
+    for (int u = 0; u < kR; ++u) yv[u][1] = yq[yo0 + u * YK];
     yr[1] = yq[yor];
     if (HAS_I) {
       const T *yqm = slot_of(qbeg - 1);
-      y0[0] = yqm[yo0];
-      y1[0] = yqm[yo1];
+#pragma unroll
+      for (int u = 0; u < kR; ++u) yv[u][0] = yqm[yo0 + u * YK];
       yr[0] = yqm[yor];
     }
   }
 
   auto step = [&](auto S, int q) {
     constexpr int M = decltype(S)::value, C = (M + 1) % 3, P = (M + 2) % 3;
-    x0[P] = T(0);
-    x1[P] = T(0);
+#pragma unroll
+    for (int u = 0; u < kR; ++u) xv[u][P] = T(0);
     if (q < d.d0) {
       if (tid == 0) {
         const int pn = q + 1 + kDist;
@@ -277,38 +363,35 @@ __device__ __forceinline__ void star_tma_body(const CUtensorMap *ymap, const Sta
       }
       const T *yc = slot_of(q);
       const T *yp = slot_of(q + 1);
-      T *xw = xs + (q & 3) * XS;
-      const uint32_t mi = ai[q - i0 + 1];
-      if (HAS_I) {
-        y0[P] = yp[yo0];
-        y1[P] = yp[yo1];
-      }
-      // short dependency chains: four partial sums per point
-      T p0 = a0 * y0[C], p1 = a0 * y1[C];
-      if (HAS_I) {
-        p0 = fma(a1, y0[M], p0);
-        p1 = fma(a1, y1[M], p1);
-      }
-      T q0 = a4 * y1[C], q1 = a3 * y0[C];
-      if (HAS_I) {
-        q0 = fma(a2, y0[P], q0);
-        q1 = fma(a2, y1[P], q1);
-      }
-      const T r0 = fma(a5, yc[yo0 - 1], a3 * yc[yo0 - YK]);
-      const T r1 = fma(a5, yc[yo1 - 1], a4 * yc[yo1 + YK]);
-      p0 = fma(a6, yc[yo0 + 1], p0);
-      p1 = fma(a6, yc[yo1 + 1], p1);
-      T acc0 = (p0 + q0) + r0, acc1 = (p1 + q1) + r1;
+      T *xw = xs + (q % NXS) * XS;
+      const uint32_t mi = W.ai[q - i0 + 1];
       const bool fast = ((mi & jka) & xfast_m) == xfast_m;
-      if (!fast) {
-        const bool own = q >= i0 && q < i1;
-        acc0 = x_tilde(acc0, mi & mx0, rel0, own, q);
-        acc1 = x_tilde(acc1, mi & mx1, rel1, own, q);
+      const bool own = q >= i0 && q < i1;
+      if (!fast) cp_async_wait_all();  // this thread's staged old values of plane q
+      prefetch_xo(q + 1);
+      if (HAS_I) {
+#pragma unroll
+        for (int u = 0; u < kR; ++u) yv[u][P] = yp[yo0 + u * YK];
       }
-      x0[P] = acc0;
-      x1[P] = acc1;
-      xw[xo0] = acc0;
-      xw[xo1] = acc1;
+      const T up = yc[yo0 - YK], dn = yc[yo0 + kR * YK];
+#pragma unroll
+      for (int u = 0; u < kR; ++u) {
+        const T jm = u == 0 ? up : yv[u - 1][C];
+        const T jp = u == kR - 1 ? dn : yv[u + 1][C];
+        // short dependency chains: three partial sums per point
+        T p0 = a0 * yv[u][C];
+        T p1 = a4 * jp;
+        if (HAS_I) {
+          p0 = fma(a1, yv[u][M], p0);
+          p1 = fma(a2, yv[u][P], p1);
+        }
+        const T p2 = fma(a5, yc[yo0 + u * YK - 1], a3 * jm);
+        p0 = fma(a6, yc[yo0 + u * YK + 1], p0);
+        T acc = (p0 + p1) + p2;
+        if (!fast) acc = x_tilde(acc, mi & mx[u], u, rel0 + u * rs, own, q);
+        xv[u][P] = acc;
+        xw[xo0 + u * HX] = acc;
+      }
       if (ring) {
         const T yrp = HAS_I ? yp[yor] : T(0);
         T pr = a0 * yr[C];
@@ -316,7 +399,7 @@ __device__ __forceinline__ void star_tma_body(const CUtensorMap *ymap, const Sta
         const T qr = fma(a3, yc[yor - YK], a4 * yc[yor + YK]);
         const T rr = fma(a5, yc[yor - 1], a6 * yc[yor + 1]);
         T acc = (pr + qr) + rr;
-        if (!fast) acc = x_tilde(acc, mi & mxr, relr, false, q);
+        if (!fast) acc = x_tilde(acc, mi & mxr, kR, relr, false, q);
         xw[xor_] = acc;
         yr[P] = yrp;
       }
@@ -324,44 +407,45 @@ __device__ __forceinline__ void star_tma_body(const CUtensorMap *ymap, const Sta
     __syncthreads();
     const int i = HAS_I ? q - 1 : q;
     if (i >= i0 && i < i1) {
-      const T *xc = xs + (i & 3) * XS;
-      // centre values: X~(i) and, along dim 0, X~(i -/+ 1) from registers
-      const T c0 = HAS_I ? x0[C] : x0[P], c1 = HAS_I ? x1[C] : x1[P];
-      T p0 = b0 * c0, p1 = b0 * c1;
-      if (HAS_I) {
-        p0 = fma(b1, x0[M], p0);
-        p1 = fma(b1, x1[M], p1);
+      const T *xc = xs + (i % NXS) * XS;
+      const T up = xc[xo0 - HX], dn = xc[xo0 + kR * HX];
+      T z[kR];
+#pragma unroll
+      for (int u = 0; u < kR; ++u) {
+        // centre values: X~(i) and, along dim 0, X~(i -/+ 1) from registers
+        const T cu = HAS_I ? xv[u][C] : xv[u][P];
+        const T jm = u == 0 ? up : (HAS_I ? xv[u - 1][C] : xv[u - 1][P]);
+        const T jp = u == kR - 1 ? dn : (HAS_I ? xv[u + 1][C] : xv[u + 1][P]);
+        T p0 = b0 * cu;
+        T p1 = b4 * jp;
+        if (HAS_I) {
+          p0 = fma(b1, xv[u][M], p0);
+          p1 = fma(b2, xv[u][P], p1);
+        }
+        const T p2 = fma(b5, xc[xo0 + u * HX - 1], b3 * jm);
+        p0 = fma(b6, xc[xo0 + u * HX + 1], p0);
+        z[u] = (p0 + p1) + p2;
       }
-      T q0 = b4 * c1, q1 = b3 * c0;
-      if (HAS_I) {
-        q0 = fma(b2, x0[P], q0);
-        q1 = fma(b2, x1[P], q1);
-      }
-      const T r0 = fma(b5, xc[xo0 - 1], b3 * xc[xo0 - HX]);
-      const T r1 = fma(b5, xc[xo1 - 1], b4 * xc[xo1 + HX]);
-      p0 = fma(b6, xc[xo0 + 1], p0);
-      p1 = fma(b6, xc[xo1 + 1], p1);
-      T z0 = (p0 + q0) + r0, z1 = (p1 + q1) + r1;
       T *zrow = Zn + (size_t)i * ps + rel0;
-      const uint32_t mi = bi[i - i0];
+      const uint32_t mi = W.bi[i - i0];
       if (((mi & jkb) & zmask) == zmask) {
-        zrow[0] = z0;
-        zrow[rs] = z1;
+#pragma unroll
+        for (int u = 0; u < kR; ++u) zrow[u * rs] = z[u];
       } else {
         const T *zold = Zo + (size_t)i * ps + rel0;
 #pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          const uint32_t w = mi & (h ? mz1 : mz0);
-          T z = h ? z1 : z0;
-          const int o = h ? rs : 0;
+        for (int u = 0; u < kR; ++u) {
+          const uint32_t w = mi & mz[u];
+          T zz = z[u];
           if ((w & zmask) != zval) {
             if (!(w & kArray)) continue;
+            if (!(w & kRegion) && d.skipz) continue;  // the twin already holds this copy
             if (!(w & kRegion))
-              z = zold[o];
+              zz = zold[u * rs];
             else if (bmode == 0 || (bmode == 2 && !(w & kClear)))
-              z += zold[o];
+              zz += zold[u * rs];
           }
-          zrow[o] = z;
+          zrow[u * rs] = zz;
         }
       }
     }
@@ -369,6 +453,7 @@ __device__ __forceinline__ void star_tma_body(const CUtensorMap *ymap, const Sta
   using I0 = std::integral_constant<int, 0>;
   using I1 = std::integral_constant<int, 1>;
   using I2 = std::integral_constant<int, 2>;
+#if GFB_STAR_UNROLL
   for (int q = qbeg; q <= qend; q += 3) {
     step(I0{}, q);
     if (q + 1 > qend) break;
@@ -376,25 +461,42 @@ __device__ __forceinline__ void star_tma_body(const CUtensorMap *ymap, const Sta
     if (q + 2 > qend) break;
     step(I2{}, q + 2);
   }
+#else
+  // one step body, registers rotated by moves (smaller code)
+  for (int q = qbeg; q <= qend; ++q) {
+    step(I0{}, q);
+#pragma unroll
+    for (int u = 0; u < kR; ++u) {
+      yv[u][0] = yv[u][1];
+      yv[u][1] = yv[u][2];
+      xv[u][0] = xv[u][1];
+      xv[u][1] = xv[u][2];
+    }
+    yr[0] = yr[1];
+    yr[1] = yr[2];
+  }
+  (void)I1{};
+  (void)I2{};
+#endif
 }
 
 template <typename T>
-__global__ void __launch_bounds__(kTT, 3)
+__global__ void __launch_bounds__(tThreads, 512 / tThreads)
     star_pair_tma_kernel(const __grid_constant__ CUtensorMap ymap, const __grid_constant__ StarPairDev d) {
   extern __shared__ __align__(128) unsigned char smem[];
   constexpr size_t ybytes = (size_t)NSY * yslot<T>() * sizeof(T);
   T *ys = reinterpret_cast<T *>(smem);
   T *xs = reinterpret_cast<T *>(smem + ybytes);
-  uint64_t *mbar = reinterpret_cast<uint64_t *>(smem + ybytes + (size_t)4 * XS * sizeof(T));
-  __shared__ uint32_t aj[kPY + 2], ak[kPX + 2], bj[kPY], bk[kPX], ai[kPM + 2], bi[kPM];
-  __shared__ uint32_t s_and_a, s_or_a, s_and_b, s_or_b;
-  const int tid = threadIdx.y * kPX + threadIdx.x;
-  const int i0 = d.zlo + blockIdx.z * kPM, i1 = min(i0 + kPM, d.zhi);
-  star_prologue(d, i0, i1, tid, aj, ak, bj, bk, ai, bi, s_and_a, s_or_a, s_and_b, s_or_b);
+  uint64_t *mbar = reinterpret_cast<uint64_t *>(smem + ybytes + (size_t)NXS * XS * sizeof(T));
+  __shared__ TmaWords words;
+  __shared__ T xst[2][kR + 1][tThreads];  // staged old X values (fix-up points), by plane parity
+  const int tid = threadIdx.y * tPX + threadIdx.x;
+  const int i0 = d.zlo + blockIdx.z * tPM, i1 = min(i0 + tPM, d.zhi);
+  tma_prologue(d, i0, blockIdx.y * tPY, blockIdx.x * tPX, tid, words);
   if (d.d0 > 1)
-    star_tma_body<T, true>(&ymap, d, ys, xs, mbar, aj, ak, bj, bk, ai, bi, i0, i1);
+    star_tma_body<T, true>(&ymap, d, ys, xs, mbar, words, xst, i0, i1);
   else
-    star_tma_body<T, false>(&ymap, d, ys, xs, mbar, aj, ak, bj, bk, ai, bi, i0, i1);
+    star_tma_body<T, false>(&ymap, d, ys, xs, mbar, words, xst, i0, i1);
 }
 
 static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
@@ -415,7 +517,20 @@ bool star_tma_usable(const StarPairDev &d, int dtype) {
          getenv("GFB_NO_TMA") == nullptr;
 }
 
-int launch_star_pair_tma(const StarPairDev &d, int dtype, dim3 grid, cudaStream_t st) {
+template <typename T>
+static int launch_tma(const CUtensorMap &map, const StarPairDev &d, cudaStream_t st) {
+  static bool attr = false;
+  const size_t sm = star_tma_smem_bytes<T>();
+  if (!attr) {
+    cudaFuncSetAttribute(star_pair_tma_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    attr = true;
+  }
+  dim3 grid((unsigned)ceil_div(d.d2, tPX), (unsigned)ceil_div(d.d1, tPY), (unsigned)ceil_div(d.zhi - d.zlo, tPM));
+  star_pair_tma_kernel<T><<<grid, dim3(tPX, tPY / kR), sm, st>>>(map, d);
+  return check_launch("star_pair_tma");
+}
+
+int launch_star_pair_tma(const StarPairDev &d, int dtype, dim3, cudaStream_t st) {
   const int64_t es = dtype == GFB_F64 ? 8 : 4;
   CUtensorMap map;
   cuuint64_t dims[3] = {(cuuint64_t)d.d2, (cuuint64_t)d.d1, (cuuint64_t)d.d0};
@@ -427,25 +542,7 @@ int launch_star_pair_tma(const StarPairDev &d, int dtype, dim3 grid, cudaStream_
                            CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return set_error(GFB_ECUDA, "cuTensorMapEncodeTiled failed for the star-pair source");
-  dim3 block(kPX, kPY / 2);
-  if (dtype == GFB_F64) {
-    static bool attr = false;
-    const size_t sm = star_tma_smem_bytes<double>();
-    if (!attr) {
-      cudaFuncSetAttribute(star_pair_tma_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-      attr = true;
-    }
-    star_pair_tma_kernel<double><<<grid, block, sm, st>>>(map, d);
-  } else {
-    static bool attr = false;
-    const size_t sm = star_tma_smem_bytes<float>();
-    if (!attr) {
-      cudaFuncSetAttribute(star_pair_tma_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-      attr = true;
-    }
-    star_pair_tma_kernel<float><<<grid, block, sm, st>>>(map, d);
-  }
-  return check_launch("star_pair_tma");
+  return dtype == GFB_F64 ? launch_tma<double>(map, d, st) : launch_tma<float>(map, d, st);
 }
 
 }  // namespace gfb

@@ -1273,6 +1273,8 @@ class StarPairOp(Op):
         self.xwrite, self.dead = xwrite, dead
         self.xout = self.X
         self.zout = self.Z
+        # out-of-region copies already in place in the target twin
+        self.skip_zcopy = self.skip_xcopy = False
         # slab placement (decomp.py): global plane of local plane 0, local
         # planes produced, global extent of dim 0; single device: whole array
         self.plane0, self.zrange, self.global_d0 = 0, None, None
@@ -1300,6 +1302,7 @@ class StarPairOp(Op):
         rank = len(self.Z.shape)
         d.rank, d.dtype = rank, self.Z.dtype
         d.xwrite = 1 if self.xwrite else 0
+        d.flags = (L.STAR_SKIP_ZCOPY if self.skip_zcopy else 0) | (L.STAR_SKIP_XCOPY if self.skip_xcopy else 0)
         for r in range(rank):
             d.dims[r] = self.Z.shape[r]
         _fill_star(d.a, self.a, self.fa[1])
@@ -1392,6 +1395,8 @@ class Lowering:
             self.materialize(b)
         if os.environ.get("GFB_FUSE", "1") != "0":
             self._fuse_star_pairs(observed)
+            if os.environ.get("GFB_SYNC_ELIDE", "1") != "0":
+                self._elide_synced_copies()
         self._elide_copies()
 
     def resolve(self, buf: Buffer) -> Buffer:
@@ -1448,6 +1453,43 @@ class Lowering:
                 op.remap(phys)
         self.final = dict(cur)
         self.ops = fused
+
+    def _elide_synced_copies(self):
+        """Outside its region a fused sweep copies the old value into the
+        ping-pong twin. Track, in launch order, which twin pairs are known to
+        hold equal values outside which region; a copy into a twin that
+        already holds it is skipped (heat_3d / jacobi_2d: every timestep after
+        the first two). Any other write to a buffer forgets its pairs."""
+        synced = set()  # (frozenset of two root bids, region)
+
+        def forget(b):
+            r = b.root().bid
+            for e in [e for e in synced if r in e[0]]:
+                synced.discard(e)
+
+        for op in self.ops:
+            if not isinstance(op, StarPairOp):
+                for b in op.writes:
+                    forget(b)
+                continue
+            Z, zout = op.Z.root(), op.zout.root()
+            X, xout = op.X.root(), op.xout.root()
+            if zout is not Z:
+                key = (frozenset((Z.bid, zout.bid)), tuple(op.b.region))
+                op.skip_zcopy = key in synced
+            if op.xwrite and xout is not X:
+                xkey = (frozenset((X.bid, xout.bid)), tuple(op.a.region))
+                op.skip_xcopy = xkey in synced
+            # after the launch: the targets changed inside the regions, and
+            # hold their old twins' values outside
+            forget(op.zout)
+            if zout is not Z:
+                synced.add((frozenset((Z.bid, zout.bid)), tuple(op.b.region)))
+            if op.xwrite:
+                forget(op.xout)
+                full = op.dead is None or box_contains(op.a.region, op.dead)
+                if xout is not X and full:
+                    synced.add((frozenset((X.bid, xout.bid)), tuple(op.a.region)))
 
     def _x_liveness(self, X: Buffer, start: int, obs: set):
         """(write X back?, dead box) for the intermediate of a fused pair."""

@@ -429,7 +429,20 @@ class Emulator:
         Xn = _star_apply(d.a, Y, Xo, rank, dims, p0)
         Zn = _star_apply(d.b, Xn, Zo, rank, dims, p0)
         zv = view(d.zout)
-        zv[zlo:zhi] = Zn[zlo:zhi]
+        ys = list(np.meshgrid(*[np.arange(k) for k in dims], indexing="ij"))
+        ys[0] = ys[0] + p0
+
+        def inside(lo, hi):
+            m = np.ones(ys[0].shape, dtype=bool)
+            for r in range(rank):
+                m &= (ys[r] >= lo[r]) & (ys[r] < hi[r])
+            return m
+
+        zsel = np.zeros(ys[0].shape, dtype=bool)
+        zsel[zlo:zhi] = True
+        if d.flags & L.STAR_SKIP_ZCOPY:  # out-of-region copies are left to the twin
+            zsel &= inside(d.b.lo, d.b.hi)
+        zv[zsel] = Zn[zsel]
         if d.xwrite:
             ys = list(np.meshgrid(*[np.arange(k) for k in dims], indexing="ij"))
             ys[0] = ys[0] + p0
@@ -442,6 +455,8 @@ class Emulator:
             own[zlo:zhi] = True
             out = view(d.xout)
             sel = ~dead & own
+            if d.flags & L.STAR_SKIP_XCOPY:
+                sel &= inside(d.a.lo, d.a.hi)
             out[sel] = Xn[sel]
 
     def stencil(self, d):

@@ -49,8 +49,19 @@ def fp64_tensor_peak():
     return 2 * 8192**3 * 5 / (s.elapsed_time(e) * 1e-3) / 1e12
 
 
+FP32_FFMA_NOMINAL = 148 * 128 * 2 * 1.965e9 / 1e12  # TFLOP/s, no measured fp32 SIMT figure
+
+
+def family(op):
+    """matmul launches with a unit dimension are HBM-bound matrix-vector /
+    rank-1 passes; the rest are contractions."""
+    if op.family == "matmul" and min(op.M, op.N, op.K) == 1:
+        return "matvec"
+    return op.family
+
+
 def roofline(exe, inputs, peak_hbm, fp64_peak):
-    rows = exe.timed_eager(inputs)
+    rows = [(family(op), op, ms) for _, op, ms in exe.timed_eager(inputs)]
     fam_t, fam_b, fam_n, fam_f = {}, {}, {}, {}
     for fam, op, ms in rows:
         fam_t[fam] = fam_t.get(fam, 0.0) + ms
@@ -61,11 +72,16 @@ def roofline(exe, inputs, peak_hbm, fp64_peak):
     total = sum(fam_t.values())
     dom = max(fam_t, key=fam_t.get)
     shares = {k: round(v / total, 4) for k, v in sorted(fam_t.items(), key=lambda kv: -kv[1])}
-    if dom == "matmul" and fam_f.get(dom):
+    if dom in ("matmul", "contract") and fam_f.get(dom):
         ach = fam_f[dom] / (fam_t[dom] * 1e-3) / 1e12
-        return {"bound": "tensor(fp64 DMMA)", "kernel": dom, "achieved": round(ach, 2), "unit": "TFLOP/s",
-                "peak": round(fp64_peak, 2), "peak_kind": "cuBLAS DGEMM 8192^3 measured in this run",
-                "frac": round(ach / fp64_peak, 4), "step_share": shares}
+        f64 = any(op.dst.dtype == 1 if hasattr(op, "dst") else op.out.dtype == 1 for f, op, _ in rows if f == dom)
+        if f64 and dom == "matmul":
+            return {"bound": "tensor(fp64 DMMA)", "kernel": dom, "achieved": round(ach, 2), "unit": "TFLOP/s",
+                    "peak": round(fp64_peak, 2), "peak_kind": "cuBLAS DGEMM 8192^3 measured in this run",
+                    "frac": round(ach / fp64_peak, 4), "step_share": shares}
+        return {"bound": "fp32 FFMA", "kernel": dom, "achieved": round(ach, 2), "unit": "TFLOP/s",
+                "peak": round(FP32_FFMA_NOMINAL, 1), "peak_kind": "nominal 148 SMs x 128 FMA/clk x 1965 MHz",
+                "frac": round(ach / FP32_FFMA_NOMINAL, 4), "step_share": shares}
     ach = fam_b[dom] / (fam_t[dom] * 1e-3) / 1e9
     return {"bound": "hbm", "kernel": dom, "achieved": round(ach, 1), "unit": "GB/s", "peak": peak_hbm,
             "peak_kind": "measured", "frac": round(ach / peak_hbm, 4), "step_share": shares,
