@@ -192,7 +192,9 @@ static void launch_contract(const gfb_contract_desc &d, cudaStream_t st) {
 template <typename T>
 static void launch_contract_t(const gfb_contract_desc &d, cudaStream_t st) {
   // variant choice mirrored by lowering.contract_tile
-  if (d.N <= 16)
+  if (d.M <= 48 * 4 && d.N <= 32)
+    launch_contract<T, 48, 32, 3, 2>(d, st);  // few outputs, long k (weight adjoints)
+  else if (d.N <= 16)
     launch_contract<T, 128, 16, 4, 2>(d, st);
   else if (d.N <= 32)
     launch_contract<T, 128, 32, 4, 4>(d, st);

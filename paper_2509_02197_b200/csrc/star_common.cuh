@@ -29,6 +29,7 @@ struct StarPairDev {
   int32_t zlo, zhi;     // local planes to produce
   int32_t xwrite;  // write X back (outside the dead box)
   int32_t skipz, skipx;  // out-of-region Z copy / X write-back already in place
+  int32_t tpm;           // planes per CTA (TMA kernel)
   int32_t ps, rs;  // plane / row strides (arrays < 2^31 elements)
   StarOpDev a, b;
   const void *y;      // source of a

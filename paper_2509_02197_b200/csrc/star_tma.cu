@@ -1,7 +1,7 @@
 // TMA-fed variant of the fused star-pair kernel (see star.cu for the
 // algorithm: X = a(Y); Z = b(X), two radius-1 star sweeps in one launch).
 //
-// One CTA owns a (tPY x tPX) = 32 x 32 column of Z over tPM planes and
+// One CTA owns a (tPY x tPX) = 32 x 32 column of Z over up to tPM planes and
 // marches along dim 0. The source planes Y(q), with a two-point halo in
 // (j, k), are moved into a shared-memory ring by the Tensor Memory
 // Accelerator (cp.async.bulk.tensor, one elected thread, mbarrier
@@ -26,6 +26,7 @@
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
+#include <algorithm>
 #include <type_traits>
 
 #include "gfb_internal.h"
@@ -138,7 +139,9 @@ struct TmaWords {
 
 __device__ __forceinline__ void tma_prologue(const StarPairDev &d, int i0, int j0, int k0, int tid, TmaWords &w) {
   auto srcb = [&](int dim, int c) { return (c >= d.b.smlo[dim] && c < d.b.smhi[dim]) ? kSrcB : 0u; };
-  constexpr int nA = tPY + 2, nB = nA + tPX + 2, nC = nB + tPY, nD = nC + tPX, nE = nD + tPM + 2, nF = nE + tPM;
+  const int tpm = d.tpm;  // planes per CTA (launch-time choice, <= tPM)
+  constexpr int nA = tPY + 2, nB = nA + tPX + 2, nC = nB + tPY, nD = nC + tPX;
+  const int nE = nD + tpm + 2, nF = nE + tpm;
   for (int e = tid; e < nF; e += tThreads) {
     if (e < nA) {
       w.aj[e] = coord_bits(d.a, 1, j0 - 1 + e, d.d1, d.dlo, d.dhi) | srcb(1, j0 - 1 + e);
@@ -491,7 +494,7 @@ __global__ void __launch_bounds__(tThreads, 512 / tThreads)
   __shared__ TmaWords words;
   __shared__ T xst[2][kR + 1][tThreads];  // staged old X values (fix-up points), by plane parity
   const int tid = threadIdx.y * tPX + threadIdx.x;
-  const int i0 = d.zlo + blockIdx.z * tPM, i1 = min(i0 + tPM, d.zhi);
+  const int i0 = d.zlo + blockIdx.z * d.tpm, i1 = min(i0 + d.tpm, d.zhi);
   tma_prologue(d, i0, blockIdx.y * tPY, blockIdx.x * tPX, tid, words);
   if (d.d0 > 1)
     star_tma_body<T, true>(&ymap, d, ys, xs, mbar, words, xst, i0, i1);
@@ -525,8 +528,13 @@ static int launch_tma(const CUtensorMap &map, const StarPairDev &d, cudaStream_t
     cudaFuncSetAttribute(star_pair_tma_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     attr = true;
   }
-  dim3 grid((unsigned)ceil_div(d.d2, tPX), (unsigned)ceil_div(d.d1, tPY), (unsigned)ceil_div(d.zhi - d.zlo, tPM));
-  star_pair_tma_kernel<T><<<grid, dim3(tPX, tPY / kR), sm, st>>>(map, d);
+  // planes per CTA: as many as keep >= 4 CTAs per SM worth of work in the
+  // grid (small domains get short marches rather than idle SMs)
+  StarPairDev dd = d;
+  const int64_t tiles = ceil_div(d.d2, tPX) * ceil_div(d.d1, tPY), planes = d.zhi - d.zlo;
+  dd.tpm = (int32_t)std::max<int64_t>(2, std::min<int64_t>(tPM, planes * tiles / (4 * (int64_t)sm_count())));
+  dim3 grid((unsigned)ceil_div(d.d2, tPX), (unsigned)ceil_div(d.d1, tPY), (unsigned)ceil_div(planes, dd.tpm));
+  star_pair_tma_kernel<T><<<grid, dim3(tPX, tPY / kR), sm, st>>>(map, dd);
   return check_launch("star_pair_tma");
 }
 

@@ -974,8 +974,10 @@ def map2_reduce(space, acc, ins, dst, ybox, clear_mode, cbox, code, seg, compute
     return op
 
 
-def contract_tile(N: int):
+def contract_tile(M: int, N: int):
     """(BM, BN) of the contraction kernel variant gfb_contract_launch picks."""
+    if M <= 48 * 4 and N <= 32:
+        return 48, 32
     if N <= 16:
         return 128, 16
     if N <= 32:
@@ -1214,7 +1216,7 @@ def contract_form(space, body, acc, ins, dst, ybox, clear_mode, cbox):
         return None
     a_kfast = 1 if kdims and abs(int(fa[rank + free.index(kdims[-1])])) == 1 else 0
     b_nfast = 1 if ndims and abs(int(fb[ndims[-1]])) == 1 else 0
-    BM, BN = contract_tile(N)
+    BM, BN = contract_tile(M, N)
     tiles = -(-M // BM) * -(-N // BN)
     nsplit = 1
     if tiles < 2 * 148 and K >= 64 * 16:

@@ -1,0 +1,122 @@
+"""Turn one tools/capture_profiles.sh run (gpurun_out/) into the committed
+profiles/ summaries for a round:
+
+    python tools/summarize_profiles.py r01
+
+writes profiles/<tag>_bench.jsonl, _configs.jsonl, _ops.txt, _pytest_gpu.log,
+_launches_summary.txt, _ncu_star_pair.txt and profiles/ncu_traffic.json (the
+DRAM bytes per launch bench.py reports as roofline.traffic).
+"""
+from __future__ import annotations
+
+import csv
+import io
+import json
+import os
+import shutil
+import subprocess
+import sys
+
+REPO = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+OUT = os.path.join(REPO, "gpurun_out")
+PROF = os.path.join(REPO, "profiles")
+
+
+def launches(tag):
+    path = os.path.join(OUT, "launches.csv")
+    if not os.path.exists(path):
+        return
+    lines = open(path).read().splitlines()
+    start = next(i for i, l in enumerate(lines) if l.startswith('"ID"'))
+    rows = list(csv.DictReader(io.StringIO("\n".join(lines[start:]))))
+    agg = {}
+    for r in rows:
+        if r.get("Metric Name") != "gpu__time_duration.sum":
+            continue
+        name = r["Kernel Name"]
+        v = float(r["Metric Value"].replace(",", ""))
+        unit = r.get("Metric Unit", "ns")
+        us = v / 1000.0 if unit == "ns" else (v * 1000.0 if unit == "ms" else v)
+        n, t = agg.get(name, (0, 0.0))
+        agg[name] = (n + 1, t + us)
+    tot = sum(t for _, t in agg.values()) or 1.0
+    with open(os.path.join(PROF, f"{tag}_launches_summary.txt"), "w") as f:
+        f.write("ncu --metrics gpu__time_duration.sum --clock-control none, "
+                "python bench.py --steps 2 --warmup 1 --no-cpu-baseline --no-e2e (every launch of the run;\n"
+                "cold-cache serialised times: compare shares, not absolutes)\n")
+        f.write(f"{'kernel':90s} {'launches':>8s} {'total_us':>12s} {'avg_us':>10s} {'share':>6s}\n")
+        for name, (n, t) in sorted(agg.items(), key=lambda kv: -kv[1][1]):
+            f.write(f"{name[:90]:90s} {n:8d} {t:12.1f} {t / n:10.2f} {t / tot:6.3f}\n")
+
+
+METRICS = [
+    ("gpu__time_duration.sum", "duration"),
+    ("dram__bytes_read.sum", "dram read"),
+    ("dram__bytes_write.sum", "dram write"),
+    ("smsp__inst_executed.sum", "warp instructions"),
+    ("sm__inst_issued.avg.pct_of_peak_sustained_active", "issue active %"),
+    ("sm__warps_active.avg.pct_of_peak_sustained_active", "warps active %"),
+    ("launch__registers_per_thread", "registers/thread"),
+    ("l1tex__data_pipe_lsu_wavefronts_mem_shared_op_ld.sum", "smem load wavefronts"),
+    ("l1tex__data_bank_conflicts_pipe_lsu_mem_shared_op_ld.sum", "smem load bank conflicts"),
+    ("dram__throughput.avg.pct_of_peak_sustained_elapsed", "dram throughput %"),
+]
+
+
+def ncu_full(tag):
+    rep = os.path.join(OUT, "prof_top.ncu-rep")
+    if not os.path.exists(rep):
+        return
+    raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    rows = list(csv.reader(io.StringIO(raw)))
+    hdr, units = rows[0], rows[1]
+    idx = {h: i for i, h in enumerate(hdr)}
+    out = ["ncu --set full --clock-control none --import-source on -k regex:star_pair -c 4 "
+           "python tools/prof_stencil.py heat_3d 512 3", ""]
+    traffic = []
+    for n, r in enumerate(rows[2:]):
+        out.append(f"launch {n}: {r[idx['Kernel Name']]}  grid {r[idx.get('launch__grid_size', 0)]}")
+        for key, label in METRICS:
+            if key in idx:
+                out.append(f"  {label:28s} {r[idx[key]]:>16s} {units[idx[key]]}")
+        st = {h: float(r[i]) for h, i in idx.items()
+              if h.startswith("smsp__pcsamp_warps_issue_stalled") and not h.endswith("not_issued") and r[i]}
+        tot = sum(st.values()) or 1.0
+        out.append("  stall samples: " + ", ".join(
+            f"{k.replace('smsp__pcsamp_warps_issue_stalled_', '')} {v / tot * 100:.0f}%"
+            for k, v in sorted(st.items(), key=lambda kv: -kv[1])[:8]))
+        rd = float(r[idx["dram__bytes_read.sum"]]) * (1e9 if units[idx["dram__bytes_read.sum"]] == "Gbyte" else 1e6)
+        wr = float(r[idx["dram__bytes_write.sum"]]) * (1e9 if units[idx["dram__bytes_write.sum"]] == "Gbyte" else 1e6)
+        traffic.append(rd + wr)
+        out.append("")
+    with open(os.path.join(PROF, f"{tag}_ncu_star_pair.txt"), "w") as f:
+        f.write("\n".join(out))
+    with open(os.path.join(PROF, "ncu_traffic.json"), "w") as f:
+        json.dump({"star_pair": {"dram_bytes_per_launch": sum(traffic) / len(traffic),
+                                 "launches": len(traffic),
+                                 "source": f"profiles/{tag}_ncu_star_pair.txt (dram__bytes_read.sum + "
+                                           "dram__bytes_write.sum, heat_3d 512^3, first forward launches)"}},
+                  f, indent=1)
+
+
+def main():
+    tag = sys.argv[1] if len(sys.argv) > 1 else "r01"
+    os.makedirs(PROF, exist_ok=True)
+    lines = []
+    for name in ("bench.jsonl", "bench_ref.jsonl"):
+        p = os.path.join(OUT, name)
+        if os.path.exists(p):
+            lines += [l for l in open(p).read().splitlines() if l.startswith("{")]
+    if lines:
+        open(os.path.join(PROF, f"{tag}_bench.jsonl"), "w").write("\n".join(lines) + "\n")
+    for src, dst in (("configs.jsonl", f"{tag}_configs.jsonl"), ("ops.txt", f"{tag}_ops.txt"),
+                     ("pytest_gpu.log", f"{tag}_pytest_gpu.log")):
+        if os.path.exists(os.path.join(OUT, src)):
+            shutil.copy(os.path.join(OUT, src), os.path.join(PROF, dst))
+    launches(tag)
+    ncu_full(tag)
+    print("\n".join(sorted(os.listdir(PROF))))
+
+
+if __name__ == "__main__":
+    main()
