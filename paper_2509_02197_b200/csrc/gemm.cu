@@ -421,6 +421,7 @@ extern "C" int64_t gfb_matmul_workspace_bytes(int32_t dtype, int32_t ta, int32_t
   int64_t es = dtype == GFB_F64 ? 8 : 4;
   if (K > 1 && N == 1 && ta) return colsum_splits(M, K) * M * es;
   if (K > 1 && M == 1 && !tb && N > 1) return colsum_splits(N, K) * N * es;
+  if (dtype != GFB_F64 && K > 1 && M > 1 && N > 1 && sgemm_tc_usable(M, N, K)) return sgemm_tc_workspace(M, N, K);
   if (dtype != GFB_F64 && K > 1 && M > 1 && N > 1) {
     const int64_t ns = sgemm_splits(M, N, K);
     if (ns > 1) {
@@ -451,6 +452,9 @@ extern "C" int gfb_matmul(int32_t dtype, int32_t ta, int32_t tb, int64_t M, int6
   rc = matmul_t<float>(ta, tb, M, N, K, (const float *)A, lda, (const float *)B, ldb, (float *)C, ldc, accumulate,
                        workspace, st);
   if (rc >= 0) return rc;
+  if (sgemm_tc_usable(M, N, K))
+    return sgemm_tc(ta, tb, M, N, K, (const float *)A, lda, (const float *)B, ldb, (float *)C, ldc, accumulate,
+                    workspace, st);
   return sgemm(ta, tb, M, N, K, (const float *)A, lda, (const float *)B, ldb, (float *)C, ldc, accumulate, workspace,
                st);
 }

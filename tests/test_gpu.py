@@ -264,3 +264,29 @@ def test_planned_device_payload_respects_the_budget(cid):
     assert used <= meta["t_star"], (used, meta["t_star"], limit)
     if limit is not None:
         assert used <= limit
+
+
+@pytest.mark.parametrize("ta,tb", [(0, 0), (1, 0), (0, 1), (1, 1)])
+@pytest.mark.parametrize("M,N,K", [(64, 4096, 512), (130, 70, 33), (512, 96, 1024), (7, 300, 2000)])
+def test_fp32_matmul_tensor_core_3xtf32(M, N, K, ta, tb):
+    """gfb_matmul fp32 (tcgen05 3xTF32 path, split-K for skinny shapes)
+    against an fp64 product, with and without accumulation, through the C ABI."""
+    from paper_2509_02197_b200 import _lib as L
+
+    lib = L.load()
+    g = torch.Generator(device="cuda").manual_seed(M * 7 + N * 3 + K + 11 * ta + 5 * tb)
+    A = torch.rand((K, M) if ta else (M, K), generator=g, device="cuda", dtype=torch.float32) - 0.3
+    B = torch.rand((N, K) if tb else (K, N), generator=g, device="cuda", dtype=torch.float32) - 0.3
+    C0 = torch.rand((M, N), generator=g, device="cuda", dtype=torch.float32)
+    ref = (A.double().T if ta else A.double()) @ (B.double().T if tb else B.double())
+    ws = torch.empty(max(lib.gfb_matmul_workspace_bytes(L.F32, ta, tb, M, N, K), 16), dtype=torch.uint8,
+                     device="cuda")
+    st = torch.cuda.current_stream().cuda_stream
+    for acc in (0, 1):
+        C = C0.clone()
+        L.check(lib.gfb_matmul(L.F32, ta, tb, M, N, K, A.data_ptr(), A.shape[1], B.data_ptr(), B.shape[1],
+                               C.data_ptr(), N, acc, ws.data_ptr(), st), "matmul")
+        torch.cuda.synchronize()
+        want = ref + (C0.double() if acc else 0)
+        err = ((C.double() - want).abs() / want.abs().clamp(min=1)).max().item()
+        assert err <= 1e-5, (acc, err)
