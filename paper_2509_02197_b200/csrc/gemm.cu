@@ -8,6 +8,8 @@
 //   otherwise         tiled GEMM: fp64 on the DMMA tensor path
 //                     (mma.sync.m8n8k4.f64 -> DMMA), fp32 on FFMA (split-K
 //                     when the tile grid does not cover the SMs)
+#include <algorithm>
+
 #include "gfb_common.cuh"
 #include "gfb_internal.h"
 
@@ -353,6 +355,179 @@ __global__ void __launch_bounds__(256) rank1_kernel(int64_t M, int64_t N, const 
   }
 }
 
+// 16-byte vector variants (aligned operands, unit-stride vectors): half /
+// a quarter of the load instructions, four independent 16-byte partial sums
+// in flight per lane.
+template <typename T>
+struct Vec16;
+template <>
+struct Vec16<double> {
+  using type = double2;
+  static constexpr int W = 2;
+  __device__ static double dot(double2 a, double2 b) { return fma(a.x, b.x, a.y * b.y); }
+  __device__ static double2 fmav(double2 a, double2 b, double2 c) {
+    return make_double2(fma(a.x, b.x, c.x), fma(a.y, b.y, c.y));
+  }
+  __device__ static double2 zero() { return make_double2(0.0, 0.0); }
+  __device__ static double2 splat(double s) { return make_double2(s, s); }
+  __device__ static double get(double2 v, int i) { return i == 0 ? v.x : v.y; }
+};
+template <>
+struct Vec16<float> {
+  using type = float4;
+  static constexpr int W = 4;
+  __device__ static float dot(float4 a, float4 b) { return fmaf(a.x, b.x, fmaf(a.y, b.y, fmaf(a.z, b.z, a.w * b.w))); }
+  __device__ static float4 fmav(float4 a, float4 b, float4 c) {
+    return make_float4(fmaf(a.x, b.x, c.x), fmaf(a.y, b.y, c.y), fmaf(a.z, b.z, c.z), fmaf(a.w, b.w, c.w));
+  }
+  __device__ static float4 zero() { return make_float4(0.f, 0.f, 0.f, 0.f); }
+  __device__ static float4 splat(float s) { return make_float4(s, s, s, s); }
+  __device__ static float get(float4 v, int i) { return i == 0 ? v.x : i == 1 ? v.y : i == 2 ? v.z : v.w; }
+};
+
+template <typename T>
+__global__ void __launch_bounds__(256) gemv_rowdot_vec_kernel(int64_t M, int64_t K, const T *__restrict__ A,
+                                                              int64_t lda, const T *__restrict__ x, T *y,
+                                                              int64_t incy, int accumulate) {
+  using VT = Vec16<T>;
+  using V = typename VT::type;
+  constexpr int W = VT::W;
+  const int lane = threadIdx.x & 31;
+  const int64_t nv = K / W;
+  const V *xv = reinterpret_cast<const V *>(x);
+  for (int64_t row = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5); row < M; row += (int64_t)gridDim.x * 8) {
+    const V *a = reinterpret_cast<const V *>(A + row * lda);
+    T p[4] = {T(0), T(0), T(0), T(0)};
+    int64_t j = lane;
+    for (; j + 96 < nv; j += 128) {
+#pragma unroll
+      for (int u = 0; u < 4; ++u) p[u] += VT::dot(a[j + 32 * u], xv[j + 32 * u]);
+    }
+    for (; j < nv; j += 32) p[0] += VT::dot(a[j], xv[j]);
+    for (int64_t k = nv * W + lane; k < K; k += 32) p[1] = fma(A[row * lda + k], x[k], p[1]);
+    T acc = (p[0] + p[1]) + (p[2] + p[3]);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_down_sync(0xffffffffu, acc, o);
+    if (lane == 0) {
+      T *o = y + row * incy;
+      *o = accumulate ? (T)(*o + acc) : acc;
+    }
+  }
+}
+
+// column sums with W adjacent columns per lane (32*W per CTA)
+template <typename T>
+__global__ void __launch_bounds__(256) gemv_colsum_vec_kernel(int64_t M, int64_t K, const T *__restrict__ S,
+                                                              int64_t lds, const T *__restrict__ x, int64_t incx,
+                                                              T *partial, int64_t kchunk) {
+  using VT = Vec16<T>;
+  using V = typename VT::type;
+  constexpr int W = VT::W;
+  __shared__ V red[8][32];
+  const int lane = threadIdx.x & 31, g = threadIdx.x >> 5;
+  const int64_t i = ((int64_t)blockIdx.x * 32 + lane) * W;  // first of this lane's W columns (M % W == 0)
+  const int64_t kb = (int64_t)blockIdx.y * kchunk, ke = min(kb + kchunk, K);
+  V p[4] = {VT::zero(), VT::zero(), VT::zero(), VT::zero()};
+  if (i < M) {
+    int64_t k = kb + g;
+    for (; k + 24 < ke; k += 32) {
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int64_t kk = k + 8 * u;
+        p[u] = VT::fmav(*reinterpret_cast<const V *>(S + kk * lds + i), VT::splat(x[kk * incx]), p[u]);
+      }
+    }
+    for (; k < ke; k += 8) p[0] = VT::fmav(*reinterpret_cast<const V *>(S + k * lds + i), VT::splat(x[k * incx]), p[0]);
+  }
+  V t;
+  if constexpr (W == 2) {
+    t = make_double2((p[0].x + p[1].x) + (p[2].x + p[3].x), (p[0].y + p[1].y) + (p[2].y + p[3].y));
+  } else {
+    t = make_float4((p[0].x + p[1].x) + (p[2].x + p[3].x), (p[0].y + p[1].y) + (p[2].y + p[3].y),
+                    (p[0].z + p[1].z) + (p[2].z + p[3].z), (p[0].w + p[1].w) + (p[2].w + p[3].w));
+  }
+  red[g][lane] = t;
+  __syncthreads();
+  if (g == 0 && i < M) {
+    T sum[W];
+#pragma unroll
+    for (int c = 0; c < W; ++c) sum[c] = T(0);
+#pragma unroll
+    for (int q = 0; q < 8; ++q)
+#pragma unroll
+      for (int c = 0; c < W; ++c) sum[c] += VT::get(red[q][lane], c);
+#pragma unroll
+    for (int c = 0; c < W; ++c) partial[(int64_t)blockIdx.y * M + i + c] = sum[c];
+  }
+}
+
+// rank-1 with 16-byte row stores (C rows aligned, v contiguous)
+template <typename T>
+__global__ void __launch_bounds__(256) rank1_vec_kernel(int64_t M, int64_t N, const T *__restrict__ u, int64_t incu,
+                                                        const T *__restrict__ v, T *C, int64_t ldc,
+                                                        int accumulate) {
+  using VT = Vec16<T>;
+  using V = typename VT::type;
+  constexpr int W = VT::W;
+  const int64_t nv = N / W;
+  const V *vv = reinterpret_cast<const V *>(v);
+  for (int64_t i = blockIdx.y; i < M; i += gridDim.y) {
+    const T ui = u[i * incu];
+    V *row = reinterpret_cast<V *>(C + i * ldc);
+    for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < nv; j += (int64_t)gridDim.x * blockDim.x) {
+      const V r = VT::fmav(VT::splat(ui), vv[j], accumulate ? row[j] : VT::zero());
+      row[j] = r;
+    }
+    if (blockIdx.x == 0)
+      for (int64_t j = nv * W + threadIdx.x; j < N; j += blockDim.x) {
+        const T r = ui * v[j];
+        C[i * ldc + j] = accumulate ? (T)(C[i * ldc + j] + r) : r;
+      }
+  }
+}
+
+static bool aligned16(const void *p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
+
+// Row dots with a whole CTA per row (grid-stride over rows): the row's
+// 16-byte vectors are spread over 256 threads, so one row is a single round
+// of loads in flight instead of a warp's long sequential walk.
+template <typename T>
+__global__ void __launch_bounds__(256) gemv_rowdot_cta_kernel(int64_t M, int64_t K, const T *__restrict__ A,
+                                                              int64_t lda, const T *__restrict__ x, T *y,
+                                                              int64_t incy, int accumulate) {
+  using VT = Vec16<T>;
+  using V = typename VT::type;
+  constexpr int W = VT::W;
+  __shared__ T red[8];
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  const int64_t nv = K / W;
+  const V *xv = reinterpret_cast<const V *>(x);
+  for (int64_t row = blockIdx.x; row < M; row += gridDim.x) {
+    const V *a = reinterpret_cast<const V *>(A + row * lda);
+    T p[4] = {T(0), T(0), T(0), T(0)};
+    int64_t j = t;
+    for (; j + 768 < nv; j += 1024) {
+#pragma unroll
+      for (int u = 0; u < 4; ++u) p[u] += VT::dot(a[j + 256 * u], xv[j + 256 * u]);
+    }
+    for (; j < nv; j += 256) p[0] += VT::dot(a[j], xv[j]);
+    for (int64_t k = nv * W + t; k < K; k += 256) p[1] = fma(A[row * lda + k], x[k], p[1]);
+    T acc = (p[0] + p[1]) + (p[2] + p[3]);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_down_sync(0xffffffffu, acc, o);
+    if (lane == 0) red[warp] = acc;
+    __syncthreads();
+    if (t == 0) {
+      T s = T(0);
+#pragma unroll
+      for (int w = 0; w < 8; ++w) s += red[w];
+      T *o = y + row * incy;
+      *o = accumulate ? (T)(*o + s) : s;
+    }
+    __syncthreads();
+  }
+}
+
 static int64_t colsum_splits(int64_t M, int64_t K) {
   int64_t cols_blocks = ceil_div(M, 32);
   int64_t want = ceil_div((int64_t)sm_count() * 4, cols_blocks);
@@ -367,8 +542,14 @@ static int gemv_colsum(int64_t M, int64_t K, const T *S, int64_t lds, const T *x
   int64_t ns = colsum_splits(M, K);
   int64_t chunk = ceil_div(K, ns);
   T *partial = (T *)ws;
-  dim3 grid((unsigned)ceil_div(M, 32), (unsigned)ns);
-  gemv_colsum_kernel<T><<<grid, 256, 0, st>>>(M, K, S, lds, x, incx, partial, chunk);
+  constexpr int W = Vec16<T>::W;
+  if (aligned16(S) && lds % W == 0 && M % W == 0) {
+    dim3 grid((unsigned)ceil_div(M, 32 * W), (unsigned)ns);
+    gemv_colsum_vec_kernel<T><<<grid, 256, 0, st>>>(M, K, S, lds, x, incx, partial, chunk);
+  } else {
+    dim3 grid((unsigned)ceil_div(M, 32), (unsigned)ns);
+    gemv_colsum_kernel<T><<<grid, 256, 0, st>>>(M, K, S, lds, x, incx, partial, chunk);
+  }
   splits_finish_kernel<T><<<(unsigned)ceil_div(M, 256), 256, 0, st>>>(M, ns, partial, y, incy, accumulate);
   return check_launch("gemv_colsum");
 }
@@ -387,15 +568,28 @@ static int matmul_t(int ta, int tb, int64_t M, int64_t N, int64_t K, const T *A,
     // op(A) column 0: element i at A[i*lda] (no ta) or A[i] (ta: A stored [1, M])
     int64_t incu = ta ? 1 : lda;
     int64_t incv = tb ? ldb : 1;  // op(B) row 0: B[j] (no tb) or B[j*ldb] (tb: stored [N,1])
-    dim3 grid((unsigned)min(ceil_div(N, 256), (int64_t)8), (unsigned)min(M, (int64_t)65535));
-    rank1_kernel<T><<<grid, 256, 0, st>>>(M, N, A, incu, B, incv, C, ldc, accumulate);
+    constexpr int W = Vec16<T>::W;
+    if (incv == 1 && aligned16(B) && aligned16(C) && ldc % W == 0) {
+      dim3 grid((unsigned)min(ceil_div(N / W, 256 * 8), (int64_t)8),
+                (unsigned)min(M, (int64_t)sm_count() * 8));
+      rank1_vec_kernel<T><<<grid, 256, 0, st>>>(M, N, A, incu, B, C, ldc, accumulate);
+    } else {
+      dim3 grid((unsigned)min(ceil_div(N, 256), (int64_t)8), (unsigned)min(M, (int64_t)65535));
+      rank1_kernel<T><<<grid, 256, 0, st>>>(M, N, A, incu, B, incv, C, ldc, accumulate);
+    }
     return check_launch("rank1");
   }
   if (N == 1) {
     // x = op(B)(:,0): B[k*ldb] (no tb) or B[k] (tb)
     int64_t incx = tb ? 1 : ldb;
     if (!ta) {
-      gemv_rowdot_kernel<T><<<(unsigned)ceil_div(M, 8), 256, 0, st>>>(M, K, A, lda, B, incx, C, ldc, accumulate);
+      constexpr int W = Vec16<T>::W;
+      if (incx == 1 && aligned16(A) && aligned16(B) && lda % W == 0) {
+        const unsigned blocks = (unsigned)min(M, (int64_t)sm_count() * 8);
+        gemv_rowdot_cta_kernel<T><<<blocks, 256, 0, st>>>(M, K, A, lda, B, C, ldc, accumulate);
+      } else {
+        gemv_rowdot_kernel<T><<<(unsigned)ceil_div(M, 8), 256, 0, st>>>(M, K, A, lda, B, incx, C, ldc, accumulate);
+      }
       return check_launch("gemv_rowdot");
     }
     return gemv_colsum<T>(M, K, A, lda, B, incx, C, ldc, accumulate, ws, st);
@@ -404,7 +598,13 @@ static int matmul_t(int ta, int tb, int64_t M, int64_t N, int64_t K, const T *A,
     // y[j] = sum_k op(A)(0,k) op(B)(k,j); op(A) row 0: A[k] (no ta) or A[k*lda] (ta)
     int64_t incx = ta ? lda : 1;
     if (tb) {  // op(B)(k,j) = B[j*ldb + k]: row dots
-      gemv_rowdot_kernel<T><<<(unsigned)ceil_div(N, 8), 256, 0, st>>>(N, K, B, ldb, A, incx, C, 1, accumulate);
+      constexpr int W = Vec16<T>::W;
+      if (incx == 1 && aligned16(A) && aligned16(B) && ldb % W == 0) {
+        const unsigned blocks = (unsigned)min(N, (int64_t)sm_count() * 8);
+        gemv_rowdot_cta_kernel<T><<<blocks, 256, 0, st>>>(N, K, B, ldb, A, C, 1, accumulate);
+      } else {
+        gemv_rowdot_kernel<T><<<(unsigned)ceil_div(N, 8), 256, 0, st>>>(N, K, B, ldb, A, incx, C, 1, accumulate);
+      }
       return check_launch("gemv_rowdot");
     }
     return gemv_colsum<T>(N, K, B, ldb, A, incx, C, 1, accumulate, ws, st);

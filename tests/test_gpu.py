@@ -290,3 +290,34 @@ def test_fp32_matmul_tensor_core_3xtf32(M, N, K, ta, tb):
         want = ref + (C0.double() if acc else 0)
         err = ((C.double() - want).abs() / want.abs().clamp(min=1)).max().item()
         assert err <= 1e-5, (acc, err)
+
+
+@pytest.mark.parametrize("dtype", ["f64", "f32"])
+@pytest.mark.parametrize("M,N,K,ta,tb", [(4000, 1, 4000, 0, 0), (4000, 1, 4000, 1, 0), (1, 3000, 2000, 0, 1),
+                                         (1, 3000, 2000, 0, 0), (4000, 4000, 1, 0, 0), (333, 1, 257, 0, 0),
+                                         (333, 1, 257, 1, 0), (301, 299, 1, 1, 1)])
+def test_matvec_and_rank1_paths(M, N, K, ta, tb, dtype):
+    """gfb_matmul shape classes N == 1 / M == 1 (row dots, split column sums)
+    and K == 1 (rank-1), vectorised and scalar variants, against fp64."""
+    from paper_2509_02197_b200 import _lib as L
+
+    lib = L.load()
+    td = torch.float64 if dtype == "f64" else torch.float32
+    code = L.F64 if dtype == "f64" else L.F32
+    g = torch.Generator(device="cuda").manual_seed(M + 3 * N + 7 * K + ta + 2 * tb)
+    A = torch.rand((K, M) if ta else (M, K), generator=g, device="cuda", dtype=td) - 0.5
+    B = torch.rand((N, K) if tb else (K, N), generator=g, device="cuda", dtype=td) - 0.5
+    C0 = torch.rand((M, N), generator=g, device="cuda", dtype=td)
+    ref = (A.double().T if ta else A.double()) @ (B.double().T if tb else B.double())
+    ws = torch.empty(max(lib.gfb_matmul_workspace_bytes(code, ta, tb, M, N, K), 16), dtype=torch.uint8,
+                     device="cuda")
+    st = torch.cuda.current_stream().cuda_stream
+    tol = 1e-10 if dtype == "f64" else 1e-5
+    for acc in (0, 1):
+        C = C0.clone()
+        L.check(lib.gfb_matmul(code, ta, tb, M, N, K, A.data_ptr(), A.shape[1], B.data_ptr(), B.shape[1],
+                               C.data_ptr(), N, acc, ws.data_ptr(), st), "matmul")
+        torch.cuda.synchronize()
+        want = ref + (C0.double() if acc else 0)
+        err = ((C.double() - want).abs() / want.abs().clamp(min=1)).max().item()
+        assert err <= tol, (acc, err)
