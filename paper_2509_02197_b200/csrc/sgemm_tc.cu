@@ -4,12 +4,14 @@
 // The mlp matmuls and their adjoints (reference matmul library node,
 // interpreter.py:433-446; adjoint jobs autodiff.py:780-802) are fp32 with a
 // 1e-5 relative tolerance, which plain TF32 (10-bit mantissa) cannot meet.
-// Each operand is split as x = hi + lo with hi = tf32(x), lo = tf32(x - hi),
+// Each operand is split as x = hi + lo with hi = x truncated to TF32 and
+// lo = x - hi (exact; the tensor core keeps its top bits),
 // and C = A_hi B_hi + A_hi B_lo + A_lo B_hi is accumulated in fp32 TMEM
 // (the dropped A_lo B_lo term is ~2^-22 relative).
 //
-// CTA: 256 threads, tile 128 (M) x BN (N) x 32 (K) per stage, two smem
-// stages. All threads stage a k-slab as 16-byte chunks (row, 4 k): the
+// CTA: 256 threads, tile 128 (M) x BN (N, 32..128) x 32 (K) per stage,
+// three smem stages; skinny problems run transposed (C^T = B^T A^T) so the
+// large dimension fills the MMA's 128 rows. All threads stage a k-slab as 16-byte chunks (row, 4 k): the
 // global loads of slab t are issued before waiting for its smem slot, then
 // hi/lo split and stored into the K-major SWIZZLE_128B canonical layout the
 // UMMA smem descriptors describe (row = 32 fp32 = 128 B; 8-row atoms of
@@ -39,6 +41,11 @@ __device__ __forceinline__ float tf32_round(float x) {
 // k-slab lives at byte r*128 + ((k/4) ^ (r%8))*16 + (k%4)*4
 __device__ __forceinline__ uint32_t sw128(int r, int k) {
   return (uint32_t)(r * 128 + ((((k >> 2) ^ (r & 7)) << 4) | ((k & 3) << 2)));
+}
+
+__device__ __forceinline__ void sts128(uint32_t addr, float4 v) {
+  asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w)
+               : "memory");
 }
 
 __device__ __forceinline__ uint64_t umma_desc_sw128(uint32_t saddr) {
@@ -83,20 +90,28 @@ __device__ __forceinline__ void tc_commit(uint64_t *bar) {
                : "memory");
 }
 
+constexpr int kTcStages = 3;
+
 template <int BN>
 struct TcSmem {
   // [stage][hi/lo] slabs; 1 KiB aligned (swizzle atoms)
-  alignas(1024) float a[2][2][kTcM * kTcK];
-  alignas(1024) float b[2][2][BN * kTcK];
-  uint64_t mbar[2];
+  alignas(1024) float a[kTcStages][2][kTcM * kTcK];
+  alignas(1024) float b[kTcStages][2][BN * kTcK];
+  uint64_t mbar[kTcStages];
   uint64_t done;
   uint32_t tmem;
 };
 
+// hi = x with the low 13 mantissa bits cleared (exactly a TF32 value);
+// lo = x - hi is exact in fp32 and the tensor core reads its top 19 bits
+__device__ __forceinline__ float tf32_hi(float x) { return __uint_as_float(__float_as_uint(x) & 0xFFFFE000u); }
+
+// C[m * csm + n * csn] (+)= sum_k op(A)(m, k) op(B)(k, n); the host maps the
+// transposed orientation (C^T = op(B)^T op(A)^T) onto this with csm = 1
 template <int BN, bool TA, bool TB>
 __global__ void __launch_bounds__(kTcThreads, 1)
     sgemm_tc_kernel(int M, int N, int K, const float *__restrict__ A, int64_t lda, const float *__restrict__ B,
-                    int64_t ldb, float *C, int64_t ldc, int accumulate, float *partial, int kchunk) {
+                    int64_t ldb, float *C, int64_t csm, int64_t csn, int accumulate, float *partial, int kchunk) {
   extern __shared__ __align__(1024) unsigned char tc_raw[];
   // align the dynamic region to 1 KiB by hand (the runtime guarantees 16 B)
   TcSmem<BN> &S = *reinterpret_cast<TcSmem<BN> *>((reinterpret_cast<uintptr_t>(tc_raw) + 1023) & ~(uintptr_t)1023);
@@ -104,15 +119,15 @@ __global__ void __launch_bounds__(kTcThreads, 1)
   const int m0 = blockIdx.y * kTcM, n0 = blockIdx.x * BN;
   const int kb = blockIdx.z * kchunk, ke = min(kb + kchunk, K);
   const int nslab = (ke - kb + kTcK - 1) / kTcK;
+  constexpr int kCols = BN < 32 ? 32 : BN;
 
   if (warp == 0) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(tc_smem(&S.tmem)),
-                 "r"(BN < 32 ? 32 : BN));
+                 "r"(kCols));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   if (tid == 0) {
-    tc_mbar_init(&S.mbar[0]);
-    tc_mbar_init(&S.mbar[1]);
+    for (int i = 0; i < kTcStages; ++i) tc_mbar_init(&S.mbar[i]);
     tc_mbar_init(&S.done);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -120,6 +135,14 @@ __global__ void __launch_bounds__(kTcThreads, 1)
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem = S.tmem;
+  uint32_t sa_hi[kTcStages], sa_lo[kTcStages], sb_hi[kTcStages], sb_lo[kTcStages];
+#pragma unroll
+  for (int i = 0; i < kTcStages; ++i) {
+    sa_hi[i] = tc_smem(S.a[i][0]);
+    sa_lo[i] = tc_smem(S.a[i][1]);
+    sb_hi[i] = tc_smem(S.b[i][0]);
+    sb_lo[i] = tc_smem(S.b[i][1]);
+  }
 
   // instruction descriptor: D f32, A/B tf32, both K-major, N, M
   const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(BN >> 3) << 17) |
@@ -128,8 +151,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
   // A k-slab is staged as 16-byte chunks: (row, 4 consecutive k). Chunk c
   // of a thread: rows of op(A) first (kTcM * 8 chunks), then op(B)^T.
   constexpr int kChA = kTcM * (kTcK / 4), kChB = BN * (kTcK / 4);
-  constexpr int kPer = (kChA + kChB) / kTcThreads;
-  static_assert((kChA + kChB) % kTcThreads == 0, "chunks / threads");
+  constexpr int kPer = (kChA + kChB + kTcThreads - 1) / kTcThreads;
   const bool avec = !TA && (lda % 4 == 0) && ((reinterpret_cast<uintptr_t>(A) & 15) == 0);
   const bool bvec = TB && (ldb % 4 == 0) && ((reinterpret_cast<uintptr_t>(B) & 15) == 0);
   // chunk -> (operand, row, k-chunk). Consecutive lanes walk the contiguous
@@ -140,8 +162,8 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     const int rows = isb ? BN : kTcM;
     const bool kfast = isb ? TB : !TA;
     if (kfast) {  // lanes along k: 8 chunks of one row, then the next row
-      kc = e % 8;
-      r = e / 8;
+      kc = e & 7;
+      r = e >> 3;
     } else {  // lanes along the row index
       r = e % rows;
       kc = e / rows;
@@ -150,9 +172,11 @@ __global__ void __launch_bounds__(kTcThreads, 1)
   auto load = [&](float4(&reg)[kPer], int k0) {
 #pragma unroll
     for (int i = 0; i < kPer; ++i) {
+      const int c = tid + i * kTcThreads;
+      if ((kChA + kChB) % kTcThreads != 0 && c >= kChA + kChB) break;
       bool isb;
       int r, kc;
-      chunk_of(tid + i * kTcThreads, isb, r, kc);
+      chunk_of(c, isb, r, kc);
       const int gk = k0 + kc * 4;
       float v[4] = {0.f, 0.f, 0.f, 0.f};
       if (!isb) {
@@ -186,18 +210,19 @@ __global__ void __launch_bounds__(kTcThreads, 1)
   auto store = [&](const float4(&reg)[kPer], int s) {
 #pragma unroll
     for (int i = 0; i < kPer; ++i) {
+      const int c = tid + i * kTcThreads;
+      if ((kChA + kChB) % kTcThreads != 0 && c >= kChA + kChB) break;
       bool isb;
       int r, kc;
-      chunk_of(tid + i * kTcThreads, isb, r, kc);
-      unsigned char *hi = reinterpret_cast<unsigned char *>(isb ? S.b[s][0] : S.a[s][0]);
-      unsigned char *lo = reinterpret_cast<unsigned char *>(isb ? S.b[s][1] : S.a[s][1]);
+      chunk_of(c, isb, r, kc);
+      // 32-bit shared addresses keep these st.shared (not generic stores)
+      const uint32_t hi = isb ? sb_hi[s] : sa_hi[s], lo = isb ? sb_lo[s] : sa_lo[s];
       const float4 x = reg[i];
-      const float4 h = make_float4(tf32_round(x.x), tf32_round(x.y), tf32_round(x.z), tf32_round(x.w));
-      const float4 l = make_float4(tf32_round(x.x - h.x), tf32_round(x.y - h.y), tf32_round(x.z - h.z),
-                                   tf32_round(x.w - h.w));
+      const float4 h = make_float4(tf32_hi(x.x), tf32_hi(x.y), tf32_hi(x.z), tf32_hi(x.w));
+      const float4 l = make_float4(x.x - h.x, x.y - h.y, x.z - h.z, x.w - h.w);
       const uint32_t o = sw128(r, kc * 4);
-      *reinterpret_cast<float4 *>(hi + o) = h;
-      *reinterpret_cast<float4 *>(lo + o) = l;
+      sts128(hi + o, h);
+      sts128(lo + o, l);
     }
     // make the generic-proxy stores visible to the tensor core's async proxy
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -205,17 +230,16 @@ __global__ void __launch_bounds__(kTcThreads, 1)
 
   // one slab: its registers were loaded two slabs ago; the loads of slab
   // t + 2 go out first so two slabs of global latency overlap the staging
-  // and the MMAs
+  // and the MMAs; the smem ring has kTcStages slots
   auto slab = [&](int t, float4(&cur)[kPer], float4(&ahead)[kPer]) {
-    const int s = t & 1;
+    const int s = t % kTcStages;
     if (t + 2 < nslab) load(ahead, kb + (t + 2) * kTcK);
-    if (t >= 2) tc_mbar_wait(&S.mbar[s], (uint32_t)(((t - 2) >> 1) & 1));
+    if (t >= kTcStages) tc_mbar_wait(&S.mbar[s], (uint32_t)(((t - kTcStages) / kTcStages) & 1));
     store(cur, s);
     __syncthreads();
     if (tid == 0) {
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-      const uint32_t ah = tc_smem(S.a[s][0]), al = tc_smem(S.a[s][1]);
-      const uint32_t bh = tc_smem(S.b[s][0]), bl = tc_smem(S.b[s][1]);
+      const uint32_t ah = sa_hi[s], al = sa_lo[s], bh = sb_hi[s], bl = sb_lo[s];
 #pragma unroll
       for (int ks = 0; ks < kTcK / 8; ++ks) {  // 8 tf32 = 32 B per MMA k-step
         const uint32_t off = ks * 32;
@@ -245,49 +269,86 @@ __global__ void __launch_bounds__(kTcThreads, 1)
   // half w / 4; thread = one row
   const int quarter = warp & 3, half = warp >> 2;
   const int row = quarter * 32 + lane, gm = m0 + row;
+  constexpr int kHalf = BN / 2 < 8 ? 8 : BN / 2;
+  constexpr int kGrp = kHalf < 32 ? kHalf : 32;  // columns per round: all loads of a round in flight
 #pragma unroll 1
-  for (int c = half * (BN / 2); c < (half + 1) * (BN / 2); c += 8) {
-    uint32_t v[8];
-    const uint32_t taddr = tmem + ((uint32_t)(quarter * 32) << 16) + (uint32_t)c;
-    asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
-                 : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7])
-                 : "r"(taddr));
-    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-    if (gm >= M) continue;
+  for (int c0 = half * kHalf; c0 < (half + 1) * kHalf && c0 < BN; c0 += kGrp) {
+    uint32_t v[kGrp];
 #pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      const int gn = n0 + c + j;
+    for (int g = 0; g < kGrp; g += 8) {
+      const uint32_t taddr = tmem + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(c0 + g);
+      asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+                   : "=r"(v[g]), "=r"(v[g + 1]), "=r"(v[g + 2]), "=r"(v[g + 3]), "=r"(v[g + 4]), "=r"(v[g + 5]),
+                     "=r"(v[g + 6]), "=r"(v[g + 7])
+                   : "r"(taddr));
+    }
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+    if (csn == 1 && !partial) {
+      // row-major C: transpose the warp's 32 rows x kGrp columns through
+      // (now idle) stage memory so lanes walk consecutive columns of a row
+      float *scr = S.a[0][0] + warp * (32 * (kGrp + 1));
+#pragma unroll
+      for (int j = 0; j < kGrp; ++j) scr[lane * (kGrp + 1) + j] = nslab > 0 ? __uint_as_float(v[j]) : 0.f;
+      __syncwarp();
+      if (lane < kGrp) {
+        const int gn = n0 + c0 + lane;
+        for (int r = 0; r < 32; ++r) {
+          const int rm = m0 + quarter * 32 + r;
+          if (rm >= M || gn >= N) continue;
+          const float x = scr[r * (kGrp + 1) + lane];
+          float *o = C + (int64_t)rm * csm + gn;
+          *o = accumulate ? *o + x : x;
+        }
+      }
+      __syncwarp();
+      continue;
+    }
+    if (gm >= M) continue;
+    float old[kGrp];
+    if (!partial && accumulate) {
+#pragma unroll
+      for (int j = 0; j < kGrp; ++j) {
+        const int gn = n0 + c0 + j;
+        old[j] = gn < N ? C[(int64_t)gm * csm + (int64_t)gn * csn] : 0.f;
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < kGrp; ++j) {
+      const int gn = n0 + c0 + j;
       if (gn >= N) continue;
       const float x = nslab > 0 ? __uint_as_float(v[j]) : 0.f;
-      if (partial) {
+      if (partial)
         partial[((int64_t)blockIdx.z * M + gm) * N + gn] = x;
-      } else {
-        float *o = C + (int64_t)gm * ldc + gn;
-        *o = accumulate ? *o + x : x;
-      }
+      else
+        C[(int64_t)gm * csm + (int64_t)gn * csn] = accumulate ? old[j] + x : x;
     }
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
-  if (warp == 0)
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(BN < 32 ? 32 : BN));
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kCols));
 }
 
 __global__ void tc_splits_finish(int64_t M, int64_t N, int64_t ns, const float *__restrict__ partial, float *C,
-                                 int64_t ldc, int accumulate) {
+                                 int64_t csm, int64_t csn, int accumulate) {
   const int64_t MN = M * N;
   for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < MN; e += (int64_t)gridDim.x * blockDim.x) {
     float s = 0.f;
     for (int64_t q = 0; q < ns; ++q) s += partial[q * MN + e];
     const int64_t m = e / N, n = e - m * N;
-    float *c = C + m * ldc + n;
+    float *c = C + m * csm + n * csn;
     *c = accumulate ? *c + s : s;
   }
 }
 
-static int tc_bn(int64_t N) { return N <= 64 ? 64 : 128; }
+static int tc_bn(int64_t N) { return N <= 32 ? 32 : (N <= 64 ? 64 : 128); }
+
+// Orientation: the MMA's M side is fixed at 128 rows, its N side is 32..128;
+// put the larger output dimension on the M side (skinny problems such as
+// the mlp's batch-64 layers then waste no rows)
+static bool tc_swap(int64_t M, int64_t N) { return M < N && M <= 128; }
 
 int64_t sgemm_tc_splits(int64_t M, int64_t N, int64_t K) {
+  if (tc_swap(M, N)) std::swap(M, N);
   const int64_t tiles = ceil_div(M, kTcM) * ceil_div(N, tc_bn(N));
   const int64_t target = (int64_t)sm_count();
   if (tiles >= target) return 1;
@@ -304,47 +365,65 @@ bool sgemm_tc_usable(int64_t M, int64_t N, int64_t K) {
 
 template <int BN, bool TA, bool TB>
 static void launch_tc(dim3 grid, int M, int N, int K, const float *A, int64_t lda, const float *B, int64_t ldb,
-                      float *C, int64_t ldc, int accumulate, float *partial, int kchunk, cudaStream_t st) {
+                      float *C, int64_t csm, int64_t csn, int accumulate, float *partial, int kchunk,
+                      cudaStream_t st) {
   const size_t smem = sizeof(TcSmem<BN>) + 1024;
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(sgemm_tc_kernel<BN, TA, TB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     attr = true;
   }
-  sgemm_tc_kernel<BN, TA, TB><<<grid, kTcThreads, smem, st>>>(M, N, K, A, lda, B, ldb, C, ldc, accumulate, partial,
-                                                               kchunk);
+  sgemm_tc_kernel<BN, TA, TB><<<grid, kTcThreads, smem, st>>>(M, N, K, A, lda, B, ldb, C, csm, csn, accumulate,
+                                                               partial, kchunk);
 }
 
 template <int BN>
 static void launch_tc_t(int ta, int tb, dim3 grid, int M, int N, int K, const float *A, int64_t lda,
-                        const float *B, int64_t ldb, float *C, int64_t ldc, int accumulate, float *partial,
-                        int kchunk, cudaStream_t st) {
+                        const float *B, int64_t ldb, float *C, int64_t csm, int64_t csn, int accumulate,
+                        float *partial, int kchunk, cudaStream_t st) {
   if (ta && tb)
-    launch_tc<BN, true, true>(grid, M, N, K, A, lda, B, ldb, C, ldc, accumulate, partial, kchunk, st);
+    launch_tc<BN, true, true>(grid, M, N, K, A, lda, B, ldb, C, csm, csn, accumulate, partial, kchunk, st);
   else if (ta)
-    launch_tc<BN, true, false>(grid, M, N, K, A, lda, B, ldb, C, ldc, accumulate, partial, kchunk, st);
+    launch_tc<BN, true, false>(grid, M, N, K, A, lda, B, ldb, C, csm, csn, accumulate, partial, kchunk, st);
   else if (tb)
-    launch_tc<BN, false, true>(grid, M, N, K, A, lda, B, ldb, C, ldc, accumulate, partial, kchunk, st);
+    launch_tc<BN, false, true>(grid, M, N, K, A, lda, B, ldb, C, csm, csn, accumulate, partial, kchunk, st);
   else
-    launch_tc<BN, false, false>(grid, M, N, K, A, lda, B, ldb, C, ldc, accumulate, partial, kchunk, st);
+    launch_tc<BN, false, false>(grid, M, N, K, A, lda, B, ldb, C, csm, csn, accumulate, partial, kchunk, st);
 }
 
 int sgemm_tc(int ta, int tb, int64_t M, int64_t N, int64_t K, const float *A, int64_t lda, const float *B,
              int64_t ldb, float *C, int64_t ldc, int accumulate, void *ws, cudaStream_t st) {
-  const int BN = tc_bn(N);
   const int64_t ns = sgemm_tc_splits(M, N, K);
+  int64_t csm = ldc, csn = 1;
+  if (tc_swap(M, N)) {
+    // C^T = op(B)^T op(A)^T: op'(A') = op(B)^T is "transposed" exactly when
+    // op(B) is not, and likewise for B'
+    std::swap(M, N);
+    std::swap(A, B);
+    std::swap(lda, ldb);
+    const int nta = tb ? 0 : 1, ntb = ta ? 0 : 1;
+    ta = nta;
+    tb = ntb;
+    csm = 1;
+    csn = ldc;
+  }
+  const int BN = tc_bn(N);
   const int64_t chunk = ceil_div(ceil_div(K, ns), kTcK) * kTcK;
   const int64_t nz = ceil_div(K, chunk);
   float *partial = nz > 1 ? (float *)ws : nullptr;
   dim3 grid((unsigned)ceil_div(N, BN), (unsigned)ceil_div(M, kTcM), (unsigned)nz);
-  if (BN == 64)
-    launch_tc_t<64>(ta, tb, grid, (int)M, (int)N, (int)K, A, lda, B, ldb, C, ldc, accumulate, partial, (int)chunk, st);
+  if (BN == 32)
+    launch_tc_t<32>(ta, tb, grid, (int)M, (int)N, (int)K, A, lda, B, ldb, C, csm, csn, accumulate, partial,
+                    (int)chunk, st);
+  else if (BN == 64)
+    launch_tc_t<64>(ta, tb, grid, (int)M, (int)N, (int)K, A, lda, B, ldb, C, csm, csn, accumulate, partial,
+                    (int)chunk, st);
   else
-    launch_tc_t<128>(ta, tb, grid, (int)M, (int)N, (int)K, A, lda, B, ldb, C, ldc, accumulate, partial, (int)chunk,
-                     st);
+    launch_tc_t<128>(ta, tb, grid, (int)M, (int)N, (int)K, A, lda, B, ldb, C, csm, csn, accumulate, partial,
+                     (int)chunk, st);
   if (nz > 1) {
     const unsigned blocks = (unsigned)std::min<int64_t>(ceil_div(M * N, 256), (int64_t)sm_count() * 8);
-    tc_splits_finish<<<blocks, 256, 0, st>>>(M, N, nz, partial, C, ldc, accumulate);
+    tc_splits_finish<<<blocks, 256, 0, st>>>(M, N, nz, partial, C, csm, csn, accumulate);
   }
   return check_launch("sgemm_tc");
 }
