@@ -270,8 +270,10 @@ typedef struct {
   int32_t dtype;
   int32_t clear_mode;
   int32_t ncm, ncn;
-  int32_t a_kfast;   /* A contiguous along k (else along m): load layout */
-  int32_t b_nfast;   /* B contiguous along n (else along k) */
+  int32_t a_kfast;   /* bit 0: A contiguous along k (else along m): load layout;
+                        bit 1: 16-byte quads along that direction (fp32: offsets
+                        consecutive and 4-aligned, constraints equal within a quad) */
+  int32_t b_nfast;   /* bit 0: B contiguous along n (else along k); bit 1 as above */
   int32_t nsplit;
   int32_t mstride, nstride, kstride;  /* int32 words per table entry */
   int64_t M, N, K;

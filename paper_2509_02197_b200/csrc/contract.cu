@@ -35,9 +35,13 @@ __global__ void __launch_bounds__((BM / TM) * (BN / TN))
   const int ncm = d.ncm, ncn = d.ncn;
   const int64_t M = d.M, N = d.N, K = d.K;
   const int s = blockIdx.z;
-  const int64_t kb = K * s / d.nsplit, ke = K * (s + 1) / d.nsplit;
+  // split boundaries on BK multiples (16-byte k-quads never straddle two splits)
+  const int64_t kchunk = (K + (int64_t)d.nsplit * BK - 1) / ((int64_t)d.nsplit * BK) * BK;
+  const int64_t kb = min((int64_t)s * kchunk, K), ke = min(kb + kchunk, K);
   const T *__restrict__ Ag = (const T *)d.a;
   const T *__restrict__ Bg = (const T *)d.b;
+  const bool aq = sizeof(T) == 4 && (d.a_kfast & 2) && (reinterpret_cast<uintptr_t>(Ag) & 15) == 0;
+  const bool bq = sizeof(T) == 4 && (d.b_nfast & 2) && (reinterpret_cast<uintptr_t>(Bg) & 15) == 0;
 
   for (int i = tid; i < BM; i += NT) {
     const int64_t m = m0 + i;
@@ -98,30 +102,97 @@ __global__ void __launch_bounds__((BM / TM) * (BN / TN))
       }
       return ok ? Bg[(int64_t)snb[nn] + skb[kk]] : T(0);
     };
-    if (d.a_kfast) {
-#pragma unroll
-      for (int r = 0; r < BM * BK / NT; ++r) {
-        const int e = tid + r * NT, kk = e % BK, mm = e / BK;
-        As[kk][mm] = a_elem(mm, kk);
+    // 16-byte quads (bit 1 of a_kfast / b_nfast, fp32): the host proved
+    // four consecutive elements along the fast direction contiguous, aligned
+    // and under equal constraints, so one check and one vector load serve four
+    auto a_quad_ok = [&](int mm, int kk) -> bool {  // element (mm, kk) starts a quad
+      if (m0 + mm >= M || k0 + kk >= ke) return false;
+      bool ok = true;
+      for (int c = 0; c < ncm; ++c) {
+        const int32_t v = smc[c][mm] + skc[c][kk];
+        ok &= v >= d.lo[c] && v < d.hi[c];
       }
-    } else {
-#pragma unroll
-      for (int r = 0; r < BM * BK / NT; ++r) {
-        const int e = tid + r * NT, mm = e % BM, kk = e / BM;
-        As[kk][mm] = a_elem(mm, kk);
+      return ok;
+    };
+    auto b_quad_ok = [&](int nn, int kk) -> bool {
+      if (n0 + nn >= N || k0 + kk >= ke) return false;
+      bool ok = true;
+      for (int c = 0; c < ncn; ++c) {
+        const int32_t v = snc[c][nn] + skc[ncm + c][kk];
+        ok &= v >= d.lo[ncm + c] && v < d.hi[ncm + c];
+      }
+      return ok;
+    };
+    if constexpr (sizeof(T) == 4) {
+      if (aq) {
+        if (d.a_kfast & 1) {
+          for (int e = tid; e < BM * BK / 4; e += NT) {
+            const int kq = e % (BK / 4), mm = e / (BK / 4), kk = 4 * kq;
+            float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+            if (a_quad_ok(mm, kk)) v = *reinterpret_cast<const float4 *>(Ag + (int64_t)sma[mm] + ska[kk]);
+            As[kk][mm] = v.x;
+            As[kk + 1][mm] = v.y;
+            As[kk + 2][mm] = v.z;
+            As[kk + 3][mm] = v.w;
+          }
+        } else {
+          for (int e = tid; e < BM * BK / 4; e += NT) {
+            const int mq = e % (BM / 4), kk = e / (BM / 4), mm = 4 * mq;
+            float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+            if (a_quad_ok(mm, kk)) v = *reinterpret_cast<const float4 *>(Ag + (int64_t)sma[mm] + ska[kk]);
+            *reinterpret_cast<float4 *>(&As[kk][mm]) = v;
+          }
+        }
+      }
+      if (bq) {
+        if (d.b_nfast & 1) {
+          for (int e = tid; e < BN * BK / 4; e += NT) {
+            const int nq = e % (BN / 4), kk = e / (BN / 4), nn = 4 * nq;
+            float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+            if (b_quad_ok(nn, kk)) v = *reinterpret_cast<const float4 *>(Bg + (int64_t)snb[nn] + skb[kk]);
+            *reinterpret_cast<float4 *>(&Bs[kk][nn]) = v;
+          }
+        } else {
+          for (int e = tid; e < BN * BK / 4; e += NT) {
+            const int kq = e % (BK / 4), nn = e / (BK / 4), kk = 4 * kq;
+            float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+            if (b_quad_ok(nn, kk)) v = *reinterpret_cast<const float4 *>(Bg + (int64_t)snb[nn] + skb[kk]);
+            Bs[kk][nn] = v.x;
+            Bs[kk + 1][nn] = v.y;
+            Bs[kk + 2][nn] = v.z;
+            Bs[kk + 3][nn] = v.w;
+          }
+        }
       }
     }
-    if (d.b_nfast) {
+    if (!aq) {
+      if (d.a_kfast & 1) {
 #pragma unroll
-      for (int r = 0; r < BN * BK / NT; ++r) {
-        const int e = tid + r * NT, nn = e % BN, kk = e / BN;
-        Bs[kk][nn] = b_elem(nn, kk);
+        for (int r = 0; r < BM * BK / NT; ++r) {
+          const int e = tid + r * NT, kk = e % BK, mm = e / BK;
+          As[kk][mm] = a_elem(mm, kk);
+        }
+      } else {
+#pragma unroll
+        for (int r = 0; r < BM * BK / NT; ++r) {
+          const int e = tid + r * NT, mm = e % BM, kk = e / BM;
+          As[kk][mm] = a_elem(mm, kk);
+        }
       }
-    } else {
+    }
+    if (!bq) {
+      if (d.b_nfast & 1) {
 #pragma unroll
-      for (int r = 0; r < BN * BK / NT; ++r) {
-        const int e = tid + r * NT, kk = e % BK, nn = e / BK;
-        Bs[kk][nn] = b_elem(nn, kk);
+        for (int r = 0; r < BN * BK / NT; ++r) {
+          const int e = tid + r * NT, nn = e % BN, kk = e / BN;
+          Bs[kk][nn] = b_elem(nn, kk);
+        }
+      } else {
+#pragma unroll
+        for (int r = 0; r < BN * BK / NT; ++r) {
+          const int e = tid + r * NT, kk = e % BK, nn = e / BK;
+          Bs[kk][nn] = b_elem(nn, kk);
+        }
       }
     }
     __syncthreads();

@@ -1091,6 +1091,23 @@ def _i32(a):
     return np.ascontiguousarray(a.astype(np.int32))
 
 
+def _quads(fast_off, fast_cons, other_off) -> bool:
+    """Four consecutive entries along the fast table form 16-byte quads:
+    offsets consecutive and 4-aligned, constraint parts equal within each
+    quad, and every other-side offset 4-aligned (count a multiple of 4)."""
+    n = len(fast_off)
+    if n % 4 or n == 0:
+        return False
+    q = np.asarray(fast_off, dtype=np.int64).reshape(-1, 4)
+    if np.any(q[:, 0] % 4) or np.any(q - q[:, :1] != np.arange(4)):
+        return False
+    if fast_cons.size:
+        c = np.asarray(fast_cons, dtype=np.int64).reshape(-1, 4, fast_cons.shape[1])
+        if np.any(c != c[:, :1, :]):
+            return False
+    return not np.any(np.asarray(other_off, dtype=np.int64) % 4)
+
+
 def contract_form(space, body, acc, ins, dst, ybox, clear_mode, cbox):
     """Build the ContractOp of a single-term gather whose body is a scaled
     product of two reads, or None when the pass does not have that shape
@@ -1216,6 +1233,18 @@ def contract_form(space, body, acc, ins, dst, ybox, clear_mode, cbox):
         return None
     a_kfast = 1 if kdims and abs(int(fa[rank + free.index(kdims[-1])])) == 1 else 0
     b_nfast = 1 if ndims and abs(int(fb[ndims[-1]])) == 1 else 0
+    ncm, ncn = len(cons_m), len(cons_n)
+    # 16-byte quads along each operand's fast direction (bit 1)
+    if a_kfast:
+        a_q = _quads(ktab[:, 0], ktab[:, 2:2 + ncm], mtab[:, 0])
+    else:
+        a_q = _quads(mtab[:, 0], mtab[:, 3:3 + ncm], ktab[:, 0])
+    if b_nfast:
+        b_q = _quads(ntab[:, 0], ntab[:, 3:3 + ncn], ktab[:, 1])
+    else:
+        b_q = _quads(ktab[:, 1], ktab[:, 2 + ncm:2 + ncm + ncn], ntab[:, 0])
+    a_kfast |= 2 if a_q and A.buf.dtype == L.F32 else 0
+    b_nfast |= 2 if b_q and B.buf.dtype == L.F32 else 0
     BM, BN = contract_tile(M, N)
     tiles = -(-M // BM) * -(-N // BN)
     nsplit = 1
