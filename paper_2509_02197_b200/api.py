@@ -215,9 +215,9 @@ class Lowered:
 
 
 def lower_gradient(program: Program, bundle: Bundle, params: dict, shapes: dict, *, trip_limit=None,
-                   record=None, plan: PlanBundle | None = None) -> Lowered:
+                   record=None, plan: PlanBundle | None = None, fuse_small=False) -> Lowered:
     """Forward (recording the tape) + backward as one launch list."""
-    low = Lowering(trip_limit=trip_limit)
+    low = Lowering(trip_limit=trip_limit, fuse_small=fuse_small)
     fwd_prog = plan.forward if plan else program
     bwd_prog = plan.backward if plan else bundle.backward
     forwarding = plan.forwarding if plan else bundle.forwarding

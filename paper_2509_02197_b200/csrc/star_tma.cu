@@ -528,11 +528,13 @@ static int launch_tma(const CUtensorMap &map, const StarPairDev &d, cudaStream_t
     cudaFuncSetAttribute(star_pair_tma_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     attr = true;
   }
-  // planes per CTA: as many as keep >= 4 CTAs per SM worth of work in the
-  // grid (small domains get short marches rather than idle SMs)
+  // planes per CTA: the longest march (up to tPM) that still puts every
+  // tile-column segment in one wave of resident CTAs (2 per SM); small
+  // domains get short marches rather than idle SMs or a straggler wave
   StarPairDev dd = d;
   const int64_t tiles = ceil_div(d.d2, tPX) * ceil_div(d.d1, tPY), planes = d.zhi - d.zlo;
-  dd.tpm = (int32_t)std::max<int64_t>(2, std::min<int64_t>(tPM, planes * tiles / (4 * (int64_t)sm_count())));
+  const int64_t slots = 2 * (int64_t)sm_count();
+  dd.tpm = (int32_t)std::max<int64_t>(2, std::min<int64_t>(tPM, ceil_div(planes * tiles, slots)));
   dim3 grid((unsigned)ceil_div(d.d2, tPX), (unsigned)ceil_div(d.d1, tPY), (unsigned)ceil_div(planes, dd.tpm));
   star_pair_tma_kernel<T><<<grid, dim3(tPX, tPY / kR), sm, st>>>(map, dd);
   return check_launch("star_pair_tma");

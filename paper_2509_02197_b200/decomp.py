@@ -214,7 +214,7 @@ class SlabEngine:
         prog, bundle = W.load(name)
         self.program = prog
         shapes = W.input_shapes(prog, params)
-        lw = lower_gradient(prog, bundle, params, shapes)
+        lw = lower_gradient(prog, bundle, params, shapes, fuse_small=True)
         N = next(iter(shapes.values()))[0]
         self.plan = SlabPlan(N, world, rank)
         self.dl = decompose(lw, self.plan, TorchComm())

@@ -31,7 +31,7 @@ def _run_rank(rank, world, port, params, q):
     try:
         prog, bundle = W.load("heat_3d")
         shapes = W.input_shapes(prog, params)
-        lw = lower_gradient(prog, bundle, params, shapes)
+        lw = lower_gradient(prog, bundle, params, shapes, fuse_small=True)
         plan = SlabPlan(params["N"], world, rank)
         dl = decompose(lw, plan, TorchComm())
         full = W.make_inputs("heat_3d", prog, params, 0)

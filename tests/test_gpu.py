@@ -201,7 +201,7 @@ def test_slab_decomposition_kernels_in_lockstep(world):
     comm = _LockstepComm()
     ranks = []
     for r in range(world):
-        lw = lower_gradient(prog, b, params, shapes)
+        lw = lower_gradient(prog, b, params, shapes, fuse_small=True)
         plan = SlabPlan(params["N"], world, r)
         dl = decompose(lw, plan, comm)
         exe = Executable(dl.low, dl.inputs, dl.outputs, seed_buf=dl.seed_buf, use_graph=False)

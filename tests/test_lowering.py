@@ -70,7 +70,7 @@ def test_stencil_timestep_is_one_fused_launch_with_clears_folded():
     prog, b = _bundle("heat_3d")
     params = {"N": 10, "TSTEPS": 5}
     inputs = W.make_inputs("heat_3d", prog, params, 0)
-    lw = lower_gradient(prog, b, params, _check_inputs(prog, inputs, params))
+    lw = lower_gradient(prog, b, params, _check_inputs(prog, inputs, params), fuse_small=True)
     pairs = [op for op in lw.low.ops if isinstance(op, StarPairOp)]
     assert len(pairs) == 2 * (params["TSTEPS"] - 1)
     assert not any(isinstance(op, (FillOp, StencilOp)) for op in lw.low.ops)
@@ -95,7 +95,7 @@ def test_tape_snapshot_is_aliased_when_never_overwritten():
     prog, b = _bundle("atax")
     params = {"M": 6, "N": 5}
     inputs = W.make_inputs("atax", prog, params, 0)
-    lw = lower_gradient(prog, b, params, _check_inputs(prog, inputs, params))
+    lw = lower_gradient(prog, b, params, _check_inputs(prog, inputs, params), fuse_small=True)
     slots = list(lw.tape.values.values())
     assert slots and all(s.alias_of is not None for s in slots)
 

@@ -3,6 +3,8 @@ oracle on small heat_3d / jacobi_2d cases."""
 import os
 import sys
 
+os.environ.setdefault("GFB_SMALL_FUSE_BYTES", "0")  # exercise the fused kernels at small sizes
+
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np  # noqa: E402
 
