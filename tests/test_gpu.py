@@ -321,3 +321,44 @@ def test_matvec_and_rank1_paths(M, N, K, ta, tb, dtype):
         want = ref + (C0.double() if acc else 0)
         err = ((C.double() - want).abs() / want.abs().clamp(min=1)).max().item()
         assert err <= tol, (acc, err)
+
+
+def _torch_c4(name, inputs, params):
+    """Independent fp64 torch-autograd restatement of the C4 programs (the
+    same math as tools/workloads_ref.py), for full-size parity (SURVEY 8(c)
+    tier ii)."""
+    t = {k: torch.tensor(v, dtype=torch.float64, device="cuda", requires_grad=True) for k, v in inputs.items()}
+    if name == "softmax":
+        e = torch.exp(t["x"])
+        O = (e / e.sum(dim=1, keepdim=True) * t["w"]).sum()
+        wrt = ["x"]
+    elif name == "mlp":
+        h = t["x"]
+        for k in (1, 2, 3):
+            h = h @ t[f"W{k}"] + t[f"b{k}"]
+            if k < 3:
+                h = torch.clamp(h, min=0.0)
+        e = torch.exp(h)
+        O = (e / e.sum(dim=1, keepdim=True) * t["w"]).sum()
+        wrt = ["x", "W1", "W2", "W3", "b1", "b2", "b3"]
+    else:  # conv2d_bias, NHWC valid convolution
+        acc = torch.nn.functional.conv2d(t["inp"].permute(0, 3, 1, 2), t["wt"].permute(3, 2, 0, 1))
+        out = acc.permute(0, 2, 3, 1) + t["bias"]
+        O = (out * t["w"]).sum()
+        wrt = ["inp", "wt", "bias"]
+    O.backward()
+    return float(O.detach()), {k: t[k].grad.cpu().numpy() for k in wrt}
+
+
+@pytest.mark.parametrize("cfg", ["C4/softmax", "C4/mlp", "C4/conv2d_bias"])
+def test_c4_full_size_against_torch_fp64_autograd(cfg):
+    """C4 at its config sizes (fp32 engine) against an fp64 torch-autograd
+    restatement of the same program, rtol 1e-5 in the reference metric."""
+    name, params = W.CONFIGS[cfg]
+    prog, b = _bundle(name)
+    inputs = W.make_inputs(name, prog, params, 0)
+    res = gradient(prog, inputs, params, bundle=b)
+    v, g = _torch_c4(name, inputs, params)
+    assert rel_err(res.value, v) <= 1e-5
+    for k, ref in g.items():
+        assert rel_err(res.grads[k], ref) <= 1e-5, k
