@@ -93,6 +93,90 @@ __global__ void __launch_bounds__(kThreads) ew_kernel(int op, T c, const T *__re
   }
 }
 
+// Vectorised elementwise for the common operators on full-length,
+// 16-byte-aligned operands: the operator is a template parameter (no
+// per-element dispatch) and every access is a 16-byte vector.
+template <typename T>
+struct EwVec;
+template <>
+struct EwVec<float> {
+  using V = float4;
+  static constexpr int W = 4;
+};
+template <>
+struct EwVec<double> {
+  using V = double2;
+  static constexpr int W = 2;
+};
+
+template <typename T, int OP>
+__device__ __forceinline__ T ew_apply(T x, T y, T c, uint32_t &bad) {
+  if constexpr (OP == GFB_OP_IN) return x;
+  if constexpr (OP == -1) return x * c;  // scale by a constant
+  if constexpr (OP == GFB_OP_ADD) return x + y;
+  if constexpr (OP == GFB_OP_SUB) return x - y;
+  if constexpr (OP == GFB_OP_MUL) return x * y;
+  if constexpr (OP == GFB_OP_DIV) {
+    if (y == T(0)) bad |= GFB_EBIT_DIV0;
+    return x / y;
+  }
+  if constexpr (OP == GFB_OP_EXP) return t_exp(x);
+  return x;
+}
+
+template <typename T, int OP, bool HASB>
+__global__ void __launch_bounds__(kThreads) ew_vec_kernel(T c, const T *__restrict__ a, const T *__restrict__ b,
+                                                          T *out, int64_t nv, int accumulate, uint32_t *err) {
+  using V = typename EwVec<T>::V;
+  constexpr int W = EwVec<T>::W;
+  const V *av = reinterpret_cast<const V *>(a);
+  const V *bv = reinterpret_cast<const V *>(b);
+  V *ov = reinterpret_cast<V *>(out);
+  uint32_t bad = 0;
+  const int64_t stride = (int64_t)gridDim.x * kThreads;
+  for (int64_t i = (int64_t)blockIdx.x * kThreads + threadIdx.x; i < nv; i += stride) {
+    const V x = av[i];
+    V y = x;
+    if (HASB) y = bv[i];
+    V o = accumulate ? ov[i] : V{};
+    const T *xs = reinterpret_cast<const T *>(&x);
+    const T *ys = reinterpret_cast<const T *>(&y);
+    T *os = reinterpret_cast<T *>(&o);
+#pragma unroll
+    for (int w = 0; w < W; ++w) {
+      const T r = ew_apply<T, OP>(xs[w], ys[w], c, bad);
+      os[w] = accumulate ? os[w] + r : r;
+    }
+    ov[i] = o;
+  }
+  if (bad) raise_bits(err, bad);
+}
+
+template <typename T>
+static bool ew_vec_launch(int op, T c, const T *a, int64_t n_a, const T *b, int64_t n_b, T *out, int64_t n,
+                          int accumulate, uint32_t *err, cudaStream_t st) {
+  constexpr int W = EwVec<T>::W;
+  auto al = [](const void *p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
+  if (n % W || n_a != n || !al(a) || !al(out) || (b && (n_b != n || !al(b)))) return false;
+  const int64_t nv = n / W;
+  const unsigned blocks = (unsigned)stream_blocks(nv, 2);
+#define GFB_EW(OPC, HB) ew_vec_kernel<T, OPC, HB><<<blocks, kThreads, 0, st>>>(c, a, b, out, nv, accumulate, err)
+  if (!b) {
+    if (op == GFB_OP_IN) GFB_EW(GFB_OP_IN, false);
+    else if (op == GFB_OP_MUL) GFB_EW(-1, false);
+    else if (op == GFB_OP_EXP) GFB_EW(GFB_OP_EXP, false);
+    else return false;
+  } else {
+    if (op == GFB_OP_ADD) GFB_EW(GFB_OP_ADD, true);
+    else if (op == GFB_OP_SUB) GFB_EW(GFB_OP_SUB, true);
+    else if (op == GFB_OP_MUL) GFB_EW(GFB_OP_MUL, true);
+    else if (op == GFB_OP_DIV) GFB_EW(GFB_OP_DIV, true);
+    else return false;
+  }
+#undef GFB_EW
+  return true;
+}
+
 template <typename T>
 __global__ void __launch_bounds__(kThreads) broadcast_kernel(const void *src, int32_t src_dtype, double scale,
                                                              T *out, int64_t n, int accumulate) {
@@ -150,6 +234,11 @@ extern "C" int gfb_elementwise(int32_t op, double c, const void *a, int64_t n_a,
   if (n <= 0) return GFB_OK;
   if (!a || !out) return set_error(GFB_EINVAL, "gfb_elementwise: null pointer");
   cudaStream_t st = (cudaStream_t)stream;
+  if (dtype == GFB_F64 ? ew_vec_launch<double>(op, c, (const double *)a, n_a, (const double *)b, n_b,
+                                               (double *)out, n, accumulate, err, st)
+                       : ew_vec_launch<float>(op, (float)c, (const float *)a, n_a, (const float *)b, n_b,
+                                              (float *)out, n, accumulate, err, st))
+    return check_launch("elementwise");
   unsigned blocks = (unsigned)stream_blocks(n, 4);
   if (dtype == GFB_F64)
     ew_kernel<double><<<blocks, kThreads, 0, st>>>(op, c, (const double *)a, n_a, (const double *)b, n_b,

@@ -16,6 +16,7 @@
 #pragma once
 
 #include <algorithm>
+#include <type_traits>
 
 #include "gfb_common.cuh"
 #include "gfb_internal.h"
@@ -416,6 +417,193 @@ __global__ void map2_finish_kernel(const __grid_constant__ gfb_map2_desc d) {
   }
 }
 
+// 16-byte variant (fp32, two loop dimensions, inner strides 0 or 1, host-
+// checked alignment): lane l owns the four consecutive points 4l..4l+3 of a
+// 128-point chunk, so a stride-1 operand is one float4 load / store and a
+// stride-0 operand (broadcast along the row) one scalar load.
+struct M2FetchVec4 {
+  const gfb_map2_desc &d;
+  int32_t row, i0;
+  uint32_t vm;
+  __device__ __forceinline__ void operator()(int k, float (&dst)[4]) const {
+    const gfb_m2_operand &o = d.in[k];
+    const float *p = (const float *)o.base + ((int32_t)o.c0 + (int32_t)o.s[0] * row);
+    if (!vm) {
+      dst[0] = dst[1] = dst[2] = dst[3] = 1.f;
+    } else if (o.s[1] == 0) {
+      dst[0] = dst[1] = dst[2] = dst[3] = p[0];
+    } else {
+      const float4 q = *reinterpret_cast<const float4 *>(p + i0);
+      dst[0] = q.x, dst[1] = q.y, dst[2] = q.z, dst[3] = q.w;
+    }
+  }
+};
+
+// FLAT: rows shorter than 128 points; a warp item is 128 consecutive points
+// of the flattened space and each lane finds its own (row, column)
+template <typename Body, bool FLAT>
+__global__ void __launch_bounds__(256) map2_pointwise_vec4_kernel(const __grid_constant__ gfb_map2_desc d,
+                                                                  int32_t rows, int32_t cpr) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int32_t E = (int32_t)d.ext[1];
+  const int32_t items = FLAT ? (int32_t)ceil_div((int64_t)rows * E, 128) : rows * cpr;
+  for (int32_t it = blockIdx.x * kM2Warps + w; it < items; it += gridDim.x * kM2Warps) {
+    int32_t row, i0;
+    uint32_t vm;
+    if (FLAT) {
+      const int32_t f = it * 128 + lane * 4;
+      row = f / E;
+      i0 = f - row * E;
+      vm = row < rows ? 0xFu : 0u;
+    } else {
+      row = cpr == 1 ? it : it / cpr;
+      i0 = (it - row * cpr) * 128 + lane * 4;
+      vm = i0 < E ? 0xFu : 0u;
+    }
+    M2FetchVec4 fetch{d, row, i0, vm};
+    for (int o = 0; o < d.n_out; ++o) {
+      float r[4];
+      Body::template eval<float, 4>(d, o, fetch, vm, r);
+      if (!vm) continue;
+      const gfb_m2_operand &wo = d.out[o];
+      float *p = (float *)wo.base + ((int32_t)wo.c0 + (int32_t)wo.s[0] * row + i0);
+      float4 v = make_float4(r[0], r[1], r[2], r[3]);
+      if (d.wcr[o]) {
+        const float4 a = *reinterpret_cast<const float4 *>(p);
+        v.x += a.x, v.y += a.y, v.z += a.z, v.w += a.w;
+      }
+      *reinterpret_cast<float4 *>(p) = v;
+    }
+  }
+}
+
+template <typename Body>
+__global__ void __launch_bounds__(256) map2_reduce_inner_vec4_kernel(const __grid_constant__ gfb_map2_desc d,
+                                                                     int32_t rows) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int32_t E = (int32_t)d.ext[1];
+  for (int32_t row = blockIdx.x * kM2Warps + w; row < rows; row += gridDim.x * kM2Warps) {
+    float acc = 0.f;
+    for (int32_t c0 = 0; c0 < E; c0 += 128) {
+      const int32_t i0 = c0 + lane * 4;
+      const uint32_t vm = i0 < E ? 0xFu : 0u;
+      M2FetchVec4 fetch{d, row, i0, vm};
+      float r[4];
+      Body::template eval<float, 4>(d, 0, fetch, vm, r);
+      if (vm) acc += (r[0] + r[1]) + (r[2] + r[3]);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_down_sync(0xffffffffu, acc, o);
+    if (lane == 0) {
+      const gfb_m2_operand &wo = d.out[0];
+      const int32_t off = (int32_t)wo.c0 + (int32_t)wo.s[0] * row;
+      const bool inside = d.clear_mode == 2 ? (row >= d.clear_lo[0] && row < d.clear_hi[0]) : true;
+      store_as<float>(const_cast<void *>(wo.base), wo.dtype, off, m2_base<float>(d, inside, off) + acc);
+    }
+  }
+}
+
+// column sums (mode 2) with 16-byte column quads: a warp instruction covers
+// 32 / qpr rows x qpr quads (qpr = quads per row slice, a power of two
+// <= 32), four row groups in flight per iteration; lanes holding the same
+// quad combine by shuffles, warps through shared memory
+struct M2FetchVec4Row {
+  const gfb_map2_desc &d;
+  int32_t row, col;
+  uint32_t vm;
+  __device__ __forceinline__ void operator()(int k, float (&dst)[4]) const {
+    const gfb_m2_operand &o = d.in[k];
+    const float *p = (const float *)o.base + ((int32_t)o.c0 + (int32_t)o.s[0] * row);
+    if (!vm) {
+      dst[0] = dst[1] = dst[2] = dst[3] = 1.f;
+    } else if (o.s[1] == 0) {
+      dst[0] = dst[1] = dst[2] = dst[3] = p[0];
+    } else {
+      const float4 q = *reinterpret_cast<const float4 *>(p + col);
+      dst[0] = q.x, dst[1] = q.y, dst[2] = q.z, dst[3] = q.w;
+    }
+  }
+};
+
+template <typename Body>
+__global__ void __launch_bounds__(256) map2_reduce_outer_vec4_kernel(const __grid_constant__ gfb_map2_desc d,
+                                                                     int qpr) {
+  __shared__ float4 red[kM2Warps][32];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int32_t R = (int32_t)d.ext[0], E = (int32_t)d.ext[1];
+  const int s = blockIdx.y, ns = d.nsplit;
+  const int32_t rb = (int32_t)((int64_t)R * s / ns), re = (int32_t)((int64_t)R * (s + 1) / ns);
+  const int rpi = 32 / qpr, q = lane % qpr, rsub = lane / qpr;
+  const int32_t col = blockIdx.x * 128 + 4 * q;
+  const bool colok = col < E;
+  float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+  const int32_t step = kM2Warps * rpi;
+  for (int32_t r0 = rb + w * rpi + rsub; r0 < re; r0 += 4 * step) {
+    float v[4][4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int32_t r = r0 + u * step;
+      const uint32_t vm = (colok && r < re) ? 0xFu : 0u;
+      M2FetchVec4Row fetch{d, r, col, vm};
+      Body::template eval<float, 4>(d, 0, fetch, vm, v[u]);
+      if (!vm) v[u][0] = v[u][1] = v[u][2] = v[u][3] = 0.f;
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      acc.x += v[u][0];
+      acc.y += v[u][1];
+      acc.z += v[u][2];
+      acc.w += v[u][3];
+    }
+  }
+  for (int o = qpr; o < 32; o <<= 1) {
+    acc.x += __shfl_down_sync(0xffffffffu, acc.x, o);
+    acc.y += __shfl_down_sync(0xffffffffu, acc.y, o);
+    acc.z += __shfl_down_sync(0xffffffffu, acc.z, o);
+    acc.w += __shfl_down_sync(0xffffffffu, acc.w, o);
+  }
+  red[w][lane] = acc;
+  __syncthreads();
+  if (w != 0 || lane >= qpr || !colok) return;
+  float4 t = make_float4(0.f, 0.f, 0.f, 0.f);
+  for (int ww = 0; ww < kM2Warps; ++ww) {
+    t.x += red[ww][lane].x;
+    t.y += red[ww][lane].y;
+    t.z += red[ww][lane].z;
+    t.w += red[ww][lane].w;
+  }
+  const float tv[4] = {t.x, t.y, t.z, t.w};
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const int32_t i = col + j;
+    if (ns > 1) {
+      ((double *)d.workspace)[(int64_t)s * E + i] = (double)tv[j];
+    } else {
+      const gfb_m2_operand &wo = d.out[0];
+      const int32_t off = (int32_t)wo.c0 + (int32_t)wo.s[1] * i;
+      const bool inside = i >= d.clear_lo[1] && i < d.clear_hi[1];
+      store_as<float>(const_cast<void *>(wo.base), wo.dtype, off, m2_base<float>(d, inside, off) + tv[j]);
+    }
+  }
+}
+
+// host: may the fp32 two-dimensional launch use the 16-byte variant?
+inline bool m2_vec4_ok(const gfb_map2_desc &d) {
+  if (d.compute_f64 || d.ndim != 2 || d.ext[1] % 4 != 0) return false;
+  if (d.mode == 2) {  // column quads: 128-column blocks, or one power-of-two slice
+    const int64_t E = d.ext[1];
+    if (E % 128 != 0 && !(E < 128 && ((E / 4) & (E / 4 - 1)) == 0)) return false;
+  }
+  for (int k = 0; k < d.n_in + d.n_out; ++k) {
+    const gfb_m2_operand &o = k < d.n_in ? d.in[k] : d.out[k - d.n_in];
+    if (o.dtype != GFB_F32) return false;
+    if (d.mode != 0 && k >= d.n_in) continue;  // reduction targets are written by single lanes
+    if (o.s[1] == 0) continue;
+    if (o.s[1] != 1 || o.c0 % 4 || o.s[0] % 4 || (reinterpret_cast<uintptr_t>(o.base) & 15)) return false;
+  }
+  return true;
+}
+
 // MODE: the one mode a generated body is used with, or -1 (every mode)
 template <typename T, int V, typename Body, int MODE = -1>
 inline int launch_map2(const gfb_map2_desc &d, cudaStream_t st) {
@@ -425,6 +613,45 @@ inline int launch_map2(const gfb_map2_desc &d, cudaStream_t st) {
   for (int dd = 0; dd < nd - 1; ++dd) rows *= d.ext[dd];
   const int64_t cap = (int64_t)sm_count() * 8;  // resident CTAs of 256 threads
   if (d.mode != MODE && MODE != -1) return set_error(GFB_EINVAL, "gfb_map2_launch: generated body used in another mode");
+  if constexpr (std::is_same<T, float>::value && V == 4) {
+    if (m2_vec4_ok(d)) {
+      if constexpr (MODE == -1 || MODE == 0) {
+        if (d.mode == 0) {
+          const int64_t cpr = ceil_div(E, 128);
+          if (E < 128) {
+            const int64_t blocks =
+                std::max<int64_t>(std::min<int64_t>(ceil_div(rows * E, 128 * kM2Warps), cap * 4), 1);
+            map2_pointwise_vec4_kernel<Body, true><<<(unsigned)blocks, 256, 0, st>>>(d, (int32_t)rows, 1);
+          } else {
+            const int64_t blocks =
+                std::max<int64_t>(std::min<int64_t>(ceil_div(rows * cpr, kM2Warps), cap * 4), 1);
+            map2_pointwise_vec4_kernel<Body, false><<<(unsigned)blocks, 256, 0, st>>>(d, (int32_t)rows,
+                                                                                       (int32_t)cpr);
+          }
+          return check_launch("map2");
+        }
+      }
+      if constexpr (MODE == -1 || MODE == 1) {
+        if (d.mode == 1) {
+          const int64_t blocks = std::max<int64_t>(std::min<int64_t>(ceil_div(rows, kM2Warps), cap * 4), 1);
+          map2_reduce_inner_vec4_kernel<Body><<<(unsigned)blocks, 256, 0, st>>>(d, (int32_t)rows);
+          return check_launch("map2");
+        }
+      }
+      if constexpr (MODE == -1 || MODE == 2) {
+        if (d.mode == 2) {
+          const int qpr = (int)std::min<int64_t>(E, 128) / 4;
+          dim3 grid((unsigned)ceil_div(E, 128), (unsigned)d.nsplit);
+          map2_reduce_outer_vec4_kernel<Body><<<grid, 256, 0, st>>>(d, qpr);
+          if (d.nsplit > 1) {
+            const unsigned blocks = (unsigned)std::min<int64_t>(ceil_div(E, 256), cap);
+            map2_finish_kernel<T><<<blocks, 256, 0, st>>>(d);
+          }
+          return check_launch("map2");
+        }
+      }
+    }
+  }
   if constexpr (MODE == -1 || MODE == 0) {
     if (d.mode == 0) {
       const int64_t cpr = ceil_div(E, 32 * V);
