@@ -48,10 +48,28 @@ __device__ __forceinline__ double block_sum(double v) {
 template <typename TI>
 __global__ void __launch_bounds__(kThreads) reduce_pass1(const TI *__restrict__ x, int64_t n,
                                                          double *__restrict__ part) {
-  double acc = 0.0;
+  double acc[4] = {0.0, 0.0, 0.0, 0.0};
   const int64_t stride = (int64_t)gridDim.x * kThreads;
-  for (int64_t i = (int64_t)blockIdx.x * kThreads + threadIdx.x; i < n; i += stride) acc += (double)x[i];
-  double s = block_sum<TI>(acc);
+  const int64_t t0 = (int64_t)blockIdx.x * kThreads + threadIdx.x;
+  if ((reinterpret_cast<uintptr_t>(x) & 15) == 0) {
+    // 16-byte vectors, four independent fp64 partial sums per thread
+    constexpr int W = 16 / sizeof(TI);
+    const int64_t nv = n / W;
+    for (int64_t i = t0; i < nv; i += stride) {
+      const TI *v = x + i * W;
+      if constexpr (W == 4) {
+        const float4 q = *reinterpret_cast<const float4 *>(v);
+        acc[0] += q.x, acc[1] += q.y, acc[2] += q.z, acc[3] += q.w;
+      } else {
+        const double2 q = *reinterpret_cast<const double2 *>(v);
+        acc[0] += q.x, acc[1] += q.y;
+      }
+    }
+    for (int64_t i = nv * W + t0; i < n; i += stride) acc[2] += (double)x[i];
+  } else {
+    for (int64_t i = t0; i < n; i += stride) acc[0] += (double)x[i];
+  }
+  double s = block_sum<TI>((acc[0] + acc[1]) + (acc[2] + acc[3]));
   if (threadIdx.x == 0) part[blockIdx.x] = s;
 }
 
@@ -184,8 +202,23 @@ __global__ void __launch_bounds__(kThreads) broadcast_kernel(const void *src, in
   if (src) v *= (src_dtype == GFB_F64 ? *(const double *)src : (double)*(const float *)src);
   const T tv = (T)v;
   const int64_t stride = (int64_t)gridDim.x * kThreads;
-  for (int64_t i = (int64_t)blockIdx.x * kThreads + threadIdx.x; i < n; i += stride)
-    out[i] = accumulate ? (T)(out[i] + tv) : tv;
+  const int64_t t0 = (int64_t)blockIdx.x * kThreads + threadIdx.x;
+  int64_t done = 0;
+  if ((reinterpret_cast<uintptr_t>(out) & 15) == 0) {  // 16-byte stores
+    using V = typename EwVec<T>::V;
+    constexpr int W = EwVec<T>::W;
+    const int64_t nv = n / W;
+    V *ov = reinterpret_cast<V *>(out);
+    for (int64_t i = t0; i < nv; i += stride) {
+      V o = accumulate ? ov[i] : V{};
+      T *os = reinterpret_cast<T *>(&o);
+#pragma unroll
+      for (int w = 0; w < W; ++w) os[w] = accumulate ? (T)(os[w] + tv) : tv;
+      ov[i] = o;
+    }
+    done = nv * W;
+  }
+  for (int64_t i = done + t0; i < n; i += stride) out[i] = accumulate ? (T)(out[i] + tv) : tv;
 }
 
 template <typename T>

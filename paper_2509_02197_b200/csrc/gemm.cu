@@ -9,6 +9,7 @@
 //                     (mma.sync.m8n8k4.f64 -> DMMA), fp32 on FFMA (split-K
 //                     when the tile grid does not cover the SMs)
 #include <algorithm>
+#include <cstdlib>
 
 #include "gfb_common.cuh"
 #include "gfb_internal.h"
