@@ -5,8 +5,8 @@ outermost dimension: rank r owns a contiguous range of planes and keeps a
 two-plane halo on each side. The single-device launch list (lowering.py,
 after star-pair fusion and ping-pong placement) is rewritten per rank:
 
-* each fused timestep (StarPairOp) becomes a halo exchange of its source
-  (width 2: X is recomputed on a one-plane halo from Y) and of the old
+* each fused timestep (StarPairOp) becomes one grouped halo exchange of its
+  source (width 2: X is recomputed on a one-plane halo from Y) and of the old
   intermediate (width 1), followed by the same kernel restricted to the
   owned planes, with masks/regions still in global coordinates;
 * a reduction over a decomposed array becomes a local reduction over the
@@ -80,32 +80,34 @@ class TorchComm:
 
 
 class HaloOp(Op):
-    """Refresh the halo planes of a decomposed buffer from the neighbours."""
+    """Refresh the halo planes of decomposed buffers from the neighbours:
+    [(buffer, width)], all exchanged in one grouped send/recv batch (one
+    round trip per timestep instead of one per array)."""
 
     family = "halo"
 
-    def __init__(self, buf: Buffer, width: int, plan: SlabPlan, comm):
-        self.buf, self.width, self.plan, self.comm = buf, width, plan, comm
-        self.reads = (buf,)
-        self.writes = (buf,)
+    def __init__(self, items, plan: SlabPlan, comm):
+        self.items, self.plan, self.comm = list(items), plan, comm
+        self.reads = tuple(b for b, _ in self.items)
+        self.writes = tuple(b for b, _ in self.items)
 
     def run(self, view):
-        p, w = self.plan, self.width
-        v = view(self.buf)
+        p = self.plan
         ol, oh = p.own_local
         pairs = []
-        if p.rank > 0:
-            pairs.append((p.rank - 1, v[ol:ol + w].contiguous(), v[ol - w:ol]))
-        if p.rank < p.world - 1:
-            pairs.append((p.rank + 1, v[oh - w:oh].contiguous(), v[oh:oh + w]))
+        for buf, w in self.items:
+            v = view(buf)
+            if p.rank > 0:
+                pairs.append((p.rank - 1, v[ol:ol + w].contiguous(), v[ol - w:ol]))
+            if p.rank < p.world - 1:
+                pairs.append((p.rank + 1, v[oh - w:oh].contiguous(), v[oh:oh + w]))
         self.comm.exchange(pairs)
 
     def launch(self, rt, stream):
         self.run(rt.view)
 
     def algorithmic_bytes(self) -> int:
-        plane = self.buf.numel // self.buf.shape[0]
-        return 2 * self.width * plane * self.buf.itemsize
+        return sum(2 * w * (b.numel // b.shape[0]) * b.itemsize for b, w in self.items)
 
 
 class AllReduceOp(Op):
@@ -170,9 +172,10 @@ def decompose(lw, plan: SlabPlan, comm) -> DistLowered:
 
     for op in ops:
         if isinstance(op, StarPairOp):
-            low.emit(HaloOp(loc(op.Y), 2, plan, comm))
+            items = [(loc(op.Y), 2)]
             if op.X.root() is not op.Y.root():
-                low.emit(HaloOp(loc(op.X), 1, plan, comm))
+                items.append((loc(op.X), 1))
+            low.emit(HaloOp(items, plan, comm))
             new = StarPairOp(op.a, op.b, op.fa, op.fb, op.xwrite, op.dead)
             new.X, new.Y, new.Z = loc(op.X), loc(op.Y), loc(op.Z)
             new.xout, new.zout = loc(op.xout), loc(op.zout)

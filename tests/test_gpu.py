@@ -222,14 +222,16 @@ def test_slab_decomposition_kernels_in_lockstep(world):
             else:
                 op.launch(exe, stream)
         if isinstance(ranks[0][1].low.ops[k], HaloOp):
-            # pair rank r's sends with the peer's receives
-            recvs = {}
+            # pair rank r's sends to a peer with that peer's receives from r,
+            # in posting order (one grouped batch may carry several arrays)
+            sends, recvs = {}, {}
             for r, items in comm.pending.items():
                 for peer, snd, rcv in items:
-                    recvs[(r, peer)] = rcv
-            for r, items in comm.pending.items():
-                for peer, snd, rcv in items:
-                    recvs[(peer, r)].copy_(snd)
+                    sends.setdefault((r, peer), []).append(snd)
+                    recvs.setdefault((r, peer), []).append(rcv)
+            for (r, peer), lst in sends.items():
+                for snd, rcv in zip(lst, recvs[(peer, r)]):
+                    rcv.copy_(snd)
         elif isinstance(ranks[0][1].low.ops[k], AllReduceOp):
             ts = [items[0][1] for _, items in sorted(comm.pending.items())]
             total = sum(t.clone() for t in ts)
