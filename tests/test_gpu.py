@@ -364,3 +364,23 @@ def test_c4_full_size_against_torch_fp64_autograd(cfg):
     assert rel_err(res.value, v) <= 1e-5
     for k, ref in g.items():
         assert rel_err(res.grads[k], ref) <= 1e-5, k
+
+
+FD_CASES = ["jacobi_2d__N9_TSTEPS2", "heat_3d__N6_TSTEPS2", "atax__M6_N5", "softmax__R6_SM5",
+            "mlp__NB4_C3_S06_S15_S24", "conv2d_bias__NB2_H6_W5_CI2_CO3_K3", "corpus_exp_sin_chain__n9",
+            "corpus_double_read__n8", "corpus_triangular__n6", "corpus_matmul_transpose__d5"]
+
+
+@pytest.mark.parametrize("cid", [c for c in FD_CASES if c in IDX["cases"] or c in IDX["examples"]])
+def test_gpu_finite_difference_oracle_matches_reference_gradients(cid):
+    """The GPU finite-difference oracle (reference verification.py:53-120,
+    fp64-promoted central differences) against the reference's own adjoint
+    gradients for the golden case, at FD accuracy."""
+    from paper_2509_02197_b200 import finite_difference_gradient
+
+    meta = IDX["cases"].get(cid) or IDX["examples"][cid]
+    prog, b = _bundle(meta["workload"])
+    inputs, value, grads, _ = load_case(cid)
+    fd = finite_difference_gradient(prog, inputs, meta["params"])
+    for k, ref in grads.items():
+        assert rel_err(fd[k], ref) <= 1e-5, k
