@@ -386,36 +386,6 @@ struct Vec16<float> {
   __device__ static float get(float4 v, int i) { return i == 0 ? v.x : i == 1 ? v.y : i == 2 ? v.z : v.w; }
 };
 
-template <typename T>
-__global__ void __launch_bounds__(256) gemv_rowdot_vec_kernel(int64_t M, int64_t K, const T *__restrict__ A,
-                                                              int64_t lda, const T *__restrict__ x, T *y,
-                                                              int64_t incy, int accumulate) {
-  using VT = Vec16<T>;
-  using V = typename VT::type;
-  constexpr int W = VT::W;
-  const int lane = threadIdx.x & 31;
-  const int64_t nv = K / W;
-  const V *xv = reinterpret_cast<const V *>(x);
-  for (int64_t row = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5); row < M; row += (int64_t)gridDim.x * 8) {
-    const V *a = reinterpret_cast<const V *>(A + row * lda);
-    T p[4] = {T(0), T(0), T(0), T(0)};
-    int64_t j = lane;
-    for (; j + 96 < nv; j += 128) {
-#pragma unroll
-      for (int u = 0; u < 4; ++u) p[u] += VT::dot(a[j + 32 * u], xv[j + 32 * u]);
-    }
-    for (; j < nv; j += 32) p[0] += VT::dot(a[j], xv[j]);
-    for (int64_t k = nv * W + lane; k < K; k += 32) p[1] = fma(A[row * lda + k], x[k], p[1]);
-    T acc = (p[0] + p[1]) + (p[2] + p[3]);
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) acc += __shfl_down_sync(0xffffffffu, acc, o);
-    if (lane == 0) {
-      T *o = y + row * incy;
-      *o = accumulate ? (T)(*o + acc) : acc;
-    }
-  }
-}
-
 // column sums with W adjacent columns per lane (32*W per CTA)
 template <typename T>
 __global__ void __launch_bounds__(256) gemv_colsum_vec_kernel(int64_t M, int64_t K, const T *__restrict__ S,

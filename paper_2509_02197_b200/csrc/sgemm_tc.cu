@@ -31,12 +31,6 @@ constexpr int kTcM = 128, kTcK = 32, kTcThreads = 256;
 
 __device__ __forceinline__ uint32_t tc_smem(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
 
-__device__ __forceinline__ float tf32_round(float x) {
-  uint32_t r;
-  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
-  return __uint_as_float(r);
-}
-
 // K-major SWIZZLE_128B canonical layout: element (row r, k) of a 32-wide
 // k-slab lives at byte r*128 + ((k/4) ^ (r%8))*16 + (k%4)*4
 __device__ __forceinline__ uint32_t sw128(int r, int k) {

@@ -61,28 +61,6 @@ __device__ __forceinline__ uint32_t coord_bits(const StarOpDev &o, int dim, int 
   return b;
 }
 
-template <typename T>
-__device__ __forceinline__ T star_x_point(const StarPairDev &d, const T *__restrict__ Y, const T *__restrict__ Xo,
-                                          const T (&ca)[7], uint32_t apres, uint32_t m, int off, int ps, int rs) {
-  if (!(m & kRegion)) return Xo[off];
-  T acc = (d.a.mode == 0 || (d.a.mode == 2 && !(m & kClear))) ? Xo[off] : T(0);
-  const int doff[7] = {0, -ps, ps, -rs, rs, -1, 1};
-  T t[7];
-#pragma unroll
-  for (int e = 0; e < 7; ++e) t[e] = (((apres & m) >> e) & 1) ? __ldg(Y + off + doff[e]) : T(0);
-#pragma unroll
-  for (int e = 0; e < 7; ++e) acc += ca[e] * t[e];
-  return acc;
-}
-
-// Interior fast path of one CTA: compile-time full stars, no predicates.
-// HAS_I: rank-3 arrays (taps along dim 0); rank-2 arrays have one plane.
-// X planes live in a 4-slot ring, so one barrier per plane suffices (the
-// slot written for plane q+1 was last read by Z(q-3+1) before the previous
-// barrier), and the global loads of the next plane are issued before the
-// barrier so they overlap it and the Z stage.
-
-
 // Fill the CTA's per-coordinate predicate words and the block-uniform AND /
 // OR summaries (a: X halo window, b: Z core) used to pick the fast path.
 __device__ __forceinline__ void star_prologue(const StarPairDev &d, int i0, int i1, int tid, uint32_t *aj,

@@ -266,6 +266,12 @@ __device__ __forceinline__ void star_tma_body(const CUtensorMap *ymap, const Sta
       }
     }
   };
+  // planes whose preparation is a no-op for this CTA: loaded (inside the
+  // local array), inside M_a along dim 0, and a window wholly inside M_a in
+  // (j, k) -- one compare per step instead of the full test
+  const bool jk_clean = !ysrc || (yj_in && yk_in);
+  const int clean_lo = jk_clean ? (ysrc ? max(0, d.a.smlo[0] - d.p0) : 0) : 1;
+  const int clean_hi = jk_clean ? (ysrc ? min(d.d0, d.a.smhi[0] - d.p0) : d.d0) : 0;
   // common-case predicate patterns
   const uint32_t xmask = kArray | kRegion | (amode == 2 ? kClear : 0u) | (d.xwrite ? kDead : 0u);
   const uint32_t xval = amode == 0 ? 0xffffffffu : xmask;  // mode 0: base always added -> fix-up
@@ -362,7 +368,7 @@ __device__ __forceinline__ void star_tma_body(const CUtensorMap *ymap, const Sta
         // barrier below orders this before any read of it
         const int pn = q + 2;
         if (pn <= yhi && pn > qbeg + 1) wait_plane(pn);
-        if (pn <= qend + 1 && pn > qbeg + 1) prepare_plane(pn);
+        if (pn <= qend + 1 && pn > qbeg + 1 && (pn < clean_lo || pn >= clean_hi)) prepare_plane(pn);
       }
       const T *yc = slot_of(q);
       const T *yp = slot_of(q + 1);

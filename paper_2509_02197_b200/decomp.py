@@ -52,9 +52,6 @@ class SlabPlan:
     def local_slice(self, arr):
         return arr[self.loc_lo:self.loc_hi]
 
-    def own_slice_global(self):
-        return slice(self.own_lo, self.own_hi)
-
 
 class TorchComm:
     """Neighbour exchange and scalar all-reduce through torch.distributed."""

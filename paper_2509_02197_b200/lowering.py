@@ -1329,10 +1329,6 @@ class StarPairOp(Op):
         # the two map sweeps it replaces, each one read + one write of the array
         return self.a.algorithmic_bytes() + self.b.algorithmic_bytes()
 
-    def dram_bytes(self) -> int:
-        n = self.Z.nbytes
-        return 2 * n + (n if self.xwrite and self.dead is None else 0)
-
     def prepare(self, rt):
         d = L.StarPairDesc()
         rank = len(self.Z.shape)
