@@ -253,9 +253,8 @@ __global__ void contract_finish_kernel(const __grid_constant__ gfb_contract_desc
   }
 }
 
-template <typename T, int BM, int BN, int TM, int TN>
+template <typename T, int BM, int BN, int TM, int TN, int BK = 16>
 static void launch_contract(const gfb_contract_desc &d, cudaStream_t st) {
-  constexpr int BK = 16;
   dim3 grid((unsigned)ceil_div(d.M, BM), (unsigned)ceil_div(d.N, BN), (unsigned)d.nsplit);
   contract_kernel<T, BM, BN, BK, TM, TN><<<grid, (BM / TM) * (BN / TN), 0, st>>>(d);
 }
