@@ -176,12 +176,19 @@ static int sgemm(int ta, int tb, int64_t M, int64_t N, int64_t K, const float *A
 }
 
 // ---------------------------------------------------------------------------
-// fp64 DMMA GEMM: 128x128 CTA tile, BK = 16, 8 warps each owning 64x32,
-// mma.sync.aligned.m8n8k4.row.col.f64 (-> DMMA.884 on sm_100a).
-// Operands are staged through padded shared memory with transposes resolved
-// at load time so both A and B fragments come from [k][m] / [k][n] tiles.
+// fp64 DMMA GEMM: 64x64 CTA tile, BK = 16, 4 warps each owning 32x32 (4x4
+// m8n8 tiles), mma.sync.aligned.m8n8k4.row.col.f64 (-> DMMA.8x8x4 on
+// sm_100a; the larger f64 shapes decompose into the same instruction).
+// Operands stream through a 3-stage cp.async ring in their stored
+// orientation: A as [m][k] (no ta) or [k][m] (ta), B as [k][n] (no tb) or
+// [n][k] (tb). Row pitches of 4 (mod 16) doubles keep every fragment load
+// conflict-free in either orientation. Small tiles with 3 CTAs (12 warps) per
+// SM hide the DMMA latency better than one 128x128 CTA per SM
+// (tools/lab/dgemm_lab.cu: 32.2 vs 26.7 TF/s at 4000^3; cuBLAS 34.5).
 
-constexpr int kDM = 128, kDN = 128, kDK = 16;
+static bool aligned16(const void *p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
+
+constexpr int kDM = 64, kDN = 64, kDK = 16, kDS = 3;
 
 __device__ __forceinline__ void dmma884(double &d0, double &d1, double a, double b) {
   asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
@@ -189,84 +196,132 @@ __device__ __forceinline__ void dmma884(double &d0, double &d1, double a, double
                : "d"(a), "d"(b));
 }
 
-__global__ void __launch_bounds__(256) dgemm_dmma_kernel(int ta, int tb, int64_t M, int64_t N, int64_t K,
-                                                         const double *__restrict__ A, int64_t lda,
-                                                         const double *__restrict__ B, int64_t ldb, double *C,
-                                                         int64_t ldc, int accumulate) {
-  // row stride 132 = 4 (mod 16) doubles keeps the fragment loads conflict-free
-  __shared__ double As[kDK][kDM + 4];
-  __shared__ double Bs[kDK][kDN + 4];
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int wm = (warp >> 2) * 64;  // 2 warps along M
-  const int wn = (warp & 3) * 32;   // 4 warps along N
-  const int64_t m0 = (int64_t)blockIdx.y * kDM, n0 = (int64_t)blockIdx.x * kDN;
-  double acc[8][4][2];
+template <int V>
+__device__ __forceinline__ void cp_async_f64(double *s, const double *g, bool ok) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(s);
+  if constexpr (V == 2)
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(sa), "l"(g), "r"(ok ? 16 : 0));
+  else
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(sa), "l"(g), "r"(ok ? 8 : 0));
+}
+
+// one operand tile (rows x cols of the STORED matrix, contiguous along cols)
+template <int V, int ROWS, int COLS>
+__device__ __forceinline__ void dmma_stage(double *s, const double *g, int64_t ld, int64_t r0, int64_t c0,
+                                           int64_t R, int64_t Cn, int tid) {
+  constexpr int P = COLS + 4, CH = COLS / V;
 #pragma unroll
-  for (int a = 0; a < 8; ++a)
+  for (int c = tid; c < ROWS * CH; c += 128) {
+    const int r = c / CH, cc = (c % CH) * V;
+    const int64_t gr = r0 + r, gc = c0 + cc;
+    const bool ok = gr < R && gc < Cn;  // V == 2: Cn even, so a chunk is all in or all out
+    cp_async_f64<V>(s + r * P + cc, ok ? g + gr * ld + gc : g, ok);
+  }
+}
+
+template <int TA, int TB, int V>
+__global__ void __launch_bounds__(128, 3) dgemm_dmma_kernel(int64_t M, int64_t N, int64_t K,
+                                                            const double *__restrict__ A, int64_t lda,
+                                                            const double *__restrict__ B, int64_t ldb, double *C,
+                                                            int64_t ldc, int accumulate) {
+  constexpr int SA = TA ? kDK * (kDM + 4) : kDM * (kDK + 4);
+  constexpr int SB = TB ? kDN * (kDK + 4) : kDK * (kDN + 4);
+  extern __shared__ __align__(16) double dsm[];
+  double *As = dsm, *Bs = dsm + kDS * SA;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int wm = (warp >> 1) * 32, wn = (warp & 1) * 32;
+  const int64_t m0 = (int64_t)blockIdx.y * kDM, n0 = (int64_t)blockIdx.x * kDN;
+  const int64_t ktiles = (K + kDK - 1) / kDK;
+  auto load = [&](int64_t kt, int slot) {
+    const int64_t k0 = kt * kDK;
+    if constexpr (TA) dmma_stage<V, kDK, kDM>(As + slot * SA, A, lda, k0, m0, K, M, tid);
+    else dmma_stage<V, kDM, kDK>(As + slot * SA, A, lda, m0, k0, M, K, tid);
+    if constexpr (TB) dmma_stage<V, kDN, kDK>(Bs + slot * SB, B, ldb, n0, k0, N, K, tid);
+    else dmma_stage<V, kDK, kDN>(Bs + slot * SB, B, ldb, k0, n0, K, N, tid);
+  };
+  double acc[4][4][2];
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
 #pragma unroll
     for (int b = 0; b < 4; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
-
-  double ra[8], rb[8];
-  auto fetch = [&](int64_t k0) {
 #pragma unroll
-    for (int r = 0; r < 8; ++r) {
-      int e = tid + r * 256;
-      int mm = ta ? e % kDM : e / kDK, kk = ta ? e / kDM : e % kDK;
-      int64_t gm = m0 + mm, gk = k0 + kk;
-      ra[r] = (gm < M && gk < K) ? (ta ? A[gk * lda + gm] : A[gm * lda + gk]) : 0.0;
-      int nn = tb ? e / kDK : e % kDN, kb = tb ? e % kDK : e / kDN;
-      int64_t gn = n0 + nn, gkb = k0 + kb;
-      rb[r] = (gn < N && gkb < K) ? (tb ? B[gn * ldb + gkb] : B[gkb * ldb + gn]) : 0.0;
-    }
-  };
-  auto stash = [&]() {
-#pragma unroll
-    for (int r = 0; r < 8; ++r) {
-      int e = tid + r * 256;
-      int mm = ta ? e % kDM : e / kDK, kk = ta ? e / kDM : e % kDK;
-      As[kk][mm] = ra[r];
-      int nn = tb ? e / kDK : e % kDN, kb = tb ? e % kDK : e / kDN;
-      Bs[kb][nn] = rb[r];
-    }
-  };
-
+  for (int s = 0; s < kDS - 1; ++s) {
+    if (s < ktiles) load(s, s);
+    asm volatile("cp.async.commit_group;\n");
+  }
   // m8n8k4 fragments: A(row) lane -> A[lane/4][lane%4]; B(col) lane ->
   // B[lane%4][lane/4]; D lane -> D[lane/4][2*(lane%4) + {0,1}]
   const int fr = lane >> 2, fc = lane & 3;
-  fetch(0);
-  for (int64_t k0 = 0; k0 < K; k0 += kDK) {
-    stash();
-    __syncthreads();
-    if (k0 + kDK < K) fetch(k0 + kDK);  // global loads overlap the DMMA work below
+  for (int64_t kt = 0; kt < ktiles; ++kt) {
+    asm volatile("cp.async.wait_group %0;\n" ::"n"(kDS - 2));
+    __syncthreads();  // tile kt visible to all; slot (kt-1)%S free for reuse
+    if (kt + kDS - 1 < ktiles) load(kt + kDS - 1, (int)((kt + kDS - 1) % kDS));
+    asm volatile("cp.async.commit_group;\n");
+    const double *as = As + (kt % kDS) * SA, *bs = Bs + (kt % kDS) * SB;
 #pragma unroll
     for (int ks = 0; ks < kDK; ks += 4) {
-      double af[8], bf[4];
+      double af[4], bf[4];
 #pragma unroll
-      for (int a = 0; a < 8; ++a) af[a] = As[ks + fc][wm + a * 8 + fr];
+      for (int a = 0; a < 4; ++a)
+        af[a] = TA ? as[(ks + fc) * (kDM + 4) + wm + a * 8 + fr] : as[(wm + a * 8 + fr) * (kDK + 4) + ks + fc];
 #pragma unroll
-      for (int b = 0; b < 4; ++b) bf[b] = Bs[ks + fc][wn + b * 8 + fr];
+      for (int b = 0; b < 4; ++b)
+        bf[b] = TB ? bs[(wn + b * 8 + fr) * (kDK + 4) + ks + fc] : bs[(ks + fc) * (kDN + 4) + wn + b * 8 + fr];
 #pragma unroll
-      for (int a = 0; a < 8; ++a)
+      for (int a = 0; a < 4; ++a)
 #pragma unroll
         for (int b = 0; b < 4; ++b) dmma884(acc[a][b][0], acc[a][b][1], af[a], bf[b]);
     }
-    __syncthreads();
   }
+  asm volatile("cp.async.wait_group 0;\n");
 #pragma unroll
-  for (int a = 0; a < 8; ++a) {
-    int64_t gm = m0 + wm + a * 8 + fr;
+  for (int a = 0; a < 4; ++a) {
+    const int64_t gm = m0 + wm + a * 8 + fr;
     if (gm >= M) continue;
 #pragma unroll
-    for (int b = 0; b < 4; ++b) {
+    for (int b = 0; b < 4; ++b)
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
-        int64_t gn = n0 + wn + b * 8 + 2 * fc + h;
+        const int64_t gn = n0 + wn + b * 8 + 2 * fc + h;
         if (gn >= N) continue;
         double *c = C + gm * ldc + gn;
         *c = accumulate ? *c + acc[a][b][h] : acc[a][b][h];
       }
-    }
   }
+}
+
+template <int TA, int TB, int V>
+static int dgemm_dmma_t(int64_t M, int64_t N, int64_t K, const double *A, int64_t lda, const double *B, int64_t ldb,
+                        double *C, int64_t ldc, int accumulate, cudaStream_t st) {
+  constexpr int SA = TA ? kDK * (kDM + 4) : kDM * (kDK + 4);
+  constexpr int SB = TB ? kDN * (kDK + 4) : kDK * (kDN + 4);
+  constexpr int smem = kDS * (SA + SB) * 8;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(dgemm_dmma_kernel<TA, TB, V>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    attr = true;
+  }
+  dim3 grid((unsigned)ceil_div(N, kDN), (unsigned)ceil_div(M, kDM));
+  dgemm_dmma_kernel<TA, TB, V><<<grid, 128, smem, st>>>(M, N, K, A, lda, B, ldb, C, ldc, accumulate);
+  return check_launch("dgemm_dmma");
+}
+
+static int dgemm_dmma(int ta, int tb, int64_t M, int64_t N, int64_t K, const double *A, int64_t lda, const double *B,
+                      int64_t ldb, double *C, int64_t ldc, int accumulate, cudaStream_t st) {
+  // 16-byte chunks need both operands 16-byte aligned with even leading
+  // dimensions and even extents along the contiguous axis
+  const int64_t ca = ta ? M : K, cb = tb ? K : N;
+  const bool v2 = aligned16(A) && aligned16(B) && lda % 2 == 0 && ldb % 2 == 0 && ca % 2 == 0 && cb % 2 == 0;
+#define GFB_DMMA(TA, TB)                                                                                      \
+  if (ta == TA && tb == TB)                                                                                   \
+    return v2 ? dgemm_dmma_t<TA, TB, 2>(M, N, K, A, lda, B, ldb, C, ldc, accumulate, st)                      \
+              : dgemm_dmma_t<TA, TB, 1>(M, N, K, A, lda, B, ldb, C, ldc, accumulate, st);
+  GFB_DMMA(0, 0)
+  GFB_DMMA(0, 1)
+  GFB_DMMA(1, 0)
+  GFB_DMMA(1, 1)
+#undef GFB_DMMA
+  return set_error(GFB_EINVAL, "gfb_matmul: bad transpose flags");
 }
 
 // ---------------------------------------------------------------------------
@@ -457,7 +512,6 @@ __global__ void __launch_bounds__(256) rank1_vec_kernel(int64_t M, int64_t N, co
   }
 }
 
-static bool aligned16(const void *p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
 
 // Row dots with a whole CTA per row (grid-stride over rows): the row's
 // 16-byte vectors are spread over 256 threads, so one row is a single round
@@ -615,10 +669,8 @@ extern "C" int gfb_matmul(int32_t dtype, int32_t ta, int32_t tb, int64_t M, int6
     rc = matmul_t<double>(ta, tb, M, N, K, (const double *)A, lda, (const double *)B, ldb, (double *)C, ldc,
                           accumulate, workspace, st);
     if (rc >= 0) return rc;
-    dim3 grid((unsigned)ceil_div(N, kDN), (unsigned)ceil_div(M, kDM));
-    dgemm_dmma_kernel<<<grid, 256, 0, st>>>(ta, tb, M, N, K, (const double *)A, lda, (const double *)B, ldb,
-                                             (double *)C, ldc, accumulate);
-    return check_launch("dgemm_dmma");
+    return dgemm_dmma(ta, tb, M, N, K, (const double *)A, lda, (const double *)B, ldb, (double *)C, ldc, accumulate,
+                      st);
   }
   rc = matmul_t<float>(ta, tb, M, N, K, (const float *)A, lda, (const float *)B, ldb, (float *)C, ldc, accumulate,
                        workspace, st);

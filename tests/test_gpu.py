@@ -294,6 +294,31 @@ def test_fp32_matmul_tensor_core_3xtf32(M, N, K, ta, tb):
         assert err <= 1e-5, (acc, err)
 
 
+@pytest.mark.parametrize("ta,tb", [(0, 0), (1, 0), (0, 1), (1, 1)])
+@pytest.mark.parametrize("M,N,K", [(256, 192, 4000), (130, 70, 33), (65, 63, 17), (1000, 1000, 1000)])
+def test_fp64_matmul_dmma(M, N, K, ta, tb):
+    """gfb_matmul fp64 (DMMA, cp.async ring; 16-byte chunks for even shapes,
+    8-byte chunks for odd ones) against torch fp64, with and without
+    accumulation, through the C ABI."""
+    from paper_2509_02197_b200 import _lib as L
+
+    lib = L.load()
+    g = torch.Generator(device="cuda").manual_seed(M * 5 + N * 3 + K + 11 * ta + 7 * tb)
+    A = torch.rand((K, M) if ta else (M, K), generator=g, device="cuda", dtype=torch.float64) - 0.3
+    B = torch.rand((N, K) if tb else (K, N), generator=g, device="cuda", dtype=torch.float64) - 0.3
+    C0 = torch.rand((M, N), generator=g, device="cuda", dtype=torch.float64)
+    ref = (A.T if ta else A) @ (B.T if tb else B)
+    st = torch.cuda.current_stream().cuda_stream
+    for acc in (0, 1):
+        C = C0.clone()
+        L.check(lib.gfb_matmul(L.F64, ta, tb, M, N, K, A.data_ptr(), A.shape[1], B.data_ptr(), B.shape[1],
+                               C.data_ptr(), N, acc, None, st), "matmul")
+        torch.cuda.synchronize()
+        want = ref + (C0 if acc else 0)
+        err = ((C - want).abs() / want.abs().clamp(min=1)).max().item()
+        assert err <= 1e-12, (acc, err)
+
+
 @pytest.mark.parametrize("dtype", ["f64", "f32"])
 @pytest.mark.parametrize("M,N,K,ta,tb", [(4000, 1, 4000, 0, 0), (4000, 1, 4000, 1, 0), (1, 3000, 2000, 0, 1),
                                          (1, 3000, 2000, 0, 0), (4000, 4000, 1, 0, 0), (333, 1, 257, 0, 0),
