@@ -26,7 +26,7 @@
 extern "C" {
 #endif
 
-#define GFB_ABI_VERSION 8
+#define GFB_ABI_VERSION 9
 
 #define GFB_MAX_PARAMS 8    /* map parameters (iteration-space rank) */
 #define GFB_MAX_RANK 8      /* array rank */
@@ -396,6 +396,33 @@ int gfb_matmul(int32_t dtype, int32_t ta, int32_t tb, int64_t M, int64_t N,
                int64_t K, const void *A, int64_t lda, const void *B,
                int64_t ldb, void *C, int64_t ldc, int32_t accumulate,
                void *workspace, void *stream);
+
+/* one-pass matrix-vector pair over a row-major A[R, C] (lda elements per
+ * row): r (= | +=) A u and c (= | +=) A^T v in a single streaming read of A.
+ * Replaces two N==1 matmul library nodes over the same matrix
+ * (interpreter.py:433-446) -- atax forward t = A x, y = A^T t (chain = 1:
+ * v is the new r), bicg forward s = A^T r, q = A p, and both adjoint pairs
+ * (autodiff.py:780-802). Either half may be absent (u = r = NULL, or
+ * c = NULL). Needs 16-byte aligned A / u, C and lda multiples of the 16-byte
+ * vector width; gfb_matvec_pair_usable() says whether a shape qualifies.
+ * Workspace: gfb_matvec_pair_workspace_bytes() (column partials). */
+int64_t gfb_matvec_pair_workspace_bytes(int32_t dtype, int64_t R, int64_t C,
+                                        int32_t has_col);
+int gfb_matvec_pair_usable(int32_t dtype, int64_t R, int64_t C, int64_t lda,
+                           const void *A, const void *u);
+int gfb_matvec_pair(int32_t dtype, int64_t R, int64_t C, const void *A,
+                    int64_t lda, const void *u, void *r, int32_t r_acc,
+                    const void *v, void *c, int32_t c_acc, int32_t chain,
+                    void *workspace, void *stream);
+
+/* fused outer-product adjoints into one matrix gradient (autodiff.py:
+ * 780-802, two K==1 matmul jobs with the same target):
+ * C[i,j] (= | +=) u1[i] v1[j] + u2[i] v2[j]; u2 = v2 = NULL for rank 1.
+ * Unit-stride vectors; v*, C 16-byte aligned, N and ldc multiples of the
+ * 16-byte vector width. */
+int gfb_rank2(int32_t dtype, int64_t M, int64_t N, const void *u1,
+              const void *v1, const void *u2, const void *v2, void *C,
+              int64_t ldc, int32_t accumulate, void *stream);
 
 /* device-to-device copy of n elements (tape snapshots, interpreter.py:371-386) */
 int gfb_copy(void *dst, const void *src, int64_t bytes, void *stream);

@@ -19,7 +19,7 @@ MAXCODE = 128
 MAXCONST = 24
 MAXTAPS = 32
 MAXSRCS = 4
-ABI_VERSION = 8
+ABI_VERSION = 9
 
 F32, F64 = 0, 1
 STAR_SKIP_ZCOPY, STAR_SKIP_XCOPY = 1, 2
@@ -136,6 +136,10 @@ _SIGS = [
     ("gfb_fill_box", i32, [vp, i32, i32, C.POINTER(i64), C.POINTER(i64), C.POINTER(i64), f64, vp]),
     ("gfb_matmul_workspace_bytes", i64, [i32, i32, i32, i64, i64, i64]),
     ("gfb_matmul", i32, [i32, i32, i32, i64, i64, i64, vp, i64, vp, i64, vp, i64, i32, vp, vp]),
+    ("gfb_matvec_pair_workspace_bytes", i64, [i32, i64, i64, i32]),
+    ("gfb_matvec_pair_usable", i32, [i32, i64, i64, i64, vp, vp]),
+    ("gfb_matvec_pair", i32, [i32, i64, i64, vp, i64, vp, vp, i32, vp, vp, i32, i32, vp, vp]),
+    ("gfb_rank2", i32, [i32, i64, i64, vp, vp, vp, vp, vp, i64, i32, vp]),
     ("gfb_copy", i32, [vp, vp, i64, vp]),
     ("gfb_plane_copy", i32, [vp, vp, i64, i32, i64, vp]),
 ]

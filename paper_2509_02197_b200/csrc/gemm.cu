@@ -604,9 +604,17 @@ static int matmul_t(int ta, int tb, int64_t M, int64_t N, int64_t K, const T *A,
     }
     return check_launch("rank1");
   }
+  constexpr int32_t kDt = sizeof(T) == 8 ? GFB_F64 : GFB_F32;
   if (N == 1) {
     // x = op(B)(:,0): B[k*ldb] (no tb) or B[k] (tb)
     int64_t incx = tb ? 1 : ldb;
+    // one-pass streaming kernel (matvec.cu) over A as stored
+    if (incx == 1 && ldc == 1) {
+      if (!ta && gfb_matvec_pair_usable(kDt, M, K, lda, A, B))
+        return gfb_matvec_pair(kDt, M, K, A, lda, B, C, accumulate, nullptr, nullptr, 0, 0, ws, st);
+      if (ta && gfb_matvec_pair_usable(kDt, K, M, lda, A, nullptr))
+        return gfb_matvec_pair(kDt, K, M, A, lda, nullptr, nullptr, 0, B, C, accumulate, 0, ws, st);
+    }
     if (!ta) {
       constexpr int W = Vec16<T>::W;
       if (incx == 1 && aligned16(A) && aligned16(B) && lda % W == 0) {
@@ -622,6 +630,12 @@ static int matmul_t(int ta, int tb, int64_t M, int64_t N, int64_t K, const T *A,
   if (M == 1) {
     // y[j] = sum_k op(A)(0,k) op(B)(k,j); op(A) row 0: A[k] (no ta) or A[k*lda] (ta)
     int64_t incx = ta ? lda : 1;
+    if (incx == 1) {
+      if (tb && gfb_matvec_pair_usable(kDt, N, K, ldb, B, A))
+        return gfb_matvec_pair(kDt, N, K, B, ldb, A, C, accumulate, nullptr, nullptr, 0, 0, ws, st);
+      if (!tb && gfb_matvec_pair_usable(kDt, K, N, ldb, B, nullptr))
+        return gfb_matvec_pair(kDt, K, N, B, ldb, nullptr, nullptr, 0, A, C, accumulate, 0, ws, st);
+    }
     if (tb) {  // op(B)(k,j) = B[j*ldb + k]: row dots
       constexpr int W = Vec16<T>::W;
       if (incx == 1 && aligned16(A) && aligned16(B) && ldb % W == 0) {
@@ -644,8 +658,10 @@ using namespace gfb;
 extern "C" int64_t gfb_matmul_workspace_bytes(int32_t dtype, int32_t ta, int32_t tb, int64_t M, int64_t N,
                                               int64_t K) {
   int64_t es = dtype == GFB_F64 ? 8 : 4;
-  if (K > 1 && N == 1 && ta) return colsum_splits(M, K) * M * es;
-  if (K > 1 && M == 1 && !tb && N > 1) return colsum_splits(N, K) * N * es;
+  if (K > 1 && N == 1 && ta)
+    return std::max(colsum_splits(M, K) * M * es, gfb_matvec_pair_workspace_bytes(dtype, K, M, 1));
+  if (K > 1 && M == 1 && !tb && N > 1)
+    return std::max(colsum_splits(N, K) * N * es, gfb_matvec_pair_workspace_bytes(dtype, K, N, 1));
   if (dtype != GFB_F64 && K > 1 && M > 1 && N > 1 && sgemm_tc_usable(M, N, K)) return sgemm_tc_workspace(M, N, K);
   if (dtype != GFB_F64 && K > 1 && M > 1 && N > 1) {
     const int64_t ns = sgemm_splits(M, N, K);

@@ -705,6 +705,132 @@ class MatmulOp(Op):
                                   1 if self.accumulate else 0, rt.workspace_ptr, stream), "matmul")
 
 
+def matvec_form(op):
+    """(matrix, "row" | "col", vector, out) of a matrix-vector MatmulOp
+    (K > 1 and N == 1 or M == 1) over the matrix as stored, row-major [R, C]:
+    "row" is out[i] = sum_j mat[i, j] vec[j], "col" is out[j] = sum_i mat[i, j]
+    vec[i]. Vectors of these shapes are contiguous."""
+    if not isinstance(op, MatmulOp) or op.K <= 1:
+        return None
+    if op.N == 1:
+        return op.a, ("col" if op.ta else "row"), op.b, op.out
+    if op.M == 1:
+        return op.b, ("row" if op.tb else "col"), op.a, op.out
+    return None
+
+
+def rank1_form(op):
+    """(u, v, out) of an outer-product MatmulOp (K == 1): out = u v^T."""
+    if not isinstance(op, MatmulOp) or op.K != 1 or op.M < 2 or op.N < 2:
+        return None
+    return op.a, op.b, op.out
+
+
+def _span(b: Buffer):
+    o = b.root_offset()
+    return b.root(), o, o + b.numel
+
+
+def overlaps(x: Buffer, y: Buffer) -> bool:
+    rx, x0, x1 = _span(x)
+    ry, y0, y1 = _span(y)
+    return rx is ry and x0 < y1 and y0 < x1
+
+
+def same_buffer(x: Buffer, y: Buffer) -> bool:
+    return _span(x) == _span(y) and x.shape == y.shape
+
+
+class MatvecPairOp(Op):
+    """Two matrix-vector library nodes over one matrix in one streaming pass
+    (csrc/matvec.cu): r (+)= mat @ u and c (+)= mat^T @ v, v = the new r in
+    chain mode (atax forward). Replaces ``parts`` (the original MatmulOps,
+    launched in order as the fallback when the placed buffers are not
+    16-byte aligned)."""
+    family = "matvec"
+    _bufs = ("mat", "u", "r", "v", "c")
+
+    def __init__(self, parts, mat, u, r, r_acc, v, c, c_acc, chain):
+        self.parts = parts
+        self.mat, self.u, self.r, self.v, self.c = mat, u, r, v, c
+        self.r_acc, self.c_acc, self.chain = r_acc, c_acc, chain
+        self.R, self.C = mat.shape
+        reads = [mat, u, v] + ([r] if r_acc else []) + ([c] if c_acc else [])
+        self.reads = tuple(b for b in reads if b is not None)
+        self.writes = (r, c)
+        self.use_parts = False
+
+    def remap(self, f):
+        super().remap(f)
+        for p in self.parts:
+            p.remap(f)
+
+    def workspace_bytes(self):
+        lib = L.load()
+        ws = int(lib.gfb_matvec_pair_workspace_bytes(self.mat.dtype, self.R, self.C, 1))
+        return max([ws] + [p.workspace_bytes() for p in self.parts])
+
+    def flops(self):
+        return 4 * self.R * self.C
+
+    def algorithmic_bytes(self) -> int:
+        # one read of the matrix plus the vectors
+        return sum(b.nbytes for b in set(self.reads)) + sum(b.nbytes for b in set(self.writes))
+
+    def prepare(self, rt):
+        self.use_parts = not L.load().gfb_matvec_pair_usable(self.mat.dtype, self.R, self.C, self.C, self.mat.ptr,
+                                                            self.u.ptr)
+
+    def launch(self, rt, stream):
+        if self.use_parts:
+            for p in self.parts:
+                p.launch(rt, stream)
+            return
+        L.check(rt.lib.gfb_matvec_pair(self.mat.dtype, self.R, self.C, self.mat.ptr, self.C, self.u.ptr, self.r.ptr,
+                                       int(self.r_acc), None if self.chain else self.v.ptr, self.c.ptr,
+                                       int(self.c_acc), int(self.chain), rt.workspace_ptr, stream), "matvec_pair")
+
+
+class Rank2Op(Op):
+    """Two outer-product adjoint jobs into one matrix gradient in one write
+    pass (csrc/matvec.cu gfb_rank2): out (+)= u1 v1^T + u2 v2^T."""
+    family = "rank2"
+    _bufs = ("u1", "v1", "u2", "v2", "out")
+
+    def __init__(self, parts, u1, v1, u2, v2, out, accumulate):
+        self.parts = parts
+        self.u1, self.v1, self.u2, self.v2, self.out = u1, v1, u2, v2, out
+        self.accumulate = accumulate
+        self.M, self.N = out.shape
+        self.reads = (u1, v1, u2, v2) + ((out,) if accumulate else ())
+        self.writes = (out,)
+        self.full_write = not accumulate
+        self.use_parts = False
+
+    def remap(self, f):
+        super().remap(f)
+        for p in self.parts:
+            p.remap(f)
+
+    def workspace_bytes(self):
+        return max(p.workspace_bytes() for p in self.parts)
+
+    def flops(self):
+        return 4 * self.M * self.N
+
+    def prepare(self, rt):
+        w = 16 // self.out.itemsize
+        self.use_parts = bool(self.N % w or self.out.ptr % 16 or self.v1.ptr % 16 or self.v2.ptr % 16)
+
+    def launch(self, rt, stream):
+        if self.use_parts:
+            for p in self.parts:
+                p.launch(rt, stream)
+            return
+        L.check(rt.lib.gfb_rank2(self.out.dtype, self.M, self.N, self.u1.ptr, self.v1.ptr, self.u2.ptr, self.v2.ptr,
+                                 self.out.ptr, self.N, int(self.accumulate), stream), "rank2")
+
+
 class CopyOp(Op):
     family = "copy"
     _bufs = ("dst", "src")
@@ -1430,6 +1556,9 @@ class Lowering:
             self._fuse_star_pairs(observed)
             if os.environ.get("GFB_SYNC_ELIDE", "1") != "0":
                 self._elide_synced_copies()
+        if os.environ.get("GFB_FUSE_MV", "1") != "0":
+            self._fuse_matvec_pairs()
+            self._fuse_rank2()
         self._elide_copies()
 
     def resolve(self, buf: Buffer) -> Buffer:
@@ -1528,6 +1657,95 @@ class Lowering:
                 full = op.dead is None or box_contains(op.a.region, op.dead)
                 if xout is not X and full:
                     synced.add((frozenset((X.bid, xout.bid)), tuple(op.a.region)))
+
+    def _fuse_matvec_pairs(self):
+        """Pair a row-dot and a column-sum matmul node over the same matrix
+        into one MatvecPairOp at the earlier position (one read of the matrix
+        instead of two). Legal when the later node's operands are not written
+        and its output not touched in between, and neither output aliases an
+        operand; the chain form (column sums of the row-dot result, atax) needs
+        the row dots first."""
+        ops = self.ops
+        out, used = [], set()
+        for i, a in enumerate(ops):
+            if i in used:
+                continue
+            fa = matvec_form(a)
+            if fa is None:
+                out.append(a)
+                continue
+            pair = None
+            for j in range(i + 1, len(ops)):
+                if j in used:
+                    continue
+                b = ops[j]
+                fb = matvec_form(b)
+                if fb is not None and same_buffer(fa[0], fb[0]) and {fa[1], fb[1]} == {"row", "col"}:
+                    if self._pair_legal(a, fa, b, fb, ops[i + 1:j]):
+                        pair = (j, b, fb)
+                    break
+                # stop at anything that rewrites the matrix
+                if any(overlaps(w, fa[0]) for w in b.writes):
+                    break
+            if pair is None:
+                out.append(a)
+                continue
+            j, b, fb = pair
+            used.add(j)
+            row, col = (a, b) if fa[1] == "row" else (b, a)
+            fr, fc = matvec_form(row), matvec_form(col)
+            chain = fc[2] is fr[3]
+            out.append(MatvecPairOp([a, b], fr[0], fr[2], fr[3], row.accumulate, None if chain else fc[2], fc[3],
+                                    col.accumulate, chain))
+        self.ops = out
+
+    @staticmethod
+    def _pair_legal(a, fa, b, fb, between) -> bool:
+        mat = fa[0]
+        chain = fb[2] is fa[3]
+        if chain and fa[1] != "row":
+            return False
+        ins_a, ins_b = [fa[0], fa[2]], [fb[0]] + ([] if chain else [fb[2]])
+        if overlaps(fa[3], fb[3]):
+            return False
+        for o in (fa[3], fb[3]):
+            if any(overlaps(o, x) for x in ins_a + ins_b):
+                return False
+        if not chain and overlaps(fb[2], fa[3]):
+            return False
+        for op in between:
+            for w in op.writes:
+                if overlaps(w, mat) or overlaps(w, fb[3]) or any(overlaps(w, x) for x in ins_b):
+                    return False
+                if chain and overlaps(w, fa[3]):
+                    return False
+            if any(overlaps(rd, fb[3]) for rd in op.reads):
+                return False
+        return True
+
+    def _fuse_rank2(self):
+        """Merge two outer-product nodes into the same matrix (the second one
+        accumulating) into one Rank2Op at the later position, when nothing in
+        between touches the target or rewrites the first node's vectors."""
+        ops = self.ops
+        drop, repl = set(), {}
+        for i, a in enumerate(ops):
+            fa = rank1_form(a)
+            if fa is None or i in drop:
+                continue
+            if any(overlaps(fa[2], x) for x in fa[:2]):
+                continue
+            for j in range(i + 1, len(ops)):
+                b = ops[j]
+                fb = rank1_form(b)
+                if fb is not None and same_buffer(fb[2], fa[2]) and b.accumulate and j not in repl:
+                    if not any(overlaps(fb[2], x) for x in fb[:2]):
+                        drop.add(i)
+                        repl[j] = Rank2Op([a, b], fa[0], fa[1], fb[0], fb[1], fa[2], a.accumulate)
+                    break
+                if any(overlaps(w, x) for w in b.writes for x in fa) or any(overlaps(rd, fa[2]) for rd in b.reads):
+                    break
+        self.ops = [repl.get(k, op) for k, op in enumerate(ops) if k not in drop]
 
     def _x_liveness(self, X: Buffer, start: int, obs: set):
         """(write X back?, dead box) for the intermediate of a fused pair."""

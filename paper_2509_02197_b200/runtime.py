@@ -216,6 +216,10 @@ class Executable:
         self.err.zero_()
         stream = torch.cuda.current_stream(self.device)
         evs = []
+        # hold the stream with a device-side spin while the host enqueues every
+        # launch, so each event pair brackets GPU execution only (not the
+        # host's per-launch latency); ~40 us of host time per launch
+        torch.cuda._sleep(int(min(len(self.ops) * 40e-6, 2.0) * 2e9))
         for op in self.ops:
             a = torch.cuda.Event(enable_timing=True)
             b = torch.cuda.Event(enable_timing=True)

@@ -23,6 +23,8 @@ from paper_2509_02197_b200.lowering import (
     GatherOp,
     MapOp,
     MatmulOp,
+    MatvecPairOp,
+    Rank2Op,
     ReduceOp,
     StarPairOp,
     StencilOp,
@@ -235,6 +237,10 @@ class Emulator:
             oa, oo = self.arr(op.out.ptr)
             sl = slice(oo, oo + op.out.numel)
             oa[sl] = (oa[sl] + r.reshape(-1)) if op.accumulate else r.reshape(-1)
+        elif isinstance(op, (MatvecPairOp, Rank2Op)):
+            # the fused op is, by construction, the parts run in order
+            for part in op.parts:
+                self.run_op(part)
         elif isinstance(op, CopyOp):
             if not op.elided:
                 sa, so = self.arr(op.src.ptr)

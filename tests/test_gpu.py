@@ -350,6 +350,83 @@ def test_matvec_and_rank1_paths(M, N, K, ta, tb, dtype):
         assert err <= tol, (acc, err)
 
 
+@pytest.mark.parametrize("dtype", ["f64", "f32"])
+@pytest.mark.parametrize("R,C", [(4000, 4000), (100, 4096), (1000, 8), (7, 300), (333, 2050)])
+def test_matvec_pair_one_pass(R, C, dtype):
+    """gfb_matvec_pair (one streaming pass over A): r (+)= A u together with
+    c (+)= A^T v, v independent (bicg) or the new r (chain, atax), every
+    accumulate combination, against fp64 torch."""
+    from paper_2509_02197_b200 import _lib as L
+
+    lib = L.load()
+    td = torch.float64 if dtype == "f64" else torch.float32
+    code = L.F64 if dtype == "f64" else L.F32
+    g = torch.Generator(device="cuda").manual_seed(R * 7 + C)
+    # positive operands like the configs' inputs (uniform(0.4, 1.6)): the fp32
+    # bound is about summation order, not cancellation
+    A = torch.rand((R, C), generator=g, device="cuda", dtype=td) + 0.4
+    u = torch.rand(C, generator=g, device="cuda", dtype=td) + 0.4
+    v = torch.rand(R, generator=g, device="cuda", dtype=td) + 0.4
+    r0 = torch.rand(R, generator=g, device="cuda", dtype=td)
+    c0 = torch.rand(C, generator=g, device="cuda", dtype=td)
+    assert lib.gfb_matvec_pair_usable(code, R, C, C, A.data_ptr(), u.data_ptr())
+    ws = torch.empty(max(lib.gfb_matvec_pair_workspace_bytes(code, R, C, 1), 16), dtype=torch.uint8, device="cuda")
+    st = torch.cuda.current_stream().cuda_stream
+    tol = 1e-10 if dtype == "f64" else 1e-5
+    Ad = A.double()
+    for chain in (0, 1):
+        for r_acc in (0, 1):
+            for c_acc in (0, 1):
+                r, c = r0.clone(), c0.clone()
+                L.check(lib.gfb_matvec_pair(code, R, C, A.data_ptr(), C, u.data_ptr(), r.data_ptr(), r_acc,
+                                            None if chain else v.data_ptr(), c.data_ptr(), c_acc, chain,
+                                            ws.data_ptr(), st), "matvec_pair")
+                torch.cuda.synchronize()
+                want_r = Ad @ u.double() + (r0.double() if r_acc else 0)
+                # chain: the column sums consume the rounded r the kernel produced
+                vv = r.double() if chain else v.double()
+                want_c = Ad.T @ vv + (c0.double() if c_acc else 0)
+                for got, want in ((r, want_r), (c, want_c)):
+                    err = ((got.double() - want).abs() / want.abs().clamp(min=1)).max().item()
+                    assert err <= tol, (chain, r_acc, c_acc, err)
+    # each half alone
+    r, c = r0.clone(), c0.clone()
+    L.check(lib.gfb_matvec_pair(code, R, C, A.data_ptr(), C, u.data_ptr(), r.data_ptr(), 0, None, None, 0, 0,
+                                ws.data_ptr(), st), "matvec_pair rows")
+    L.check(lib.gfb_matvec_pair(code, R, C, A.data_ptr(), C, None, None, 0, v.data_ptr(), c.data_ptr(), 0, 0,
+                                ws.data_ptr(), st), "matvec_pair cols")
+    torch.cuda.synchronize()
+    for got, want in ((r, Ad @ u.double()), (c, Ad.T @ v.double())):
+        assert ((got.double() - want).abs() / want.abs().clamp(min=1)).max().item() <= tol
+
+
+@pytest.mark.parametrize("dtype", ["f64", "f32"])
+@pytest.mark.parametrize("M,N", [(4000, 4000), (37, 4100), (5, 8)])
+def test_rank2_update(M, N, dtype):
+    """gfb_rank2: C (= | +=) u1 v1^T + u2 v2^T (and rank 1) against fp64."""
+    from paper_2509_02197_b200 import _lib as L
+
+    lib = L.load()
+    td = torch.float64 if dtype == "f64" else torch.float32
+    code = L.F64 if dtype == "f64" else L.F32
+    g = torch.Generator(device="cuda").manual_seed(M + N)
+    u1, u2 = (torch.rand(M, generator=g, device="cuda", dtype=td) for _ in range(2))
+    v1, v2 = (torch.rand(N, generator=g, device="cuda", dtype=td) for _ in range(2))
+    C0 = torch.rand((M, N), generator=g, device="cuda", dtype=td)
+    st = torch.cuda.current_stream().cuda_stream
+    tol = 1e-12 if dtype == "f64" else 1e-6
+    for two in (0, 1):
+        for acc in (0, 1):
+            C = C0.clone()
+            L.check(lib.gfb_rank2(code, M, N, u1.data_ptr(), v1.data_ptr(), u2.data_ptr() if two else None,
+                                  v2.data_ptr() if two else None, C.data_ptr(), N, acc, st), "rank2")
+            torch.cuda.synchronize()
+            want = torch.outer(u1.double(), v1.double()) + (torch.outer(u2.double(), v2.double()) if two else 0)
+            want = want + (C0.double() if acc else 0)
+            err = ((C.double() - want).abs() / want.abs().clamp(min=1)).max().item()
+            assert err <= tol, (two, acc, err)
+
+
 def _torch_c4(name, inputs, params):
     """Independent fp64 torch-autograd restatement of the C4 programs (the
     same math as tools/workloads_ref.py), for full-size parity (SURVEY 8(c)
