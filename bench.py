@@ -111,7 +111,7 @@ class ClockSampler:
 
 
 def kernels_per_op(op) -> int:
-    from paper_2509_02197_b200.lowering import CopyOp, GatherOp, MatmulOp, ReduceOp
+    from paper_2509_02197_b200.lowering import CopyOp, GatherOp, MatmulOp, MatvecPairOp, ReduceOp
 
     if isinstance(op, CopyOp):
         return 0  # device-to-device memcpy or elided alias, not a kernel
@@ -119,6 +119,8 @@ def kernels_per_op(op) -> int:
         return 2
     if isinstance(op, GatherOp):
         return 2 if op.nsplit > 1 else 1
+    if isinstance(op, MatvecPairOp):
+        return 2  # streaming pass + column-partial finish
     if isinstance(op, MatmulOp):
         return 2 if op.workspace_bytes() > 0 else 1
     return 1
