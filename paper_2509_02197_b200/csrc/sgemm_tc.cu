@@ -20,6 +20,9 @@
 // it. Epilogue: tcgen05.ld of the warp's TMEM lane quarter (rows), 8 columns
 // at a time. Skinny problems split K over blockIdx.z with fp32 partials
 // reduced in order.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
 #include <algorithm>
 
 #include "gfb_common.cuh"
@@ -322,6 +325,298 @@ __global__ void __launch_bounds__(kTcThreads, 1)
   if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kCols));
 }
 
+// ---------------------------------------------------------------------------
+// TMA-fed variant (16-byte aligned operands): one elected producer thread
+// streams raw fp32 k-slabs by cp.async.bulk.tensor into a ring; six splitter
+// warps turn each raw slab into the hi / lo TF32 operands (in place for
+// K-major slabs, which TMA already writes in the SWIZZLE_128B canonical
+// layout; through a transpose for MN-major ones); one elected thread issues
+// the MMAs. Global loads no longer wait on the staging threads, so a CTA
+// keeps several slabs of HBM traffic in flight (the skinny, weight-streaming
+// mlp shapes are HBM-bound).
+constexpr int kTmaSplitWarps = 6;
+
+template <int BN, bool AKM, bool BKM>
+struct TmaCfg {
+  static constexpr int kRawA = kTcM * kTcK * 4, kRawB = BN * kTcK * 4;  // bytes
+  // per stage: raw A (= hi A when K-major), [hi A], lo A, raw B, [hi B], lo B
+  static constexpr int kStage = kRawA * (AKM ? 2 : 3) + kRawB * (BKM ? 2 : 3);
+  static constexpr int kStages = (200 * 1024) / kStage > 4 ? 4 : (200 * 1024) / kStage;
+  static constexpr int kSmem = kStages * kStage + 1024 /* align */ + 256 /* barriers */;
+};
+
+__device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap *map, uint32_t bar, int c0, int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];"
+      ::"r"(dst), "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(bar)
+      : "memory");
+}
+
+__device__ __forceinline__ void tc_mbar_init_n(uint64_t *bar, uint32_t n) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(tc_smem(bar)), "r"(n) : "memory");
+}
+
+__device__ __forceinline__ void tc_mbar_arrive(uint64_t *bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(tc_smem(bar)) : "memory");
+}
+
+__device__ __forceinline__ void tc_mbar_expect_tx(uint64_t *bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(tc_smem(bar)), "r"(bytes)
+               : "memory");
+}
+
+// split one raw slab of `rows` rows into hi / lo K-major SW128 operands
+template <int ROWS, bool KM>
+__device__ __forceinline__ void split_slab(uint32_t raw, uint32_t hi, uint32_t lo, int st) {
+  constexpr int kNSt = kTmaSplitWarps * 32;
+  if constexpr (KM) {
+    // raw is already the canonical layout: elementwise, hi written in place
+    for (int c = st; c < ROWS * 8; c += kNSt) {
+      float4 x;
+      asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+                   : "=f"(x.x), "=f"(x.y), "=f"(x.z), "=f"(x.w)
+                   : "r"(raw + c * 16));
+      const float4 h = make_float4(tf32_hi(x.x), tf32_hi(x.y), tf32_hi(x.z), tf32_hi(x.w));
+      sts128(raw + c * 16, h);
+      sts128(lo + c * 16, make_float4(x.x - h.x, x.y - h.y, x.z - h.z, x.w - h.w));
+    }
+  } else {
+    // raw[k][r] (r contiguous): chunk (r, kc) gathers k = 4kc..4kc+3 of row r
+    for (int c = st; c < ROWS * 8; c += kNSt) {
+      const int r = c % ROWS, kc = c / ROWS;
+      float v[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+        asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v[j]) : "r"(raw + ((kc * 4 + j) * ROWS + r) * 4));
+      const float4 h = make_float4(tf32_hi(v[0]), tf32_hi(v[1]), tf32_hi(v[2]), tf32_hi(v[3]));
+      const uint32_t o = sw128(r, kc * 4);
+      sts128(hi + o, h);
+      sts128(lo + o, make_float4(v[0] - h.x, v[1] - h.y, v[2] - h.z, v[3] - h.w));
+    }
+  }
+}
+
+template <int BN, bool AKM, bool BKM>
+__global__ void __launch_bounds__(kTcThreads, 1)
+    sgemm_tma_kernel(const __grid_constant__ CUtensorMap amap, const __grid_constant__ CUtensorMap bmap, int M,
+                     int N, int K, float *C, int64_t csm, int64_t csn, int accumulate, float *partial, int kchunk) {
+  using Cfg = TmaCfg<BN, AKM, BKM>;
+  constexpr int S = Cfg::kStages;
+  extern __shared__ __align__(1024) unsigned char tm_raw[];
+  unsigned char *base = reinterpret_cast<unsigned char *>((reinterpret_cast<uintptr_t>(tm_raw) + 1023) & ~(uintptr_t)1023);
+  uint64_t *full = reinterpret_cast<uint64_t *>(base + S * Cfg::kStage);
+  uint64_t *split = full + S, *empty = split + S, *done = empty + S;
+  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(done + 1);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int m0 = blockIdx.y * kTcM, n0 = blockIdx.x * BN;
+  const int kb = blockIdx.z * kchunk, ke = min(kb + kchunk, K);
+  const int nslab = ke > kb ? (ke - kb + kTcK - 1) / kTcK : 0;
+  constexpr int kCols = BN < 32 ? 32 : BN;
+  // stage layout (byte offsets): rawA | hiA (MN-major only) | loA | rawB | hiB | loB
+  constexpr int oRawA = 0, oHiA = AKM ? 0 : Cfg::kRawA, oLoA = AKM ? Cfg::kRawA : 2 * Cfg::kRawA;
+  constexpr int oRawB = oLoA + Cfg::kRawA, oHiB = BKM ? oRawB : oRawB + Cfg::kRawB;
+  constexpr int oLoB = oHiB + Cfg::kRawB;
+  const uint32_t sbase = tc_smem(base);
+
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(tc_smem(tmem_slot)),
+                 "r"(kCols));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  if (tid == 32) {
+    for (int i = 0; i < S; ++i) {
+      tc_mbar_init_n(&full[i], 1);
+      tc_mbar_init_n(&split[i], kTmaSplitWarps);
+      tc_mbar_init_n(&empty[i], 1);
+    }
+    tc_mbar_init_n(done, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {  // producer
+      for (int t = 0; t < nslab; ++t) {
+        const int s = t % S;
+        if (t >= S) tc_mbar_wait(&empty[s], (uint32_t)(((t / S) - 1) & 1));
+        const uint32_t st = sbase + s * Cfg::kStage;
+        const int k0 = kb + t * kTcK;
+        tc_mbar_expect_tx(&full[s], Cfg::kRawA + Cfg::kRawB);
+        if (AKM)
+          tma_load_2d(st + oRawA, &amap, tc_smem(&full[s]), k0, m0);
+        else
+          tma_load_2d(st + oRawA, &amap, tc_smem(&full[s]), m0, k0);
+        if (BKM)
+          tma_load_2d(st + oRawB, &bmap, tc_smem(&full[s]), k0, n0);
+        else
+          tma_load_2d(st + oRawB, &bmap, tc_smem(&full[s]), n0, k0);
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {  // MMA issuer
+      const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(BN >> 3) << 17) |
+                             ((uint32_t)(kTcM >> 4) << 24);
+      for (int t = 0; t < nslab; ++t) {
+        const int s = t % S;
+        tc_mbar_wait(&split[s], (uint32_t)((t / S) & 1));
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        const uint32_t st = sbase + s * Cfg::kStage;
+        const uint32_t ah = st + oHiA, al = st + oLoA, bh = st + oHiB, bl = st + oLoB;
+#pragma unroll
+        for (int ks = 0; ks < kTcK / 8; ++ks) {
+          const uint32_t off = ks * 32;
+          const int acc = (t > 0 || ks > 0) ? 1 : 0;
+          tc_mma(tmem, umma_desc_sw128(ah + off), umma_desc_sw128(bh + off), idesc, acc);
+          tc_mma(tmem, umma_desc_sw128(ah + off), umma_desc_sw128(bl + off), idesc, 1);
+          tc_mma(tmem, umma_desc_sw128(al + off), umma_desc_sw128(bh + off), idesc, 1);
+        }
+        tc_commit(&empty[s]);
+      }
+      if (nslab > 0) tc_commit(done);
+    }
+  } else {  // splitters
+    const int st_id = tid - 64;
+    for (int t = 0; t < nslab; ++t) {
+      const int s = t % S;
+      tc_mbar_wait(&full[s], (uint32_t)((t / S) & 1));
+      const uint32_t st = sbase + s * Cfg::kStage;
+      split_slab<kTcM, AKM>(st + oRawA, st + oHiA, st + oLoA, st_id);
+      split_slab<BN, BKM>(st + oRawB, st + oHiB, st + oLoB, st_id);
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      __syncwarp();
+      if (lane == 0) tc_mbar_arrive(&split[s]);
+    }
+  }
+  __syncwarp();
+  if (nslab > 0) tc_mbar_wait(done, 0);
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+
+  // epilogue (as sgemm_tc_kernel): warp w reads TMEM lane quarter w % 4 and
+  // column half w / 4; the ring is idle now and serves as transpose scratch
+  const int quarter = warp & 3, half = warp >> 2;
+  const int row = quarter * 32 + lane, gm = m0 + row;
+  constexpr int kHalf = BN / 2 < 8 ? 8 : BN / 2;
+  constexpr int kGrp = kHalf < 32 ? kHalf : 32;
+#pragma unroll 1
+  for (int c0 = half * kHalf; c0 < (half + 1) * kHalf && c0 < BN; c0 += kGrp) {
+    uint32_t v[kGrp];
+#pragma unroll
+    for (int g = 0; g < kGrp; g += 8) {
+      const uint32_t taddr = tmem + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(c0 + g);
+      asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+                   : "=r"(v[g]), "=r"(v[g + 1]), "=r"(v[g + 2]), "=r"(v[g + 3]), "=r"(v[g + 4]), "=r"(v[g + 5]),
+                     "=r"(v[g + 6]), "=r"(v[g + 7])
+                   : "r"(taddr));
+    }
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+    if (csn == 1 && !partial) {
+      float *scr = reinterpret_cast<float *>(base) + warp * (32 * (kGrp + 1));
+#pragma unroll
+      for (int j = 0; j < kGrp; ++j) scr[lane * (kGrp + 1) + j] = nslab > 0 ? __uint_as_float(v[j]) : 0.f;
+      __syncwarp();
+      if (lane < kGrp) {
+        const int gn = n0 + c0 + lane;
+        for (int r = 0; r < 32; ++r) {
+          const int rm = m0 + quarter * 32 + r;
+          if (rm >= M || gn >= N) continue;
+          const float x = scr[r * (kGrp + 1) + lane];
+          float *o = C + (int64_t)rm * csm + gn;
+          *o = accumulate ? *o + x : x;
+        }
+      }
+      __syncwarp();
+      continue;
+    }
+    if (gm >= M) continue;
+    float old[kGrp];
+    if (!partial && accumulate) {
+#pragma unroll
+      for (int j = 0; j < kGrp; ++j) {
+        const int gn = n0 + c0 + j;
+        old[j] = gn < N ? C[(int64_t)gm * csm + (int64_t)gn * csn] : 0.f;
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < kGrp; ++j) {
+      const int gn = n0 + c0 + j;
+      if (gn >= N) continue;
+      const float x = nslab > 0 ? __uint_as_float(v[j]) : 0.f;
+      if (partial)
+        partial[((int64_t)blockIdx.z * M + gm) * N + gn] = x;
+      else
+        C[(int64_t)gm * csm + (int64_t)gn * csn] = accumulate ? old[j] + x : x;
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kCols));
+}
+
+static PFN_cuTensorMapEncodeTiled_v12000 tc_encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    cudaDriverEntryPointQueryResult q;
+    void *p = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = (PFN_cuTensorMapEncodeTiled_v12000)p;
+  }
+  return fn;
+}
+
+// 2-D fp32 tensor map: inner extent `inner` (contiguous), `outer` rows of
+// `ld` elements, box (bi, bo)
+static bool tc_map(CUtensorMap *map, const float *p, int64_t inner, int64_t outer, int64_t ld, int bi, int bo,
+                   bool swz) {
+  cuuint64_t dims[2] = {(cuuint64_t)inner, (cuuint64_t)outer};
+  cuuint64_t strides[1] = {(cuuint64_t)(ld * 4)};
+  cuuint32_t box[2] = {(cuuint32_t)bi, (cuuint32_t)bo};
+  cuuint32_t estr[2] = {1, 1};
+  return tc_encode_fn()(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float *>(p), dims, strides, box, estr,
+                        CU_TENSOR_MAP_INTERLEAVE_NONE,
+                        swz ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE,
+                        CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+template <int BN, bool AKM, bool BKM>
+static int launch_tma(dim3 grid, int M, int N, int K, const float *A, int64_t lda, const float *B, int64_t ldb,
+                      float *C, int64_t csm, int64_t csn, int accumulate, float *partial, int kchunk,
+                      cudaStream_t st) {
+  CUtensorMap am, bm;
+  const bool ok = (AKM ? tc_map(&am, A, K, M, lda, kTcK, kTcM, true) : tc_map(&am, A, M, K, lda, kTcM, kTcK, false)) &&
+                  (BKM ? tc_map(&bm, B, K, N, ldb, kTcK, BN, true) : tc_map(&bm, B, N, K, ldb, BN, kTcK, false));
+  if (!ok) return -1;
+  constexpr int smem = TmaCfg<BN, AKM, BKM>::kSmem;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(sgemm_tma_kernel<BN, AKM, BKM>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    attr = true;
+  }
+  sgemm_tma_kernel<BN, AKM, BKM><<<grid, kTcThreads, smem, st>>>(am, bm, M, N, K, C, csm, csn, accumulate, partial,
+                                                                 kchunk);
+  return 0;
+}
+
+template <int BN>
+static int launch_tma_t(int ta, int tb, dim3 grid, int M, int N, int K, const float *A, int64_t lda,
+                        const float *B, int64_t ldb, float *C, int64_t csm, int64_t csn, int accumulate,
+                        float *partial, int kchunk, cudaStream_t st) {
+  // op(A) K-major <=> not transposed; op(B) K-major <=> transposed
+  if (!ta && tb) return launch_tma<BN, true, true>(grid, M, N, K, A, lda, B, ldb, C, csm, csn, accumulate, partial, kchunk, st);
+  if (!ta) return launch_tma<BN, true, false>(grid, M, N, K, A, lda, B, ldb, C, csm, csn, accumulate, partial, kchunk, st);
+  if (tb) return launch_tma<BN, false, true>(grid, M, N, K, A, lda, B, ldb, C, csm, csn, accumulate, partial, kchunk, st);
+  return launch_tma<BN, false, false>(grid, M, N, K, A, lda, B, ldb, C, csm, csn, accumulate, partial, kchunk, st);
+}
+
+static bool tma_ok(const float *A, int64_t lda, const float *B, int64_t ldb) {
+  static const bool off = getenv("GFB_NO_TMA_GEMM") != nullptr;
+  return !off && tc_encode_fn() != nullptr && lda % 4 == 0 && ldb % 4 == 0 &&
+         (reinterpret_cast<uintptr_t>(A) & 15) == 0 && (reinterpret_cast<uintptr_t>(B) & 15) == 0;
+}
+
 __global__ void tc_splits_finish(int64_t M, int64_t N, int64_t ns, const float *__restrict__ partial, float *C,
                                  int64_t csm, int64_t csn, int accumulate) {
   const int64_t MN = M * N;
@@ -346,7 +641,8 @@ int64_t sgemm_tc_splits(int64_t M, int64_t N, int64_t K) {
   const int64_t tiles = ceil_div(M, kTcM) * ceil_div(N, tc_bn(N));
   const int64_t target = (int64_t)sm_count();
   if (tiles >= target) return 1;
-  int64_t ns = ceil_div(target, tiles);
+  // one CTA per SM (the ring fills shared memory): stay within one wave
+  int64_t ns = target / tiles;
   const int64_t maxs = K / (4 * kTcK);
   if (ns > maxs) ns = maxs;
   return ns < 1 ? 1 : ns;
@@ -406,7 +702,21 @@ int sgemm_tc(int ta, int tb, int64_t M, int64_t N, int64_t K, const float *A, in
   const int64_t nz = ceil_div(K, chunk);
   float *partial = nz > 1 ? (float *)ws : nullptr;
   dim3 grid((unsigned)ceil_div(N, BN), (unsigned)ceil_div(M, kTcM), (unsigned)nz);
-  if (BN == 32)
+  int rc = -1;
+  if (tma_ok(A, lda, B, ldb)) {
+    if (BN == 32)
+      rc = launch_tma_t<32>(ta, tb, grid, (int)M, (int)N, (int)K, A, lda, B, ldb, C, csm, csn, accumulate, partial,
+                            (int)chunk, st);
+    else if (BN == 64)
+      rc = launch_tma_t<64>(ta, tb, grid, (int)M, (int)N, (int)K, A, lda, B, ldb, C, csm, csn, accumulate, partial,
+                            (int)chunk, st);
+    else
+      rc = launch_tma_t<128>(ta, tb, grid, (int)M, (int)N, (int)K, A, lda, B, ldb, C, csm, csn, accumulate,
+                             partial, (int)chunk, st);
+  }
+  if (rc == 0) {
+    // TMA-fed kernel launched
+  } else if (BN == 32)
     launch_tc_t<32>(ta, tb, grid, (int)M, (int)N, (int)K, A, lda, B, ldb, C, csm, csn, accumulate, partial,
                     (int)chunk, st);
   else if (BN == 64)
