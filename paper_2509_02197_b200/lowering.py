@@ -1100,15 +1100,15 @@ def map2_reduce(space, acc, ins, dst, ybox, clear_mode, cbox, code, seg, compute
     return op
 
 
-def contract_tile(M: int, N: int):
+def contract_tile(M: int, N: int, f32: bool = True):
     """(BM, BN) of the contraction kernel variant gfb_contract_launch picks."""
     if M <= 48 * 4 and N <= 32:
         return 48, 32
     if N <= 16:
-        return 128, 16
+        return (256 if f32 else 128), 16
     if N <= 32:
-        return 128, 32
-    return 64, 64
+        return (256 if f32 else 128), 32
+    return (128, 64) if f32 else (64, 64)
 
 
 class ContractOp(Op):
@@ -1371,7 +1371,7 @@ def contract_form(space, body, acc, ins, dst, ybox, clear_mode, cbox):
         b_q = _quads(ktab[:, 1], ktab[:, 2 + ncm:2 + ncm + ncn], ntab[:, 0])
     a_kfast |= 2 if a_q and A.buf.dtype == L.F32 else 0
     b_nfast |= 2 if b_q and B.buf.dtype == L.F32 else 0
-    BM, BN = contract_tile(M, N)
+    BM, BN = contract_tile(M, N, A.buf.dtype == L.F32)
     tiles = -(-M // BM) * -(-N // BN)
     nsplit = 1
     if tiles < 2 * 148 and K >= 64 * 16:
