@@ -503,6 +503,119 @@ __global__ void __launch_bounds__(256) map2_reduce_inner_vec4_kernel(const __gri
   }
 }
 
+// Prefetched operands of one vec4 item. Generated bodies fetch with
+// constant input indices, so after inlining these are plain registers: the
+// ILP kernels below load every input of U items before evaluating any of
+// them (a warp has U items of HBM latency in flight instead of one).
+constexpr int kM2CacheIn = 4;
+struct M2Cached {
+  const float (&c)[kM2CacheIn][4];
+  __device__ __forceinline__ void operator()(int k, float (&dst)[4]) const {
+#pragma unroll
+    for (int j = 0; j < 4; ++j) dst[j] = c[k][j];
+  }
+};
+
+template <int U>
+__device__ __forceinline__ void m2_prefetch(const gfb_map2_desc &d, const int32_t (&row)[U], const int32_t (&i0)[U],
+                                            const uint32_t (&vm)[U], float (&c)[U][kM2CacheIn][4]) {
+#pragma unroll
+  for (int u = 0; u < U; ++u) {
+    M2FetchVec4 f{d, row[u], i0[u], vm[u]};
+#pragma unroll
+    for (int k = 0; k < kM2CacheIn; ++k)
+      if (k < d.n_in) f(k, c[u][k]);
+  }
+}
+
+// pointwise, U warp items per iteration (generated bodies, n_in <= 4)
+template <typename Body, bool FLAT, int U>
+__global__ void __launch_bounds__(256) map2_pointwise_ilp_kernel(const __grid_constant__ gfb_map2_desc d,
+                                                                 int32_t rows, int32_t cpr) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int32_t E = (int32_t)d.ext[1];
+  const int32_t items = FLAT ? (int32_t)ceil_div((int64_t)rows * E, 128) : rows * cpr;
+  for (int32_t it0 = (blockIdx.x * kM2Warps + w) * U; it0 < items; it0 += gridDim.x * kM2Warps * U) {
+    int32_t row[U], i0[U];
+    uint32_t vm[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int32_t it = it0 + u;
+      if (FLAT) {
+        const int32_t f = it * 128 + lane * 4;
+        row[u] = f / E;
+        i0[u] = f - row[u] * E;
+        vm[u] = (it < items && row[u] < rows) ? 0xFu : 0u;
+      } else {
+        row[u] = cpr == 1 ? it : it / cpr;
+        i0[u] = (it - row[u] * cpr) * 128 + lane * 4;
+        vm[u] = (it < items && i0[u] < E) ? 0xFu : 0u;
+      }
+    }
+    float c[U][kM2CacheIn][4];
+    m2_prefetch<U>(d, row, i0, vm, c);
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      M2Cached fetch{c[u]};
+      for (int o = 0; o < d.n_out; ++o) {
+        float r[4];
+        Body::template eval<float, 4>(d, o, fetch, vm[u], r);
+        if (!vm[u]) continue;
+        const gfb_m2_operand &wo = d.out[o];
+        float *p = (float *)wo.base + ((int32_t)wo.c0 + (int32_t)wo.s[0] * row[u] + i0[u]);
+        float4 v = make_float4(r[0], r[1], r[2], r[3]);
+        if (d.wcr[o]) {
+          const float4 a = *reinterpret_cast<const float4 *>(p);
+          v.x += a.x, v.y += a.y, v.z += a.z, v.w += a.w;
+        }
+        *reinterpret_cast<float4 *>(p) = v;
+      }
+    }
+  }
+}
+
+// row sums of rows of at most 128 points, U rows per warp iteration
+template <typename Body, int U>
+__global__ void __launch_bounds__(256) map2_reduce_row_ilp_kernel(const __grid_constant__ gfb_map2_desc d,
+                                                                  int32_t rows) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int32_t E = (int32_t)d.ext[1];
+  for (int32_t r0 = (blockIdx.x * kM2Warps + w) * U; r0 < rows; r0 += gridDim.x * kM2Warps * U) {
+    int32_t row[U], i0[U];
+    uint32_t vm[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      row[u] = r0 + u;
+      i0[u] = lane * 4;
+      vm[u] = (row[u] < rows && i0[u] < E) ? 0xFu : 0u;
+    }
+    float c[U][kM2CacheIn][4];
+    m2_prefetch<U>(d, row, i0, vm, c);
+    float acc[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      M2Cached fetch{c[u]};
+      float r[4];
+      Body::template eval<float, 4>(d, 0, fetch, vm[u], r);
+      acc[u] = vm[u] ? (r[0] + r[1]) + (r[2] + r[3]) : 0.f;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+      for (int u = 0; u < U; ++u) acc[u] += __shfl_down_sync(0xffffffffu, acc[u], o);
+    if (lane == 0) {
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        if (row[u] >= rows) continue;
+        const gfb_m2_operand &wo = d.out[0];
+        const int32_t off = (int32_t)wo.c0 + (int32_t)wo.s[0] * row[u];
+        const bool inside = d.clear_mode == 2 ? (row[u] >= d.clear_lo[0] && row[u] < d.clear_hi[0]) : true;
+        store_as<float>(const_cast<void *>(wo.base), wo.dtype, off, m2_base<float>(d, inside, off) + acc[u]);
+      }
+    }
+  }
+}
+
 // column sums (mode 2) with 16-byte column quads: a warp instruction covers
 // 32 / qpr rows x qpr quads (qpr = quads per row slice, a power of two
 // <= 32), four row groups in flight per iteration; lanes holding the same
@@ -618,6 +731,19 @@ inline int launch_map2(const gfb_map2_desc &d, cudaStream_t st) {
       if constexpr (MODE == -1 || MODE == 0) {
         if (d.mode == 0) {
           const int64_t cpr = ceil_div(E, 128);
+          if constexpr (!std::is_same<Body, VmBody>::value) {
+            if (d.n_in <= kM2CacheIn) {
+              constexpr int U = 2;
+              const int64_t items = E < 128 ? ceil_div(rows * E, 128) : rows * cpr;
+              const int64_t blocks = std::max<int64_t>(std::min<int64_t>(ceil_div(items, kM2Warps * U), cap * 4), 1);
+              if (E < 128)
+                map2_pointwise_ilp_kernel<Body, true, U><<<(unsigned)blocks, 256, 0, st>>>(d, (int32_t)rows, 1);
+              else
+                map2_pointwise_ilp_kernel<Body, false, U><<<(unsigned)blocks, 256, 0, st>>>(d, (int32_t)rows,
+                                                                                              (int32_t)cpr);
+              return check_launch("map2");
+            }
+          }
           if (E < 128) {
             const int64_t blocks =
                 std::max<int64_t>(std::min<int64_t>(ceil_div(rows * E, 128 * kM2Warps), cap * 4), 1);
@@ -633,6 +759,15 @@ inline int launch_map2(const gfb_map2_desc &d, cudaStream_t st) {
       }
       if constexpr (MODE == -1 || MODE == 1) {
         if (d.mode == 1) {
+          if constexpr (!std::is_same<Body, VmBody>::value) {
+            if (d.n_in <= kM2CacheIn && E <= 128) {
+              constexpr int U = 4;
+              const int64_t blocks =
+                  std::max<int64_t>(std::min<int64_t>(ceil_div(rows, kM2Warps * U), cap * 4), 1);
+              map2_reduce_row_ilp_kernel<Body, U><<<(unsigned)blocks, 256, 0, st>>>(d, (int32_t)rows);
+              return check_launch("map2");
+            }
+          }
           const int64_t blocks = std::max<int64_t>(std::min<int64_t>(ceil_div(rows, kM2Warps), cap * 4), 1);
           map2_reduce_inner_vec4_kernel<Body><<<(unsigned)blocks, 256, 0, st>>>(d, (int32_t)rows);
           return check_launch("map2");
