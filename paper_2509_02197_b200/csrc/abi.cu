@@ -1,4 +1,5 @@
 // C-ABI plumbing: status strings, device queries, plain copies.
+#include <cstdlib>
 #include <cstdio>
 #include <cstring>
 
@@ -21,6 +22,14 @@ int check_launch(const char *what) {
     return GFB_ECUDA;
   }
   return GFB_OK;
+}
+
+bool pdl_enabled() {
+  static const bool on = [] {
+    const char *e = getenv("GFB_PDL");
+    return !(e && e[0] == '0');
+  }();
+  return on;
 }
 
 int sm_count() {

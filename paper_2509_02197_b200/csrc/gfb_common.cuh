@@ -174,4 +174,12 @@ __device__ __forceinline__ T vm_eval(const uint8_t *code, const uint8_t *arg, in
 
 __host__ __device__ __forceinline__ int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
 
+// Programmatic dependent launch: a kernel launched with the programmatic
+// stream-serialization attribute may start (prologue from its descriptor)
+// while its predecessor drains; pdl_wait() blocks until the predecessor's
+// memory is visible and must precede every global access. No-ops for a
+// plain launch.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
 }  // namespace gfb

@@ -214,7 +214,9 @@ __global__ void __launch_bounds__(kPX *kPY, 2) star_pair_kernel(const __grid_con
   const int tx = threadIdx.x, ty = threadIdx.y, tid = ty * kPX + tx;
   const int k0 = blockIdx.x * kPX, j0 = blockIdx.y * kPY;
   const int i0 = d.zlo + blockIdx.z * kPM, i1 = min(i0 + kPM, d.zhi);
-  star_prologue(d, i0, i1, tid, aj, ak, bj, bk, ai, bi, s_and_a, s_or_a, s_and_b, s_or_b);
+  pdl_trigger();
+  star_prologue(d, i0, i1, tid, aj, ak, bj, bk, ai, bi, s_and_a, s_or_a, s_and_b, s_or_b);  // descriptor only
+  pdl_wait();
   const int rs = d.rs;
   T ca[7], cb[7];
 #pragma unroll
@@ -369,8 +371,8 @@ extern "C" int gfb_star_pair_launch(const gfb_star_pair_desc *s, void *stream) {
   if (d.a.srcmask >= 0 && d.b.srcmask >= 0 && star_tma_usable(d, s->dtype))
     return launch_star_pair_tma(d, s->dtype, grid, st);
   if (s->dtype == GFB_F64)
-    star_pair_kernel<double><<<grid, block, 0, st>>>(d);
+    launch_pdl(star_pair_kernel<double>, grid, block, 0, st, d);
   else
-    star_pair_kernel<float><<<grid, block, 0, st>>>(d);
+    launch_pdl(star_pair_kernel<float>, grid, block, 0, st, d);
   return check_launch("star_pair");
 }

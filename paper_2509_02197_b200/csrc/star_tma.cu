@@ -501,7 +501,9 @@ __global__ void __launch_bounds__(tThreads, 512 / tThreads)
   __shared__ T xst[2][kR + 1][tThreads];  // staged old X values (fix-up points), by plane parity
   const int tid = threadIdx.y * tPX + threadIdx.x;
   const int i0 = d.zlo + blockIdx.z * d.tpm, i1 = min(i0 + d.tpm, d.zhi);
-  tma_prologue(d, i0, blockIdx.y * tPY, blockIdx.x * tPX, tid, words);
+  pdl_trigger();
+  tma_prologue(d, i0, blockIdx.y * tPY, blockIdx.x * tPX, tid, words);  // descriptor only
+  pdl_wait();
   if (d.d0 > 1)
     star_tma_body<T, true>(&ymap, d, ys, xs, mbar, words, xst, i0, i1);
   else
@@ -542,7 +544,7 @@ static int launch_tma(const CUtensorMap &map, const StarPairDev &d, cudaStream_t
   const int64_t slots = 2 * (int64_t)sm_count();
   dd.tpm = (int32_t)std::max<int64_t>(2, std::min<int64_t>(tPM, ceil_div(planes * tiles, slots)));
   dim3 grid((unsigned)ceil_div(d.d2, tPX), (unsigned)ceil_div(d.d1, tPY), (unsigned)ceil_div(planes, dd.tpm));
-  star_pair_tma_kernel<T><<<grid, dim3(tPX, tPY / kR), sm, st>>>(map, dd);
+  launch_pdl(star_pair_tma_kernel<T>, grid, dim3(tPX, tPY / kR), sm, st, map, dd);
   return check_launch("star_pair_tma");
 }
 
