@@ -243,7 +243,7 @@ __global__ void __launch_bounds__((BM / TM) * (BN / TN))
 // barrier per slab (slab and k-table buffers alternate); TM x TN register
 // tiles read with 16-byte shared-memory loads.
 template <typename T, int BM, int BN, int BK, int TM, int TN>
-__global__ void __launch_bounds__((BM / TM) * (BN / TN), 512 / ((BM / TM) * (BN / TN)))
+__global__ void __launch_bounds__((BM / TM) * (BN / TN), (BM / TM) * (BN / TN) >= 256 ? 2 : 4)
     contract2_kernel(const __grid_constant__ gfb_contract_desc d) {
   constexpr int NX = BN / TN, NY = BM / TM, NT = NX * NY;
   constexpr int PAD = 16 / (int)sizeof(T);
@@ -562,19 +562,36 @@ __global__ void __launch_bounds__((BM / TM) * (BN / TN), 512 / ((BM / TM) * (BN 
 
 // split-k: fixed-order fp64 sum of the partials, then the base as above
 template <typename T>
-__global__ void contract_finish_kernel(const __grid_constant__ gfb_contract_desc d) {
+__global__ void __launch_bounds__(1024) contract_finish_kernel(const __grid_constant__ gfb_contract_desc d) {
+  // 32 outputs x 32 split groups per CTA: each group sums every 32nd split,
+  // then the groups are added in order (deterministic)
+  __shared__ double red[32][33];
   const int64_t M = d.M, N = d.N, MN = M * N;
-  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < MN; e += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t m = e / N, n = e - m * N;
-    double sum = 0.0;
-    for (int s = 0; s < d.nsplit; ++s) sum += ((const double *)d.workspace)[(int64_t)s * MN + e];
-    const int32_t *me = d.mtab + m * d.mstride, *ne = d.ntab + n * d.nstride;
-    const int64_t off = (int64_t)me[1] + ne[1];
-    T *Dg = (T *)d.d;
-    T base = T(0);
-    if (d.clear_mode == 0 || (d.clear_mode == 2 && !(me[2] && ne[2]))) base = Dg[off];
-    Dg[off] = base + (T)(d.scale * sum);
+  const int lane = threadIdx.x & 31, g = threadIdx.x >> 5;
+  const int64_t e = (int64_t)blockIdx.x * 32 + lane;
+  const double *ws = (const double *)d.workspace;
+  double s4[4] = {0.0, 0.0, 0.0, 0.0};
+  if (e < MN) {
+    int s = g;
+    for (; s + 96 < d.nsplit; s += 128) {
+#pragma unroll
+      for (int u = 0; u < 4; ++u) s4[u] += ws[(int64_t)(s + 32 * u) * MN + e];
+    }
+    for (; s < d.nsplit; s += 32) s4[0] += ws[(int64_t)s * MN + e];
   }
+  red[g][lane] = (s4[0] + s4[1]) + (s4[2] + s4[3]);
+  __syncthreads();
+  if (g != 0 || e >= MN) return;
+  double sum = 0.0;
+#pragma unroll
+  for (int q = 0; q < 32; ++q) sum += red[q][lane];
+  const int64_t m = e / N, n = e - m * N;
+  const int32_t *me = d.mtab + m * d.mstride, *ne = d.ntab + n * d.nstride;
+  const int64_t off = (int64_t)me[1] + ne[1];
+  T *Dg = (T *)d.d;
+  T base = T(0);
+  if (d.clear_mode == 0 || (d.clear_mode == 2 && !(me[2] && ne[2]))) base = Dg[off];
+  Dg[off] = base + (T)(d.scale * sum);
 }
 
 template <typename T, int BM, int BN, int TM, int TN, int BK = 16>
@@ -603,6 +620,8 @@ static void launch_contract_t(const gfb_contract_desc &d, cudaStream_t st) {
       launch_contract<T, 128, 32, 4, 4>(d, st);
     else
       launch_contract<T, 64, 64, 4, 4>(d, st);
+  } else if (f32 && d.M > 48 && d.M <= 144 && d.N <= 32) {
+    launch_contract2<T, 144, 32, 9, 8>(d, st);  // few outputs, long k: whole output per CTA (weight adjoints)
   } else if (d.M <= 48 * 4 && d.N <= 32) {
     launch_contract2<T, 48, 32, 3, 2>(d, st);  // few outputs, long k (weight adjoints)
   } else if constexpr (f32) {
@@ -620,11 +639,7 @@ static void launch_contract_t(const gfb_contract_desc &d, cudaStream_t st) {
     else
       launch_contract2<T, 64, 64, 4, 4>(d, st);
   }
-  if (d.nsplit > 1) {
-    const int64_t MN = d.M * d.N;
-    const unsigned blocks = (unsigned)std::min<int64_t>(ceil_div(MN, 256), 148 * 16);
-    contract_finish_kernel<T><<<blocks, 256, 0, st>>>(d);
-  }
+  if (d.nsplit > 1) contract_finish_kernel<T><<<(unsigned)ceil_div(d.M * d.N, 32), 1024, 0, st>>>(d);
 }
 
 }  // namespace gfb

@@ -774,8 +774,10 @@ class MatvecPairOp(Op):
         return 4 * self.R * self.C
 
     def algorithmic_bytes(self) -> int:
-        # one read of the matrix plus the vectors
-        return sum(b.nbytes for b in set(self.reads)) + sum(b.nbytes for b in set(self.writes))
+        # SURVEY 8(d) counts each matrix-vector pass as a full read of the
+        # matrix; one launch performs both passes (as a fused star-pair launch
+        # performs two sweeps), so its algorithmic bytes are its parts'
+        return sum(p.algorithmic_bytes() for p in self.parts)
 
     def prepare(self, rt):
         self.use_parts = not L.load().gfb_matvec_pair_usable(self.mat.dtype, self.R, self.C, self.C, self.mat.ptr,
@@ -1102,6 +1104,8 @@ def map2_reduce(space, acc, ins, dst, ybox, clear_mode, cbox, code, seg, compute
 
 def contract_tile(M: int, N: int, f32: bool = True):
     """(BM, BN) of the contraction kernel variant gfb_contract_launch picks."""
+    if f32 and 48 < M <= 144 and N <= 32:
+        return 144, 32
     if M <= 48 * 4 and N <= 32:
         return 48, 32
     if N <= 16:
@@ -1374,8 +1378,11 @@ def contract_form(space, body, acc, ins, dst, ybox, clear_mode, cbox):
     BM, BN = contract_tile(M, N, A.buf.dtype == L.F32)
     tiles = -(-M // BM) * -(-N // BN)
     nsplit = 1
-    if tiles < 2 * 148 and K >= 64 * 16:
-        nsplit = int(min(-(-2 * 148 // tiles), K // (32 * 16), 1024))
+    # enough CTAs to fill the SMs: two per SM, eight for the 64-thread
+    # whole-output tile (weight adjoints)
+    per_sm = 8 if (BM, BN) == (144, 32) else 2
+    if tiles < per_sm * 148 and K >= 64 * 16:
+        nsplit = int(min(-(-per_sm * 148 // tiles), K // (8 * 16), 2048))
     return ContractOp(dst, A.buf, B.buf, scale, clear_mode, M, N, K, mtab, ntab, ktab, len(cons_m), len(cons_n),
                       [lo for lo, _ in bounds], [hi for _, hi in bounds], a_kfast, b_nfast, max(nsplit, 1))
 

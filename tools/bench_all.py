@@ -52,6 +52,16 @@ def fp64_tensor_peak():
 FP32_FFMA_NOMINAL = 148 * 128 * 2 * 1.965e9 / 1e12  # TFLOP/s, no measured fp32 SIMT figure
 
 
+def tf32_peak():
+    """Dense TF32 tensor peak: half the measured bf16 figure (MEASURED_PEAKS),
+    else half the 2.25 PFLOP/s nominal bf16."""
+    path = os.path.join(REPO, "MEASURED_PEAKS.json")
+    if os.path.exists(path):
+        with open(path) as f:
+            return float(json.load(f).get("bf16_tflops", 2250.0)) / 2.0
+    return 1125.0
+
+
 def family(op):
     """matmul launches with a unit dimension are HBM-bound matrix-vector /
     rank-1 passes; the rest are contractions."""
@@ -79,6 +89,22 @@ def roofline(exe, inputs, peak_hbm, fp64_peak):
             return {"bound": "tensor(fp64 DMMA)", "kernel": dom, "achieved": round(ach, 2), "unit": "TFLOP/s",
                     "peak": round(fp64_peak, 2), "peak_kind": "cuBLAS DGEMM 8192^3 measured in this run",
                     "frac": round(ach / fp64_peak, 4), "step_share": shares}
+        if dom == "matmul":
+            # fp32 matmuls run 3xTF32 on tcgen05: each launch is bound by the
+            # larger of its HBM time (A + B + C bytes) and its tensor time
+            # (3 TF32 products); frac = roofline time / measured time
+            tf = tf32_peak()
+            t_roof = 0.0
+            for fam, op, ms in rows:
+                if fam != dom:
+                    continue
+                t_roof += max(op.algorithmic_bytes() / (peak_hbm * 1e9), 3 * op.flops() / (tf * 1e12))
+            t_meas = fam_t[dom] * 1e-3
+            return {"bound": "hbm|tensor (per launch)", "kernel": dom, "achieved": round(ach, 2),
+                    "unit": "TFLOP/s (fp32-equivalent)", "peak": None,
+                    "peak_kind": f"per launch max(bytes / {peak_hbm} GB/s, 3 x flops / {tf:.0f} TF/s TF32)",
+                    "frac": round(t_roof / t_meas, 4), "roofline_ms": round(t_roof * 1e3, 4),
+                    "measured_ms": round(t_meas * 1e3, 4), "step_share": shares}
         return {"bound": "fp32 FFMA", "kernel": dom, "achieved": round(ach, 2), "unit": "TFLOP/s",
                 "peak": round(FP32_FFMA_NOMINAL, 1), "peak_kind": "nominal 148 SMs x 128 FMA/clk x 1965 MHz",
                 "frac": round(ach / FP32_FFMA_NOMINAL, 4), "step_share": shares}
