@@ -214,9 +214,9 @@ __global__ void __launch_bounds__(kPX *kPY, 2) star_pair_kernel(const __grid_con
   const int tx = threadIdx.x, ty = threadIdx.y, tid = ty * kPX + tx;
   const int k0 = blockIdx.x * kPX, j0 = blockIdx.y * kPY;
   const int i0 = d.zlo + blockIdx.z * kPM, i1 = min(i0 + kPM, d.zhi);
-  pdl_trigger();
   star_prologue(d, i0, i1, tid, aj, ak, bj, bk, ai, bi, s_and_a, s_or_a, s_and_b, s_or_b);  // descriptor only
   pdl_wait();
+  pdl_trigger();  // after the wait: at most one launch waits ahead of the running one
   const int rs = d.rs;
   T ca[7], cb[7];
 #pragma unroll

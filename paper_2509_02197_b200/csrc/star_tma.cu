@@ -501,9 +501,9 @@ __global__ void __launch_bounds__(tThreads, 512 / tThreads)
   __shared__ T xst[2][kR + 1][tThreads];  // staged old X values (fix-up points), by plane parity
   const int tid = threadIdx.y * tPX + threadIdx.x;
   const int i0 = d.zlo + blockIdx.z * d.tpm, i1 = min(i0 + d.tpm, d.zhi);
-  pdl_trigger();
   tma_prologue(d, i0, blockIdx.y * tPY, blockIdx.x * tPX, tid, words);  // descriptor only
   pdl_wait();
+  pdl_trigger();  // after the wait: at most one launch waits ahead of the running one
   if (d.d0 > 1)
     star_tma_body<T, true>(&ymap, d, ys, xs, mbar, words, xst, i0, i1);
   else
