@@ -36,8 +36,6 @@ struct StencilGeom {
 template <typename T, int MAXT>
 __global__ void __launch_bounds__(kSX *kSY) stencil_kernel(const __grid_constant__ gfb_stencil_desc d,
                                                            const __grid_constant__ StencilGeom g) {
-  pdl_wait();
-  pdl_trigger();  // after the wait: at most one launch waits ahead of the running one
   const int64_t k = g.lo2 + (int64_t)blockIdx.x * kSX + threadIdx.x;
   const int64_t j = g.lo1 + (int64_t)blockIdx.y * kSY + threadIdx.y;
   if (k >= g.lo2 + g.e2 || j >= g.lo1 + g.e1) return;
@@ -127,9 +125,9 @@ extern "C" int gfb_stencil_launch(const gfb_stencil_desc *d, void *stream) {
   cudaStream_t st = (cudaStream_t)stream;
 #define GFB_STENCIL_LAUNCH(MT)                                      \
   if (d->dtype == GFB_F64)                                          \
-    launch_pdl(stencil_kernel<double, MT>, grid, block, 0, st, *d, g); \
+    stencil_kernel<double, MT><<<grid, block, 0, st>>>(*d, g);      \
   else                                                              \
-    launch_pdl(stencil_kernel<float, MT>, grid, block, 0, st, *d, g);
+    stencil_kernel<float, MT><<<grid, block, 0, st>>>(*d, g);
   if (d->ntaps <= 8) {
     GFB_STENCIL_LAUNCH(8)
   } else if (d->ntaps <= 16) {
