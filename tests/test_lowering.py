@@ -124,3 +124,41 @@ def test_data_dependent_branch_is_rejected_loudly():
     inputs = {"X": np.ones(8), "s": np.array(0.3)}
     with pytest.raises(UnsupportedConstruct):
         lower_gradient(prog, b, params, _check_inputs(prog, inputs, params))
+
+
+@pytest.mark.parametrize("name", ["atax", "bicg"])
+def test_matvec_pairs_and_rank2_fuse_and_match_goldens(name):
+    """Both matrix-vector pairs (forward and adjoint) become one-pass
+    MatvecPairOps and the two outer-product adjoints one Rank2Op; the fused
+    list (emulated as its parts, in order) still reproduces the reference."""
+    from paper_2509_02197_b200.lowering import MatmulOp, MatvecPairOp, Rank2Op
+
+    prog, b = _bundle(name)
+    cid = f"{name}__M40_N33"
+    inputs, value, grads, _ = load_case(cid)
+    lw, em, view = _emulate(prog, b, IDX["cases"][cid]["params"], inputs)
+    ops = lw.low.ops
+    assert sum(isinstance(op, MatvecPairOp) for op in ops) == 2
+    assert sum(isinstance(op, Rank2Op) for op in ops) == 1
+    assert not any(isinstance(op, MatmulOp) for op in ops)
+    if name == "atax":
+        assert [op.chain for op in ops if isinstance(op, MatvecPairOp)] == [True, True]
+    _check(lw, view, prog, value, grads)
+
+
+def test_matvec_pairing_respects_an_intervening_write():
+    """A write to the matrix between the two nodes blocks the pairing."""
+    from paper_2509_02197_b200.lowering import FillOp, Lowering, MatmulOp, MatvecPairOp
+
+    low = Lowering()
+    A = low.new_buffer("A", (8, 8), "real64", fresh=False)
+    x = low.new_buffer("x", (8, 1), "real64", fresh=False)
+    t = low.new_buffer("t", (8, 1), "real64", fresh=False)
+    y = low.new_buffer("y", (8, 1), "real64", fresh=False)
+    low.ops = [MatmulOp(A, x, t, False, False, 8, 1, 8, False), FillOp(A, ((0, 8), (0, 8)), 1.0),
+               MatmulOp(A, t, y, True, False, 8, 1, 8, False)]
+    low._fuse_matvec_pairs()
+    assert not any(isinstance(op, MatvecPairOp) for op in low.ops)
+    low.ops = [MatmulOp(A, x, t, False, False, 8, 1, 8, False), MatmulOp(A, t, y, True, False, 8, 1, 8, False)]
+    low._fuse_matvec_pairs()
+    assert [type(op).__name__ for op in low.ops] == ["MatvecPairOp"] and low.ops[0].chain
