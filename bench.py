@@ -115,6 +115,8 @@ def kernels_per_op(op) -> int:
 
     if isinstance(op, CopyOp):
         return 0  # device-to-device memcpy or elided alias, not a kernel
+    if op.family in ("halo", "allreduce"):
+        return 0  # NCCL communication, not one of the engine's kernels
     if isinstance(op, ReduceOp):
         return 2
     if isinstance(op, GatherOp):
@@ -326,7 +328,9 @@ def run_b200(args):
                "api": ("SlabEngine.gradient(pinned local slabs) -> numpy owned-plane grads (all ranks)" if slab
                        else "Engine.gradient(host pinned inputs) -> numpy grads")}
     peak, peak_kind = measured_peaks()
-    roof = roofline(eng.exe, dev_inputs, peak, peak_kind) if rank == 0 else None
+    # the per-launch timing pass runs the launch list, halo exchanges and the
+    # all-reduce included, so every rank takes part; rank 0 reports it
+    roof = roofline(eng.exe, dev_inputs, peak, peak_kind) if (rank == 0 or slab) else None
     launches = args.steps * sum(kernels_per_op(op) for op in eng.exe.ops)
     base = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline and not slab:
