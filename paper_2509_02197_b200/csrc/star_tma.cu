@@ -194,7 +194,7 @@ __device__ __forceinline__ void star_tma_body(const CUtensorMap *ymap, const Sta
   const int ylo = HAS_I ? max(qbeg - 1, 0) : 0;
   const int yhi = HAS_I ? min(min(qend, d.d0 - 1) + 1, d.d0 - 1) : 0;
   constexpr uint32_t kTx = (uint32_t)(YS * sizeof(T));
-  auto slot_of = [&](int p) { return ys + ((p - ylo + NSY) % NSY) * YSS; };
+  auto slot_of = [&](int p) { return ys + ((unsigned)(p - ylo + NSY) % (unsigned)NSY) * YSS; };
   auto issue = [&](int p) {
     const int sl = (p - ylo) % NSY;
     mbar_expect_tx(&mbar[sl], kTx);
@@ -372,7 +372,13 @@ __device__ __forceinline__ void star_tma_body(const CUtensorMap *ymap, const Sta
       }
       const T *yc = slot_of(q);
       const T *yp = slot_of(q + 1);
-      T *xw = xs + (q % NXS) * XS;
+      // X~ ring slots relative to the march start: compile-time in the
+      // unrolled march (step M handles planes q = qbeg + 3n + M)
+#if GFB_STAR_UNROLL
+      T *xw = xs + M * XS;
+#else
+      T *xw = xs + ((unsigned)(q - qbeg) % (unsigned)NXS) * XS;
+#endif
       const uint32_t mi = W.ai[q - i0 + 1];
       const bool fast = ((mi & jka) & xfast_m) == xfast_m;
       const bool own = q >= i0 && q < i1;
@@ -416,7 +422,11 @@ __device__ __forceinline__ void star_tma_body(const CUtensorMap *ymap, const Sta
     __syncthreads();
     const int i = HAS_I ? q - 1 : q;
     if (i >= i0 && i < i1) {
-      const T *xc = xs + (i % NXS) * XS;
+#if GFB_STAR_UNROLL
+      const T *xc = xs + (HAS_I ? (M + 2) % 3 : M) * XS;
+#else
+      const T *xc = xs + ((unsigned)(i - qbeg + NXS) % (unsigned)NXS) * XS;
+#endif
       const T up = xc[xo0 - HX], dn = xc[xo0 + kR * HX];
       T z[kR];
 #pragma unroll
