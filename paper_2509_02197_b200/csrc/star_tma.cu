@@ -196,13 +196,13 @@ __device__ __forceinline__ void star_tma_body(const CUtensorMap *ymap, const Sta
   constexpr uint32_t kTx = (uint32_t)(YS * sizeof(T));
   auto slot_of = [&](int p) { return ys + ((unsigned)(p - ylo + NSY) % (unsigned)NSY) * YSS; };
   auto issue = [&](int p) {
-    const int sl = (p - ylo) % NSY;
+    const int sl = (int)((unsigned)(p - ylo) % (unsigned)NSY);
     mbar_expect_tx(&mbar[sl], kTx);
     tma_load_3d(ys + sl * YSS, ymap, &mbar[sl], k0 - 2, j0 - 2, p);
   };
   auto wait_plane = [&](int p) {
     const int r = p - ylo;
-    mbar_wait(&mbar[r % NSY], (uint32_t)((r / NSY) & 1));
+    mbar_wait(&mbar[(unsigned)r % (unsigned)NSY], ((unsigned)r / (unsigned)NSY) & 1u);
   };
   if (tid == 0) {
     for (int s = 0; s < NSY; ++s) mbar_init(&mbar[s], 1);
