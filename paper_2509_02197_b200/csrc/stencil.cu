@@ -28,6 +28,7 @@ struct StencilGeom {
   const void *tap_base[GFB_MAX_TAPS];  // source pointer pre-shifted by the tap offset
   int64_t mlo[GFB_MAX_TAPS][3], mhi[GFB_MAX_TAPS][3];
   int64_t clo[3], chi[3];
+  int64_t march;  // planes per CTA along dim 0
 };
 
 // Taps are unrolled up to MAXT (compile-time) and their box masks are split
@@ -39,8 +40,8 @@ __global__ void __launch_bounds__(kSX *kSY) stencil_kernel(const __grid_constant
   const int64_t k = g.lo2 + (int64_t)blockIdx.x * kSX + threadIdx.x;
   const int64_t j = g.lo1 + (int64_t)blockIdx.y * kSY + threadIdx.y;
   if (k >= g.lo2 + g.e2 || j >= g.lo1 + g.e1) return;
-  const int64_t i_begin = g.lo0 + (int64_t)blockIdx.z * kMarch;
-  const int64_t i_end = min(i_begin + kMarch, g.lo0 + g.e0);
+  const int64_t i_begin = g.lo0 + (int64_t)blockIdx.z * g.march;
+  const int64_t i_end = min(i_begin + g.march, g.lo0 + g.e0);
   const int nt = d.ntaps;
   uint32_t mjk = 0;
 #pragma unroll
@@ -120,7 +121,13 @@ extern "C" int gfb_stencil_launch(const gfb_stencil_desc *d, void *stream) {
     g.chi[r] = r < pad ? INT64_MAX / 4 : d->clear_hi[r - pad];
   }
   dim3 block(kSX, kSY);
-  dim3 grid((unsigned)ceil_div(g.e2, kSX), (unsigned)ceil_div(g.e1, kSY), (unsigned)ceil_div(g.e0, kMarch));
+  // planes per CTA: kMarch on large domains; small (L2-resident) domains
+  // march fewer planes so a thread's serial chain of plane loads stays short
+  // and the grid still fills the SMs (C2 heat_3d, 70^3)
+  const int64_t tiles = ceil_div(g.e2, kSX) * ceil_div(g.e1, kSY);
+  g.march = kMarch;
+  while (g.march > 2 && tiles * ceil_div(g.e0, g.march) < (int64_t)sm_count() * 4) g.march /= 2;
+  dim3 grid((unsigned)ceil_div(g.e2, kSX), (unsigned)ceil_div(g.e1, kSY), (unsigned)ceil_div(g.e0, g.march));
   if (grid.y > 65535 || grid.z > 65535) return set_error(GFB_EUNSUPPORTED, "gfb_stencil_launch: extent too large");
   cudaStream_t st = (cudaStream_t)stream;
 #define GFB_STENCIL_LAUNCH(MT)                                      \
