@@ -28,7 +28,8 @@ struct StencilGeom {
   const void *tap_base[GFB_MAX_TAPS];  // source pointer pre-shifted by the tap offset
   int64_t mlo[GFB_MAX_TAPS][3], mhi[GFB_MAX_TAPS][3];
   int64_t clo[3], chi[3];
-  int64_t march;  // planes per CTA along dim 0
+  int64_t march;      // planes per CTA along dim 0
+  int32_t any_masked; // some tap has a mask box (else the predicate logic is skipped)
 };
 
 // Taps are unrolled up to MAXT (compile-time) and their box masks are split
@@ -43,10 +44,10 @@ __global__ void __launch_bounds__(kSX *kSY) stencil_kernel(const __grid_constant
   const int64_t i_begin = g.lo0 + (int64_t)blockIdx.z * g.march;
   const int64_t i_end = min(i_begin + g.march, g.lo0 + g.e0);
   const int nt = d.ntaps;
-  uint32_t mjk = 0;
+  uint32_t mjk = g.any_masked ? 0u : 0xffffffffu;
 #pragma unroll
   for (int t = 0; t < MAXT; ++t) {
-    if (t < nt) {
+    if (t < nt && g.any_masked) {
       bool ok = !d.tap_masked[t] ||
                 (j >= g.mlo[t][1] && j < g.mhi[t][1] && k >= g.mlo[t][2] && k < g.mhi[t][2]);
       mjk |= (uint32_t)ok << t;
@@ -56,9 +57,11 @@ __global__ void __launch_bounds__(kSX *kSY) stencil_kernel(const __grid_constant
   T *dst = (T *)d.dst;
   for (int64_t i = i_begin; i < i_end; ++i) {
     uint32_t m = mjk;
+    if (g.any_masked) {
 #pragma unroll
-    for (int t = 0; t < MAXT; ++t)
-      if (t < nt && d.tap_masked[t] && (i < g.mlo[t][0] || i >= g.mhi[t][0])) m &= ~(1u << t);
+      for (int t = 0; t < MAXT; ++t)
+        if (t < nt && d.tap_masked[t] && (i < g.mlo[t][0] || i >= g.mhi[t][0])) m &= ~(1u << t);
+    }
     const int64_t off = (i * g.d1 + j) * g.d2 + k;
     T acc;
     if (d.clear_mode == 0) {
@@ -116,6 +119,8 @@ extern "C" int gfb_stencil_launch(const gfb_stencil_desc *d, void *stream) {
       g.mhi[t][r] = r < pad ? INT64_MAX / 4 : d->tap_mhi[t][r - pad];
     }
   }
+  g.any_masked = 0;
+  for (int t = 0; t < d->ntaps; ++t) g.any_masked |= d->tap_masked[t] ? 1 : 0;
   for (int r = 0; r < 3; ++r) {
     g.clo[r] = r < pad ? INT64_MIN / 4 : d->clear_lo[r - pad];
     g.chi[r] = r < pad ? INT64_MAX / 4 : d->clear_hi[r - pad];
