@@ -1,6 +1,6 @@
 """SASS evidence of the Blackwell data paths in libgfb.so (cuobjdump):
 which kernels issue tcgen05 MMAs (UTCHMMA), TMEM loads (LDTM), TMA loads
-(UTMALDG), mbarrier transaction waits (SYNCS), cp.async (LDGSTS) and DMMA.
+(UTMALDG), 1-D bulk copies (UBLKCP), mbarrier transaction waits (SYNCS), cp.async (LDGSTS) and DMMA.
 
     python tools/sass_evidence.py > profiles/r01_sass_evidence.txt
 """
@@ -10,7 +10,7 @@ import re
 import subprocess
 
 LIB = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "paper_2509_02197_b200", "libgfb.so")
-OPS = ["UTCHMMA", "UTCBAR", "LDTM", "UTMALDG", "SYNCS.ARRIVE.TRANS64", "SYNCS.PHASECHK.TRANS64.TRYWAIT", "LDGSTS",
+OPS = ["UTCHMMA", "UTCBAR", "LDTM", "UTMALDG", "UBLKCP", "SYNCS.ARRIVE.TRANS64", "SYNCS.PHASECHK.TRANS64.TRYWAIT", "LDGSTS",
        "DMMA", "FFMA", "DFMA"]
 
 sass = subprocess.run(["cuobjdump", "-sass", LIB], capture_output=True, text=True).stdout
@@ -31,6 +31,6 @@ demangle = subprocess.run(["c++filt"], input="\n".join(per), capture_output=True
 print("cuobjdump -sass paper_2509_02197_b200/libgfb.so: static instruction counts per kernel (sm_100a)")
 print(f"{'kernel':90s} " + " ".join(f"{o.split('.')[0][:8]:>8s}" for o in OPS))
 for (name, cnt), dm in zip(per.items(), demangle):
-    if not any(cnt[o] for o in OPS[:8]):
+    if not any(cnt[o] for o in OPS[:9]):
         continue
     print(f"{dm[:90]:90s} " + " ".join(f"{cnt[o]:8d}" for o in OPS))
