@@ -1378,9 +1378,10 @@ def contract_form(space, body, acc, ins, dst, ybox, clear_mode, cbox):
     BM, BN = contract_tile(M, N, A.buf.dtype == L.F32)
     tiles = -(-M // BM) * -(-N // BN)
     nsplit = 1
-    # enough CTAs to fill the SMs: two per SM, eight for the 64-thread
-    # whole-output tile (weight adjoints)
-    per_sm = 8 if (BM, BN) == (144, 32) else 2
+    # enough CTAs to fill the SMs in one wave: two per SM, four for the
+    # 64-thread whole-output tile of the weight adjoints (its register-bound
+    # occupancy; eight per SM doubled the split-k partial traffic: 150 vs 188 us)
+    per_sm = 4 if (BM, BN) == (144, 32) else 2
     if tiles < per_sm * 148 and K >= 64 * 16:
         nsplit = int(min(-(-per_sm * 148 // tiles), K // (8 * 16), 2048))
     return ContractOp(dst, A.buf, B.buf, scale, clear_mode, M, N, K, mtab, ntab, ktab, len(cons_m), len(cons_n),
