@@ -16,6 +16,14 @@ extern const int kM2NumSpecials;
 
 // FNV-1a over the fields that determine the generated code; mirrored by
 // tools/gen_tasklets.py (m2_key)
+uint32_t m2_uniform_mask(const gfb_map2_desc &d) {
+  if (d.compute_f64 || d.ndim < 1) return 0;
+  uint32_t m = 0;
+  for (int k = 0; k < d.n_in && k < 32; ++k)
+    if (d.in[k].s[d.ndim - 1] == 0) m |= 1u << k;
+  return m;
+}
+
 uint64_t m2_key(const gfb_map2_desc &d) {
   uint64_t h = 1469598103934665603ull;
   auto mix = [&](uint32_t x) {
@@ -33,6 +41,10 @@ uint64_t m2_key(const gfb_map2_desc &d) {
     mix((uint32_t)d.code_len[o]);
     for (int pc = d.code_start[o]; pc < d.code_start[o] + d.code_len[o]; ++pc) mix(d.code[pc]);
   }
+  // fp32 inputs constant along the innermost loop dimension (row scalars):
+  // bodies generated for this pattern evaluate them once per lane
+  const uint32_t um = m2_uniform_mask(d);
+  if (um) mix(0x55000000u | um);
   return h;
 }
 

@@ -718,8 +718,14 @@ inline bool m2_vec4_ok(const gfb_map2_desc &d) {
 }
 
 // MODE: the one mode a generated body is used with, or -1 (every mode)
-template <typename T, int V, typename Body, int MODE = -1>
+template <typename T, int V, typename Body, int MODE = -1, bool UNIFORM = false>
 inline int launch_map2(const gfb_map2_desc &d, cudaStream_t st) {
+  // bodies that evaluate row-scalar inputs once per lane assume a lane's
+  // points share a row: the 16-byte (vec4) paths; anything else runs the
+  // evaluator
+  if constexpr (UNIFORM) {
+    if (!(std::is_same<T, float>::value && V == 4 && m2_vec4_ok(d))) return launch_map2<T, V, VmBody, MODE>(d, st);
+  }
   const int nd = d.ndim;
   const int64_t E = d.ext[nd - 1];
   int64_t rows = 1;

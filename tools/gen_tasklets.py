@@ -42,7 +42,7 @@ UN = {L.OP_NEG: "GFB_OP_NEG", L.OP_SIN: "GFB_OP_SIN", L.OP_COS: "GFB_OP_COS", L.
       L.OP_SIGN: "GFB_OP_SIGN"}
 
 
-def m2_key(mode, f64, n_in, segs, words) -> int:
+def m2_key(mode, f64, n_in, segs, words, umask=0) -> int:
     """FNV-1a, byte-identical to gfb::m2_key (csrc/map2.cu)."""
     h = 1469598103934665603
     mask = (1 << 64) - 1
@@ -63,12 +63,26 @@ def m2_key(mode, f64, n_in, segs, words) -> int:
         mix(n)
         for pc in range(start, start + n):
             mix(words[pc])
+    if umask:
+        mix(0x55000000 | umask)
     return h
+
+
+def uniform_mask(op: Map2Op) -> int:
+    """Inputs constant along the innermost loop dimension (gfb::m2_uniform_mask)."""
+    if op.compute_f64 or not op.ext:
+        return 0
+    m = 0
+    for k, (_b, _c0, st) in enumerate(op.ins[:32]):
+        if int(st[len(op.ext) - 1]) == 0:
+            m |= 1 << k
+    return m
 
 
 def signature(op: Map2Op):
     f64 = 1 if op.compute_f64 else 0
-    return (op.mode, f64, len(op.ins), tuple(op.segs), tuple(op.code_words[:max(s + n for s, n in op.segs)]))
+    return (op.mode, f64, len(op.ins), tuple(op.segs), tuple(op.code_words[:max(s + n for s, n in op.segs)]),
+            uniform_mask(op))
 
 
 def collect():
@@ -107,27 +121,83 @@ def collect():
     return sorted(sigs)
 
 
-def body_code(words, segs) -> str:
+def body_code(words, segs, umask=0) -> str:
+    """Straight-line body of each output's stack code. With a uniform mask
+    (row-scalar inputs) stack slots computed only from uniform inputs and
+    constants stay one-element arrays (u*): evaluated once per lane, broadcast
+    when they meet a per-point slot (s*)."""
     lines = []
     for o, (start, n) in enumerate(segs):
-        depth, maxd, stmts = 0, 0, []
+        stack, stmts, maxd, maxu = [], [], 0, 0
+
+        def push(scalar):
+            nonlocal maxd, maxu
+            depth = len(stack)
+            name = f"u{depth}" if scalar else f"s{depth}"
+            stack.append((name, scalar))
+            if scalar:
+                maxu = max(maxu, depth + 1)
+            else:
+                maxd = max(maxd, depth + 1)
+            return name
+
+        def as_vec(slot, depth):
+            name, scalar = slot
+            if not scalar:
+                return name
+            vec = f"s{depth}"
+            stmts.append(f"m2_fill<T, V>({vec}, {name}[0]);")
+            return vec
+
         for pc in range(start, start + n):
             w = words[pc]
             op, arg = w & 63, w >> 10
             if op == L.OP_IN:
-                stmts.append(f"fetch({arg}, s{depth});")
-                depth += 1
+                if (umask >> arg) & 1:
+                    nm = push(True)
+                    stmts.append(f"{{ T t_[V]; fetch({arg}, t_); {nm}[0] = t_[0]; }}")
+                else:
+                    nm = push(False)
+                    stmts.append(f"fetch({arg}, {nm});")
             elif op == L.OP_CONST:
-                stmts.append(f"m2_fill<T, V>(s{depth}, (T)d.consts[{arg}]);")
-                depth += 1
+                nm = push(bool(umask))
+                if umask:
+                    stmts.append(f"{nm}[0] = (T)d.consts[{arg}];")
+                else:
+                    stmts.append(f"m2_fill<T, V>({nm}, (T)d.consts[{arg}]);")
             elif op in UN:
-                stmts.append(f"m2_unary<T, V>({UN[op]}, s{depth - 1}, vm, bad);")
+                name, scalar = stack[-1]
+                if scalar:
+                    stmts.append(f"m2_unary<T, 1>({UN[op]}, {name}, vm ? 1u : 0u, bad);")
+                else:
+                    stmts.append(f"m2_unary<T, V>({UN[op]}, {name}, vm, bad);")
             else:
-                stmts.append(f"m2_binary<T, V>({BIN[op]}, s{depth - 2}, s{depth - 1}, vm, bad);")
-                depth -= 1
-            maxd = max(maxd, depth)
-        decl = "T " + ", ".join(f"s{i}[V]" for i in range(maxd)) + ";"
-        body = " ".join([decl] + stmts + ["m2_copy<T, V>(r, s0);"])
+                b = stack.pop()
+                a = stack.pop()
+                depth = len(stack)
+                if a[1] and b[1]:
+                    nm = push(True)
+                    if a[0] != nm:
+                        stmts.append(f"{nm}[0] = {a[0]}[0];")
+                    stmts.append(f"m2_binary<T, 1>({BIN[op]}, {nm}, {b[0]}, vm ? 1u : 0u, bad);")
+                else:
+                    # destination slot s{depth}; the right operand goes to s{depth + 1}
+                    bv = as_vec(b, depth + 1) if b[1] else b[0]
+                    if a[1]:
+                        stmts.append(f"m2_fill<T, V>(s{depth}, {a[0]}[0]);")
+                    elif a[0] != f"s{depth}":
+                        stmts.append(f"m2_copy<T, V>(s{depth}, {a[0]});")
+                    maxd = max(maxd, depth + 2)
+                    stmts.append(f"m2_binary<T, V>({BIN[op]}, s{depth}, {bv}, vm, bad);")
+                    stack.append((f"s{depth}", False))
+        res, rs = stack[-1]
+        decl = []
+        if maxd:
+            decl.append("T " + ", ".join(f"s{i}[V]" for i in range(maxd)) + ";")
+        if maxu:
+            decl.append("T " + ", ".join(f"u{i}[1]" for i in range(maxu)) + ";")
+        tail = f"m2_fill<T, V>(r, {res}[0]);" if rs else f"m2_copy<T, V>(r, {res});"
+        body = " ".join(decl + stmts + [tail])
         lines.append(f"    {'if' if o == 0 else 'else if'} (o == {o}) {{ {body} }}")
     return "\n".join(lines)
 
@@ -155,21 +225,22 @@ def generate() -> str:
         "",
     ]
     table = []
-    for i, (mode, f64, n_in, segs, words) in enumerate(sigs):
-        key = m2_key(mode, f64, n_in, segs, words)
+    for i, (mode, f64, n_in, segs, words, umask) in enumerate(sigs):
+        key = m2_key(mode, f64, n_in, segs, words, umask)
         T, V = ("double", 2) if f64 else ("float", 4)
         out += [
-            f"struct GenBody{i} {{  // mode {mode}, {'fp64' if f64 else 'fp32'}, {n_in} inputs, {len(segs)} outputs",
+            f"struct GenBody{i} {{  // mode {mode}, {'fp64' if f64 else 'fp32'}, {n_in} inputs, {len(segs)} outputs"
+            + (f", row-scalar inputs 0x{umask:x}" if umask else ""),
             "  template <typename T, int V, typename F>",
             "  static __device__ __forceinline__ void eval(const gfb_map2_desc &d, int o, F &fetch, uint32_t vm,",
             "                                              T (&r)[V]) {",
             "    uint32_t bad = 0;",
-            body_code(words, segs),
+            body_code(words, segs, umask),
             "    if (bad) raise_bits(d.err, bad);",
             "  }",
             "};",
             f"static int gen_launch{i}(const gfb_map2_desc &d, cudaStream_t st) {{",
-            f"  return launch_map2<{T}, {V}, GenBody{i}, {mode}>(d, st);",
+            f"  return launch_map2<{T}, {V}, GenBody{i}, {mode}{', true' if umask else ''}>(d, st);",
             "}",
             "",
         ]
