@@ -405,16 +405,34 @@ __global__ void __launch_bounds__(256) map2_reduce_outer_kernel(const __grid_con
 }
 
 template <typename T>
-__global__ void map2_finish_kernel(const __grid_constant__ gfb_map2_desc d) {
+__global__ void __launch_bounds__(1024) map2_finish_kernel(const __grid_constant__ gfb_map2_desc d) {
+  // 32 columns x 32 split groups per CTA: group g sums splits g, g + 32, ...
+  // (a few L2 round trips per thread instead of nsplit), then the groups are
+  // added in order (deterministic)
+  __shared__ double red[32][33];
   const int32_t E = (int32_t)d.ext[1];
-  for (int32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < E; i += gridDim.x * blockDim.x) {
-    double sum = 0.0;
-    for (int s = 0; s < d.nsplit; ++s) sum += ((const double *)d.workspace)[(int64_t)s * E + i];
-    const gfb_m2_operand &wo = d.out[0];
-    const int32_t off = (int32_t)wo.c0 + (int32_t)wo.s[1] * i;
-    const bool inside = i >= d.clear_lo[1] && i < d.clear_hi[1];
-    store_as<T>(const_cast<void *>(wo.base), wo.dtype, off, m2_base<T>(d, inside, off) + (T)sum);
+  const int lane = threadIdx.x & 31, g = threadIdx.x >> 5;
+  const int32_t i = blockIdx.x * 32 + lane;
+  const double *ws = (const double *)d.workspace;
+  double s4[4] = {0.0, 0.0, 0.0, 0.0};
+  if (i < E) {
+    int s = g;
+    for (; s + 96 < d.nsplit; s += 128) {
+#pragma unroll
+      for (int u = 0; u < 4; ++u) s4[u] += ws[(int64_t)(s + 32 * u) * E + i];
+    }
+    for (; s < d.nsplit; s += 32) s4[0] += ws[(int64_t)s * E + i];
   }
+  red[g][lane] = (s4[0] + s4[1]) + (s4[2] + s4[3]);
+  __syncthreads();
+  if (g != 0 || i >= E) return;
+  double sum = 0.0;
+#pragma unroll
+  for (int q = 0; q < 32; ++q) sum += red[q][lane];
+  const gfb_m2_operand &wo = d.out[0];
+  const int32_t off = (int32_t)wo.c0 + (int32_t)wo.s[1] * i;
+  const bool inside = i >= d.clear_lo[1] && i < d.clear_hi[1];
+  store_as<T>(const_cast<void *>(wo.base), wo.dtype, off, m2_base<T>(d, inside, off) + (T)sum);
 }
 
 // 16-byte variant (fp32, two loop dimensions, inner strides 0 or 1, host-
@@ -785,8 +803,7 @@ inline int launch_map2(const gfb_map2_desc &d, cudaStream_t st) {
           dim3 grid((unsigned)ceil_div(E, 128), (unsigned)d.nsplit);
           map2_reduce_outer_vec4_kernel<Body><<<grid, 256, 0, st>>>(d, qpr);
           if (d.nsplit > 1) {
-            const unsigned blocks = (unsigned)std::min<int64_t>(ceil_div(E, 256), cap);
-            map2_finish_kernel<T><<<blocks, 256, 0, st>>>(d);
+            map2_finish_kernel<T><<<(unsigned)ceil_div(E, 32), 1024, 0, st>>>(d);
           }
           return check_launch("map2");
         }
@@ -824,8 +841,7 @@ inline int launch_map2(const gfb_map2_desc &d, cudaStream_t st) {
       dim3 grid((unsigned)ceil_div(E, 32), (unsigned)d.nsplit);
       map2_reduce_outer_kernel<T, V, Body><<<grid, 256, 0, st>>>(d);
       if (d.nsplit > 1) {
-        const unsigned blocks = (unsigned)std::min<int64_t>(ceil_div(E, 256), cap);
-        map2_finish_kernel<T><<<blocks, 256, 0, st>>>(d);
+        map2_finish_kernel<T><<<(unsigned)ceil_div(E, 32), 1024, 0, st>>>(d);
       }
     }
   }

@@ -1092,8 +1092,11 @@ def map2_reduce(space, acc, ins, dst, ybox, clear_mode, cbox, code, seg, compute
         return None
     nsplit = 1
     if mode == 2:
-        chunks = -(-ext[1] // 32)
-        nsplit = int(max(1, min(-(-2 * 148 // chunks), ext[0] // 64, 4096)))
+        # column blocks of the launch (128 columns each, csrc/map2_kernels.cuh);
+        # row splits fill eight 256-thread CTAs per SM (the finish pass adds
+        # the split partials in 32 parallel groups)
+        chunks = -(-ext[1] // 128)
+        nsplit = int(max(1, min(-(-8 * 148 // chunks), ext[0] // 64, 4096)))
     n_in = len(ins)
     op = Map2Op(mode, ext, [(a.buf, c0, st) for a, (c0, st) in zip(ins, ops[:n_in])],
                 [(dst, ops[n_in][0], ops[n_in][1], 0)], code, [seg], compute_f64, clear_mode=clear_mode,
