@@ -1570,6 +1570,7 @@ class Lowering:
         if os.environ.get("GFB_FUSE_MV", "1") != "0":
             self._fuse_matvec_pairs()
             self._fuse_rank2()
+        self._stencil_copies()
         self._elide_copies()
 
     def resolve(self, buf: Buffer) -> Buffer:
@@ -1668,6 +1669,24 @@ class Lowering:
                 full = op.dead is None or box_contains(op.a.region, op.dead)
                 if xout is not X and full:
                     synced.add((frozenset((X.bid, xout.bid)), tuple(op.a.region)))
+
+    def _stencil_copies(self):
+        """A one-tap identity sweep over the whole array that overwrites its
+        target (the adjoint of `h = z + b` into a fresh z__grad) is a copy;
+        as a CopyOp it can become an alias (_elide_copies) instead of a launch."""
+        for i, op in enumerate(self.ops):
+            if not (isinstance(op, StencilOp) and len(op.taps) == 1):
+                continue
+            whole = whole_box(op.dst.shape)
+            overwrite = op.clear_mode in (1, 3) or (op.clear_mode == 2 and op.clear_box is not None
+                                                    and box_contains(op.clear_box, whole))
+            if not overwrite:
+                continue
+            si, coef, delta, mask = op.taps[0]
+            src = op.srcs[si]
+            if (coef == 1.0 and mask is None and not any(delta) and src is not op.dst and src.shape == op.dst.shape
+                    and src.kind == op.dst.kind and box_contains(op.region, whole)):
+                self.ops[i] = CopyOp(op.dst, src)
 
     def _fuse_matvec_pairs(self):
         """Pair a row-dot and a column-sum matmul node over the same matrix
