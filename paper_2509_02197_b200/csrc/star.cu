@@ -13,6 +13,7 @@
 // Positions: 0 centre, 1 (-1,0,0), 2 (+1,0,0), 3 (0,-1,0), 4 (0,+1,0),
 // 5 (0,0,-1), 6 (0,0,+1) on a row-major [d0][d1][d2] array (rank 2 arrays
 // are padded with d0 = 1).
+#include <cstdlib>
 #include "gfb_internal.h"
 #include "star_common.cuh"
 
@@ -266,8 +267,14 @@ __global__ void __launch_bounds__(kPX *kPY, 2) star_pair_kernel(const __grid_con
                                 rel0, rel1, zrel, ca, cb);
 }
 
+namespace tile32 {
 bool star_tma_usable(const StarPairDev &d, int dtype);
 int launch_star_pair_tma(const StarPairDev &d, int dtype, dim3 grid, cudaStream_t st);
+}  // namespace tile32
+namespace small {
+bool star_tma_usable(const StarPairDev &d, int dtype);
+int launch_star_pair_tma(const StarPairDev &d, int dtype, dim3 grid, cudaStream_t st);
+}  // namespace small
 
 static int fill_star_op(StarOpDev &o, const gfb_star_op &s, int pad) {
   o.present = s.present;
@@ -368,8 +375,13 @@ extern "C" int gfb_star_pair_launch(const gfb_star_pair_desc *s, void *stream) {
   dim3 grid((unsigned)ceil_div(d.d2, kPX), (unsigned)ceil_div(d.d1, kPY), (unsigned)ceil_div(d.zhi - d.zlo, kPM));
   cudaStream_t st = (cudaStream_t)stream;
   // the TMA kernel runs masks as data (source-mask form); general masks use the L1 kernel
-  if (d.a.srcmask >= 0 && d.b.srcmask >= 0 && star_tma_usable(d, s->dtype))
-    return launch_star_pair_tma(d, s->dtype, grid, st);
+  if (d.a.srcmask >= 0 && d.b.srcmask >= 0) {
+    // small 2-D domains (fewer 32 x 32 tiles than SMs): half-height tiles
+    const bool small2d = d.d0 == 1 && ceil_div(d.d1, 32) * ceil_div(d.d2, 32) < sm_count() &&
+                         getenv("GFB_STAR_NO_SMALL") == nullptr;
+    if (small2d && small::star_tma_usable(d, s->dtype)) return small::launch_star_pair_tma(d, s->dtype, grid, st);
+    if (tile32::star_tma_usable(d, s->dtype)) return tile32::launch_star_pair_tma(d, s->dtype, grid, st);
+  }
   if (s->dtype == GFB_F64)
     launch_pdl(star_pair_kernel<double>, grid, block, 0, st, d);
   else

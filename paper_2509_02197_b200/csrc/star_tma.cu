@@ -32,7 +32,15 @@
 #include "gfb_internal.h"
 #include "star_common.cuh"
 
+// Compiled twice (Makefile): the default 32 x 32 tile, and a 32 x 16 tile
+// with two rows per thread (namespace small) for small 2-D domains whose
+// launches are short latency chains (C1 jacobi_2d 200^2: 49 CTAs -> 98)
+#ifndef GFB_STAR_NS
+#define GFB_STAR_NS tile32
+#endif
+
 namespace gfb {
+namespace GFB_STAR_NS {
 
 #ifndef GFB_STAR_TPY
 #define GFB_STAR_TPY 32
@@ -573,4 +581,5 @@ int launch_star_pair_tma(const StarPairDev &d, int dtype, dim3, cudaStream_t st)
   return dtype == GFB_F64 ? launch_tma<double>(map, d, st) : launch_tma<float>(map, d, st);
 }
 
+}  // namespace GFB_STAR_NS
 }  // namespace gfb
