@@ -59,8 +59,17 @@ def _run_rank(rank, world, port, params, q):
             o = b.root_offset()
             return torch.from_numpy(t[o:o + b.numel].reshape(b.shape) if b.shape else t[o:o + 1].reshape(()))
 
+        # halo exchanges through their precomputed point-to-point lists (the
+        # path the engine launches), once the views are known
+        rt.view = view
         for op in dl.low.ops:
-            if isinstance(op, (HaloOp, AllReduceOp)):
+            if isinstance(op, HaloOp):
+                op.prepare(rt)
+        for op in dl.low.ops:
+            if isinstance(op, HaloOp):
+                assert op._ops is not None
+                op.launch(rt, None)
+            elif isinstance(op, AllReduceOp):
                 op.run(view)
             else:
                 em.run_op(op)
