@@ -411,7 +411,10 @@ __global__ void __launch_bounds__(kTcThreads, 1)
   const int m0 = blockIdx.y * kTcM, n0 = blockIdx.x * BN;
   const int kb = blockIdx.z * kchunk, ke = min(kb + kchunk, K);
   const int nslab = ke > kb ? (ke - kb + kTcK - 1) / kTcK : 0;
-  constexpr int kCols = BN < 32 ? 32 : BN;
+  // TMEM: columns [0, BN) accumulate A_hi B_hi + A_lo B_hi, [BN, 2 BN) A_hi B_lo
+  // (one N = 2 BN MMA over the adjacent hi | lo rows of B): two MMAs per
+  // k-step instead of three, a third less shared-memory operand traffic
+  constexpr int kCols = 2 * BN < 32 ? 32 : 2 * BN;
   // stage layout (byte offsets): rawA | hiA (MN-major only) | loA | rawB | hiB | loB
   constexpr int oRawA = 0, oHiA = AKM ? 0 : Cfg::kRawA, oLoA = AKM ? Cfg::kRawA : 2 * Cfg::kRawA;
   constexpr int oRawB = oLoA + Cfg::kRawA, oHiB = BKM ? oRawB : oRawB + Cfg::kRawB;
@@ -457,6 +460,8 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     }
   } else if (warp == 1) {
     if (lane == 0) {  // MMA issuer
+      const uint32_t idesc2 = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)((2 * BN) >> 3) << 17) |
+                              ((uint32_t)(kTcM >> 4) << 24);
       const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(BN >> 3) << 17) |
                              ((uint32_t)(kTcM >> 4) << 24);
       for (int t = 0; t < nslab; ++t) {
@@ -469,8 +474,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
         for (int ks = 0; ks < kTcK / 8; ++ks) {
           const uint32_t off = ks * 32;
           const int acc = (t > 0 || ks > 0) ? 1 : 0;
-          tc_mma(tmem, umma_desc_sw128(ah + off), umma_desc_sw128(bh + off), idesc, acc);
-          tc_mma(tmem, umma_desc_sw128(ah + off), umma_desc_sw128(bl + off), idesc, 1);
+          tc_mma(tmem, umma_desc_sw128(ah + off), umma_desc_sw128(bh + off), idesc2, acc);  // [B_hi | B_lo]
           tc_mma(tmem, umma_desc_sw128(al + off), umma_desc_sw128(bh + off), idesc, 1);
         }
         tc_commit(&empty[s]);
@@ -502,7 +506,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
   constexpr int kGrp = kHalf < 32 ? kHalf : 32;
 #pragma unroll 1
   for (int c0 = half * kHalf; c0 < (half + 1) * kHalf && c0 < BN; c0 += kGrp) {
-    uint32_t v[kGrp];
+    uint32_t v[kGrp], v2[kGrp];
 #pragma unroll
     for (int g = 0; g < kGrp; g += 8) {
       const uint32_t taddr = tmem + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(c0 + g);
@@ -510,8 +514,14 @@ __global__ void __launch_bounds__(kTcThreads, 1)
                    : "=r"(v[g]), "=r"(v[g + 1]), "=r"(v[g + 2]), "=r"(v[g + 3]), "=r"(v[g + 4]), "=r"(v[g + 5]),
                      "=r"(v[g + 6]), "=r"(v[g + 7])
                    : "r"(taddr));
+      asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+                   : "=r"(v2[g]), "=r"(v2[g + 1]), "=r"(v2[g + 2]), "=r"(v2[g + 3]), "=r"(v2[g + 4]),
+                     "=r"(v2[g + 5]), "=r"(v2[g + 6]), "=r"(v2[g + 7])
+                   : "r"(taddr + (uint32_t)BN));
     }
     asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+    for (int j = 0; j < kGrp; ++j) v[j] = __float_as_uint(__uint_as_float(v[j]) + __uint_as_float(v2[j]));
     if (csn == 1 && !partial) {
       float *scr = reinterpret_cast<float *>(base) + warp * (32 * (kGrp + 1));
 #pragma unroll
