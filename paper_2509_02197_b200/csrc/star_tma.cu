@@ -122,10 +122,6 @@ template <typename T>
 __host__ __device__ constexpr int yslot() {
   return (int)(((size_t)YJ * ypitch<T>() * sizeof(T) + 127) / 128 * 128 / sizeof(T));
 }
-template <typename T>
-__host__ __device__ constexpr size_t star_tma_smem_bytes() {
-  return (size_t)NSY * yslot<T>() * sizeof(T) + (size_t)NXS * XS * sizeof(T) + NSY * sizeof(uint64_t);
-}
 
 template <typename T>
 __device__ __forceinline__ T coef(const StarOpDev &o, int p);
@@ -507,14 +503,23 @@ __device__ __forceinline__ void star_tma_body(const CUtensorMap *ymap, const Sta
 #endif
 }
 
-template <typename T>
-__global__ void __launch_bounds__(tThreads, 512 / tThreads)
+// 2-D arrays (d0 == 1, HAS_I false) march a single plane: one Y slot and one
+// X~ slot, a kernel of its own (its own register allocation) so more CTAs
+// fit an SM and short launches are one wave
+template <typename T, bool HAS_I>
+__host__ __device__ constexpr size_t star_tma_dyn_bytes() {
+  return (size_t)(HAS_I ? NSY : 1) * yslot<T>() * sizeof(T) + (size_t)(HAS_I ? NXS : 1) * XS * sizeof(T) +
+         NSY * sizeof(uint64_t);
+}
+
+template <typename T, bool HAS_I>
+__global__ void __launch_bounds__(tThreads, HAS_I ? 512 / tThreads : 768 / tThreads)
     star_pair_tma_kernel(const __grid_constant__ CUtensorMap ymap, const __grid_constant__ StarPairDev d) {
   extern __shared__ __align__(128) unsigned char smem[];
-  constexpr size_t ybytes = (size_t)NSY * yslot<T>() * sizeof(T);
+  constexpr size_t ybytes = (size_t)(HAS_I ? NSY : 1) * yslot<T>() * sizeof(T);
   T *ys = reinterpret_cast<T *>(smem);
   T *xs = reinterpret_cast<T *>(smem + ybytes);
-  uint64_t *mbar = reinterpret_cast<uint64_t *>(smem + ybytes + (size_t)NXS * XS * sizeof(T));
+  uint64_t *mbar = reinterpret_cast<uint64_t *>(smem + ybytes + (size_t)(HAS_I ? NXS : 1) * XS * sizeof(T));
   __shared__ TmaWords words;
   __shared__ T xst[2][kR + 1][tThreads];  // staged old X values (fix-up points), by plane parity
   const int tid = threadIdx.y * tPX + threadIdx.x;
@@ -522,10 +527,7 @@ __global__ void __launch_bounds__(tThreads, 512 / tThreads)
   tma_prologue(d, i0, blockIdx.y * tPY, blockIdx.x * tPX, tid, words);  // descriptor only
   pdl_wait();
   pdl_trigger();  // after the wait: at most one launch waits ahead of the running one
-  if (d.d0 > 1)
-    star_tma_body<T, true>(&ymap, d, ys, xs, mbar, words, xst, i0, i1);
-  else
-    star_tma_body<T, false>(&ymap, d, ys, xs, mbar, words, xst, i0, i1);
+  star_tma_body<T, HAS_I>(&ymap, d, ys, xs, mbar, words, xst, i0, i1);
 }
 
 static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
@@ -546,12 +548,12 @@ bool star_tma_usable(const StarPairDev &d, int dtype) {
          getenv("GFB_NO_TMA") == nullptr;
 }
 
-template <typename T>
+template <typename T, bool HAS_I>
 static int launch_tma(const CUtensorMap &map, const StarPairDev &d, cudaStream_t st) {
   static bool attr = false;
-  const size_t sm = star_tma_smem_bytes<T>();
+  const size_t sm = star_tma_dyn_bytes<T, HAS_I>();
   if (!attr) {
-    cudaFuncSetAttribute(star_pair_tma_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    cudaFuncSetAttribute(star_pair_tma_kernel<T, HAS_I>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     attr = true;
   }
   // planes per CTA: the longest march (up to tPM) that still puts every
@@ -562,7 +564,7 @@ static int launch_tma(const CUtensorMap &map, const StarPairDev &d, cudaStream_t
   const int64_t slots = 2 * (int64_t)sm_count();
   dd.tpm = (int32_t)std::max<int64_t>(2, std::min<int64_t>(tPM, ceil_div(planes * tiles, slots)));
   dim3 grid((unsigned)ceil_div(d.d2, tPX), (unsigned)ceil_div(d.d1, tPY), (unsigned)ceil_div(planes, dd.tpm));
-  launch_pdl(star_pair_tma_kernel<T>, grid, dim3(tPX, tPY / kR), sm, st, map, dd);
+  launch_pdl(star_pair_tma_kernel<T, HAS_I>, grid, dim3(tPX, tPY / kR), sm, st, map, dd);
   return check_launch("star_pair_tma");
 }
 
@@ -578,7 +580,8 @@ int launch_star_pair_tma(const StarPairDev &d, int dtype, dim3, cudaStream_t st)
                            CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return set_error(GFB_ECUDA, "cuTensorMapEncodeTiled failed for the star-pair source");
-  return dtype == GFB_F64 ? launch_tma<double>(map, d, st) : launch_tma<float>(map, d, st);
+  if (d.d0 > 1) return dtype == GFB_F64 ? launch_tma<double, true>(map, d, st) : launch_tma<float, true>(map, d, st);
+  return dtype == GFB_F64 ? launch_tma<double, false>(map, d, st) : launch_tma<float, false>(map, d, st);
 }
 
 }  // namespace GFB_STAR_NS
