@@ -336,12 +336,14 @@ __global__ void __launch_bounds__(kTcThreads, 1)
 // mlp shapes are HBM-bound).
 constexpr int kTmaSplitWarps = 6;
 
-template <int BN, bool AKM, bool BKM>
+template <int BN, bool AKM, bool BKM, bool SK = false>
 struct TmaCfg {
   static constexpr int kRawA = kTcM * kTcK * 4, kRawB = BN * kTcK * 4;  // bytes
   // per stage: raw A (= hi A when K-major), [hi A], lo A, raw B, [hi B], lo B
   static constexpr int kStage = kRawA * (AKM ? 2 : 3) + kRawB * (BKM ? 2 : 3);
-  static constexpr int kStages = (200 * 1024) / kStage > 4 ? 4 : (200 * 1024) / kStage;
+  // SK (short k: at most two slabs per CTA): one stage, so several CTAs
+  // share an SM and one CTA's epilogue overlaps another's loads
+  static constexpr int kStages = SK ? 1 : ((200 * 1024) / kStage > 4 ? 4 : (200 * 1024) / kStage);
   static constexpr int kSmem = kStages * kStage + 1024 /* align */ + 256 /* barriers */;
 };
 
@@ -396,11 +398,11 @@ __device__ __forceinline__ void split_slab(uint32_t raw, uint32_t hi, uint32_t l
   }
 }
 
-template <int BN, bool AKM, bool BKM>
+template <int BN, bool AKM, bool BKM, bool SK>
 __global__ void __launch_bounds__(kTcThreads, 1)
     sgemm_tma_kernel(const __grid_constant__ CUtensorMap amap, const __grid_constant__ CUtensorMap bmap, int M,
                      int N, int K, float *C, int64_t csm, int64_t csn, int accumulate, float *partial, int kchunk) {
-  using Cfg = TmaCfg<BN, AKM, BKM>;
+  using Cfg = TmaCfg<BN, AKM, BKM, SK>;
   constexpr int S = Cfg::kStages;
   extern __shared__ __align__(1024) unsigned char tm_raw[];
   unsigned char *base = reinterpret_cast<unsigned char *>((reinterpret_cast<uintptr_t>(tm_raw) + 1023) & ~(uintptr_t)1023);
@@ -591,23 +593,36 @@ static bool tc_map(CUtensorMap *map, const float *p, int64_t inner, int64_t oute
                         CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-template <int BN, bool AKM, bool BKM>
-static int launch_tma(dim3 grid, int M, int N, int K, const float *A, int64_t lda, const float *B, int64_t ldb,
+template <int BN, bool AKM, bool BKM, bool SK>
+static int launch_tma_k(dim3 grid, int M, int N, int K, const float *A, int64_t lda, const float *B, int64_t ldb,
                       float *C, int64_t csm, int64_t csn, int accumulate, float *partial, int kchunk,
                       cudaStream_t st) {
   CUtensorMap am, bm;
   const bool ok = (AKM ? tc_map(&am, A, K, M, lda, kTcK, kTcM, true) : tc_map(&am, A, M, K, lda, kTcM, kTcK, false)) &&
                   (BKM ? tc_map(&bm, B, K, N, ldb, kTcK, BN, true) : tc_map(&bm, B, N, K, ldb, BN, kTcK, false));
   if (!ok) return -1;
-  constexpr int smem = TmaCfg<BN, AKM, BKM>::kSmem;
+  constexpr int smem = TmaCfg<BN, AKM, BKM, SK>::kSmem;
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(sgemm_tma_kernel<BN, AKM, BKM>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaFuncSetAttribute(sgemm_tma_kernel<BN, AKM, BKM, SK>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     attr = true;
   }
-  sgemm_tma_kernel<BN, AKM, BKM><<<grid, kTcThreads, smem, st>>>(am, bm, M, N, K, C, csm, csn, accumulate, partial,
+  sgemm_tma_kernel<BN, AKM, BKM, SK><<<grid, kTcThreads, smem, st>>>(am, bm, M, N, K, C, csm, csn, accumulate, partial,
                                                                  kchunk);
   return 0;
+}
+
+template <int BN, bool AKM, bool BKM>
+static int launch_tma(dim3 grid, int M, int N, int K, const float *A, int64_t lda, const float *B, int64_t ldb,
+                      float *C, int64_t csm, int64_t csn, int accumulate, float *partial, int kchunk,
+                      cudaStream_t st) {
+  static const bool no_sk = getenv("GFB_TMA_NO_SK") != nullptr;
+  // short k and more tiles than SMs (one-stage CTAs then share SMs)
+  if (!no_sk && kchunk <= 2 * kTcK && (int64_t)grid.x * grid.y * grid.z > (int64_t)sm_count())
+    return launch_tma_k<BN, AKM, BKM, true>(grid, M, N, K, A, lda, B, ldb, C, csm, csn, accumulate, partial, kchunk,
+                                            st);
+  return launch_tma_k<BN, AKM, BKM, false>(grid, M, N, K, A, lda, B, ldb, C, csm, csn, accumulate, partial, kchunk,
+                                           st);
 }
 
 template <int BN>
