@@ -242,7 +242,10 @@ __global__ void __launch_bounds__((BM / TM) * (BN / TN))
 // before slab t is multiplied, so their latency hides behind the FMAs; one
 // barrier per slab (slab and k-table buffers alternate); TM x TN register
 // tiles read with 16-byte shared-memory loads.
-template <typename T, int BM, int BN, int BK, int TM, int TN>
+// AQK: A staged as 16-byte quads along k (convolution forward and input
+// adjoint), fixed at compile time so the staging code carries no layout
+// branches; otherwise the layout flags are read from the descriptor
+template <typename T, int BM, int BN, int BK, int TM, int TN, bool AQK = false>
 __global__ void __launch_bounds__((BM / TM) * (BN / TN), (BM / TM) * (BN / TN) >= 256 ? 2 : 4)
     contract2_kernel(const __grid_constant__ gfb_contract_desc d) {
   constexpr int NX = BN / TN, NY = BM / TM, NT = NX * NY;
@@ -265,9 +268,9 @@ __global__ void __launch_bounds__((BM / TM) * (BN / TN), (BM / TM) * (BN / TN) >
   const int nslab = (int)((ke - kb + BK - 1) / BK);
   const T *__restrict__ Ag = (const T *)d.a;
   const T *__restrict__ Bg = (const T *)d.b;
-  const bool akf = d.a_kfast & 1, bnf = d.b_nfast & 1;
-  const bool aq = sizeof(T) == 4 && (d.a_kfast & 2) && (reinterpret_cast<uintptr_t>(Ag) & 15) == 0 &&
-                  EA % 4 == 0;
+  const bool akf = AQK || (d.a_kfast & 1), bnf = d.b_nfast & 1;
+  const bool aq = AQK || (sizeof(T) == 4 && (d.a_kfast & 2) && (reinterpret_cast<uintptr_t>(Ag) & 15) == 0 &&
+                          EA % 4 == 0);
   const bool bq = sizeof(T) == 4 && (d.b_nfast & 2) && (reinterpret_cast<uintptr_t>(Bg) & 15) == 0 &&
                   EB % 4 == 0;
 
@@ -603,7 +606,15 @@ static void launch_contract(const gfb_contract_desc &d, cudaStream_t st) {
 template <typename T, int BM, int BN, int TM, int TN, int BK = 16>
 static void launch_contract2(const gfb_contract_desc &d, cudaStream_t st) {
   dim3 grid((unsigned)ceil_div(d.M, BM), (unsigned)ceil_div(d.N, BN), (unsigned)d.nsplit);
-  contract2_kernel<T, BM, BN, BK, TM, TN><<<grid, (BM / TM) * (BN / TN), 0, st>>>(d);
+  constexpr int NT = (BM / TM) * (BN / TN);
+  constexpr bool kQuadTile = sizeof(T) == 4 && (BM * BK / NT) % 4 == 0;
+  if constexpr (kQuadTile) {
+    if ((d.a_kfast & 3) == 3 && (reinterpret_cast<uintptr_t>(d.a) & 15) == 0) {
+      contract2_kernel<T, BM, BN, BK, TM, TN, true><<<grid, NT, 0, st>>>(d);
+      return;
+    }
+  }
+  contract2_kernel<T, BM, BN, BK, TM, TN, false><<<grid, NT, 0, st>>>(d);
 }
 
 template <typename T>
