@@ -242,10 +242,11 @@ __global__ void __launch_bounds__((BM / TM) * (BN / TN))
 // before slab t is multiplied, so their latency hides behind the FMAs; one
 // barrier per slab (slab and k-table buffers alternate); TM x TN register
 // tiles read with 16-byte shared-memory loads.
-// AQK: A staged as 16-byte quads along k (convolution forward and input
-// adjoint), fixed at compile time so the staging code carries no layout
-// branches; otherwise the layout flags are read from the descriptor
-template <typename T, int BM, int BN, int BK, int TM, int TN, bool AQK = false>
+// LAYOUT fixes the staging layout at compile time so the staging code carries
+// no layout branches: 1 = A quads along k (convolution forward and input
+// adjoint), 2 = A quads along m and B quads along n (weight adjoint); 0 reads
+// the layout flags from the descriptor
+template <typename T, int BM, int BN, int BK, int TM, int TN, int LAYOUT = 0>
 __global__ void __launch_bounds__((BM / TM) * (BN / TN), (BM / TM) * (BN / TN) >= 256 ? 2 : 4)
     contract2_kernel(const __grid_constant__ gfb_contract_desc d) {
   constexpr int NX = BN / TN, NY = BM / TM, NT = NX * NY;
@@ -268,11 +269,12 @@ __global__ void __launch_bounds__((BM / TM) * (BN / TN), (BM / TM) * (BN / TN) >
   const int nslab = (int)((ke - kb + BK - 1) / BK);
   const T *__restrict__ Ag = (const T *)d.a;
   const T *__restrict__ Bg = (const T *)d.b;
-  const bool akf = AQK || (d.a_kfast & 1), bnf = d.b_nfast & 1;
-  const bool aq = AQK || (sizeof(T) == 4 && (d.a_kfast & 2) && (reinterpret_cast<uintptr_t>(Ag) & 15) == 0 &&
-                          EA % 4 == 0);
-  const bool bq = sizeof(T) == 4 && (d.b_nfast & 2) && (reinterpret_cast<uintptr_t>(Bg) & 15) == 0 &&
-                  EB % 4 == 0;
+  const bool akf = LAYOUT == 1 ? true : (LAYOUT == 2 ? false : (d.a_kfast & 1) != 0);
+  const bool bnf = LAYOUT == 2 ? true : (d.b_nfast & 1) != 0;
+  const bool aq = LAYOUT != 0 || (sizeof(T) == 4 && (d.a_kfast & 2) && (reinterpret_cast<uintptr_t>(Ag) & 15) == 0 &&
+                                  EA % 4 == 0);
+  const bool bq = LAYOUT == 2 || (sizeof(T) == 4 && (d.b_nfast & 2) && (reinterpret_cast<uintptr_t>(Bg) & 15) == 0 &&
+                                  EB % 4 == 0);
 
   for (int i = tid; i < BM; i += NT) {
     const int64_t m = m0 + i;
@@ -607,14 +609,22 @@ template <typename T, int BM, int BN, int TM, int TN, int BK = 16>
 static void launch_contract2(const gfb_contract_desc &d, cudaStream_t st) {
   dim3 grid((unsigned)ceil_div(d.M, BM), (unsigned)ceil_div(d.N, BN), (unsigned)d.nsplit);
   constexpr int NT = (BM / TM) * (BN / TN);
-  constexpr bool kQuadTile = sizeof(T) == 4 && (BM * BK / NT) % 4 == 0;
-  if constexpr (kQuadTile) {
-    if ((d.a_kfast & 3) == 3 && (reinterpret_cast<uintptr_t>(d.a) & 15) == 0) {
-      contract2_kernel<T, BM, BN, BK, TM, TN, true><<<grid, NT, 0, st>>>(d);
+  constexpr bool kQuadA = sizeof(T) == 4 && (BM * BK / NT) % 4 == 0;
+  constexpr bool kQuadB = sizeof(T) == 4 && (BN * BK / NT) % 4 == 0;
+  const bool a16 = (reinterpret_cast<uintptr_t>(d.a) & 15) == 0, b16 = (reinterpret_cast<uintptr_t>(d.b) & 15) == 0;
+  if constexpr (kQuadA) {
+    if ((d.a_kfast & 3) == 3 && a16) {
+      contract2_kernel<T, BM, BN, BK, TM, TN, 1><<<grid, NT, 0, st>>>(d);
       return;
     }
+    if constexpr (kQuadB) {
+      if ((d.a_kfast & 3) == 2 && (d.b_nfast & 3) == 3 && a16 && b16) {
+        contract2_kernel<T, BM, BN, BK, TM, TN, 2><<<grid, NT, 0, st>>>(d);
+        return;
+      }
+    }
   }
-  contract2_kernel<T, BM, BN, BK, TM, TN, false><<<grid, NT, 0, st>>>(d);
+  contract2_kernel<T, BM, BN, BK, TM, TN, 0><<<grid, NT, 0, st>>>(d);
 }
 
 template <typename T>
