@@ -179,7 +179,7 @@ __device__ __forceinline__ void tma_prologue(const StarPairDev &d, int i0, int j
   }
 }
 
-template <typename T, bool HAS_I>
+template <typename T, bool HAS_I, int MODES>
 __device__ __forceinline__ void star_tma_body(const CUtensorMap *ymap, const StarPairDev &d, T *ys, T *xs,
                                               uint64_t *mbar, const TmaWords &W, T (*xst)[kR + 1][tThreads],
                                               int i0, int i1) {
@@ -192,7 +192,8 @@ __device__ __forceinline__ void star_tma_body(const CUtensorMap *ymap, const Sta
   T *__restrict__ Xn = (T *)d.xout;
   T *__restrict__ Zn = (T *)d.zout;
   const int ps = d.ps, rs = d.rs;
-  const int amode = d.a.mode, bmode = d.b.mode;
+  // MODES >= 0: the two sweeps' base modes fixed at compile time (4 a + b)
+  const int amode = MODES >= 0 ? MODES / 4 : d.a.mode, bmode = MODES >= 0 ? MODES % 4 : d.b.mode;
   // planes: X(q) for q in [qbeg, min(qend, d0 - 1)], Y needed on [ylo, yhi]
   const int qbeg = HAS_I ? max(i0 - 1, 0) : 0, qend = HAS_I ? i1 : 0;
   const int ylo = HAS_I ? max(qbeg - 1, 0) : 0;
@@ -512,7 +513,7 @@ __host__ __device__ constexpr size_t star_tma_dyn_bytes() {
          NSY * sizeof(uint64_t);
 }
 
-template <typename T, bool HAS_I>
+template <typename T, bool HAS_I, int MODES>
 __global__ void __launch_bounds__(tThreads, HAS_I ? 512 / tThreads : 768 / tThreads)
     star_pair_tma_kernel(const __grid_constant__ CUtensorMap ymap, const __grid_constant__ StarPairDev d) {
   extern __shared__ __align__(128) unsigned char smem[];
@@ -527,7 +528,7 @@ __global__ void __launch_bounds__(tThreads, HAS_I ? 512 / tThreads : 768 / tThre
   tma_prologue(d, i0, blockIdx.y * tPY, blockIdx.x * tPX, tid, words);  // descriptor only
   pdl_wait();
   pdl_trigger();  // after the wait: at most one launch waits ahead of the running one
-  star_tma_body<T, HAS_I>(&ymap, d, ys, xs, mbar, words, xst, i0, i1);
+  star_tma_body<T, HAS_I, MODES>(&ymap, d, ys, xs, mbar, words, xst, i0, i1);
 }
 
 static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
@@ -548,12 +549,12 @@ bool star_tma_usable(const StarPairDev &d, int dtype) {
          getenv("GFB_NO_TMA") == nullptr;
 }
 
-template <typename T, bool HAS_I>
-static int launch_tma(const CUtensorMap &map, const StarPairDev &d, cudaStream_t st) {
+template <typename T, bool HAS_I, int MODES>
+static int launch_tma_m(const CUtensorMap &map, const StarPairDev &d, cudaStream_t st) {
   static bool attr = false;
   const size_t sm = star_tma_dyn_bytes<T, HAS_I>();
   if (!attr) {
-    cudaFuncSetAttribute(star_pair_tma_kernel<T, HAS_I>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    cudaFuncSetAttribute(star_pair_tma_kernel<T, HAS_I, MODES>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     attr = true;
   }
   // planes per CTA: the longest march (up to tPM) that still puts every
@@ -564,8 +565,19 @@ static int launch_tma(const CUtensorMap &map, const StarPairDev &d, cudaStream_t
   const int64_t slots = 2 * (int64_t)sm_count();
   dd.tpm = (int32_t)std::max<int64_t>(2, std::min<int64_t>(tPM, ceil_div(planes * tiles, slots)));
   dim3 grid((unsigned)ceil_div(d.d2, tPX), (unsigned)ceil_div(d.d1, tPY), (unsigned)ceil_div(planes, dd.tpm));
-  launch_pdl(star_pair_tma_kernel<T, HAS_I>, grid, dim3(tPX, tPY / kR), sm, st, map, dd);
+  launch_pdl(star_pair_tma_kernel<T, HAS_I, MODES>, grid, dim3(tPX, tPY / kR), sm, st, map, dd);
   return check_launch("star_pair_tma");
+}
+
+// the base-mode pairs of the fused timesteps (forward 3/3, adjoint 2/2 and
+// 1/2) get instantiations of their own; anything else reads the modes
+template <typename T, bool HAS_I>
+static int launch_tma(const CUtensorMap &map, const StarPairDev &d, cudaStream_t st) {
+  const int m = d.a.mode * 4 + d.b.mode;
+  if (m == 3 * 4 + 3) return launch_tma_m<T, HAS_I, 15>(map, d, st);
+  if (m == 2 * 4 + 2) return launch_tma_m<T, HAS_I, 10>(map, d, st);
+  if (m == 1 * 4 + 2) return launch_tma_m<T, HAS_I, 6>(map, d, st);
+  return launch_tma_m<T, HAS_I, -1>(map, d, st);
 }
 
 int launch_star_pair_tma(const StarPairDev &d, int dtype, dim3, cudaStream_t st) {
