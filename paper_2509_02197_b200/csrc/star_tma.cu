@@ -192,8 +192,10 @@ __device__ __forceinline__ void star_tma_body(const CUtensorMap *ymap, const Sta
   T *__restrict__ Xn = (T *)d.xout;
   T *__restrict__ Zn = (T *)d.zout;
   const int ps = d.ps, rs = d.rs;
-  // MODES >= 0: the two sweeps' base modes fixed at compile time (4 a + b)
-  const int amode = MODES >= 0 ? MODES / 4 : d.a.mode, bmode = MODES >= 0 ? MODES % 4 : d.b.mode;
+  // MODES >= 0: the two sweeps' base modes and the X write-back fixed at
+  // compile time (16 xwrite + 4 a + b)
+  const int amode = MODES >= 0 ? (MODES / 4) % 4 : d.a.mode, bmode = MODES >= 0 ? MODES % 4 : d.b.mode;
+  const bool xwrite = MODES >= 0 ? (MODES / 16) != 0 : d.xwrite != 0;
   // planes: X(q) for q in [qbeg, min(qend, d0 - 1)], Y needed on [ylo, yhi]
   const int qbeg = HAS_I ? max(i0 - 1, 0) : 0, qend = HAS_I ? i1 : 0;
   const int ylo = HAS_I ? max(qbeg - 1, 0) : 0;
@@ -278,7 +280,7 @@ __device__ __forceinline__ void star_tma_body(const CUtensorMap *ymap, const Sta
   const int clean_lo = jk_clean ? (ysrc ? max(0, d.a.smlo[0] - d.p0) : 0) : 1;
   const int clean_hi = jk_clean ? (ysrc ? min(d.d0, d.a.smhi[0] - d.p0) : d.d0) : 0;
   // common-case predicate patterns
-  const uint32_t xmask = kArray | kRegion | (amode == 2 ? kClear : 0u) | (d.xwrite ? kDead : 0u);
+  const uint32_t xmask = kArray | kRegion | (amode == 2 ? kClear : 0u) | (xwrite ? kDead : 0u);
   const uint32_t xval = amode == 0 ? 0xffffffffu : xmask;  // mode 0: base always added -> fix-up
   const uint32_t zmask = kArray | kRegion | (bmode == 2 ? kClear : 0u);
   const uint32_t zval = bmode == 0 ? 0xffffffffu : zmask;
@@ -311,7 +313,7 @@ __device__ __forceinline__ void star_tma_body(const CUtensorMap *ymap, const Sta
           acc = xst[q & 1][slot][tid];
         else if (amode == 0 || (amode == 2 && !(w & kClear)))
           acc += xst[q & 1][slot][tid];
-        if (wb && d.xwrite && !(w & kDead) && !(d.skipx && !(w & kRegion))) Xn[(size_t)q * ps + rel] = acc;
+        if (wb && xwrite && !(w & kDead) && !(d.skipx && !(w & kRegion))) Xn[(size_t)q * ps + rel] = acc;
       }
     }
     return (w & kSrcB) ? acc : T(0);
@@ -573,10 +575,12 @@ static int launch_tma_m(const CUtensorMap &map, const StarPairDev &d, cudaStream
 // 1/2) get instantiations of their own; anything else reads the modes
 template <typename T, bool HAS_I>
 static int launch_tma(const CUtensorMap &map, const StarPairDev &d, cudaStream_t st) {
-  const int m = d.a.mode * 4 + d.b.mode;
+  const int m = (d.xwrite ? 16 : 0) + d.a.mode * 4 + d.b.mode;
+  if (m == 16 + 3 * 4 + 3) return launch_tma_m<T, HAS_I, 31>(map, d, st);
+  if (m == 16 + 2 * 4 + 2) return launch_tma_m<T, HAS_I, 26>(map, d, st);
+  if (m == 16 + 1 * 4 + 2) return launch_tma_m<T, HAS_I, 22>(map, d, st);
   if (m == 3 * 4 + 3) return launch_tma_m<T, HAS_I, 15>(map, d, st);
   if (m == 2 * 4 + 2) return launch_tma_m<T, HAS_I, 10>(map, d, st);
-  if (m == 1 * 4 + 2) return launch_tma_m<T, HAS_I, 6>(map, d, st);
   return launch_tma_m<T, HAS_I, -1>(map, d, st);
 }
 
