@@ -35,7 +35,10 @@ struct StencilGeom {
 // Taps are unrolled up to MAXT (compile-time) and their box masks are split
 // per dimension: the j/k part is evaluated once per thread, the i part once
 // per plane (block-uniform), so the inner loop is predicate + load + FMA.
-template <typename T, int MAXT>
+// NTC > 0: the tap count at compile time; CM: 1 = overwrite with no masked
+// tap (forward sweeps), 2 = folded clear with masked taps (adjoint sweeps),
+// 0 = read both from the descriptor
+template <typename T, int MAXT, int NTC = 0, int CM = 0>
 __global__ void __launch_bounds__(kSX *kSY) stencil_kernel(const __grid_constant__ gfb_stencil_desc d,
                                                            const __grid_constant__ StencilGeom g) {
   const int64_t k = g.lo2 + (int64_t)blockIdx.x * kSX + threadIdx.x;
@@ -43,11 +46,13 @@ __global__ void __launch_bounds__(kSX *kSY) stencil_kernel(const __grid_constant
   if (k >= g.lo2 + g.e2 || j >= g.lo1 + g.e1) return;
   const int64_t i_begin = g.lo0 + (int64_t)blockIdx.z * g.march;
   const int64_t i_end = min(i_begin + g.march, g.lo0 + g.e0);
-  const int nt = d.ntaps;
-  uint32_t mjk = g.any_masked ? 0u : 0xffffffffu;
+  const int nt = NTC > 0 ? NTC : d.ntaps;
+  const bool any_masked = CM == 1 ? false : (CM == 2 ? true : g.any_masked != 0);
+  const int clear_mode = CM == 1 ? 1 : (CM == 2 ? 2 : d.clear_mode);
+  uint32_t mjk = any_masked ? 0u : 0xffffffffu;
 #pragma unroll
   for (int t = 0; t < MAXT; ++t) {
-    if (t < nt && g.any_masked) {
+    if (t < nt && any_masked) {
       bool ok = !d.tap_masked[t] ||
                 (j >= g.mlo[t][1] && j < g.mhi[t][1] && k >= g.mlo[t][2] && k < g.mhi[t][2]);
       mjk |= (uint32_t)ok << t;
@@ -57,16 +62,16 @@ __global__ void __launch_bounds__(kSX *kSY) stencil_kernel(const __grid_constant
   T *dst = (T *)d.dst;
   for (int64_t i = i_begin; i < i_end; ++i) {
     uint32_t m = mjk;
-    if (g.any_masked) {
+    if (any_masked) {
 #pragma unroll
       for (int t = 0; t < MAXT; ++t)
         if (t < nt && d.tap_masked[t] && (i < g.mlo[t][0] || i >= g.mhi[t][0])) m &= ~(1u << t);
     }
     const int64_t off = (i * g.d1 + j) * g.d2 + k;
     T acc;
-    if (d.clear_mode == 0) {
+    if (clear_mode == 0) {
       acc = dst[off];
-    } else if (d.clear_mode == 2) {
+    } else if (clear_mode == 2) {
       const bool in = crow && i >= g.clo[0] && i < g.chi[0];
       acc = in ? T(0) : dst[off];
     } else {
@@ -140,7 +145,17 @@ extern "C" int gfb_stencil_launch(const gfb_stencil_desc *d, void *stream) {
     stencil_kernel<double, MT><<<grid, block, 0, st>>>(*d, g);      \
   else                                                              \
     stencil_kernel<float, MT><<<grid, block, 0, st>>>(*d, g);
-  if (d->ntaps <= 8) {
+  const bool cm1 = (d->clear_mode == 1 || d->clear_mode == 3) && !g.any_masked;
+  const bool cm2 = d->clear_mode == 2 && g.any_masked;
+  if (d->ntaps == 7 && (cm1 || cm2)) {  // heat_3d sweeps (forward / adjoint)
+    if (d->dtype == GFB_F64) {
+      if (cm1) stencil_kernel<double, 8, 7, 1><<<grid, block, 0, st>>>(*d, g);
+      else stencil_kernel<double, 8, 7, 2><<<grid, block, 0, st>>>(*d, g);
+    } else {
+      if (cm1) stencil_kernel<float, 8, 7, 1><<<grid, block, 0, st>>>(*d, g);
+      else stencil_kernel<float, 8, 7, 2><<<grid, block, 0, st>>>(*d, g);
+    }
+  } else if (d->ntaps <= 8) {
     GFB_STENCIL_LAUNCH(8)
   } else if (d->ntaps <= 16) {
     GFB_STENCIL_LAUNCH(16)
