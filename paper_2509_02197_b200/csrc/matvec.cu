@@ -106,7 +106,9 @@ struct MvArgs {
 
 // Q = 16-byte column vectors per thread (C <= 256 * Q * W, Q <= 8: two CTAs
 // per SM fit the register file)
-template <typename T, int Q>
+// KIND fixes the halves at compile time: 1 rows only, 2 columns only,
+// 3 both with an independent v, 4 both in chain mode; 0 reads the descriptor
+template <typename T, int Q, int KIND>
 __global__ void __launch_bounds__(kThreads, 512 / kThreads) matvec_pair_kernel(MvArgs p) {
   using VT = V16<T>;
   using V = typename VT::type;
@@ -125,7 +127,9 @@ __global__ void __launch_bounds__(kThreads, 512 / kThreads) matvec_pair_kernel(M
   const int n = (int)(i1 - i0);
   const int cv32 = (int)cv;
   const T *A = static_cast<const T *>(p.A);
-  const bool has_row = p.u != nullptr, has_col = p.partial != nullptr;
+  const bool has_row = KIND == 0 ? p.u != nullptr : (KIND != 2);
+  const bool has_col = KIND == 0 ? p.partial != nullptr : (KIND != 1);
+  const bool chain = KIND == 0 ? chain != 0 : (KIND == 4);
 
   if (t == 0) {
     for (int s = 0; s < S; ++s) mbar_init(&bar[s], 1);
@@ -147,7 +151,7 @@ __global__ void __launch_bounds__(kThreads, 512 / kThreads) matvec_pair_kernel(M
     cq[q] = VT::zero();
   }
   // per-row scalar operands, fetched one row ahead (off the critical path)
-  const T *vsrc = p.chain ? (p.r_acc ? static_cast<const T *>(p.r) : nullptr) : static_cast<const T *>(p.v);
+  const T *vsrc = chain ? (p.r_acc ? static_cast<const T *>(p.r) : nullptr) : static_cast<const T *>(p.v);
   T vnext = (has_col && vsrc && n > 0) ? vsrc[i0] : T(0);
 
   int s = 0;
@@ -188,9 +192,9 @@ __global__ void __launch_bounds__(kThreads, 512 / kThreads) matvec_pair_kernel(M
     if (has_row && t == 0) {
       T *ro = static_cast<T *>(p.r) + i0 + k;
       // chain + r_acc: vcur is the old r[i] (read a row ahead by every thread)
-      *ro = p.r_acc ? (T)((p.chain ? vcur : *ro) + tval) : tval;
+      *ro = p.r_acc ? (T)((chain ? vcur : *ro) + tval) : tval;
     }
-    if (p.chain) vi = p.r_acc ? (T)(vcur + tval) : tval;
+    if (chain) vi = p.r_acc ? (T)(vcur + tval) : tval;
     if (has_col) {
 #pragma unroll
       for (int q = 0; q < Q; ++q) VT::axpy(cq[q], a[q], vi);
@@ -294,9 +298,13 @@ int launch_pair(const MvArgs &a0, int64_t nblocks, cudaStream_t st) {
   a.stages = S;
   const size_t smem = (size_t)S * stage_bytes + (size_t)S * 8 + 2 * (kThreads / 32) * sizeof(T);
   const dim3 grid((unsigned)nblocks);
+  const int kind = (a.u && a.partial) ? (a.chain ? 4 : 3) : (a.u ? 1 : 2);
 #define GFB_MV_CASE(QQ)                                                                                  \
   if (cv <= (int64_t)kThreads * QQ) {                                                                    \
-    auto k = matvec_pair_kernel<T, QQ>;                                                                  \
+    auto k = kind == 4   ? matvec_pair_kernel<T, QQ, 4>                                                  \
+             : kind == 3 ? matvec_pair_kernel<T, QQ, 3>                                                  \
+             : kind == 1 ? matvec_pair_kernel<T, QQ, 1>                                                  \
+                         : matvec_pair_kernel<T, QQ, 2>;                                                 \
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);                     \
     k<<<grid, kThreads, smem, st>>>(a);                                                                  \
     return check_launch("matvec_pair");                                                                  \
