@@ -195,7 +195,7 @@ __device__ __forceinline__ void star_tma_body(const CUtensorMap *ymap, const Sta
   // MODES >= 0: the two sweeps' base modes and the X write-back fixed at
   // compile time (16 xwrite + 4 a + b)
   const int amode = MODES >= 0 ? (MODES / 4) % 4 : d.a.mode, bmode = MODES >= 0 ? MODES % 4 : d.b.mode;
-  const bool xwrite = MODES >= 0 ? (MODES / 16) != 0 : d.xwrite != 0;
+  const bool xwrite = MODES >= 0 ? ((MODES / 16) & 1) != 0 : d.xwrite != 0;
   // planes: X(q) for q in [qbeg, min(qend, d0 - 1)], Y needed on [ylo, yhi]
   const int qbeg = HAS_I ? max(i0 - 1, 0) : 0, qend = HAS_I ? i1 : 0;
   const int ylo = HAS_I ? max(qbeg - 1, 0) : 0;
@@ -254,7 +254,7 @@ __device__ __forceinline__ void star_tma_body(const CUtensorMap *ymap, const Sta
   }
   const uint32_t mxr = ring ? (W.aj[rj] & W.ak[rk]) : 0u;
 
-  const bool ysrc = d.a.srcmask == 1;
+  const bool ysrc = MODES >= 0 ? ((MODES / 32) & 1) != 0 : d.a.srcmask == 1;
   const bool yj_in = j0 - 2 >= d.a.smlo[1] && j0 + tPY + 2 <= d.a.smhi[1];
   const bool yk_in = k0 - 2 >= d.a.smlo[2] && k0 + tPX + 2 <= d.a.smhi[2];
   auto prepare_plane = [&](int p) {
@@ -575,13 +575,16 @@ static int launch_tma_m(const CUtensorMap &map, const StarPairDev &d, cudaStream
 // 1/2) get instantiations of their own; anything else reads the modes
 template <typename T, bool HAS_I>
 static int launch_tma(const CUtensorMap &map, const StarPairDev &d, cudaStream_t st) {
-  const int m = (d.xwrite ? 16 : 0) + d.a.mode * 4 + d.b.mode;
-  if (m == 16 + 3 * 4 + 3) return launch_tma_m<T, HAS_I, 31>(map, d, st);
-  if (m == 16 + 2 * 4 + 2) return launch_tma_m<T, HAS_I, 26>(map, d, st);
-  if (m == 16 + 1 * 4 + 2) return launch_tma_m<T, HAS_I, 22>(map, d, st);
-  if (m == 3 * 4 + 3) return launch_tma_m<T, HAS_I, 15>(map, d, st);
-  if (m == 2 * 4 + 2) return launch_tma_m<T, HAS_I, 10>(map, d, st);
-  return launch_tma_m<T, HAS_I, -1>(map, d, st);
+  // 32 source-mask form + 16 X write-back + 4 a + b
+  const int m = (d.a.srcmask == 1 ? 32 : 0) + (d.xwrite ? 16 : 0) + d.a.mode * 4 + d.b.mode;
+  switch (m) {
+    case 16 + 3 * 4 + 3: return launch_tma_m<T, HAS_I, 16 + 3 * 4 + 3>(map, d, st);       // forward
+    case 3 * 4 + 3: return launch_tma_m<T, HAS_I, 3 * 4 + 3>(map, d, st);                 // last forward
+    case 32 + 16 + 2 * 4 + 2: return launch_tma_m<T, HAS_I, 32 + 16 + 2 * 4 + 2>(map, d, st);  // adjoint
+    case 32 + 16 + 1 * 4 + 2: return launch_tma_m<T, HAS_I, 32 + 16 + 1 * 4 + 2>(map, d, st);  // first adjoint
+    case 32 + 2 * 4 + 2: return launch_tma_m<T, HAS_I, 32 + 2 * 4 + 2>(map, d, st);       // last adjoint
+    default: return launch_tma_m<T, HAS_I, -1>(map, d, st);
+  }
 }
 
 int launch_star_pair_tma(const StarPairDev &d, int dtype, dim3, cudaStream_t st) {
