@@ -73,6 +73,20 @@ __global__ void __launch_bounds__(kThreads) reduce_pass1(const TI *__restrict__ 
   if (threadIdx.x == 0) part[blockIdx.x] = s;
 }
 
+// n small enough for one block (nb == 1): one launch instead of two (a
+// fixed-order strided sum and block sum, deterministic)
+template <typename TI, typename TO>
+__global__ void __launch_bounds__(kThreads) reduce_single(const TI *__restrict__ x, int64_t n, TO *out,
+                                                          int accumulate) {
+  double acc = 0.0;
+  for (int64_t i = threadIdx.x; i < n; i += kThreads) acc += (double)x[i];
+  double s = block_sum<TI>(acc);
+  if (threadIdx.x == 0) {
+    TO r = (TO)s;
+    *out = accumulate ? (TO)(*out + r) : r;
+  }
+}
+
 template <typename TO>
 __global__ void __launch_bounds__(kThreads) reduce_pass2(const double *__restrict__ part, int64_t nb, TO *out,
                                                          int accumulate) {
@@ -246,6 +260,16 @@ extern "C" int gfb_reduce_sum(const void *x, int32_t xdtype, int64_t n, void *ou
   cudaStream_t st = (cudaStream_t)stream;
   int64_t nb = reduce_blocks(n);
   double *part = (double *)workspace;
+  if (n > 0 && nb == 1) {
+#define GFB_RS(TI, TO) reduce_single<TI, TO><<<1, kThreads, 0, st>>>((const TI *)x, n, (TO *)out, accumulate)
+    if (xdtype == GFB_F64) {
+      if (odtype == GFB_F64) GFB_RS(double, double); else GFB_RS(double, float);
+    } else {
+      if (odtype == GFB_F64) GFB_RS(float, double); else GFB_RS(float, float);
+    }
+#undef GFB_RS
+    return check_launch("reduce_sum");
+  }
   if (n <= 0) {
     nb = 1;
     cudaMemsetAsync(part, 0, 8, st);
