@@ -358,6 +358,11 @@ __device__ __forceinline__ void star_tma_body(const CUtensorMap *ymap, const Sta
     }
   }
 
+  // Y ring slot of plane q and slot / phase of plane q + 2, advanced once per
+  // step (no modulo in the march)
+  unsigned ysl = (unsigned)(qbeg - ylo + NSY) % (unsigned)NSY;
+  unsigned wsl = (unsigned)(qbeg + 2 - ylo) % (unsigned)NSY;
+  uint32_t wph = ((unsigned)(qbeg + 2 - ylo) / (unsigned)NSY) & 1u;
   auto step = [&](auto S, int q) {
     constexpr int M = decltype(S)::value, C = (M + 1) % 3, P = (M + 2) % 3;
 #pragma unroll
@@ -374,11 +379,11 @@ __device__ __forceinline__ void star_tma_body(const CUtensorMap *ymap, const Sta
         // plane q + 2 is needed by X(q + 1): land it and mask it now; the
         // barrier below orders this before any read of it
         const int pn = q + 2;
-        if (pn <= yhi && pn > qbeg + 1) wait_plane(pn);
+        if (pn <= yhi && pn > qbeg + 1) mbar_wait(&mbar[wsl], wph);
         if (pn <= qend + 1 && pn > qbeg + 1 && (pn < clean_lo || pn >= clean_hi)) prepare_plane(pn);
       }
-      const T *yc = slot_of(q);
-      const T *yp = slot_of(q + 1);
+      const T *yc = ys + ysl * YSS;
+      const T *yp = ys + (ysl + 1 == (unsigned)NSY ? 0u : ysl + 1) * YSS;
       // X~ ring slots relative to the march start: compile-time in the
       // unrolled march (step M handles planes q = qbeg + 3n + M)
 #if GFB_STAR_UNROLL
@@ -474,6 +479,11 @@ __device__ __forceinline__ void star_tma_body(const CUtensorMap *ymap, const Sta
           zrow[u * rs] = zz;
         }
       }
+    }
+    ysl = ysl + 1 == (unsigned)NSY ? 0u : ysl + 1;
+    if (++wsl == (unsigned)NSY) {
+      wsl = 0;
+      wph ^= 1u;
     }
   };
   using I0 = std::integral_constant<int, 0>;
