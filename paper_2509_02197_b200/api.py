@@ -41,7 +41,7 @@ from .ir import (
     number_writes,
     pristine_inputs,
 )
-from .lowering import Lowering, LTape, ProgramRun, required_record
+from .lowering import Lowering, LTape, NeedValues, ProgramRun, required_record
 from .runtime import NP_DTYPE, Executable
 
 # ---------------------------------------------------------------------------
@@ -214,15 +214,45 @@ class Lowered:
     backward_program: Program
 
 
+def probe_values(nv: NeedValues, inputs: dict, seed=1.0) -> dict:
+    """Run the launches lowered before a data-dependent decision and read the
+    snapshots it needs (host copies, name -> ndarray)."""
+    low = nv.low
+    slots = list(nv.slots.values())
+    low.finish(slots)
+    exe = Executable(low, low.entry_inputs, {}, seed_buf=low.entry_seed, use_graph=False,
+                     pinned=[low.resolve(b) for b in slots])
+    exe.run({k: inputs[k] for k in low.entry_inputs}, seed)
+    return {n: exe.view(low.resolve(b)).cpu().numpy().copy() for n, b in nv.slots.items()}
+
+
+def probe_lower(lower, inputs: dict | None, seed=1.0):
+    """``lower(known)`` until no decision is missing: each ``NeedValues``
+    runs the prefix on the device and appends its values to ``known``
+    (reference data-dependent branches / loop headers, interpreter.py:
+    210-219, 342-347, evaluated at the same program point)."""
+    known = []
+    while True:
+        try:
+            return lower(known)
+        except NeedValues as nv:
+            if inputs is None:
+                raise UnsupportedConstruct(
+                    f"control flow depends on runtime data ({', '.join(sorted(nv.slots))}); "
+                    "the launch list needs input values to be lowered") from None
+            known.append(probe_values(nv, inputs, seed))
+
+
 def lower_gradient(program: Program, bundle: Bundle, params: dict, shapes: dict, *, trip_limit=None,
-                   record=None, plan: PlanBundle | None = None, fuse_small=False) -> Lowered:
+                   record=None, plan: PlanBundle | None = None, fuse_small=False, known=None) -> Lowered:
     """Forward (recording the tape) + backward as one launch list."""
-    low = Lowering(trip_limit=trip_limit, fuse_small=fuse_small)
+    low = Lowering(trip_limit=trip_limit, fuse_small=fuse_small, known=known)
     fwd_prog = plan.forward if plan else program
     bwd_prog = plan.backward if plan else bundle.backward
     forwarding = plan.forwarding if plan else bundle.forwarding
     rec = set(plan.keep) if plan else set(bundle.required if record is None else record)
     fenv, inputs = _init_env(low, fwd_prog, shapes, "")
+    low.entry_inputs = inputs
     tape = LTape()
     for name, b in list(fenv.items()):
         if (name, 0) in rec:
@@ -252,6 +282,7 @@ def lower_gradient(program: Program, bundle: Bundle, params: dict, shapes: dict,
     if seed_name in bwd_prog.descriptors and seed_name not in benv:
         seed_buf = low.new_buffer(seed_name, (), bwd_prog.descriptors[seed_name].element_kind, fresh=False)
         benv[seed_name] = seed_buf
+    low.entry_seed = seed_buf
     br = ProgramRun(low, bwd_prog, params, benv, src_tape=tape, forwarding=forwarding)
     br.run()
     outputs = {"value": dep}
@@ -267,8 +298,13 @@ def lower_gradient(program: Program, bundle: Bundle, params: dict, shapes: dict,
 
 
 def build_gradient_executable(program: Program, bundle: Bundle, params: dict, shapes: dict, *, trip_limit=None,
-                              record=None, plan: PlanBundle | None = None) -> Executable:
-    lw = lower_gradient(program, bundle, params, shapes, trip_limit=trip_limit, record=record, plan=plan)
+                              record=None, plan: PlanBundle | None = None, inputs: dict | None = None,
+                              seed=1.0) -> Executable:
+    """``inputs`` (host or device values) are needed only by programs whose
+    control flow reads runtime data; the launch list then holds the path
+    those inputs take (``Executable.decisions_hold`` re-checks it)."""
+    lw = probe_lower(lambda known: lower_gradient(program, bundle, params, shapes, trip_limit=trip_limit,
+                                                  record=record, plan=plan, known=known), inputs, seed)
     exe = Executable(lw.low, lw.inputs, lw.outputs, seed_buf=lw.seed_buf)
     exe.forward_env, exe.backward_env, exe.tape = lw.forward_env, lw.backward_env, lw.tape
     exe.forward_program, exe.backward_program = lw.forward_program, lw.backward_program
@@ -288,6 +324,19 @@ def _cached(key, keep_alive, build):
             _CACHE.pop(next(iter(_CACHE)))
         _CACHE[key] = exe
         exe._keep_alive = keep_alive
+    return exe
+
+
+def _run_guarded(key, keep_alive, build, inputs, seed):
+    """Run the cached executable; when its data-dependent decisions do not
+    hold for these inputs, lower again along the path they take."""
+    exe = _cached(key, keep_alive, build)
+    exe.run(inputs, seed)
+    if exe.low.decisions and not exe.decisions_hold():
+        exe = build()
+        exe._keep_alive = keep_alive
+        _CACHE[key] = exe
+        exe.run(inputs, seed)
     return exe
 
 
@@ -329,9 +378,9 @@ def gradient(program, inputs: dict, params: dict | None = None, *, seed=1.0, tri
         bundle_eng = as_bundle(bundle)
     shapes = _check_inputs(prog, inputs, params)
     key = ("grad", id(program), id(bundle), tuple(sorted(params.items())), tuple(sorted(shapes.items())), trip_limit)
-    exe = _cached(key, (program, bundle),
-                  lambda: build_gradient_executable(prog, bundle_eng, params, shapes, trip_limit=trip_limit))
-    exe.run(inputs, seed)
+    build = lambda: build_gradient_executable(prog, bundle_eng, params, shapes, trip_limit=trip_limit,  # noqa: E731
+                                              inputs=inputs, seed=seed)
+    exe = _run_guarded(key, (program, bundle), build, inputs, seed)
     return _result(exe, prog, inputs, bundle if bundle is not None else bundle_eng)
 
 
@@ -341,9 +390,9 @@ def run_planned(result, inputs: dict, params: dict | None = None, *, seed=1.0, t
     pb = as_plan(result)
     shapes = _check_inputs(pb.forward, inputs, params)
     key = ("plan", id(result), tuple(sorted(params.items())), tuple(sorted(shapes.items())), trip_limit)
-    exe = _cached(key, (result,),
-                  lambda: build_gradient_executable(pb.forward, None, params, shapes, trip_limit=trip_limit, plan=pb))
-    exe.run(inputs, seed)
+    build = lambda: build_gradient_executable(pb.forward, None, params, shapes, trip_limit=trip_limit,  # noqa: E731
+                                              plan=pb, inputs=inputs, seed=seed)
+    exe = _run_guarded(key, (result,), build, inputs, seed)
     return _result(exe, pb.forward, inputs, getattr(result, "bundle", None))
 
 
@@ -365,18 +414,23 @@ def run_forward(program, inputs: dict, params: dict | None = None, *, record=Non
     params = dict(params or {})
     prog = adopt(program)
     shapes = _check_inputs(prog, inputs, params)
-    low = Lowering(trip_limit=trip_limit)
-    env, ins = _init_env(low, prog, shapes, "")
-    tape = LTape() if record is not None else None
-    if tape is not None:
-        from .lowering import CopyOp
+    def lower(known):
+        low = Lowering(trip_limit=trip_limit, known=known)
+        env, ins = _init_env(low, prog, shapes, "")
+        low.entry_inputs = ins
+        tape = LTape() if record is not None else None
+        if tape is not None:
+            from .lowering import CopyOp
 
-        for name, b in list(env.items()):
-            if record == "all" or (name, 0) in record:
-                slot = low.new_buffer(f"{name}@v0", b.shape, b.kind, fresh=False)
-                low.emit(CopyOp(slot, b))
-                tape.values[(name, 0, ())] = slot
-    ProgramRun(low, prog, params, env, record=record, tape=tape, versions=number_writes(prog)).run()
+            for name, b in list(env.items()):
+                if record == "all" or (name, 0) in record:
+                    slot = low.new_buffer(f"{name}@v0", b.shape, b.kind, fresh=False)
+                    low.emit(CopyOp(slot, b))
+                    tape.values[(name, 0, ())] = slot
+        ProgramRun(low, prog, params, env, record=record, tape=tape, versions=number_writes(prog)).run()
+        return low, env, ins, tape
+
+    low, env, ins, tape = probe_lower(lower, inputs)
     dep = env.get(prog.dependent)
     if dep is None:
         raise UnboundName(f"dependent '{prog.dependent}' was never written")
@@ -400,23 +454,27 @@ def run_backward(program, backward, inputs: dict, params: dict | None = None, *,
     bwd = adopt(backward)
     fw = adopt_forwarding(forwarding) if forwarding and not isinstance(next(iter(forwarding.values())), type(None)) \
         else {}
-    low = Lowering(trip_limit=trip_limit)
     pass_in = {k: v for k, v in inputs.items() if k in bwd.descriptors}
-    shapes = _check_inputs(bwd, pass_in, params)
-    env, ins = _init_env(low, bwd, shapes, "")
-    extra_in = {}
-    for k, v in (extra_env or {}).items():
-        if k in bwd.descriptors:
+    extra_in = {k: v for k, v in (extra_env or {}).items() if k in bwd.descriptors}
+    seed_name = prog.dependent + "__grad"
+
+    def lower(known):
+        low = Lowering(trip_limit=trip_limit, known=known)
+        shapes = _check_inputs(bwd, pass_in, params)
+        env, ins = _init_env(low, bwd, shapes, "")
+        for k, v in extra_in.items():
             b = low.new_buffer(k, tuple(np.shape(v)), bwd.descriptors[k].element_kind, fresh=False)
             env[k] = b
             ins[k] = b
-            extra_in[k] = v
-    seed_name = prog.dependent + "__grad"
-    seed_buf = None
-    if seed_name in bwd.descriptors and seed_name not in env:
-        seed_buf = low.new_buffer(seed_name, (), bwd.descriptors[seed_name].element_kind, fresh=False)
-        env[seed_name] = seed_buf
-    ProgramRun(low, bwd, params, env, src_tape=tape, forwarding=fw).run()
+        seed_buf = None
+        if seed_name in bwd.descriptors and seed_name not in env:
+            seed_buf = low.new_buffer(seed_name, (), bwd.descriptors[seed_name].element_kind, fresh=False)
+            env[seed_name] = seed_buf
+        low.entry_inputs, low.entry_seed = ins, seed_buf
+        ProgramRun(low, bwd, params, env, src_tape=tape, forwarding=fw).run()
+        return low, env, ins, seed_buf
+
+    low, env, ins, seed_buf = probe_lower(lower, {**pass_in, **extra_in}, seed)
     low.finish(list(env.values()))
     outputs = {"value": seed_buf} if seed_buf is not None else {}
     exe = Executable(low, ins, outputs, seed_buf=seed_buf, use_graph=False,

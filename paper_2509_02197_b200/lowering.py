@@ -1507,6 +1507,14 @@ class LoopCtx:
         return self.iterates[self.pos]
 
 
+def _host_index(vals: dict, base: str, idx: tuple):
+    """``idx`` read in a condition (reference symexpr.py:180-184: numpy
+    indexing of the env array, so negative indices wrap)."""
+    if base not in vals:
+        raise UnboundName(f"no array available for '{base}'")
+    return vals[base][(Ellipsis, *idx)]
+
+
 class LTape:
     """Lowering-time image of the reference Tape (interpreter.py:70-75)."""
 
@@ -1516,11 +1524,33 @@ class LTape:
         self.iterate_records = {}  # label -> {coords: [int]}
 
 
+class NeedValues(Exception):
+    """Raised while lowering when control flow reads runtime data: a
+    data-dependent branch condition (reference interpreter.py:342-347) or a
+    loop header bound to a scalar (``_header_bindings``, :210-219).
+
+    ``slots`` maps each data name to a device snapshot taken at that point of
+    the launch list. The caller (``api.probe_lower``) runs the launches
+    emitted so far, reads the snapshots back and lowers again with the values
+    appended to ``Lowering.known``; the finished launch list keeps the
+    snapshots, and ``Executable`` re-checks every decision after each run."""
+
+    def __init__(self, slots: dict):
+        super().__init__("runtime values needed: " + ", ".join(sorted(slots)))
+        self.slots = slots
+
+
 class Lowering:
     """Accumulates launches for one or more program runs over shared buffers."""
 
-    def __init__(self, *, trip_limit=None, fuse_small=False):
+    def __init__(self, *, trip_limit=None, fuse_small=False, known=None):
         self.fuse_small = fuse_small  # fuse small 3-D domains too (slab decomposition needs fused pairs)
+        # runtime control-flow values observed by earlier probe runs, in
+        # decision order; decisions = [(slots, key_fn, key)] taken this lowering
+        self.known: list = list(known or [])
+        self.decisions: list = []
+        self.entry_inputs: dict = {}  # caller name -> Buffer (for probe runs of a prefix)
+        self.entry_seed = None
         self.ops: list[Op] = []
         self.buffers: list[Buffer] = []
         self.flops = 0
@@ -1929,13 +1959,56 @@ class ProgramRun:
             else:
                 self.branch(b)
 
+    def runtime_values(self, names, key_fn) -> dict:
+        """Host values of the data ``names`` at this point of the program.
+
+        Emits a device snapshot of each (so later writes do not disturb it)
+        and returns the values a probe run observed for this decision; raises
+        ``NeedValues`` when no probe has reached it yet. ``key_fn(values)`` is
+        what the decision depends on (a branch outcome, a loop's header
+        scalars): the executable re-evaluates it from the snapshots after
+        every run and rebuilds when it changes."""
+        low = self.low
+        slots = {}
+        for n in sorted(names):
+            src = self.env.get(n)
+            if src is None:
+                continue  # unbound: evaluation raises UnboundName as in the reference
+            low.materialize(src)
+            slot = low.new_buffer(f"{n}@probe{len(low.decisions)}", src.shape, src.kind, fresh=False)
+            low.emit(CopyOp(slot, src))
+            slots[n] = slot
+        i = len(low.decisions)
+        if i >= len(low.known):
+            nv = NeedValues(slots)
+            nv.low = low
+            raise nv
+        vals = low.known[i]
+        low.decisions.append((slots, key_fn, key_fn(vals)))
+        return vals
+
     def _header_bind(self, loop):
         need = (free_names(loop.init) | free_names(loop.bound) | free_names(loop.update)) - {loop.iterator}
-        for name in need:
-            if name not in self.bind and name in self.program.descriptors:
-                raise UnsupportedConstruct(
-                    f"loop '{loop.label}' header reads runtime data '{name}'; the engine needs static headers")
-        return dict(self.bind)
+        data = {n for n in need if n not in self.bind and n in self.program.descriptors
+                and self.program.descriptors[n].rank == 0}
+        if not data:
+            return dict(self.bind)
+        label = loop.label
+
+        def key(vals, label=label):
+            out = []
+            for n in sorted(vals):
+                f = float(vals[n].reshape(-1)[0])
+                if not f.is_integer():
+                    raise DomainError(f"scalar '{n}' in a loop header evaluated to non-integer {f} "
+                                      f"(loop '{label}')")
+                out.append(int(f))
+            return tuple(out)
+
+        vals = self.runtime_values(data, key)
+        b = dict(self.bind)
+        b.update(zip(sorted(vals), key(vals)))
+        return b
 
     def simulate(self, loop) -> list:
         b = self._header_bind(loop)
@@ -2030,12 +2103,19 @@ class ProgramRun:
             self.branch_down[br.trace_ref] = cursor
             outcome = outcomes[cursor]
         else:
-            data = free_names(br.condition) & set(self.program.descriptors)
+            data = (free_names(br.condition) & set(self.program.descriptors)) - set(self.bind)
             if data:
-                raise UnsupportedConstruct(
-                    f"branch '{br.label}' depends on runtime data {sorted(data)}; data-dependent control "
-                    "flow is not lowered to the device yet")
-            outcome = bool(evaluate(br.condition, dict(self.bind)))
+                cond, label = br.condition, br.label
+                descs = self.program.descriptors
+
+                def key(vals, cond=cond, label=label):
+                    b = dict(self.bind)
+                    b.update({n: v.reshape(()).item() for n, v in vals.items() if descs[n].rank == 0})
+                    return bool(evaluate(cond, b, lambda base, idx: _host_index(vals, base, idx)))
+
+                outcome = key(self.runtime_values(data, key))
+            else:
+                outcome = bool(evaluate(br.condition, dict(self.bind)))
             if self.tape is not None:
                 self.tape.branch_trace.setdefault(br.label, []).append(outcome)
         self.region(br.then_body if outcome else br.else_body)

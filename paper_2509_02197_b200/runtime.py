@@ -81,7 +81,8 @@ class Executable:
         self.use_graph = env_graph if use_graph is None else use_graph
         self.graph = None
         self.runs = 0
-        self.pinned = list(pinned)
+        # decision snapshots (data-dependent control flow) stay readable
+        self.pinned = list(pinned) + [low.resolve(b) for slots, _, _ in low.decisions for b in slots.values()]
         self.reuse = (os.environ.get("GFB_ARENA", "1") != "0") if reuse is None else reuse
         self._allocate()
         for op in self.ops:
@@ -193,6 +194,17 @@ class Executable:
         if bits:
             msgs = [m for b, m in L.EBITS.items() if bits & b]
             raise DomainError("; ".join(msgs) or f"device error bits {bits:#x}")
+
+    def decisions_hold(self) -> bool:
+        """Re-evaluate every data-dependent control-flow decision this launch
+        list was lowered with, from the device snapshots of the run just
+        finished; False means the inputs took another path and the caller
+        must lower again."""
+        for slots, key_fn, key in self.low.decisions:
+            vals = {n: self.view(self.low.resolve(b)).cpu().numpy() for n, b in slots.items()}
+            if key_fn(vals) != key:
+                return False
+        return True
 
     def output(self, key) -> torch.Tensor:
         return self.view(self.outputs[key])

@@ -29,7 +29,7 @@ def _bundle(name):
     return load_program(stem + ".fwd.json"), load_bundle(stem + ".bwd.json", stem + ".fwdreq.json")
 
 
-CASES = sorted(IDX["cases"]) + sorted(c for c in IDX["examples"] if "branchy" not in c)
+CASES = sorted(IDX["cases"]) + sorted(IDX["examples"])
 
 
 @pytest.mark.parametrize("cid", CASES)
@@ -163,10 +163,32 @@ def test_c2_literal_budget_is_infeasible_like_the_reference():
         assert rec["min_peak_bytes"] == 2 * n**d * 8
 
 
-def test_unsupported_constructs_fail_loudly():
+def test_data_dependent_branch_follows_each_call_inputs():
+    """Reference interpreter.py:342-347: the branch reads the scalar input s.
+    One cached executable per (program, params, shapes); a call whose inputs
+    take the other arm is detected from the device snapshot and lowered
+    again, so each call returns that call's gradient."""
+    from paper_2509_02197_b200.api import _CACHE
+
+    prog, b = _bundle("corpus_branchy_scale")
+    rng = np.random.default_rng(5)
+    x = rng.uniform(0.4, 1.6, 8)
+    for s in (0.3, 0.9, 0.3, 0.5, 0.49):
+        inputs = {"X": x, "s": np.array(s)}
+        res = gradient(prog, inputs, {"n": 8}, bundle=b)
+        v, g, _ = O.gradient(prog, b.backward, b.forwarding, b.required, inputs, {"n": 8})
+        assert rel_err(res.value, v) <= 1e-10
+        assert rel_err(res.grads["X"], g["X"]) <= 1e-10
+        want = np.full(8, 2.0) if s < 0.5 else np.cos(x)
+        assert np.allclose(res.grads["X"], want, rtol=1e-14, atol=0)
+    exes = [e for k, e in _CACHE.items() if k[0] == "grad" and k[1] == id(prog)]
+    assert len(exes) == 1 and len(exes[0].low.decisions) == 1
+
+
+def test_engine_without_inputs_rejects_data_dependent_control_loudly():
     prog, b = _bundle("corpus_branchy_scale")
     with pytest.raises(UnsupportedConstruct):
-        gradient(prog, {"X": np.ones(8), "s": np.array(0.3)}, {"n": 8}, bundle=b)
+        Engine(prog, b, {"n": 8})
 
 
 class _LockstepComm:

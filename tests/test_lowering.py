@@ -13,7 +13,8 @@ from paper_2509_02197_b200 import workloads as W
 from paper_2509_02197_b200.api import _check_inputs, load_bundle, load_plan, lower_gradient
 from paper_2509_02197_b200.errors import DomainError, OutOfBounds, UnsupportedConstruct
 from paper_2509_02197_b200.ir import load_program
-from paper_2509_02197_b200.lowering import FillOp, StencilOp
+from paper_2509_02197_b200.lowering import FillOp, NeedValues, StencilOp
+from oracle import interp as O
 
 IDX = golden_index()
 
@@ -118,12 +119,60 @@ def test_domain_error_bit_from_emulated_kernel():
     assert int(em.err[0]) & 0x1
 
 
-def test_data_dependent_branch_is_rejected_loudly():
+def _emulate_probing(prog, bundle, params, inputs):
+    """lower_gradient with the api's probe loop, every probe run (and the
+    final launch list) on the emulator instead of the device."""
+    shapes = _check_inputs(prog, inputs, params)
+    known = []
+    while True:
+        try:
+            lw = lower_gradient(prog, bundle, params, shapes, known=known)
+            break
+        except NeedValues as nv:
+            low = nv.low
+            low.finish(list(nv.slots.values()))
+            _, pview = E.execute(low, {k: inputs[k] for k in low.entry_inputs}, low.entry_inputs, low.entry_seed)
+            known.append({n: np.array(pview(low.resolve(b))) for n, b in nv.slots.items()})
+    em, view = E.execute(lw.low, inputs, lw.inputs, lw.seed_buf)
+    return lw, em, view, known
+
+
+def test_data_dependent_branch_needs_a_probe():
     prog, b = _bundle("corpus_branchy_scale")
     params = {"n": 8}
     inputs = {"X": np.ones(8), "s": np.array(0.3)}
-    with pytest.raises(UnsupportedConstruct):
+    with pytest.raises(NeedValues) as ei:
         lower_gradient(prog, b, params, _check_inputs(prog, inputs, params))
+    assert sorted(ei.value.slots) == ["s"]
+
+
+def test_data_dependent_branch_matches_reference_golden():
+    """Reference interpreter.py:342-347: the condition reads the scalar input
+    s; the golden draws s = 1.57, so the 'high' (sin) arm runs."""
+    prog, b = _bundle("corpus_branchy_scale")
+    inputs, value, grads, op_count = load_case("corpus_branchy_scale__n8")
+    lw, em, view, known = _emulate_probing(prog, b, {"n": 8}, inputs)
+    _check(lw, view, prog, value, grads)
+    assert lw.low.flops == op_count
+    assert len(known) == 1 and len(lw.low.decisions) == 1
+    slots, key_fn, key = lw.low.decisions[0]
+    assert key is False
+    # the recorded decision re-evaluates from the final run's snapshot
+    assert key_fn({n: np.array(view(lw.low.resolve(s))) for n, s in slots.items()}) is False
+    assert key_fn({"s": np.array(0.3)}) is True
+
+
+@pytest.mark.parametrize("s", [0.3, 0.5, 0.9])
+def test_data_dependent_branch_both_arms_match_oracle(s):
+    prog, b = _bundle("corpus_branchy_scale")
+    params = {"n": 8}
+    rng = np.random.default_rng(3)
+    inputs = {"X": rng.uniform(0.4, 1.6, 8), "s": np.array(s)}
+    lw, em, view, _ = _emulate_probing(prog, b, params, inputs)
+    v, g, _ = O.gradient(prog, b.backward, b.forwarding, b.required, inputs, params)
+    _check(lw, view, prog, v, g)
+    want = 2.0 if s < 0.5 else np.cos(inputs["X"])
+    assert np.allclose(view(lw.outputs["grad:X"]), want, rtol=1e-14, atol=0)
 
 
 @pytest.mark.parametrize("name", ["atax", "bicg"])
