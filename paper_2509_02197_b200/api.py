@@ -511,3 +511,20 @@ class Engine:
     def gradient(self, inputs: dict, seed=1.0) -> GradientResult:
         self.exe.run(inputs, seed)
         return _result(self.exe, self.program, inputs, self.bundle)
+
+    def gradients(self, batches, seed=1.0):
+        """One ``GradientResult`` per input dict of ``batches``, with host
+        inputs in and host results out, pipelined across calls
+        (``Executable.run_pipelined``): the next batch's H2D copy and the
+        previous result's D2H copy overlap the current batch's launches.
+        Results carry value and grads (fresh host arrays); ``forward`` /
+        ``backward`` envs are not kept per batch (None)."""
+        outs = {k: self.exe.output(k) for k in self.exe.outputs if k == "value" or k.startswith("grad:")}
+        for host in self.exe.run_pipelined(batches, outs, seed):
+            grads = {}
+            for ind in self.program.independents:
+                t = host.get("grad:" + ind)
+                grads[ind] = t.numpy() if t is not None else np.zeros(
+                    self.shapes[ind], dtype=NP_DTYPE[self.program.descriptors[ind].element_kind])
+            yield GradientResult(value=host["value"].numpy(), grads=grads, forward=None, backward=None,
+                                 bundle=self.bundle)

@@ -259,6 +259,21 @@ class SlabEngine:
     def check(self):
         self.exe.check()
 
+    def gradients(self, batches, seed=1.0):
+        """Pipelined end-to-end calls on this rank (``Executable.run_pipelined``):
+        value and owned planes of every gradient per batch of local slabs."""
+        from .api import GradientResult
+
+        lo, hi = self.plan.own_local
+        outs = {"value": self.exe.output("value")}
+        for key in self.exe.outputs:
+            if key.startswith("grad:"):
+                outs[key] = self.exe.output(key)[lo:hi]
+        for host in self.exe.run_pipelined(batches, outs, seed):
+            yield GradientResult(value=host.pop("value").numpy(),
+                                 grads={k[5:]: v.numpy() for k, v in host.items()}, forward=None,
+                                 backward=None, bundle=None)
+
     def gradient(self, host_local_inputs: dict, seed=1.0):
         """End-to-end call on this rank: H2D of the local slabs, the run,
         D2H of the value and of the owned planes of every gradient."""

@@ -185,6 +185,31 @@ def test_data_dependent_branch_follows_each_call_inputs():
     assert len(exes) == 1 and len(exes[0].low.decisions) == 1
 
 
+@pytest.mark.parametrize("name", ["jacobi_2d", "softmax"])
+def test_pipelined_gradients_match_single_calls(name):
+    """Engine.gradients overlaps H2D / launches / D2H across batches; every
+    batch's result must equal its own synchronous Engine.gradient call."""
+    import itertools
+
+    params = {"jacobi_2d": {"N": 40, "TSTEPS": 6}, "softmax": {"R": 64, "SM": 32}}[name]
+    prog, b = W.load(name)
+    eng = Engine(prog, b, params)
+    batches = []
+    for seed in range(5):
+        inp = W.make_inputs(name, prog, params, seed)
+        batches.append({k: torch.from_numpy(v).pin_memory() for k, v in inp.items()})
+    want = []
+    for bt in batches:
+        r = eng.gradient(bt)
+        want.append((np.array(r.value), {k: np.array(v) for k, v in r.grads.items()}))
+    got = list(eng.gradients(itertools.chain(batches, batches[:2])))
+    assert len(got) == 7
+    for r, (v, g) in zip(got, want + want[:2]):
+        assert np.array_equal(r.value, v)
+        for k in g:
+            assert np.array_equal(r.grads[k], g[k]), k
+
+
 def test_engine_without_inputs_rejects_data_dependent_control_loudly():
     prog, b = _bundle("corpus_branchy_scale")
     with pytest.raises(UnsupportedConstruct):
