@@ -210,6 +210,25 @@ def test_pipelined_gradients_match_single_calls(name):
             assert np.array_equal(r.grads[k], g[k]), k
 
 
+def test_run_forward_scalar_trip_count_loop():
+    """run_forward of a loop whose bound is a scalar input, against the
+    reference run_forward (tests/golden/scalar_trip_loop.json)."""
+    import json
+
+    from paper_2509_02197_b200 import run_forward
+
+    rec = json.load(open(os.path.join(GOLD, "scalar_trip_loop.json")))
+    prog = load_program(os.path.join(GOLD, "scalar_trip_loop.fwd.json"))
+    x = np.array(rec["X"])
+    for run in rec["runs"]:
+        r = run_forward(prog, {"X": x, "k": np.array(run["k"])}, rec["params"])
+        assert rel_err(r.value, run["value"]) <= 1e-10
+        assert rel_err(r.env["Y"].cpu().numpy(), np.array(run["Y"])) <= 1e-10
+        assert r.op_count == run["op_count"]
+    with pytest.raises(DomainError):
+        run_forward(prog, {"X": x, "k": np.array(2.5)}, rec["params"])
+
+
 def test_engine_without_inputs_rejects_data_dependent_control_loudly():
     prog, b = _bundle("corpus_branchy_scale")
     with pytest.raises(UnsupportedConstruct):

@@ -175,6 +175,52 @@ def test_data_dependent_branch_both_arms_match_oracle(s):
     assert np.allclose(view(lw.outputs["grad:X"]), want, rtol=1e-14, atol=0)
 
 
+def _scalar_loop():
+    import json
+
+    rec = json.load(open(os.path.join(GOLD, "scalar_trip_loop.json")))
+    return load_program(os.path.join(GOLD, "scalar_trip_loop.fwd.json")), rec
+
+
+def _emulate_forward_probing(prog, params, inputs):
+    from paper_2509_02197_b200.api import _init_env
+    from paper_2509_02197_b200.ir import number_writes
+    from paper_2509_02197_b200.lowering import Lowering, ProgramRun
+
+    shapes = _check_inputs(prog, inputs, params)
+    known = []
+    while True:
+        low = Lowering(known=known)
+        env, ins = _init_env(low, prog, shapes, "")
+        low.entry_inputs = ins
+        try:
+            ProgramRun(low, prog, params, env, versions=number_writes(prog)).run()
+            break
+        except NeedValues as nv:
+            low.finish(list(nv.slots.values()))
+            _, pview = E.execute(low, inputs, ins)
+            known.append({n: np.array(pview(low.resolve(b))) for n, b in nv.slots.items()})
+    low.finish(list(env.values()))
+    _, view = E.execute(low, inputs, ins)
+    return low, env, view, known
+
+
+def test_scalar_trip_count_loop_matches_reference_forward():
+    """Loop header bound to a scalar input (reference interpreter.py:210-219):
+    the trip count comes from a probe of k, then the loop unrolls."""
+    prog, rec = _scalar_loop()
+    x = np.array(rec["X"])
+    for run in rec["runs"]:
+        low, env, view, known = _emulate_forward_probing(prog, rec["params"], {"X": x, "k": np.array(run["k"])})
+        assert len(known) == 1
+        assert abs(float(view(low.resolve(env["O"]))) - run["value"]) <= 1e-10
+        assert np.allclose(view(low.resolve(env["Y"])), run["Y"], rtol=1e-12, atol=0)
+        assert low.flops == run["op_count"]
+    assert rec["non_integer"] == "DomainError"
+    with pytest.raises(DomainError):
+        _emulate_forward_probing(prog, rec["params"], {"X": x, "k": np.array(2.5)})
+
+
 @pytest.mark.parametrize("name", ["atax", "bicg"])
 def test_matvec_pairs_and_rank2_fuse_and_match_goldens(name):
     """Both matrix-vector pairs (forward and adjoint) become one-pass
