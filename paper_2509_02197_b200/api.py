@@ -214,6 +214,10 @@ class Lowered:
     backward_program: Program
 
 
+class NeedsInputs(UnsupportedConstruct):
+    """Lowering reached data-dependent control flow without input values."""
+
+
 def probe_values(nv: NeedValues, inputs: dict, seed=1.0) -> dict:
     """Run the launches lowered before a data-dependent decision and read the
     snapshots it needs (host copies, name -> ndarray)."""
@@ -237,7 +241,7 @@ def probe_lower(lower, inputs: dict | None, seed=1.0):
             return lower(known)
         except NeedValues as nv:
             if inputs is None:
-                raise UnsupportedConstruct(
+                raise NeedsInputs(
                     f"control flow depends on runtime data ({', '.join(sorted(nv.slots))}); "
                     "the launch list needs input values to be lowered") from None
             known.append(probe_values(nv, inputs, seed))
@@ -499,17 +503,34 @@ class Engine:
             shapes = {n: tuple(eval_int(s, self.params) for s in d.shape)
                       for n, d in self.program.descriptors.items() if d.role == "input"}
         self.shapes = dict(shapes)
-        self.exe = build_gradient_executable(self.program, self.bundle, self.params, self.shapes,
-                                             trip_limit=trip_limit, plan=plan)
+        self.trip_limit = trip_limit
+        # programs whose control flow reads runtime data are lowered at the
+        # first call, along the path its inputs take (api.probe_lower)
+        try:
+            self.exe = self._build(None)
+        except NeedsInputs:
+            self.exe = None
+
+    def _build(self, inputs, seed=1.0):
+        return build_gradient_executable(self.program, self.bundle, self.params, self.shapes,
+                                         trip_limit=self.trip_limit, plan=self.plan, inputs=inputs, seed=seed)
+
+    def _run(self, inputs, seed, sync):
+        if self.exe is None:
+            self.exe = self._build(inputs, seed)
+        self.exe.run(inputs, seed, sync=sync)
+        if self.exe.low.decisions and not self.exe.decisions_hold():
+            self.exe = self._build(inputs, seed)
+            self.exe.run(inputs, seed, sync=sync)
 
     def step(self, inputs: dict, seed=1.0, sync=False):
-        self.exe.run(inputs, seed, sync=sync)
+        self._run(inputs, seed, sync)
 
     def check(self):
         self.exe.check()
 
     def gradient(self, inputs: dict, seed=1.0) -> GradientResult:
-        self.exe.run(inputs, seed)
+        self._run(inputs, seed, True)
         return _result(self.exe, self.program, inputs, self.bundle)
 
     def gradients(self, batches, seed=1.0):
@@ -518,7 +539,15 @@ class Engine:
         (``Executable.run_pipelined``): the next batch's H2D copy and the
         previous result's D2H copy overlap the current batch's launches.
         Results carry value and grads (fresh host arrays); ``forward`` /
-        ``backward`` envs are not kept per batch (None)."""
+        ``backward`` envs are not kept per batch (None). Programs with
+        data-dependent control flow run the calls one after another (each
+        call's path is known only after its decisions are read back)."""
+        if self.exe is None or self.exe.low.decisions:
+            for inputs in batches:
+                r = self.gradient(inputs, seed)
+                yield GradientResult(value=np.array(r.value), grads={k: np.array(v) for k, v in r.grads.items()},
+                                     forward=None, backward=None, bundle=self.bundle)
+            return
         outs = {k: self.exe.output(k) for k in self.exe.outputs if k == "value" or k.startswith("grad:")}
         for host in self.exe.run_pipelined(batches, outs, seed):
             grads = {}

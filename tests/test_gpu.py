@@ -229,10 +229,23 @@ def test_run_forward_scalar_trip_count_loop():
         run_forward(prog, {"X": x, "k": np.array(2.5)}, rec["params"])
 
 
-def test_engine_without_inputs_rejects_data_dependent_control_loudly():
+def test_engine_lowers_data_dependent_programs_at_the_first_call():
+    """Engine has no input values at construction; a program whose branch
+    reads runtime data is lowered at the first call and re-lowered when a
+    later call takes the other arm (step, gradient and gradients)."""
     prog, b = _bundle("corpus_branchy_scale")
-    with pytest.raises(UnsupportedConstruct):
-        Engine(prog, b, {"n": 8})
+    eng = Engine(prog, b, {"n": 8})
+    assert eng.exe is None
+    x = np.random.default_rng(6).uniform(0.4, 1.6, 8)
+    batches = [{"X": x, "s": np.array(s)} for s in (0.2, 0.8, 0.8, 0.1)]
+    want = [np.full(8, 2.0) if bt["s"] < 0.5 else np.cos(x) for bt in batches]
+    for bt, w in zip(batches, want):
+        assert np.allclose(eng.gradient(bt).grads["X"], w, rtol=1e-14, atol=0)
+    for r, w in zip(eng.gradients(batches), want):
+        assert np.allclose(r.grads["X"], w, rtol=1e-14, atol=0)
+    dev = {k: torch.as_tensor(v, device="cuda") for k, v in batches[1].items()}
+    eng.step(dev, sync=True)
+    assert np.allclose(eng.exe.output("grad:X").cpu().numpy(), want[1], rtol=1e-14, atol=0)
 
 
 class _LockstepComm:
