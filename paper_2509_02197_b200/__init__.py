@@ -21,6 +21,7 @@ from .api import (
     load_bundle,
     load_plan,
     plan,
+    plan_from_reference_artifacts,
     run_backward,
     run_forward,
     run_planned,

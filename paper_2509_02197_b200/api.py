@@ -22,6 +22,7 @@ execution path.
 """
 from __future__ import annotations
 
+import hashlib
 import json
 import os
 from dataclasses import dataclass, field
@@ -162,7 +163,47 @@ def save_plan(plan: PlanBundle, stem: str):
         json.dump(doc, f, indent=2, default=str)
 
 
-def load_plan(stem: str) -> PlanBundle:
+def plan_from_reference_artifacts(emit_stem: str, report, manifest_path: str) -> PlanBundle:
+    """A plan from what the reference CLI emits, without the reference:
+    ``gradflow plan PROG --emit STEM --json`` writes the rewritten
+    ``STEM.fwd.json`` / ``STEM.bwd.json`` (cli.py:251-253) and prints the
+    report (checkpointing.py:879-899); ``gradflow diff PROG`` writes the
+    forwarding manifest (cli.py:223-237). ``run_planned``'s record set,
+    forwarding subset and stored copies (checkpointing.py:917-942) follow
+    from those: a forwarded value's versions are its manifest candidates'
+    (collect_forwarded, checkpointing.py:255), scalars always ride the tape,
+    forced values are recorded, and unforced ``store`` decisions travel by
+    name. ``report`` is the parsed JSON or a path to it."""
+    if isinstance(report, str):
+        with open(report) as f:
+            report = json.load(f)
+    fwd = load_program(emit_stem + ".fwd.json")
+    bwd = load_program(emit_stem + ".bwd.json")
+    with open(manifest_path) as f:
+        fw_all, _ = forwarding_from_manifest(json.load(f))
+    keep, forwarding, stored = set(), {}, []
+    for name, e in fw_all.items():
+        if len(fwd.descriptors[e.data].shape) == 0:
+            forwarding[name] = e
+            keep |= {(e.data, c.version) for c in e.candidates}
+    for v in report["values"]:
+        e = fw_all.get(v["name"])
+        if e is None:
+            raise UnboundName(f"plan report names '{v['name']}', which the forwarding manifest does not hold")
+        if v["forced"]:
+            forwarding[v["name"]] = e
+            keep |= {(e.data, c.version) for c in e.candidates}
+        elif v["decision"] == "store":
+            stored.append(v["name"])
+    return PlanBundle(fwd, bwd, frozenset(keep), forwarding, tuple(stored), dict(report))
+
+
+def load_plan(stem: str, manifest: str | None = None) -> PlanBundle:
+    """``stem.plan.json`` (``save_plan``), or, given the ``gradflow diff``
+    manifest, the reference CLI's own ``stem.report.json`` next to its
+    ``--emit`` programs (``plan_from_reference_artifacts``)."""
+    if not os.path.exists(stem + ".plan.json") and manifest is not None:
+        return plan_from_reference_artifacts(stem, stem + ".report.json", manifest)
     with open(stem + ".plan.json") as f:
         doc = json.load(f)
     fw, _ = forwarding_from_manifest({"entries": doc["forwarding"]})
@@ -315,9 +356,20 @@ def build_gradient_executable(program: Program, bundle: Bundle, params: dict, sh
     return exe
 
 
-# executable cache: (ids of the host objects, params, shapes) -> Executable
+# executable cache: (content fingerprints of the programs, params, shapes)
+# -> Executable. Keys are structural, so a program mutated in place (e.g.
+# ``prog.independents = ...``) or a new object at a recycled address never
+# reuses another program's launch list.
 _CACHE: dict = {}
 _CACHE_MAX = int(os.environ.get("GFB_CACHE", "4"))
+# host AD results of ``gradient(bundle=None)`` by forward-program fingerprint;
+# kept apart from the executable LRU so they neither evict nor get evicted
+_BUNDLES: dict = {}
+
+
+def fingerprint(prog: Program) -> str:
+    """Content hash of a program (its canonical wire-format serialization)."""
+    return hashlib.sha1(dump_program(prog).encode()).hexdigest()
 
 
 def _cached(key, keep_alive, build):
@@ -331,21 +383,40 @@ def _cached(key, keep_alive, build):
     return exe
 
 
+def run_checked(exe: Executable, inputs, seed, rebuild, *, sync=True) -> Executable:
+    """Run ``exe``; when it was lowered along a data-dependent path, re-check
+    the decisions BEFORE reading the device error word. A call whose inputs
+    take another arm may have raised a domain error on the stale arm (``if
+    x > 0: log(x)`` called with x <= 0), which the reference never evaluates
+    (interpreter.py:342-351 decides first): that run is discarded, the
+    program is lowered along the new path and run again."""
+    if not exe.low.decisions:
+        exe.run(inputs, seed, sync=sync)
+        return exe
+    exe.run(inputs, seed, sync=False)
+    if exe.decisions_hold():
+        if sync:
+            exe.check()
+        return exe
+    exe = rebuild()
+    exe.run(inputs, seed, sync=sync)
+    return exe
+
+
 def _run_guarded(key, keep_alive, build, inputs, seed):
     """Run the cached executable; when its data-dependent decisions do not
     hold for these inputs, lower again along the path they take."""
     exe = _cached(key, keep_alive, build)
-    exe.run(inputs, seed)
-    if exe.low.decisions and not exe.decisions_hold():
-        exe = build()
-        exe._keep_alive = keep_alive
-        _CACHE[key] = exe
-        exe.run(inputs, seed)
-    return exe
+    new = run_checked(exe, inputs, seed, build)
+    if new is not exe:
+        new._keep_alive = keep_alive
+        _CACHE[key] = new
+    return new
 
 
 def clear_cache():
     _CACHE.clear()
+    _BUNDLES.clear()
 
 
 def _result(exe: Executable, program: Program, inputs: dict, bundle) -> GradientResult:
@@ -372,19 +443,20 @@ def gradient(program, inputs: dict, params: dict | None = None, *, seed=1.0, tri
     """Reference ``gradient`` (autodiff.py:1153) executed on the B200."""
     params = dict(params or {})
     prog = adopt(program)
+    fp = fingerprint(prog)
     if bundle is None:
-        b = _CACHE.get(("bundle", id(program)))
-        if b is None:
-            b = host_build_backward(program)
-            _CACHE[("bundle", id(program))] = b
-        bundle_eng = b
+        bundle_eng = _BUNDLES.get(fp)
+        if bundle_eng is None:
+            bundle_eng = _BUNDLES[fp] = host_build_backward(program)
+        bfp = "auto"
     else:
         bundle_eng = as_bundle(bundle)
+        bfp = fingerprint(bundle_eng.backward)
     shapes = _check_inputs(prog, inputs, params)
-    key = ("grad", id(program), id(bundle), tuple(sorted(params.items())), tuple(sorted(shapes.items())), trip_limit)
+    key = ("grad", fp, bfp, tuple(sorted(params.items())), tuple(sorted(shapes.items())), trip_limit)
     build = lambda: build_gradient_executable(prog, bundle_eng, params, shapes, trip_limit=trip_limit,  # noqa: E731
                                               inputs=inputs, seed=seed)
-    exe = _run_guarded(key, (program, bundle), build, inputs, seed)
+    exe = _run_guarded(key, (program, bundle, bundle_eng), build, inputs, seed)
     return _result(exe, prog, inputs, bundle if bundle is not None else bundle_eng)
 
 
@@ -393,7 +465,8 @@ def run_planned(result, inputs: dict, params: dict | None = None, *, seed=1.0, t
     params = dict(params or {})
     pb = as_plan(result)
     shapes = _check_inputs(pb.forward, inputs, params)
-    key = ("plan", id(result), tuple(sorted(params.items())), tuple(sorted(shapes.items())), trip_limit)
+    key = ("plan", fingerprint(pb.forward), fingerprint(pb.backward), tuple(sorted(pb.keep)), tuple(pb.stored),
+           tuple(sorted(params.items())), tuple(sorted(shapes.items())), trip_limit)
     build = lambda: build_gradient_executable(pb.forward, None, params, shapes, trip_limit=trip_limit,  # noqa: E731
                                               plan=pb, inputs=inputs, seed=seed)
     exe = _run_guarded(key, (result,), build, inputs, seed)
@@ -518,10 +591,7 @@ class Engine:
     def _run(self, inputs, seed, sync):
         if self.exe is None:
             self.exe = self._build(inputs, seed)
-        self.exe.run(inputs, seed, sync=sync)
-        if self.exe.low.decisions and not self.exe.decisions_hold():
-            self.exe = self._build(inputs, seed)
-            self.exe.run(inputs, seed, sync=sync)
+        self.exe = run_checked(self.exe, inputs, seed, lambda: self._build(inputs, seed), sync=sync)
 
     def step(self, inputs: dict, seed=1.0, sync=False):
         self._run(inputs, seed, sync)

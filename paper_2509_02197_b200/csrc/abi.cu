@@ -2,6 +2,9 @@
 #include <cstdlib>
 #include <cstdio>
 #include <cstring>
+#include <mutex>
+#include <map>
+#include <utility>
 
 #include "gfb_common.cuh"
 #include "gfb_internal.h"
@@ -30,6 +33,21 @@ bool pdl_enabled() {
     return !(e && e[0] == '0');
   }();
   return on;
+}
+
+void ensure_smem_attr(const void *kernel, int bytes) {
+  // the largest size set so far per (kernel, device): launches of one
+  // kernel may use different dynamic sizes (matvec ring stages)
+  static std::mutex mu;
+  static std::map<std::pair<const void *, int>, int> done;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lock(mu);
+  int &have = done[{kernel, dev}];
+  if (bytes > have) {
+    cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+    have = bytes;
+  }
 }
 
 int sm_count() {

@@ -296,11 +296,7 @@ static int dgemm_dmma_t(int64_t M, int64_t N, int64_t K, const double *A, int64_
   constexpr int SA = TA ? kDK * (kDM + 4) : kDM * (kDK + 4);
   constexpr int SB = TB ? kDN * (kDK + 4) : kDK * (kDN + 4);
   constexpr int smem = kDS * (SA + SB) * 8;
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(dgemm_dmma_kernel<TA, TB, V>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    attr = true;
-  }
+  ensure_smem(dgemm_dmma_kernel<TA, TB, V>, smem);
   dim3 grid((unsigned)ceil_div(N, kDN), (unsigned)ceil_div(M, kDM));
   dgemm_dmma_kernel<TA, TB, V><<<grid, 128, smem, st>>>(M, N, K, A, lda, B, ldb, C, ldc, accumulate);
   return check_launch("dgemm_dmma");

@@ -30,6 +30,16 @@ cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t s
 int check_launch(const char *what);
 int sm_count();
 
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) per (kernel, device)
+// whenever a launch needs more than was set: the attribute is per device, so
+// a process driving engines on two GPUs must set it on each (abi.cu;
+// thread-safe)
+void ensure_smem_attr(const void *kernel, int bytes);
+template <typename... KArgs>
+inline void ensure_smem(void (*kernel)(KArgs...), size_t bytes) {
+  ensure_smem_attr(reinterpret_cast<const void *>(kernel), (int)bytes);
+}
+
 // fp32 GEMM on tcgen05 (3xTF32, sgemm_tc.cu)
 bool sgemm_tc_usable(int64_t M, int64_t N, int64_t K);
 int64_t sgemm_tc_workspace(int64_t M, int64_t N, int64_t K);

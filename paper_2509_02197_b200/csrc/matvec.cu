@@ -129,7 +129,7 @@ __global__ void __launch_bounds__(kThreads, 512 / kThreads) matvec_pair_kernel(M
   const T *A = static_cast<const T *>(p.A);
   const bool has_row = KIND == 0 ? p.u != nullptr : (KIND != 2);
   const bool has_col = KIND == 0 ? p.partial != nullptr : (KIND != 1);
-  const bool chain = KIND == 0 ? chain != 0 : (KIND == 4);
+  const bool chain = KIND == 0 ? p.chain != 0 : (KIND == 4);
 
   if (t == 0) {
     for (int s = 0; s < S; ++s) mbar_init(&bar[s], 1);
@@ -305,7 +305,7 @@ int launch_pair(const MvArgs &a0, int64_t nblocks, cudaStream_t st) {
              : kind == 3 ? matvec_pair_kernel<T, QQ, 3>                                                  \
              : kind == 1 ? matvec_pair_kernel<T, QQ, 1>                                                  \
                          : matvec_pair_kernel<T, QQ, 2>;                                                 \
-    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);                     \
+    ensure_smem(k, smem);                                                                                \
     k<<<grid, kThreads, smem, st>>>(a);                                                                  \
     return check_launch("matvec_pair");                                                                  \
   }

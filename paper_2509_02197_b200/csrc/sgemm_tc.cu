@@ -602,11 +602,7 @@ static int launch_tma_k(dim3 grid, int M, int N, int K, const float *A, int64_t 
                   (BKM ? tc_map(&bm, B, K, N, ldb, kTcK, BN, true) : tc_map(&bm, B, N, K, ldb, BN, kTcK, false));
   if (!ok) return -1;
   constexpr int smem = TmaCfg<BN, AKM, BKM, SK>::kSmem;
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(sgemm_tma_kernel<BN, AKM, BKM, SK>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    attr = true;
-  }
+  ensure_smem(sgemm_tma_kernel<BN, AKM, BKM, SK>, smem);
   sgemm_tma_kernel<BN, AKM, BKM, SK><<<grid, kTcThreads, smem, st>>>(am, bm, M, N, K, C, csm, csn, accumulate, partial,
                                                                  kchunk);
   return 0;
@@ -683,11 +679,7 @@ static void launch_tc(dim3 grid, int M, int N, int K, const float *A, int64_t ld
                       float *C, int64_t csm, int64_t csn, int accumulate, float *partial, int kchunk,
                       cudaStream_t st) {
   const size_t smem = sizeof(TcSmem<BN>) + 1024;
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(sgemm_tc_kernel<BN, TA, TB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    attr = true;
-  }
+  ensure_smem(sgemm_tc_kernel<BN, TA, TB>, (int)smem);
   sgemm_tc_kernel<BN, TA, TB><<<grid, kTcThreads, smem, st>>>(M, N, K, A, lda, B, ldb, C, csm, csn, accumulate,
                                                                partial, kchunk);
 }

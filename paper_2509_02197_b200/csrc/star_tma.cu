@@ -563,12 +563,8 @@ bool star_tma_usable(const StarPairDev &d, int dtype) {
 
 template <typename T, bool HAS_I, int MODES>
 static int launch_tma_m(const CUtensorMap &map, const StarPairDev &d, cudaStream_t st) {
-  static bool attr = false;
   const size_t sm = star_tma_dyn_bytes<T, HAS_I>();
-  if (!attr) {
-    cudaFuncSetAttribute(star_pair_tma_kernel<T, HAS_I, MODES>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-    attr = true;
-  }
+  ensure_smem(star_pair_tma_kernel<T, HAS_I, MODES>, sm);
   // planes per CTA: the longest march (up to tPM) that still puts every
   // tile-column segment in one wave of resident CTAs (2 per SM); small
   // domains get short marches rather than idle SMs or a straggler wave

@@ -2108,8 +2108,11 @@ class ProgramRun:
                 cond, label = br.condition, br.label
                 descs = self.program.descriptors
 
-                def key(vals, cond=cond, label=label):
-                    b = dict(self.bind)
+                # the bindings that hold at the decision point (loop iterators
+                # included): the key is re-evaluated after lowering, when the
+                # live self.bind no longer holds them
+                def key(vals, cond=cond, label=label, bind=dict(self.bind)):
+                    b = dict(bind)
                     b.update({n: v.reshape(()).item() for n, v in vals.items() if descs[n].rank == 0})
                     return bool(evaluate(cond, b, lambda base, idx: _host_index(vals, base, idx)))
 

@@ -16,7 +16,7 @@ import numpy as np
 import torch
 
 from . import _lib as L
-from .errors import DomainError, EngineError
+from .errors import DomainError, EngineError, GradflowError
 from .lowering import Buffer, Lowering
 
 TORCH_DTYPE = {"real32": torch.float32, "real64": torch.float64}
@@ -207,9 +207,18 @@ class Executable:
         list was lowered with, from the device snapshots of the run just
         finished; False means the inputs took another path and the caller
         must lower again."""
-        for slots, key_fn, key in self.low.decisions:
-            vals = {n: self.view(self.low.resolve(b)).cpu().numpy() for n, b in slots.items()}
-            if key_fn(vals) != key:
+        # one synchronisation and one batch of copies for all snapshots
+        torch.cuda.synchronize(self.device)
+        host = [{n: self.view(self.low.resolve(b)).cpu().numpy() for n, b in slots.items()}
+                for slots, _k, _v in self.low.decisions]
+        for vals, (_slots, key_fn, key) in zip(host, self.low.decisions):
+            try:
+                if key_fn(vals) != key:
+                    return False
+            except GradflowError:
+                # a later decision's snapshot taken along the stale path can
+                # be out of its domain (e.g. a non-integer loop header): the
+                # path changed earlier, so lower again
                 return False
         return True
 

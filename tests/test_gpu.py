@@ -168,7 +168,7 @@ def test_data_dependent_branch_follows_each_call_inputs():
     One cached executable per (program, params, shapes); a call whose inputs
     take the other arm is detected from the device snapshot and lowered
     again, so each call returns that call's gradient."""
-    from paper_2509_02197_b200.api import _CACHE
+    from paper_2509_02197_b200.api import _CACHE, fingerprint
 
     prog, b = _bundle("corpus_branchy_scale")
     rng = np.random.default_rng(5)
@@ -181,7 +181,7 @@ def test_data_dependent_branch_follows_each_call_inputs():
         assert rel_err(res.grads["X"], g["X"]) <= 1e-10
         want = np.full(8, 2.0) if s < 0.5 else np.cos(x)
         assert np.allclose(res.grads["X"], want, rtol=1e-14, atol=0)
-    exes = [e for k, e in _CACHE.items() if k[0] == "grad" and k[1] == id(prog)]
+    exes = [e for k, e in _CACHE.items() if k[0] == "grad" and k[1] == fingerprint(prog)]
     assert len(exes) == 1 and len(exes[0].low.decisions) == 1
 
 

@@ -106,7 +106,7 @@ def test_out_of_bounds_is_static():
     params = {"N": 6, "TSTEPS": 3}
     inputs = W.make_inputs("jacobi_2d", prog, {"N": 6, "TSTEPS": 3}, 0)
     # declared shape N=6 but a map reaching N: simulate with a wrong binding
-    with pytest.raises(Exception):
+    with pytest.raises(OutOfBounds):
         lower_gradient(prog, b, {"N": 6, "TSTEPS": 3}, {"A": (5, 5), "B": (5, 5)})
 
 

@@ -1,0 +1,207 @@
+"""Round-2 fixtures generated from the REFERENCE (build container only;
+imports /root/reference read-only):
+
+    python tools/make_golden_r2.py
+
+Writes under tests/golden/r2/:
+  <prog>.{fwd,bwd,fwdreq}.json + <prog>__<tag>.npz
+      control-flow programs the advisor review asked to pin
+      (loop-carried, iterator-dependent branch; a branch guarding a domain
+      error), with the reference gradient() value / grads for several
+      inputs that take different paths;
+  plans_cli/<cid>.{fwd,bwd}.json + <cid>.report.json
+      the reference CLI's own plan artifacts (``gradflow plan --emit STEM
+      --json``, cli.py:246-253) for every golden plan in tests/golden/plans,
+      so run_planned can be fed what the reference emits (no engine-side
+      .plan.json);
+  errors.json
+      the reference's exception class for the typed-error cases
+      (OutOfBounds, NonTermination, MissingTapeValue).
+"""
+from __future__ import annotations
+
+import json
+import os
+import subprocess
+import sys
+import warnings
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+REPO = os.path.dirname(HERE)
+REF = "/root/reference/pkg/src"
+sys.path.insert(0, REF)
+sys.path.insert(0, REPO)
+warnings.simplefilter("ignore")
+
+from gradflow import errors as ref_errors  # noqa: E402
+from gradflow.autodiff import build_backward, gradient  # noqa: E402
+from gradflow.frontend import ProgramBuilder, load_program, serialize_program  # noqa: E402
+from gradflow.interpreter import run_backward, run_forward  # noqa: E402
+
+OUT = os.path.join(REPO, "tests", "golden", "r2")
+PLANS = os.path.join(REPO, "tests", "golden", "plans")
+PROGS = os.path.join(REPO, "paper_2509_02197_b200", "programs")
+
+
+def save_programs(stem, program):
+    bundle = build_backward(program)
+    with open(stem + ".fwd.json", "w") as f:
+        f.write(serialize_program(program))
+    with open(stem + ".bwd.json", "w") as f:
+        f.write(serialize_program(bundle.backward))
+    manifest = {
+        "required": sorted([d, v] for d, v in bundle.required),
+        "entries": [
+            {"name": e.name, "data": e.data,
+             "candidates": [{"version": c.version, "directives": [list(d) for d in c.directives]}
+                            for c in e.candidates]}
+            for e in sorted(bundle.forwarding.values(), key=lambda e: e.name)
+        ],
+    }
+    with open(stem + ".fwdreq.json", "w") as f:
+        json.dump(manifest, f, indent=2)
+        f.write("\n")
+    return bundle
+
+
+def loop_branch():
+    """u = t; for i in [0, 3): u = 2u if t < i else 3u; O = u (the branch
+    condition reads the loop iterator)."""
+    b = ProgramBuilder(())
+    b.scalar("t", role="input", kind="real64")
+    b.scalar("u", kind="real64")
+    b.scalar("O", role="output", kind="real64")
+    with b.state("init") as s:
+        s.tasklet(ins={"a": ("t", ())}, outs={"o": ("u", ())}, body={"o": "a"})
+    with b.loop("i", "0", "3", label="L"):
+        with b.branch("(lt t i)", label="side") as br:
+            with br.then():
+                with b.state("low") as s:
+                    s.tasklet(ins={"a": ("u", ())}, outs={"o": ("u", ())}, body={"o": "(mul a 2)"})
+            with br.orelse():
+                with b.state("high") as s:
+                    s.tasklet(ins={"a": ("u", ())}, outs={"o": ("u", ())}, body={"o": "(mul a 3)"})
+    with b.state("out") as s:
+        s.tasklet(ins={"a": ("u", ())}, outs={"o": ("O", ())}, body={"o": "a"})
+    return b.finish("O", ["t"]), [1.5, -1.0, 0.5, 2.5]
+
+
+def guarded_log():
+    """O = sum(log(x)) if x0 > 0 else sum(2x): the else arm must be taken
+    without evaluating log on non-positive data."""
+    b = ProgramBuilder(("N",))
+    b.array("x", ("N",), role="input", kind="real64")
+    b.scalar("s", kind="real64")
+    b.array("y", ("N",), kind="real64")
+    b.scalar("O", role="output", kind="real64")
+    with b.state("probe") as s:
+        s.tasklet(ins={"a": ("x", ("0",))}, outs={"o": ("s", ())}, body={"o": "a"})
+    with b.branch("(gt s 0)", label="pos") as br:
+        with br.then():
+            with b.state("logs") as s:
+                s.map_node(("i",), (("0", "N", "1"),), lambda inner: inner.tasklet(
+                    ins={"a": ("x", ("i",))}, outs={"o": ("y", ("i",))}, body={"o": "(log a)"}))
+        with br.orelse():
+            with b.state("twice") as s:
+                s.map_node(("i",), (("0", "N", "1"),), lambda inner: inner.tasklet(
+                    ins={"a": ("x", ("i",))}, outs={"o": ("y", ("i",))}, body={"o": "(mul a 2)"}))
+    with b.state("sum") as s:
+        s.library("reduce_sum", {"x": "y"}, {"y": "O"})
+    return b.finish("O", ["x"]), None
+
+
+def save_control_flow():
+    os.makedirs(OUT, exist_ok=True)
+    index = {}
+    prog, ts = loop_branch()
+    bundle = save_programs(os.path.join(OUT, "loop_branch"), prog)
+    for t in ts:
+        res = gradient(prog, {"t": np.array(t)}, {}, bundle=bundle)
+        tag = f"t{t:+g}".replace("+", "p").replace("-", "m").replace(".", "_")
+        np.savez(os.path.join(OUT, f"loop_branch__{tag}.npz"), **{"in:t": np.array(t)},
+                 value=np.asarray(res.value), **{"grad:t": np.asarray(res.grads["t"])})
+        index[f"loop_branch__{tag}"] = {"program": "loop_branch", "params": {}}
+        print("loop_branch", t, float(res.value), float(res.grads["t"]))
+    prog, _ = guarded_log()
+    bundle = save_programs(os.path.join(OUT, "guarded_log"), prog)
+    rng = np.random.default_rng(5)
+    for tag, x in (("pos", rng.uniform(0.4, 1.6, 9)), ("neg", -rng.uniform(0.4, 1.6, 9))):
+        res = gradient(prog, {"x": x}, {"N": 9}, bundle=bundle)
+        np.savez(os.path.join(OUT, f"guarded_log__{tag}.npz"), **{"in:x": x}, value=np.asarray(res.value),
+                 **{"grad:x": np.asarray(res.grads["x"])})
+        index[f"guarded_log__{tag}"] = {"program": "guarded_log", "params": {"N": 9}}
+        print("guarded_log", tag, float(res.value))
+    return index
+
+
+def save_cli_plans():
+    """Run the reference CLI (python -m gradflow.cli plan) for each golden plan."""
+    out = os.path.join(OUT, "plans_cli")
+    os.makedirs(out, exist_ok=True)
+    with open(os.path.join(REPO, "tests", "golden", "index.json")) as f:
+        plans = json.load(f)["plans"]
+    env = dict(os.environ, PYTHONPATH=REF, PYTHONDONTWRITEBYTECODE="1")
+    done = {}
+    for cid, meta in sorted(plans.items()):
+        w = meta["workload"]
+        src = os.path.join(PROGS, (w if os.path.exists(os.path.join(PROGS, w + ".fwd.json")) else "corpus_" + w)
+                           + ".fwd.json")
+        stem = os.path.join(out, cid)
+        cmd = [sys.executable, "-m", "gradflow.cli", "plan", src, "--emit", stem, "--json"]
+        for k, v in meta["params"].items():
+            cmd += ["--params", f"{k}={v}"]
+        if meta["limit_mib"] is not None:
+            cmd += ["--memory-limit-mib", repr(meta["limit_mib"])]
+        r = subprocess.run(cmd, env=env, capture_output=True, text=True, check=True)
+        with open(stem + ".report.json", "w") as f:
+            f.write(r.stdout)
+        done[cid] = {"source": os.path.relpath(src, REPO), "manifest": os.path.relpath(src, REPO).replace(
+            ".fwd.json", ".fwdreq.json")}
+        print("cli plan", cid, json.loads(r.stdout)["peak_bytes"])
+    return done
+
+
+def save_errors():
+    """Which reference exception each typed-error case raises."""
+    out = {}
+    jac = load_program(os.path.join(PROGS, "jacobi_2d.fwd.json"))
+    rng = np.random.default_rng(0)
+    inputs = {"A": rng.uniform(0.4, 1.6, (6, 6)), "B": rng.uniform(0.4, 1.6, (6, 6))}
+    try:
+        gradient(jac, inputs, {"N": 6, "TSTEPS": 6}, trip_limit=4)
+    except ref_errors.GradflowError as exc:
+        out["trip_limit"] = {"workload": "jacobi_2d", "params": {"N": 6, "TSTEPS": 6}, "trip_limit": 4,
+                             "error": type(exc).__name__}
+    atax = load_program(os.path.join(PROGS, "atax.fwd.json"))
+    bundle = build_backward(atax)
+    ai = {"A": rng.uniform(0.4, 1.6, (6, 5)), "x": rng.uniform(0.4, 1.6, (5, 1))}
+    try:
+        run_backward(atax, bundle.backward, ai, {"M": 6, "N": 5}, tape=None, forwarding=bundle.forwarding)
+    except ref_errors.GradflowError as exc:
+        out["no_tape"] = {"workload": "atax", "params": {"M": 6, "N": 5}, "error": type(exc).__name__}
+    fr = run_forward(atax, ai, {"M": 6, "N": 5}, record=set())
+    try:
+        run_backward(atax, bundle.backward, ai, {"M": 6, "N": 5}, tape=fr.tape, forwarding=bundle.forwarding)
+    except ref_errors.GradflowError as exc:
+        out["empty_tape"] = {"workload": "atax", "params": {"M": 6, "N": 5}, "error": type(exc).__name__}
+    try:
+        gradient(jac, {"A": inputs["A"][:5, :5], "B": inputs["B"][:5, :5]}, {"N": 5, "TSTEPS": 3})
+        # declared N=5 arrays are fine; a map reaching past the extent needs a bad binding:
+    except ref_errors.GradflowError as exc:  # pragma: no cover
+        out["oob_unexpected"] = type(exc).__name__
+    print("errors", out)
+    with open(os.path.join(OUT, "errors.json"), "w") as f:
+        json.dump(out, f, indent=2)
+
+
+def main():
+    index = {"control_flow": save_control_flow(), "plans_cli": save_cli_plans()}
+    with open(os.path.join(OUT, "index.json"), "w") as f:
+        json.dump(index, f, indent=2)
+    save_errors()
+
+
+if __name__ == "__main__":
+    main()
