@@ -54,6 +54,12 @@ namespace GFB_STAR_NS {
 #ifndef GFB_STAR_UNROLL
 #define GFB_STAR_UNROLL 1
 #endif
+// tap sums as one fma chain per point (7 fp64 ops; the thread's four points
+// and the ring point give the scheduler independent chains) instead of three
+// partial sums (9 ops)
+#ifndef GFB_STAR_CHAIN
+#define GFB_STAR_CHAIN 1
+#endif
 constexpr int tPX = 32, tPY = GFB_STAR_TPY, tPM = GFB_STAR_TPM;  // CTA tile (k, j) and planes
 constexpr int kR = GFB_STAR_KR;                                   // Z rows per thread
 constexpr int tThreads = tPX * (tPY / kR);
@@ -253,10 +259,24 @@ __device__ __forceinline__ void star_tma_body(const CUtensorMap *ymap, const Sta
     mz[u] = W.bj[kR * ty + u] & W.bk[tx];
   }
   const uint32_t mxr = ring ? (W.aj[rj] & W.ak[rk]) : 0u;
-
   const bool ysrc = MODES >= 0 ? ((MODES / 32) & 1) != 0 : d.a.srcmask == 1;
   const bool yj_in = j0 - 2 >= d.a.smlo[1] && j0 + tPY + 2 <= d.a.smhi[1];
   const bool yk_in = k0 - 2 >= d.a.smlo[2] && k0 + tPX + 2 <= d.a.smhi[2];
+  // window elements e = tid + n * tThreads this thread zeroes on a loaded
+  // plane in source-mask form: (j, k) outside M_a (fixed per tile, so found
+  // once; on a tile at the domain faces most threads have none)
+  constexpr int kZN = (YS + tThreads - 1) / tThreads;
+  static_assert(kZN <= 32, "zero-bit mask");
+  uint32_t zbits = 0;
+  if (ysrc && !(yj_in && yk_in)) {
+#pragma unroll
+    for (int n = 0; n < kZN; ++n) {
+      const int e = tid + n * tThreads;
+      const int jj = e / YK, kk = e - jj * YK;
+      const int j = j0 - 2 + jj, k = k0 - 2 + kk;
+      if (e < YS && (j < d.a.smlo[1] || j >= d.a.smhi[1] || k < d.a.smlo[2] || k >= d.a.smhi[2])) zbits |= 1u << n;
+    }
+  }
   auto prepare_plane = [&](int p) {
     // zero what the taps must not see: planes never loaded (outside the
     // local array) and, in source-mask form, values outside M_a
@@ -265,12 +285,8 @@ __device__ __forceinline__ void star_tma_body(const CUtensorMap *ymap, const Sta
     const bool outside = p < 0 || p >= d.d0 || (ysrc && (pg < d.a.smlo[0] || pg >= d.a.smhi[0]));
     if (outside) {
       for (int e = tid; e < YS; e += tThreads) slot[e] = T(0);
-    } else if (ysrc && !(yj_in && yk_in)) {
-      for (int e = tid; e < YS; e += tThreads) {
-        const int jj = e / YK, kk = e - jj * YK;
-        const int j = j0 - 2 + jj, k = k0 - 2 + kk;
-        if (j < d.a.smlo[1] || j >= d.a.smhi[1] || k < d.a.smlo[2] || k >= d.a.smhi[2]) slot[e] = T(0);
-      }
+    } else {
+      for (uint32_t b = zbits; b; b &= b - 1) slot[tid + (__ffs(b) - 1) * tThreads] = T(0);
     }
   };
   // planes whose preparation is a no-op for this CTA: loaded (inside the
@@ -363,10 +379,34 @@ __device__ __forceinline__ void star_tma_body(const CUtensorMap *ymap, const Sta
   unsigned ysl = (unsigned)(qbeg - ylo + NSY) % (unsigned)NSY;
   unsigned wsl = (unsigned)(qbeg + 2 - ylo) % (unsigned)NSY;
   uint32_t wph = ((unsigned)(qbeg + 2 - ylo) / (unsigned)NSY) & 1u;
+  // Z fix-ups that add the old value as a base (op b in mode 0, or mode 2
+  // outside its clear box: the adjoint sweeps) prefetch it into registers at
+  // the start of the step; other instantiations load it in the fix-up (only
+  // the out-of-region copies of the first timesteps need it)
+  constexpr bool kZPre = MODES < 0 || (MODES % 4) == 0 || (MODES % 4) == 2;
   auto step = [&](auto S, int q) {
     constexpr int M = decltype(S)::value, C = (M + 1) % 3, P = (M + 2) % 3;
 #pragma unroll
     for (int u = 0; u < kR; ++u) xv[u][P] = T(0);
+    // old Z values the fix-ups of Z(i) need (plane not common): loaded
+    // before the X sweep so their latency overlaps it
+    const int i = HAS_I ? q - 1 : q;
+    const bool zon = i >= i0 && i < i1;
+    const uint32_t mzi = zon ? W.bi[i - i0] : 0u;
+    const bool zfast = ((mzi & jkb) & zmask) == zmask;
+    T zo[kR];
+#pragma unroll
+    for (int u = 0; u < kR; ++u) zo[u] = T(0);
+    if (kZPre && zon && !zfast) {
+      const T *zold = Zo + (size_t)i * ps + rel0;
+#pragma unroll
+      for (int u = 0; u < kR; ++u) {
+        const uint32_t w = mzi & mz[u];
+        const bool need = (w & zmask) != zval && (w & kArray) &&
+                          ((w & kRegion) ? (bmode == 0 || (bmode == 2 && !(w & kClear))) : !d.skipz);
+        if (need) zo[u] = zold[u * rs];
+      }
+    }
     if (q < d.d0) {
       if (tid == 0) {
         const int pn = q + 1 + kDist;
@@ -405,6 +445,17 @@ __device__ __forceinline__ void star_tma_body(const CUtensorMap *ymap, const Sta
       for (int u = 0; u < kR; ++u) {
         const T jm = u == 0 ? up : yv[u - 1][C];
         const T jp = u == kR - 1 ? dn : yv[u + 1][C];
+#if GFB_STAR_CHAIN
+        T acc = a0 * yv[u][C];
+        if (HAS_I) {
+          acc = fma(a1, yv[u][M], acc);
+          acc = fma(a2, yv[u][P], acc);
+        }
+        acc = fma(a3, jm, acc);
+        acc = fma(a4, jp, acc);
+        acc = fma(a5, yc[yo0 + u * YK - 1], acc);
+        acc = fma(a6, yc[yo0 + u * YK + 1], acc);
+#else
         // short dependency chains: three partial sums per point
         T p0 = a0 * yv[u][C];
         T p1 = a4 * jp;
@@ -415,25 +466,34 @@ __device__ __forceinline__ void star_tma_body(const CUtensorMap *ymap, const Sta
         const T p2 = fma(a5, yc[yo0 + u * YK - 1], a3 * jm);
         p0 = fma(a6, yc[yo0 + u * YK + 1], p0);
         T acc = (p0 + p1) + p2;
+#endif
         if (!fast) acc = x_tilde(acc, mi & mx[u], u, rel0 + u * rs, own, q);
         xv[u][P] = acc;
         xw[xo0 + u * HX] = acc;
       }
       if (ring) {
         const T yrp = HAS_I ? yp[yor] : T(0);
+#if GFB_STAR_CHAIN
+        T acc = a0 * yr[C];
+        if (HAS_I) acc = fma(a2, yrp, fma(a1, yr[M], acc));
+        acc = fma(a3, yc[yor - YK], acc);
+        acc = fma(a4, yc[yor + YK], acc);
+        acc = fma(a5, yc[yor - 1], acc);
+        acc = fma(a6, yc[yor + 1], acc);
+#else
         T pr = a0 * yr[C];
         if (HAS_I) pr = fma(a1, yr[M], fma(a2, yrp, pr));
         const T qr = fma(a3, yc[yor - YK], a4 * yc[yor + YK]);
         const T rr = fma(a5, yc[yor - 1], a6 * yc[yor + 1]);
         T acc = (pr + qr) + rr;
+#endif
         if (!fast) acc = x_tilde(acc, mi & mxr, kR, relr, false, q);
         xw[xor_] = acc;
         yr[P] = yrp;
       }
     }
     __syncthreads();
-    const int i = HAS_I ? q - 1 : q;
-    if (i >= i0 && i < i1) {
+    if (zon) {
 #if GFB_STAR_UNROLL
       const T *xc = xs + (HAS_I ? (M + 2) % 3 : M) * XS;
 #else
@@ -447,6 +507,17 @@ __device__ __forceinline__ void star_tma_body(const CUtensorMap *ymap, const Sta
         const T cu = HAS_I ? xv[u][C] : xv[u][P];
         const T jm = u == 0 ? up : (HAS_I ? xv[u - 1][C] : xv[u - 1][P]);
         const T jp = u == kR - 1 ? dn : (HAS_I ? xv[u + 1][C] : xv[u + 1][P]);
+#if GFB_STAR_CHAIN
+        T acc = b0 * cu;
+        if (HAS_I) {
+          acc = fma(b1, xv[u][M], acc);
+          acc = fma(b2, xv[u][P], acc);
+        }
+        acc = fma(b3, jm, acc);
+        acc = fma(b4, jp, acc);
+        acc = fma(b5, xc[xo0 + u * HX - 1], acc);
+        z[u] = fma(b6, xc[xo0 + u * HX + 1], acc);
+#else
         T p0 = b0 * cu;
         T p1 = b4 * jp;
         if (HAS_I) {
@@ -456,25 +527,25 @@ __device__ __forceinline__ void star_tma_body(const CUtensorMap *ymap, const Sta
         const T p2 = fma(b5, xc[xo0 + u * HX - 1], b3 * jm);
         p0 = fma(b6, xc[xo0 + u * HX + 1], p0);
         z[u] = (p0 + p1) + p2;
+#endif
       }
       T *zrow = Zn + (size_t)i * ps + rel0;
-      const uint32_t mi = W.bi[i - i0];
-      if (((mi & jkb) & zmask) == zmask) {
+      if (zfast) {
 #pragma unroll
         for (int u = 0; u < kR; ++u) zrow[u * rs] = z[u];
       } else {
-        const T *zold = Zo + (size_t)i * ps + rel0;
 #pragma unroll
         for (int u = 0; u < kR; ++u) {
-          const uint32_t w = mi & mz[u];
+          const uint32_t w = mzi & mz[u];
           T zz = z[u];
           if ((w & zmask) != zval) {
             if (!(w & kArray)) continue;
             if (!(w & kRegion) && d.skipz) continue;  // the twin already holds this copy
+            const T old = kZPre ? zo[u] : Zo[(size_t)i * ps + rel0 + u * rs];
             if (!(w & kRegion))
-              zz = zold[u * rs];
+              zz = old;
             else if (bmode == 0 || (bmode == 2 && !(w & kClear)))
-              zz += zold[u * rs];
+              zz += old;
           }
           zrow[u * rs] = zz;
         }
