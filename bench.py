@@ -115,7 +115,7 @@ def kernels_per_op(op) -> int:
 
     if isinstance(op, CopyOp):
         return 0  # device-to-device memcpy or elided alias, not a kernel
-    if op.family in ("halo", "allreduce"):
+    if op.family in ("halo", "halo_wait", "allreduce"):
         return 0  # NCCL communication, not one of the engine's kernels
     if isinstance(op, ReduceOp):
         return 2
@@ -263,7 +263,7 @@ def run_b200(args):
     if slab:
         from paper_2509_02197_b200.decomp import SlabEngine
 
-        eng = SlabEngine(name, params, rank, world, dev)
+        eng = SlabEngine.from_workload(name, params, rank, world, dev)
         dev_inputs = eng.local_inputs(seed=0)
         host_inputs = {k: v.cpu().pin_memory() for k, v in dev_inputs.items()}
     else:

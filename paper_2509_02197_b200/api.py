@@ -417,6 +417,7 @@ def _run_guarded(key, keep_alive, build, inputs, seed):
 def clear_cache():
     _CACHE.clear()
     _BUNDLES.clear()
+    _SLABS.clear()
 
 
 def _result(exe: Executable, program: Program, inputs: dict, bundle) -> GradientResult:
@@ -439,11 +440,39 @@ def _result(exe: Executable, program: Program, inputs: dict, bundle) -> Gradient
     return GradientResult(value=value, grads=grads, forward=fwd, backward=bwd, bundle=bundle)
 
 
-def gradient(program, inputs: dict, params: dict | None = None, *, seed=1.0, trip_limit=None, bundle=None):
-    """Reference ``gradient`` (autodiff.py:1153) executed on the B200."""
+_SLABS: dict = {}
+
+
+def _slab_gradient(program, prog, fp, inputs, params, seed, trip_limit, bundle, group):
+    """``gradient(..., group=pg)``: the stencil program slab-decomposed over
+    the ranks of ``pg`` (decomp.py), one GPU per rank. Every rank passes the
+    full inputs and gets the value and the full gradients back."""
+    from .decomp import SlabEngine
+
+    shapes = _check_inputs(prog, inputs, params)
+    key = (fp, None if bundle is None else fingerprint(as_bundle(bundle).backward), tuple(sorted(params.items())),
+           tuple(sorted(shapes.items())), trip_limit, id(group))
+    eng = _SLABS.get(key)
+    if eng is None:
+        eng = SlabEngine(prog, bundle if bundle is not None else _BUNDLES.get(fp) or host_build_backward(program),
+                         params, group=group, trip_limit=trip_limit)
+        eng._keep_alive = (program, bundle, group)
+        _SLABS[key] = eng
+    return eng.full_gradient(inputs, seed)
+
+
+def gradient(program, inputs: dict, params: dict | None = None, *, seed=1.0, trip_limit=None, bundle=None,
+             group=None):
+    """Reference ``gradient`` (autodiff.py:1153) executed on the B200.
+
+    ``group`` (engine extension, keyword-only, default None): a
+    torch.distributed process group; the program is then slab-decomposed
+    over its ranks (one GPU each, NCCL halo exchange per timestep)."""
     params = dict(params or {})
     prog = adopt(program)
     fp = fingerprint(prog)
+    if group is not None:
+        return _slab_gradient(program, prog, fp, inputs, params, seed, trip_limit, bundle, group)
     if bundle is None:
         bundle_eng = _BUNDLES.get(fp)
         if bundle_eng is None:

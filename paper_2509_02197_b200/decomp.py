@@ -5,10 +5,17 @@ outermost dimension: rank r owns a contiguous range of planes and keeps a
 two-plane halo on each side. The single-device launch list (lowering.py,
 after star-pair fusion and ping-pong placement) is rewritten per rank:
 
-* each fused timestep (StarPairOp) becomes one grouped halo exchange of its
-  source (width 2: X is recomputed on a one-plane halo from Y) and of the old
-  intermediate (width 1), followed by the same kernel restricted to the
-  owned planes, with masks/regions still in global coordinates;
+* each fused timestep (StarPairOp) becomes
+    - one grouped halo exchange (HaloOp) of its source (width 2: X is
+      recomputed on a one-plane halo from Y) and of the old intermediate
+      (width 1), issued on a communication stream once the previous
+      timestep's edge planes are written;
+    - the same kernel on the interior planes [own_lo + 2, own_hi - 2), which
+      read no halo plane and run on the compute stream WHILE the exchange
+      is in flight;
+    - a wait for the exchange (HaloWaitOp), then the kernel on the two edge
+      plane ranges (two planes at each slab end);
+  masks / regions stay in global coordinates (plane0 in the descriptor);
 * a reduction over a decomposed array becomes a local reduction over the
   owned planes plus an all-reduce of the scalar (the reference's dependent
   is a scalar sum, interpreter.py:447-451);
@@ -16,8 +23,10 @@ after star-pair fusion and ping-pong placement) is rewritten per rank:
 
 The exchange is the only data-path communication: one send/recv pair per
 neighbour per array per timestep, NCCL point-to-point over NVLink through
-torch.distributed (gloo on CPU for the multi-process tests). Anything else
-in the launch list is rejected loudly (UnsupportedConstruct).
+torch.distributed (gloo on CPU for the multi-process tests). With a single
+rank there is nothing to exchange: the rewritten list has no communication
+op and is captured in a CUDA graph like the single-device engine. Anything
+else in the launch list is rejected loudly (UnsupportedConstruct).
 """
 from __future__ import annotations
 
@@ -54,12 +63,18 @@ class SlabPlan:
 
 
 class TorchComm:
-    """Neighbour exchange and scalar all-reduce through torch.distributed."""
+    """Neighbour exchange and scalar all-reduce through torch.distributed
+    (NCCL on the GPUs of a node; gloo in the CPU tests). ``group`` is an
+    optional process group; peers are ranks within it."""
 
-    def __init__(self):
+    def __init__(self, group=None):
         import torch.distributed as dist
 
         self.dist = dist
+        self.group = group
+
+    def _peer(self, r):
+        return r if self.group is None else self.dist.get_global_rank(self.group, r)
 
     def plan_exchange(self, pairs):
         """Build the point-to-point op list for [(peer, send, recv)] once (the
@@ -68,8 +83,8 @@ class TorchComm:
         dist = self.dist
         ops = []
         for peer, snd, rcv in pairs:
-            ops.append(dist.P2POp(dist.isend, snd, peer))
-            ops.append(dist.P2POp(dist.irecv, rcv, peer))
+            ops.append(dist.P2POp(dist.isend, snd, self._peer(peer), self.group))
+            ops.append(dist.P2POp(dist.irecv, rcv, self._peer(peer), self.group))
         return ops
 
     def run_exchange(self, ops):
@@ -82,7 +97,7 @@ class TorchComm:
         self.run_exchange(self.plan_exchange(pairs))
 
     def allreduce_sum(self, t):
-        self.dist.all_reduce(t, op=self.dist.ReduceOp.SUM)
+        self.dist.all_reduce(t, op=self.dist.ReduceOp.SUM, group=self.group)
 
 
 class HaloOp(Op):
@@ -120,10 +135,43 @@ class HaloOp(Op):
 
     def launch(self, rt, stream):
         ops = getattr(self, "_ops", None)
-        if ops is not None:
-            self.comm.run_exchange(ops)
-        else:
+        comm_stream = getattr(rt, "comm_stream", None)
+        if ops is None:
             self.run(rt.view)
+            return
+        if comm_stream is None:
+            self.comm.run_exchange(ops)
+            return
+        import torch
+
+        # the exchange starts once everything issued so far on the compute
+        # stream (the previous timestep's edge planes) is done, and runs
+        # beside the interior kernel that follows; HaloWaitOp joins it
+        compute = torch.cuda.current_stream(rt.device)
+        comm_stream.wait_stream(compute)
+        with torch.cuda.stream(comm_stream):
+            self.comm.run_exchange(ops)
+        self.done = torch.cuda.Event()
+        self.done.record(comm_stream)
+
+
+class HaloWaitOp(Op):
+    """The compute stream waits for a HaloOp's exchange (before the edge
+    planes, which read the halo)."""
+
+    family = "halo_wait"
+
+    def __init__(self, halo: HaloOp):
+        self.halo = halo
+        self.reads = self.writes = ()
+
+    def launch(self, rt, stream):
+        ev = getattr(self.halo, "done", None)
+        if ev is not None:
+            import torch
+
+            torch.cuda.current_stream(rt.device).wait_event(ev)
+            self.halo.done = None
 
     def algorithmic_bytes(self) -> int:
         return sum(2 * w * (b.numel // b.shape[0]) * b.itemsize for b, w in self.items)
@@ -189,23 +237,43 @@ def decompose(lw, plan: SlabPlan, comm) -> DistLowered:
         v.offset = plan.own_local[0] * plane_elems
         return v
 
+    solo = plan.world == 1
+    ol, oh = plan.own_local
+    w = plan.halo
+
+    def pair_on(op, zr):
+        new = StarPairOp(op.a, op.b, op.fa, op.fb, op.xwrite, op.dead)
+        new.X, new.Y, new.Z = loc(op.X), loc(op.Y), loc(op.Z)
+        new.xout, new.zout = loc(op.xout), loc(op.zout)
+        new.skip_zcopy, new.skip_xcopy = op.skip_zcopy, op.skip_xcopy
+        new.plane0, new.zrange, new.global_d0 = plan.loc_lo, zr, plan.N
+        new._refresh()
+        low.emit(new)
+
     for op in ops:
         if isinstance(op, StarPairOp):
+            if solo:
+                pair_on(op, (ol, oh))
+                continue
             items = [(loc(op.Y), 2)]
             if op.X.root() is not op.Y.root():
                 items.append((loc(op.X), 1))
-            low.emit(HaloOp(items, plan, comm))
-            new = StarPairOp(op.a, op.b, op.fa, op.fb, op.xwrite, op.dead)
-            new.X, new.Y, new.Z = loc(op.X), loc(op.Y), loc(op.Z)
-            new.xout, new.zout = loc(op.xout), loc(op.zout)
-            new.plane0, new.zrange, new.global_d0 = plan.loc_lo, plan.own_local, plan.N
-            new._refresh()
-            low.emit(new)
+            halo = HaloOp(items, plan, comm)
+            low.emit(halo)
+            # interior planes read no halo plane: they overlap the exchange
+            lo_edge, hi_edge = (ol, min(ol + w, oh)), (max(oh - w, ol + w), oh)
+            if hi_edge[0] > lo_edge[1]:
+                pair_on(op, (lo_edge[1], hi_edge[0]))
+            low.emit(HaloWaitOp(halo))
+            pair_on(op, lo_edge)
+            if hi_edge[1] > hi_edge[0]:
+                pair_on(op, hi_edge)
         elif isinstance(op, ReduceOp) and op.x.root().shape == shape:
             if op.accumulate:
                 raise UnsupportedConstruct("slab decomposition: accumulating reduction")
             low.emit(ReduceOp(own_view(loc(op.x)), loc(op.out), False))
-            low.emit(AllReduceOp(loc(op.out), comm))
+            if not solo:
+                low.emit(AllReduceOp(loc(op.out), comm))
         elif isinstance(op, BroadcastOp):
             low.emit(BroadcastOp(loc(op.src), op.scale, loc(op.out), op.accumulate))
         elif isinstance(op, FillOp) and op.box == whole_box(op.dst.shape):
@@ -225,24 +293,60 @@ def torch_empty_pinned(t):
 
 
 class SlabEngine:
-    """One rank of a slab-decomposed gradient (bench.py under torchrun)."""
+    """One rank of a slab-decomposed gradient: the caller's stencil program
+    (any program whose fused launch list decomposes, e.g. heat_3d) over the
+    ranks of a process group, one GPU per rank.
 
-    def __init__(self, name: str, params: dict, rank: int, world: int, device):
-        from . import workloads as W
-        from .api import lower_gradient
+    ``step(local_inputs)`` runs on device-resident local slabs (halo planes
+    included, ``local_inputs``); ``gradient(host_local_inputs)`` and
+    ``gradients(batches)`` are the end-to-end calls returning the owned
+    planes; ``api.gradient(..., group=...)`` wraps it for full arrays."""
+
+    def __init__(self, program, bundle=None, params=None, *, rank=None, world=None, device=None, group=None,
+                 trip_limit=None):
+        import torch
+        import torch.distributed as dist
+
+        from .api import as_bundle, host_build_backward, lower_gradient
+        from .ir import adopt, eval_int
         from .runtime import Executable
 
-        self.name, self.params = name, dict(params)
-        prog, bundle = W.load(name)
-        self.program = prog
-        shapes = W.input_shapes(prog, params)
-        lw = lower_gradient(prog, bundle, params, shapes, fuse_small=True)
+        self.params = dict(params or {})
+        self.program = adopt(program)
+        bundle = as_bundle(bundle) if bundle is not None else host_build_backward(program)
+        if world is None:
+            world = dist.get_world_size(group) if dist.is_initialized() else 1
+        if rank is None:
+            rank = dist.get_rank(group) if dist.is_initialized() else 0
+        shapes = {n: tuple(eval_int(s, self.params) for s in d.shape)
+                  for n, d in self.program.descriptors.items() if d.role == "input"}
+        self.shapes = shapes
+        lw = lower_gradient(self.program, bundle, self.params, shapes, fuse_small=True, trip_limit=trip_limit)
         N = next(iter(shapes.values()))[0]
         self.plan = SlabPlan(N, world, rank)
-        self.dl = decompose(lw, self.plan, TorchComm())
+        self.dl = decompose(lw, self.plan, TorchComm(group))
+        self.device = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+        # one rank: no communication op, so the list is captured in a CUDA
+        # graph like the single-device engine; several ranks run it eagerly
+        # with the exchanges on a communication stream
         self.exe = Executable(self.dl.low, self.dl.inputs, self.dl.outputs, seed_buf=self.dl.seed_buf,
-                              device=device, use_graph=False)
-        self.device = device
+                              device=self.device, use_graph=world == 1)
+        if world > 1:
+            self.exe.comm_stream = torch.cuda.Stream(self.device)
+        self.group = group
+
+    @classmethod
+    def from_workload(cls, name: str, params: dict, rank: int, world: int, device):
+        from . import workloads as W
+
+        prog, bundle = W.load(name)
+        eng = cls(prog, bundle, params, rank=rank, world=world, device=device)
+        eng.name = name
+        return eng
+
+    def local_slices(self, full: dict) -> dict:
+        """This rank's slabs (halo planes included) of full host arrays."""
+        return {k: np.ascontiguousarray(self.plan.local_slice(np.asarray(v))) for k, v in full.items()}
 
     def local_inputs(self, seed=0) -> dict:
         import torch
@@ -250,8 +354,7 @@ class SlabEngine:
         from . import workloads as W
 
         full = W.make_inputs(self.name, self.program, self.params, seed)
-        return {k: torch.from_numpy(np.ascontiguousarray(self.plan.local_slice(v))).to(self.device)
-                for k, v in full.items()}
+        return {k: torch.from_numpy(v).to(self.device) for k, v in self.local_slices(full).items()}
 
     def step(self, inputs, seed=1.0, sync=False):
         self.exe.run(inputs, seed, sync=sync)
@@ -294,6 +397,38 @@ class SlabEngine:
         torch.cuda.current_stream(self.device).synchronize()
         return GradientResult(value=value, grads={k: v.numpy() for k, v in grads.items()}, forward=None,
                               backward=None, bundle=None)
+
+    def full_gradient(self, full_inputs: dict, seed=1.0):
+        """The reference call shape on every rank: full host arrays in, the
+        value and the FULL gradients out (owned planes all-gathered over the
+        group, so every rank returns the same arrays as the reference)."""
+        import torch
+        import torch.distributed as dist
+
+        from .api import GradientResult
+        from .runtime import NP_DTYPE
+
+        res = self.gradient(self.local_slices(full_inputs), seed)
+        world = self.plan.world
+        grads = {}
+        for ind in self.program.independents:
+            desc = self.program.descriptors[ind]
+            shape = self.shapes[ind]
+            part = res.grads.get(ind)
+            if part is None:
+                grads[ind] = np.zeros(shape, dtype=NP_DTYPE[desc.element_kind])
+                continue
+            if world == 1:
+                grads[ind] = np.array(part)
+                continue
+            rows = [SlabPlan(self.plan.N, world, r) for r in range(world)]
+            pad = max(p.own_hi - p.own_lo for p in rows)
+            mine = torch.zeros((pad,) + tuple(shape[1:]), dtype=torch.from_numpy(part).dtype, device=self.device)
+            mine[:part.shape[0]].copy_(torch.from_numpy(part))
+            got = [torch.empty_like(mine) for _ in range(world)]
+            dist.all_gather(got, mine, group=self.group)
+            grads[ind] = np.concatenate([g[:p.own_hi - p.own_lo].cpu().numpy() for g, p in zip(got, rows)])
+        return GradientResult(value=res.value, grads=grads, forward=None, backward=None, bundle=None)
 
     def own_grad(self, name: str):
         g = self.exe.output("grad:" + name)

@@ -15,7 +15,7 @@ import torch.multiprocessing as mp
 import emulator as E
 from paper_2509_02197_b200 import workloads as W
 from paper_2509_02197_b200.api import lower_gradient
-from paper_2509_02197_b200.decomp import AllReduceOp, HaloOp, SlabPlan, TorchComm, decompose
+from paper_2509_02197_b200.decomp import AllReduceOp, HaloOp, HaloWaitOp, SlabPlan, StarPairOp, TorchComm, decompose
 
 
 def _free_port():
@@ -71,6 +71,8 @@ def _run_rank(rank, world, port, params, q):
                 op.launch(rt, None)
             elif isinstance(op, AllReduceOp):
                 op.run(view)
+            elif isinstance(op, HaloWaitOp):
+                op.launch(rt, None)  # no exchange in flight on the emulator: a no-op
             else:
                 em.run_op(op)
         value = float(view(dl.outputs["value"]))
@@ -81,7 +83,8 @@ def _run_rank(rank, world, port, params, q):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world,params", [(2, {"N": 12, "TSTEPS": 4}), (3, {"N": 14, "TSTEPS": 3})])
+@pytest.mark.parametrize("world,params", [(2, {"N": 12, "TSTEPS": 4}), (3, {"N": 14, "TSTEPS": 3}),
+                                          (4, {"N": 22, "TSTEPS": 5}), (4, {"N": 16, "TSTEPS": 3})])
 def test_slab_decomposition_matches_oracle(world, params):
     from oracle import interp as O
 
@@ -112,3 +115,32 @@ def test_slab_plan_covers_domain():
         for a, b in zip(plans, plans[1:]):
             assert a.own_hi == b.own_lo
             assert a.loc_hi >= a.own_hi + 2 and b.loc_lo <= b.own_lo - 2
+
+
+def _ops_of(world, rank, params):
+    prog, bundle = W.load("heat_3d")
+    lw = lower_gradient(prog, bundle, params, W.input_shapes(prog, params), fuse_small=True)
+    return decompose(lw, SlabPlan(params["N"], world, rank), TorchComm.__new__(TorchComm)).low.ops
+
+
+def test_timestep_splits_into_overlapped_interior_and_edges():
+    """Per fused timestep: exchange, interior planes (no halo read, run while
+    the exchange is in flight), wait, then the two edge plane ranges."""
+    params = {"N": 64, "TSTEPS": 3}
+    ops = _ops_of(4, 1, params)
+    plan = SlabPlan(64, 4, 1)
+    ol, oh = plan.own_local
+    kinds = [type(op).__name__ for op in ops]
+    first = kinds.index("HaloOp")
+    assert kinds[first:first + 5] == ["HaloOp", "StarPairOp", "HaloWaitOp", "StarPairOp", "StarPairOp"]
+    pairs = [op for op in ops[first:first + 5] if isinstance(op, StarPairOp)]
+    assert [p.zrange for p in pairs] == [(ol + 2, oh - 2), (ol, ol + 2), (oh - 2, oh)]
+    # interior: its source planes [zlo - 2, zhi + 2) are owned, never halo
+    zlo, zhi = pairs[0].zrange
+    assert zlo - 2 >= ol and zhi + 2 <= oh
+    assert ops[first + 2].halo is ops[first]
+
+
+def test_single_rank_has_no_communication():
+    ops = _ops_of(1, 0, {"N": 24, "TSTEPS": 3})
+    assert not any(isinstance(op, (HaloOp, HaloWaitOp, AllReduceOp)) for op in ops)

@@ -264,7 +264,7 @@ class _LockstepComm:
         self.pending.setdefault(self.rank, []).append(("sum", t))
 
 
-@pytest.mark.parametrize("world", [2, 3])
+@pytest.mark.parametrize("world", [2, 3, 4])
 def test_slab_decomposition_kernels_in_lockstep(world):
     """The decomposed launch lists of `world` ranks (plane offsets, owned
     plane ranges, halo refresh) run on one GPU in lockstep and reproduce the

@@ -211,3 +211,55 @@ def test_run_planned_on_reference_cli_artifacts(cid):
     assert rel_err(res.value, value) <= tol
     for k, ref in grads.items():
         assert rel_err(res.grads[k], ref) <= tol, k
+
+
+# -- multi-GPU path reachable from the drop-in API ---------------------------------
+
+
+def test_gradient_over_a_process_group_single_rank():
+    """``gradient(..., group=pg)`` slab-decomposes the caller's program over
+    the group (decomp.SlabEngine). With one rank the list carries no
+    communication and is graph-captured; value and full gradient match the
+    oracle, and the N=1 slab step costs what the single-device step does."""
+    import socket
+
+    import torch.distributed as dist
+
+    from paper_2509_02197_b200.decomp import HaloOp, SlabEngine
+
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{port}", rank=0, world_size=1,
+                            device_id=torch.device("cuda", 0))
+    try:
+        params = {"N": 48, "TSTEPS": 5}
+        prog, b = _bundle("heat_3d")
+        inputs = W.make_inputs("heat_3d", prog, params, 2)
+        res = gradient(prog, inputs, params, bundle=b, group=dist.group.WORLD)
+        v, g = SR.gradient("heat_3d", params, inputs)
+        assert rel_err(res.value, v) <= 1e-10
+        assert rel_err(res.grads["A"], g) <= 1e-10
+        res2 = gradient(prog, inputs, params, bundle=b, group=dist.group.WORLD)  # graph replay
+        assert rel_err(res2.grads["A"], g) <= 1e-10
+        eng = SlabEngine(prog, b, {"N": 256, "TSTEPS": 6}, group=dist.group.WORLD)
+        assert not any(isinstance(op, HaloOp) for op in eng.exe.ops) and eng.exe.use_graph
+        ref = Engine(prog, b, {"N": 256, "TSTEPS": 6})
+        dev = {k: torch.from_numpy(x).cuda() for k, x in W.make_inputs("heat_3d", prog, {"N": 256, "TSTEPS": 6},
+                                                                       0).items()}
+
+        def timed(e):
+            for _ in range(3):
+                e.step(dev)
+            s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            s0.record()
+            for _ in range(5):
+                e.step(dev)
+            s1.record()
+            torch.cuda.synchronize()
+            return s0.elapsed_time(s1) / 5
+
+        t_slab, t_ref = timed(eng), timed(ref)
+        assert t_slab <= 1.05 * t_ref, (t_slab, t_ref)
+    finally:
+        dist.destroy_process_group()
