@@ -89,6 +89,22 @@ class GradientResult:
     bundle: object
 
 
+def fused_backward(plan: "PlanBundle") -> Program:
+    """The plan's reverse program with its elementwise recompute stages
+    evaluated inside the consuming adjoint kernels (recompute.py; the
+    north_star's "recomputation fused into the adjoint kernel that consumes
+    it"). GFB_FUSE_RECOMPUTE=0 runs the reference's rec_* blocks as written."""
+    if os.environ.get("GFB_FUSE_RECOMPUTE", "1") == "0":
+        return plan.backward
+    got = plan.__dict__.get("_fused")
+    if got is None or got[0] is not plan.backward:
+        from .recompute import fuse_recompute
+
+        prog, names = fuse_recompute(plan.backward)
+        got = plan.__dict__["_fused"] = (plan.backward, prog, tuple(names))
+    return got[1]
+
+
 def _ref_available() -> bool:
     import importlib.util
 
@@ -293,7 +309,7 @@ def lower_gradient(program: Program, bundle: Bundle, params: dict, shapes: dict,
     """Forward (recording the tape) + backward as one launch list."""
     low = Lowering(trip_limit=trip_limit, fuse_small=fuse_small, known=known)
     fwd_prog = plan.forward if plan else program
-    bwd_prog = plan.backward if plan else bundle.backward
+    bwd_prog = fused_backward(plan) if plan else bundle.backward
     forwarding = plan.forwarding if plan else bundle.forwarding
     rec = set(plan.keep) if plan else set(bundle.required if record is None else record)
     fenv, inputs = _init_env(low, fwd_prog, shapes, "")

@@ -136,6 +136,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--only", default="")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--plans", action="store_true", help="also the config-scale checkpoint plans")
     args = ap.parse_args()
     peak, _ = bench.measured_peaks()
     fp64_peak = fp64_tensor_peak()
@@ -172,6 +173,44 @@ def main():
         print(json.dumps(line), flush=True)
         del eng, dev
         torch.cuda.empty_cache()
+    if args.plans or "plans" in only:
+        planned(args, peak, fp64_peak)
+
+
+def planned(args, peak, fp64_peak):
+    """The config-scale checkpoint plans (paper_2509_02197_b200/programs/plans,
+    reference plan() decisions) through the engine, recompute fused and not."""
+    from paper_2509_02197_b200.api import load_plan
+
+    pdir = os.path.join(W.PROG_DIR, "plans")
+    index = json.load(open(os.path.join(pdir, "index.json")))
+    for cid, meta in index.items():
+        for fuse in ("1", "0"):
+            os.environ["GFB_FUSE_RECOMPUTE"] = fuse
+            pb = load_plan(os.path.join(pdir, cid))
+            params = meta["params"]
+            eng = Engine(None, params=params, plan=pb)
+            host = W.make_inputs(meta["workload"], pb.forward, params, 0)
+            dev = {k: torch.from_numpy(v).cuda() for k, v in host.items()}
+            for _ in range(args.warmup):
+                eng.step(dev)
+            torch.cuda.synchronize()
+            s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            s.record()
+            for _ in range(args.steps):
+                eng.step(dev)
+            e.record()
+            torch.cuda.synchronize()
+            eng.check()
+            ms = s.elapsed_time(e) / args.steps
+            print(json.dumps({"config": "plan:" + cid, "fused_recompute": fuse == "1", "ms_per_step": round(ms, 5),
+                              "value": round(1000.0 / ms, 3), "unit": "evals/s", "ops_per_step": len(eng.exe.ops),
+                              "payload_peak": eng.exe.payload_peak, "t_star": meta["t_star"],
+                              "limit_bytes": meta["limit_bytes"], "decisions": meta["decisions"],
+                              "roofline": roofline(eng.exe, dev, peak, fp64_peak)}), flush=True)
+            del eng, dev
+            torch.cuda.empty_cache()
+    os.environ.pop("GFB_FUSE_RECOMPUTE", None)
 
 
 if __name__ == "__main__":

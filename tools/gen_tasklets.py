@@ -118,6 +118,15 @@ def collect():
                                     plan=pb).low)
             except Exception:
                 pass
+    # the config-scale checkpoint plans (recompute fused into the adjoint maps)
+    pidx = os.path.join(W.PROG_DIR, "plans", "index.json")
+    if os.path.exists(pidx):
+        from paper_2509_02197_b200.api import load_plan
+
+        for cid, meta in json.load(open(pidx)).items():
+            pb = load_plan(os.path.join(W.PROG_DIR, "plans", cid))
+            take(lower_gradient(pb.forward, None, meta["params"], W.input_shapes(pb.forward, meta["params"]),
+                                plan=pb).low)
     return sorted(sigs)
 
 

@@ -17,6 +17,12 @@ Writes under tests/golden/r2/:
   errors.json
       the reference's exception class for the typed-error cases
       (OutOfBounds, NonTermination, MissingTapeValue).
+Writes under paper_2509_02197_b200/programs/plans/:
+  <cid>.{fwd,bwd}.json + <cid>.plan.json
+      reference plan() results at the CONFIG sizes: C4 softmax
+      and mlp at floor + 25 % of the gap to store-all, and the paper's
+      Listing-1 chain (scaled_product_chain, N=3620) at 500 MiB; with the
+      decisions, t*, store-all and floor in plans/index.json.
 """
 from __future__ import annotations
 
@@ -196,7 +202,46 @@ def save_errors():
         json.dump(out, f, indent=2)
 
 
+def save_config_plans():
+    """Reference plan() at the config sizes (host, milliseconds)."""
+    sys.path.insert(0, HERE)
+    import gradflow.examples as ref_examples
+    from gradflow.checkpointing import plan
+    from workloads_ref import WORKLOADS
+
+    from paper_2509_02197_b200.api import as_plan, save_plan
+
+    mib = 1 << 20
+    out = os.path.join(PROGS, "plans")
+    os.makedirs(out, exist_ok=True)
+    index = {}
+    targets = [("softmax", WORKLOADS["softmax"](), {"R": 64 * 16 * 128, "SM": 128}, "tight"),
+               ("mlp", WORKLOADS["mlp"](), {"NB": 64, "C": 512, "S0": 4096, "S1": 4096, "S2": 1024}, "tight"),
+               ("scaled_product_chain", ref_examples.build("scaled_product_chain"), {"N": 3620}, 500.0)]
+    for name, program, params, budget in targets:
+        store_all = plan(program, None, params).solution.t_star
+        try:
+            plan(program, 0.0, params)
+            floor = 0
+        except ref_errors.Infeasible as exc:
+            floor = exc.min_peak_bytes
+        limit = (floor + 0.25 * (store_all - floor)) / mib if budget == "tight" else budget
+        res = plan(program, limit, params)
+        tag = "tight" if budget == "tight" else f"{budget:g}MiB"
+        cid = f"{name}__" + "_".join(f"{k}{v}" for k, v in params.items()) + f"__{tag}"
+        save_plan(as_plan(res), os.path.join(out, cid))
+        index[cid] = {"workload": name, "params": params, "limit_mib": limit, "store_all": store_all,
+                      "floor": floor, "t_star": res.solution.t_star,
+                      "limit_bytes": res.report["limit_bytes"],
+                      "decisions": [v["decision"] for v in res.report["values"]],
+                      "names": [v["name"] for v in res.report["values"]]}
+        print("config plan", cid, index[cid]["decisions"], res.solution.t_star)
+    with open(os.path.join(out, "index.json"), "w") as f:
+        json.dump(index, f, indent=2)
+
+
 def main():
+    save_config_plans()
     index = {"control_flow": save_control_flow(), "plans_cli": save_cli_plans()}
     with open(os.path.join(OUT, "index.json"), "w") as f:
         json.dump(index, f, indent=2)
