@@ -28,20 +28,66 @@ def require_cuda():
         raise EngineError("the B200 engine needs a CUDA device; none is visible (no CPU fallback)")
 
 
-def plan_arena(ops, roots, keep, to_end=frozenset()):
-    """Liveness-planned placement of the non-pinned root buffers in one arena:
-    live interval = [first, last] launch index touching the buffer (aliases
-    and views count for their root); greedy first-fit by interval start.
-    Returns ({bid: byte offset}, arena bytes)."""
+def live_intervals(ops, to_end=frozenset()):
+    """[first, last] launch index touching each root buffer (aliases and views
+    count for their root); results stay live until read back after the run."""
     first, last = {}, {}
     for i, op in enumerate(ops):
         for b in tuple(op.reads) + tuple(op.writes):
             r = b.root().bid
             first.setdefault(r, i)
             last[r] = i
-    for r in to_end:  # results: live from first write until read back after the run
+    for r in to_end:
         if r in first:
             last[r] = len(ops)
+    return first, last
+
+
+def memory_timeline(ops, roots, keep, to_end=frozenset(), offsets=None, buffers=()):
+    """Resident bytes of the arena-placed buffers launch by launch, in the
+    vocabulary of the reference ``MemoryTimeline`` (verification.py:220-226):
+    events (label, delta, resident) with ``alloc <array>`` at the first
+    launch that touches a buffer and ``free <array>`` after its last, plus the
+    peak. Inputs, the seed and pinned buffers (the planner does not count
+    them, checkpointing.py:10-17) are excluded, as in ``plan_arena``. With the
+    placement ``offsets``, ``high_water`` is the highest byte addressed while
+    each event holds (<= the arena size). ``aliases`` maps each placed
+    buffer's name to the names of every buffer sharing its storage (copies
+    the engine elides, twins), from ``buffers``."""
+    first, last = live_intervals(ops, to_end)
+    aliases = {}
+    for b in buffers:
+        aliases.setdefault(b.root().name, set()).add(b.name)
+    bufs = {b.bid: b for b in roots if b.bid not in keep and b.bid in first and b.shape != ()}
+    n = len(ops)
+    starts, ends = {}, {}
+    for bid, b in bufs.items():
+        starts.setdefault(first[bid], []).append(b)
+        ends.setdefault(last[bid], []).append(b)
+    events, cur, peak, live = [], 0, 0, {}
+    high = 0
+    for i in range(n + 1):
+        for b in sorted(starts.get(i, ()), key=lambda b: b.name):
+            cur += b.nbytes
+            live[b.bid] = b
+            peak = max(peak, cur)
+            if offsets is not None:
+                high = max(high, offsets[b.bid] + b.nbytes)
+            events.append((f"alloc {b.name}", b.nbytes, cur, i))
+        for b in sorted(ends.get(i, ()), key=lambda b: b.name):
+            cur -= b.nbytes
+            live.pop(b.bid, None)
+            events.append((f"free {b.name}", -b.nbytes, cur, i))
+    return {"events": events, "peak": peak, "high_water": high,
+            "aliases": {k: sorted(v) for k, v in aliases.items()}}
+
+
+def plan_arena(ops, roots, keep, to_end=frozenset()):
+    """Liveness-planned placement of the non-pinned root buffers in one arena:
+    live interval = [first, last] launch index touching the buffer (aliases
+    and views count for their root); greedy first-fit by interval start.
+    Returns ({bid: byte offset}, arena bytes)."""
+    first, last = live_intervals(ops, to_end)
     # scalars stay outside (the planner counts them as free, checkpointing.py:10-17)
     placed = [b for b in roots if b.bid not in keep and b.bid in first and b.shape != ()]
     # largest first, each at the lowest offset free over its whole interval
@@ -111,6 +157,7 @@ class Executable:
             keep.add(self.seed_buf.root().bid)
         outs = {b.root().bid for b in self.outputs.values()}
         offsets, arena = plan_arena(self.ops, roots, keep, outs) if self.reuse else ({}, 0)
+        self._placement = (roots, keep, outs, offsets)
         total = 0
         placed = [b for b in roots if b.bid in offsets]
         for b in roots:
@@ -136,6 +183,12 @@ class Executable:
         self.err_ptr = self.err.data_ptr()
         self.aux = []  # static per-launch tables (index tables of contractions)
         self.device_bytes = total + self.workspace.numel()
+
+    def memory_timeline(self) -> dict:
+        """Arena residency launch by launch (``memory_timeline``) of this
+        executable's actual placement."""
+        roots, keep, outs, offsets = self._placement
+        return memory_timeline(self.ops, roots, keep, outs, offsets if offsets else None, self.low.buffers)
 
     def upload(self, arr: np.ndarray) -> int:
         """Copy a static host table to device memory owned by this executable;

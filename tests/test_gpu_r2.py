@@ -333,3 +333,45 @@ def test_config_scale_plan_fused_recompute_within_budget(cid):
     assert exe.payload_peak <= meta["t_star"]
     if meta["limit_bytes"] is not None:
         assert exe.payload_peak <= meta["limit_bytes"]
+
+
+TIMELINES = json.load(open(os.path.join(R2, "timelines.json")))
+
+
+@pytest.mark.parametrize("cid", sorted(TIMELINES))
+def test_measured_device_memory_of_planned_runs(cid):
+    """Device allocation measured around a planned run (torch's allocator
+    counters) against the reference simulate_memory peak and the budget:
+    the arena the executable actually allocates and the residency timeline of
+    its placement stay within t* (<= limit); everything else it allocates is
+    inputs, results, the seed and workspace, which the planner does not
+    count (checkpointing.py:10-17)."""
+    from paper_2509_02197_b200 import api
+
+    gold = IDX["plans"].get(cid)
+    if gold is not None:
+        pb, params = load_plan(os.path.join(GOLD, "plans", cid)), gold["params"]
+    else:
+        pb, params = load_plan(os.path.join(PLANS, cid)), PIDX[cid]["params"]
+    inputs = W.make_inputs(PIDX[cid]["workload"] if gold is None else gold["workload"], pb.forward, params, 0)
+    clear_cache()
+    torch.cuda.synchronize()
+    before = torch.cuda.memory_allocated()
+    torch.cuda.reset_peak_memory_stats()
+    run_planned(pb, inputs, params)
+    torch.cuda.synchronize()
+    exe = next(iter(api._CACHE.values()))
+    held = torch.cuda.memory_allocated() - before
+    ref = TIMELINES[cid]
+    t_star = ref["model_peak_bytes"]
+    arena = exe.arena.numel()
+    tl = exe.memory_timeline()
+    assert tl["peak"] <= max(p["peak_bytes"] for p in ref["paths"])
+    assert tl["high_water"] <= arena <= max(t_star, 256)
+    if ref["limit_bytes"] is not None:
+        assert arena <= max(ref["limit_bytes"], 256)
+    uncounted = sum(exe.view(b).numel() * exe.view(b).element_size() for b in exe.inputs.values()) + \
+        sum(t.numel() * t.element_size() for t in [exe.workspace, exe.err] + list(exe.aux))
+    fixed = exe.device_bytes - arena - exe.workspace.numel()
+    assert held >= arena  # the arena is really allocated ...
+    assert held <= arena + fixed + uncounted + 64 * 1024  # ... and nothing unaccounted besides it

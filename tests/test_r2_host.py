@@ -171,3 +171,75 @@ def test_program_fingerprint_tracks_content_not_identity():
     mutated = load_program(os.path.join(W.PROG_DIR, "jacobi_2d.fwd.json"))
     mutated.independents = ("A", "B")
     assert fingerprint(mutated) != fingerprint(prog)
+
+
+# -- device memory timeline vs the reference simulate_memory (f4) -----------------
+
+TIMELINES = json.load(open(os.path.join(R2, "timelines.json")))
+_CFG_PLANS = json.load(open(os.path.join(W.PROG_DIR, "plans", "index.json")))
+_GOLD_PLANS = json.load(open(os.path.join(GOLD, "index.json")))["plans"]
+
+
+def _engine_timeline(cid):
+    from paper_2509_02197_b200.runtime import memory_timeline, plan_arena
+
+    if cid in _GOLD_PLANS:
+        meta, pb = _GOLD_PLANS[cid], load_plan(os.path.join(GOLD, "plans", cid))
+    else:
+        meta, pb = _CFG_PLANS[cid], load_plan(os.path.join(W.PROG_DIR, "plans", cid))
+    lw = lower_gradient(pb.forward, None, meta["params"], W.input_shapes(pb.forward, meta["params"]), plan=pb)
+    low = lw.low
+    roots = [b for b in low.buffers if b.alias_of is None]
+    keep = {b.root().bid for b in lw.inputs.values()}
+    if lw.seed_buf is not None:
+        keep.add(lw.seed_buf.root().bid)
+    outs = {b.root().bid for b in lw.outputs.values()}
+    offsets, arena = plan_arena(low.ops, roots, keep, outs)
+    return memory_timeline(low.ops, roots, keep, outs, offsets, low.buffers), arena
+
+
+def _lifetimes(events):
+    """array -> (first event index, last event index) from alloc/keep/
+    recompute ... free events."""
+    out = {}
+    for k, ev in enumerate(events):
+        kind, name = ev[0].split(" ", 1)
+        if kind in ("alloc", "keep", "recompute", "snapshot"):
+            out.setdefault(name, [k, None])
+        elif kind == "free" and name in out:
+            out[name][1] = k
+    return {n: (a, len(events) if f is None else f) for n, (a, f) in out.items()}
+
+
+@pytest.mark.parametrize("cid", sorted(TIMELINES))
+def test_engine_memory_timeline_within_reference_simulation(cid):
+    """The engine's arena residency, launch by launch (runtime.memory_timeline
+    over the actual liveness placement), against the reference's
+    simulate_memory for the same plan (verification.py:228-323): the peak and
+    the arena never exceed the modelled peak t* (<= the budget), and any two
+    arrays the engine holds at the same time are also both resident in the
+    reference's timeline (the engine's lifetimes are nested in the model's;
+    recompute scratch is inside the model's recompute spikes)."""
+    tl, arena = _engine_timeline(cid)
+    ref = TIMELINES[cid]
+    ref_peak = max(p["peak_bytes"] for p in ref["paths"])
+    assert tl["peak"] <= ref_peak and arena <= ref["model_peak_bytes"]
+    assert tl["high_water"] <= arena
+    if ref["limit_bytes"] is not None:
+        assert arena <= ref["limit_bytes"]
+    eng = _lifetimes([(e[0], e[1], e[2]) for e in tl["events"]])
+    rl = _lifetimes(ref["paths"][0]["events"])
+    # an engine buffer stands for every array sharing its storage (an elided
+    # copy z1__grad = h1__grad lives in h1__grad's memory)
+    names = {x: [n for n in tl["aliases"].get(x, [x]) if n in rl] or [x] for x in eng}
+    both = sorted(x for x in eng if any(n in rl for n in names[x]))
+
+    def ref_overlap(x, y):
+        return any(rl[a][0] < rl[b][1] and rl[b][0] < rl[a][1] for a in names[x] if a in rl
+                   for b in names[y] if b in rl)
+
+    for i, x in enumerate(both):
+        for y in both[i + 1:]:
+            (ea, ef), (fa, ff) = eng[x], eng[y]
+            if ea < ff and fa < ef:  # overlap in the engine
+                assert ref_overlap(x, y), (x, y)

@@ -240,7 +240,40 @@ def save_config_plans():
         json.dump(index, f, indent=2)
 
 
+def save_timelines():
+    """Reference simulate_memory (verification.py:228-323) for every committed
+    plan, as ``gradflow mem-report --json`` computes it (cli.py:330-342)."""
+    from gradflow.checkpointing import plan
+    from gradflow.frontend import load_program as ref_load
+    from gradflow.verification import simulate_memory
+
+    out = {}
+    sets = [(os.path.join(REPO, "tests", "golden", "index.json"), "plans",
+             os.path.join(REPO, "tests", "golden", "plans")),
+            (os.path.join(PROGS, "plans", "index.json"), None, os.path.join(PROGS, "plans"))]
+    for idx_path, key, _ in sets:
+        idx = json.load(open(idx_path))
+        idx = idx[key] if key else idx
+        for cid, meta in sorted(idx.items()):
+            w = meta["workload"]
+            src = os.path.join(PROGS, (w if os.path.exists(os.path.join(PROGS, w + ".fwd.json")) else "corpus_" + w)
+                               + ".fwd.json")
+            res = plan(ref_load(src), meta["limit_mib"], meta["params"])
+            hints = {fv.name: fv.total_bytes for fv in res.fvs if fv.forced}
+            paths = []
+            for seq in res.sequences:
+                tl = simulate_memory(res.forward, res.backward, meta["params"], dict(seq.outcomes),
+                                     stored_hints=hints)
+                paths.append({"peak_bytes": tl.peak, "events": [list(e) for e in tl.events]})
+            out[cid] = {"limit_bytes": res.report["limit_bytes"], "model_peak_bytes": res.solution.t_star,
+                        "paths": paths}
+            print("timeline", cid, [p["peak_bytes"] for p in paths], res.solution.t_star)
+    with open(os.path.join(OUT, "timelines.json"), "w") as f:
+        json.dump(out, f, indent=1)
+
+
 def main():
+    save_timelines()
     save_config_plans()
     index = {"control_flow": save_control_flow(), "plans_cli": save_cli_plans()}
     with open(os.path.join(OUT, "index.json"), "w") as f:
