@@ -191,6 +191,43 @@ def cpu_baseline_stencil(name, params):
                       f"and {hi} ({times[2]:.2f}s, {times[hi]:.2f}s), extrapolated to TSTEPS={T}: {full:.1f}s/eval"}
 
 
+def reference_interpreter_sample(name, params):
+    """The UNMODIFIED reference interpreter (gradflow ``gradient()``, installed
+    offline into baseline/_ref), timed on this host at a reduced size and
+    extrapolated (BASELINE.md CPU plan step 1): per-timestep slope between
+    two trip counts at edge length n, scaled by the interior volume
+    ((N - 2) / (n - 2))^d to the config, times the config's timesteps. It is
+    one Python thread (the interpreter visits map points one at a time)."""
+    ref = os.path.join(REPO, "baseline", "_ref")
+    if not os.path.isdir(os.path.join(ref, "gradflow")):
+        return {"unavailable": "baseline/_ref has no gradflow install"}
+    if ref not in sys.path:
+        sys.path.insert(0, ref)
+    from gradflow.autodiff import gradient as ref_gradient  # the reference itself
+    from gradflow.frontend import load_program as ref_load
+
+    from paper_2509_02197_b200 import workloads as W
+
+    prog = ref_load(os.path.join(W.PROG_DIR, name + ".fwd.json"))
+    d = 3 if name == "heat_3d" else 2
+    n, (t_lo, t_hi) = (12, (3, 5)) if d == 3 else (40, (3, 7))
+    times = {}
+    for ts in (t_lo, t_hi):
+        p = {"N": n, "TSTEPS": ts}
+        inputs = W.make_inputs(name, W.load(name)[0], p, 0)
+        t0 = time.perf_counter()
+        ref_gradient(prog, inputs, p)
+        times[ts] = time.perf_counter() - t0
+    per_step = max((times[t_hi] - times[t_lo]) / (t_hi - t_lo), 1e-9)
+    scale = ((params["N"] - 2) / (n - 2)) ** d
+    full = per_step * scale * (params["TSTEPS"] - 1)
+    return {"value": 1.0 / full, "unit": "evals/s", "cores": 1, "kind": "reference", "extrapolated": True,
+            "sample": f"gradflow.gradient (reference interpreter, baseline/_ref) of {name} at N={n}, "
+                      f"TSTEPS={t_lo} and {t_hi} ({times[t_lo]:.2f}s, {times[t_hi]:.2f}s): {per_step:.3f}s per "
+                      f"timestep, x{scale:.0f} volume to N={params['N']}, x{params['TSTEPS'] - 1} timesteps = "
+                      f"{full:.0f}s/eval ({full / 86400:.1f} days)"}
+
+
 def cpu_baseline_generic(name, params, budget_s=20.0):
     from oracle import interp as O
     from paper_2509_02197_b200 import workloads as W
@@ -211,7 +248,12 @@ def cpu_baseline_generic(name, params, budget_s=20.0):
 
 def cpu_baseline(name, params):
     if name in ("heat_3d", "jacobi_2d"):
-        return cpu_baseline_stencil(name, params)
+        base = cpu_baseline_stencil(name, params)
+        try:
+            base["reference_interpreter"] = reference_interpreter_sample(name, params)
+        except Exception as exc:  # reported, never fatal for the bench
+            base["reference_interpreter"] = {"unavailable": f"{type(exc).__name__}: {exc}"}
+        return base
     return cpu_baseline_generic(name, params)
 
 

@@ -2,7 +2,7 @@
 which kernels issue tcgen05 MMAs (UTCHMMA), TMEM loads (LDTM), TMA loads
 (UTMALDG), 1-D bulk copies (UBLKCP), mbarrier transaction waits (SYNCS), cp.async (LDGSTS) and DMMA.
 
-    python tools/sass_evidence.py > profiles/r01_sass_evidence.txt
+    python tools/sass_evidence.py > profiles/rNN_sass_evidence.txt
 """
 import collections
 import os
