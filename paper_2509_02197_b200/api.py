@@ -232,7 +232,10 @@ def load_plan(stem: str, manifest: str | None = None) -> PlanBundle:
 # executable construction
 
 
-def _check_inputs(program: Program, inputs: dict, params: dict):
+def _check_inputs(program: Program, inputs: dict, params: dict, *, batch=()):
+    """Declared shapes of the inputs (reference _prepare_inputs,
+    interpreter.py:604-618). An input may carry the leading ``batch`` dims
+    (``batch_of``); any other leading dims are rejected."""
     shapes = {}
     for name, value in inputs.items():
         desc = program.descriptors.get(name)
@@ -242,10 +245,68 @@ def _check_inputs(program: Program, inputs: dict, params: dict):
         shape = tuple(getattr(value, "shape", np.shape(value)))
         if desc.shape and tuple(shape[len(shape) - len(declared):]) != declared:
             raise ShapeMismatch(f"input '{name}': trailing shape {shape} does not end with {declared}")
-        if len(shape) != len(declared):
-            raise UnsupportedConstruct(f"input '{name}': leading batch dimensions are not supported")
+        if len(shape) != len(declared) and tuple(shape[:len(shape) - len(declared)]) != tuple(batch):
+            raise ShapeMismatch(f"input '{name}': leading dims {shape[:len(shape) - len(declared)]} are not the "
+                                f"batch shape {tuple(batch)}")
         shapes[name] = declared
     return shapes
+
+
+def batch_of(program: Program, inputs: dict) -> tuple:
+    """The leading batch shape (reference Executor._batch_shape,
+    interpreter.py:161-169): the extra leading dims of the first input that
+    has any; inputs without them are shared by every batch element."""
+    for name, value in inputs.items():
+        desc = program.descriptors.get(name)
+        if desc is None:
+            continue
+        shape = tuple(getattr(value, "shape", np.shape(value)))
+        if len(shape) > desc.rank:
+            return shape[:len(shape) - desc.rank]
+    return ()
+
+
+def _element(program: Program, inputs: dict, batch: tuple, idx: tuple) -> dict:
+    """Inputs of one batch element (batched arrays indexed, shared ones as is)."""
+    out = {}
+    for name, value in inputs.items():
+        desc = program.descriptors[name]
+        nd = len(getattr(value, "shape", np.shape(value)))
+        out[name] = value[idx] if nd > desc.rank else value
+    return out
+
+
+def _batched(program: Program, inputs: dict, batch: tuple, run_one, keys):
+    """Run ``run_one(element_inputs, first)`` for every batch element in order;
+    each call returns {key: array}; results are stacked to batch + shape.
+    Batch elements are independent in the reference (every operation acts
+    per element along the leading dims; control flow must agree across the
+    batch, else BatchDivergence, interpreter.py:190-196), so element-wise
+    execution of the same launch list is the same computation. Device inputs
+    are uploaded once; element copies are device-to-device."""
+    import torch
+
+    dev_inputs = {}
+    for k, v in inputs.items():
+        desc = program.descriptors[k]
+        if len(np.shape(v)) > desc.rank and not isinstance(v, torch.Tensor) and torch.cuda.is_available():
+            dev_inputs[k] = torch.from_numpy(np.ascontiguousarray(np.asarray(v, dtype=NP_DTYPE[desc.element_kind]))
+                                             ).cuda()
+        else:
+            dev_inputs[k] = v
+    results = {}
+    first = True
+    for idx in np.ndindex(*batch):
+        got = run_one(_element(program, dev_inputs, batch, idx), first)
+        for k in keys:
+            v = got.get(k)
+            if v is None:
+                continue
+            if k not in results:
+                results[k] = np.empty(tuple(batch) + np.shape(v), dtype=np.asarray(v).dtype)
+            results[k][idx] = v
+        first = False
+    return results
 
 
 def _init_env(low: Lowering, program: Program, shapes: dict, prefix: str):
@@ -453,7 +514,9 @@ def _result(exe: Executable, program: Program, inputs: dict, bundle) -> Gradient
     benv = {k: exe.view(b) for k, b in exe.backward_env.items() if kept is None or b.root().bid in kept}
     fwd = RunResult(env=fenv, value=value, op_count=exe.flops, tape=exe.tape)
     bwd = RunResult(env=benv, value=None, op_count=exe.flops)
-    return GradientResult(value=value, grads=grads, forward=fwd, backward=bwd, bundle=bundle)
+    res = GradientResult(value=value, grads=grads, forward=fwd, backward=bwd, bundle=bundle)
+    res._decisions = tuple(k for _, _, k in exe.low.decisions)  # the control-flow path taken
+    return res
 
 
 _SLABS: dict = {}
@@ -489,6 +552,9 @@ def gradient(program, inputs: dict, params: dict | None = None, *, seed=1.0, tri
     fp = fingerprint(prog)
     if group is not None:
         return _slab_gradient(program, prog, fp, inputs, params, seed, trip_limit, bundle, group)
+    batch = batch_of(prog, inputs)
+    if batch:
+        return _gradient_batched(program, prog, inputs, params, batch, seed, trip_limit, bundle)
     if bundle is None:
         bundle_eng = _BUNDLES.get(fp)
         if bundle_eng is None:
@@ -505,10 +571,69 @@ def gradient(program, inputs: dict, params: dict | None = None, *, seed=1.0, tri
     return _result(exe, prog, inputs, bundle if bundle is not None else bundle_eng)
 
 
+def _gradient_batched(program, prog, inputs, params, batch, seed, trip_limit, bundle):
+    """``gradient`` over leading batch dims: every element through the cached
+    launch list (graph replays), results stacked; an element whose data-
+    dependent control flow differs from element 0's raises BatchDivergence
+    like the reference (interpreter.py:190-219)."""
+    from .errors import BatchDivergence
+
+    _check_inputs(prog, inputs, params, batch=batch)
+    paths = []
+
+    def one(elem, first):
+        r = gradient(program, elem, params, seed=seed, trip_limit=trip_limit, bundle=bundle)
+        paths.append(r._decisions)
+        if paths[-1] != paths[0]:
+            raise BatchDivergence("a data-dependent branch or loop header differs across the batch")
+        out = {"value": np.asarray(r.value)}
+        out.update({"grad:" + k: np.asarray(v) for k, v in r.grads.items()})
+        return out
+
+    res = _batched(prog, inputs, batch, one, ["value"] + ["grad:" + k for k in prog.independents])
+    b = as_bundle(bundle) if bundle is not None else _BUNDLES.get(fingerprint(prog))
+    return GradientResult(value=res["value"], grads=_backward_batch(prog, b.backward, b.forwarding, inputs, res),
+                          forward=None, backward=None, bundle=bundle)
+
+
+def _backward_batch(prog, backward, forwarding, inputs, res) -> dict:
+    """The reference batches the reverse run only when an input it reads
+    carries the batch dims or it reads recorded forward values
+    (run_backward sizes the seed and zero-initialised gradients from its own
+    env, interpreter.py:681-689, :161-169); otherwise the gradient is the
+    unbatched one of a single element (a linear program's adjoint does not
+    depend on the point)."""
+    batched = bool(forwarding) or any(
+        k in backward.descriptors and len(np.shape(v)) > prog.descriptors[k].rank for k, v in inputs.items())
+    grads = {}
+    for k in prog.independents:
+        g = res["grad:" + k]
+        grads[k] = g if batched else g.reshape((-1,) + g.shape[g.ndim - prog.descriptors[k].rank:])[0]
+    return grads
+
+
 def run_planned(result, inputs: dict, params: dict | None = None, *, seed=1.0, trip_limit=None):
     """Reference ``run_planned`` (checkpointing.py:903) executed on the B200."""
     params = dict(params or {})
     pb = as_plan(result)
+    batch = batch_of(pb.forward, inputs)
+    if batch:
+        from .errors import BatchDivergence
+
+        _check_inputs(pb.forward, inputs, params, batch=batch)
+        paths = []
+
+        def one(elem, first):
+            r = run_planned(result, elem, params, seed=seed, trip_limit=trip_limit)
+            paths.append(r._decisions)
+            if paths[-1] != paths[0]:
+                raise BatchDivergence("a data-dependent branch or loop header differs across the batch")
+            return {"value": np.asarray(r.value), **{"grad:" + k: np.asarray(v) for k, v in r.grads.items()}}
+
+        res = _batched(pb.forward, inputs, batch, one, ["value"] + ["grad:" + k for k in pb.forward.independents])
+        return GradientResult(value=res["value"],
+                              grads=_backward_batch(pb.forward, pb.backward, pb.forwarding, inputs, res),
+                              forward=None, backward=None, bundle=getattr(result, "bundle", None))
     shapes = _check_inputs(pb.forward, inputs, params)
     key = ("plan", fingerprint(pb.forward), fingerprint(pb.backward), tuple(sorted(pb.keep)), tuple(pb.stored),
            tuple(sorted(params.items())), tuple(sorted(shapes.items())), trip_limit)
@@ -530,11 +655,92 @@ def plan(program, limit_mib, params=None, *, trip_limit=None):
     return ref_plan(ref_prog, limit_mib, params, trip_limit=trip_limit)
 
 
+def _forward_batched(prog, inputs, params, batch, trip_limit):
+    """``run_forward`` over leading batch dims, record None (the reference FD
+    oracle's use, verification.py:96-108): the forward launch list is built
+    once and replayed per element as a CUDA graph with device-to-device input
+    copies; the dependent of every element lands in a device vector and the
+    host synchronises once. Programs with data-dependent control flow run
+    element by element and raise BatchDivergence when the path differs."""
+    import torch
+
+    from .errors import BatchDivergence
+
+    shapes = _check_inputs(prog, inputs, params, batch=batch)
+    key = ("fwd", fingerprint(prog), tuple(sorted(params.items())), tuple(sorted(shapes.items())), trip_limit)
+
+    def build(elem):
+        low, env, ins, _tape = probe_lower(lambda known: _lower_forward(prog, shapes, params, None, trip_limit,
+                                                                         known), elem)
+        dep = env.get(prog.dependent)
+        if dep is None:
+            raise UnboundName(f"dependent '{prog.dependent}' was never written")
+        low.finish([dep])
+        return Executable(low, ins, {"value": low.resolve(dep)})
+
+    exe = _CACHE.get(key)
+    vals, paths = None, []
+
+    def one(elem, first):
+        nonlocal exe, vals
+        if exe is None:
+            exe = build(elem)
+            exe._keep_alive = (prog,)
+            _CACHE[key] = exe
+        if exe.low.decisions:
+            exe = run_checked(exe, elem, 1.0, lambda: build(elem))
+            _CACHE[key] = exe
+            paths.append(tuple(k for _, _, k in exe.low.decisions))
+            if paths[-1] != paths[0]:
+                raise BatchDivergence("a data-dependent branch or loop header differs across the batch")
+            return {"value": exe.output_host("value")}
+        exe.run(elem, sync=False, clear_err=first)
+        v = exe.output("value")
+        if vals is None:
+            vals = torch.empty((int(np.prod(batch)),) + tuple(v.shape), dtype=v.dtype, device=v.device)
+        vals[idx_of[0]] = v
+        idx_of[0] = idx_of[0] + 1
+        return {}
+
+    idx_of = [0]
+    res = _batched(prog, inputs, batch, one, ["value"])
+    if vals is not None:
+        exe.check()
+        value = vals.cpu().numpy().reshape(tuple(batch) + tuple(vals.shape[len(batch):]))
+    else:
+        value = res["value"]
+    return RunResult(env={}, value=value, op_count=exe.flops)
+
+
+def _lower_forward(prog, shapes, params, record, trip_limit, known):
+    low = Lowering(trip_limit=trip_limit, known=known)
+    env, ins = _init_env(low, prog, shapes, "")
+    low.entry_inputs = ins
+    tape = LTape() if record is not None else None
+    if tape is not None:
+        from .lowering import CopyOp
+
+        for name, b in list(env.items()):
+            if record == "all" or (name, 0) in record:
+                slot = low.new_buffer(f"{name}@v0", b.shape, b.kind, fresh=False)
+                low.emit(CopyOp(slot, b))
+                tape.values[(name, 0, ())] = slot
+    ProgramRun(low, prog, params, env, record=record, tape=tape, versions=number_writes(prog)).run()
+    return low, env, ins, tape
+
+
 def run_forward(program, inputs: dict, params: dict | None = None, *, record=None, trip_limit=None, vinfo=None):
     """Reference ``run_forward`` (interpreter.py:621): the forward program
-    alone; ``record`` None, "all" or a set of (name, version)."""
+    alone; ``record`` None, "all" or a set of (name, version). Inputs may
+    carry leading batch dims (record None): see ``_forward_batched``."""
     params = dict(params or {})
     prog = adopt(program)
+    batch = batch_of(prog, inputs)
+    if batch:
+        if record is not None:
+            raise UnsupportedConstruct("run_forward: recording a tape over a batch is not supported; "
+                                       "use gradient() on the batch")
+        return _forward_batched(prog, inputs, params, batch, trip_limit)
     shapes = _check_inputs(prog, inputs, params)
     def lower(known):
         low = Lowering(trip_limit=trip_limit, known=known)

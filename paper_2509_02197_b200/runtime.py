@@ -227,11 +227,12 @@ class Executable:
         for op in self.ops:
             op.launch(self, stream)
 
-    def run(self, inputs: dict, seed=1.0, *, sync=True):
+    def run(self, inputs: dict, seed=1.0, *, sync=True, clear_err=True):
         self.load_inputs(inputs)
         if self.seed_buf is not None:
             self.view(self.seed_buf).fill_(float(seed))
-        self.err.zero_()
+        if clear_err:
+            self.err.zero_()
         if self.graph is None and self.use_graph and self.runs >= 1:
             self._capture()
         self.launch_all()

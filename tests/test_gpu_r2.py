@@ -375,3 +375,38 @@ def test_measured_device_memory_of_planned_runs(cid):
     fixed = exe.device_bytes - arena - exe.workspace.numel()
     assert held >= arena  # the arena is really allocated ...
     assert held <= arena + fixed + uncounted + 64 * 1024  # ... and nothing unaccounted besides it
+
+
+# -- leading batch axes (reference interpreter.py:161-169, :604-618) ----------------
+
+
+@pytest.mark.parametrize("cid", sorted(c for c in R2IDX["batched"] if not c.endswith("diverge")))
+def test_batched_gradient_and_forward_match_reference(cid):
+    from paper_2509_02197_b200 import run_forward
+
+    meta = R2IDX["batched"][cid]
+    prog, b = _bundle(meta["workload"])
+    g = np.load(os.path.join(R2, cid + ".npz"))
+    inputs = {k[3:]: g[k] for k in g.files if k.startswith("in:")}
+    res = gradient(prog, inputs, meta["params"], bundle=b)
+    tol = tol_for(prog)
+    assert np.shape(res.value) == g["value"].shape
+    assert rel_err(res.value, g["value"]) <= tol
+    for k in (f[5:] for f in g.files if f.startswith("grad:")):
+        assert res.grads[k].shape == g["grad:" + k].shape, k
+        assert rel_err(res.grads[k], g["grad:" + k]) <= tol, k
+    fr = run_forward(prog, inputs, meta["params"])
+    assert np.shape(fr.value) == g["fwd_value"].shape
+    assert rel_err(fr.value, g["fwd_value"]) <= tol
+
+
+def test_batch_whose_branch_diverges_raises_like_the_reference():
+    from paper_2509_02197_b200.errors import BatchDivergence
+
+    meta = R2IDX["batched"]["corpus_branchy_scale__diverge"]
+    assert meta["error"] == "BatchDivergence"
+    prog, b = _bundle("corpus_branchy_scale")
+    g = np.load(os.path.join(R2, "corpus_branchy_scale__diverge.npz"))
+    inputs = {k[3:]: g[k] for k in g.files if k.startswith("in:")}
+    with pytest.raises(BatchDivergence):
+        gradient(prog, inputs, meta["params"], bundle=b)

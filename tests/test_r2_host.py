@@ -243,3 +243,20 @@ def test_engine_memory_timeline_within_reference_simulation(cid):
             (ea, ef), (fa, ff) = eng[x], eng[y]
             if ea < ff and fa < ef:  # overlap in the engine
                 assert ref_overlap(x, y), (x, y)
+
+
+def test_batch_shape_follows_the_reference_rule():
+    """The first input with extra leading dims fixes the batch shape
+    (interpreter.py:161-169); shared inputs keep their declared shape;
+    mismatched leading dims are a ShapeMismatch."""
+    from paper_2509_02197_b200.api import batch_of
+    from paper_2509_02197_b200.errors import ShapeMismatch
+
+    prog, _ = _bundle("atax")
+    params = {"M": 6, "N": 5}
+    A, x = np.ones((6, 5)), np.ones((4, 3, 5, 1))
+    assert batch_of(prog, {"A": A, "x": x}) == (4, 3)
+    assert _check_inputs(prog, {"A": A, "x": x}, params, batch=(4, 3)) == {"A": (6, 5), "x": (5, 1)}
+    with pytest.raises(ShapeMismatch):
+        _check_inputs(prog, {"A": np.ones((2, 6, 5)), "x": x}, params, batch=(4, 3))
+    assert batch_of(prog, {"A": A, "x": np.ones((5, 1))}) == ()

@@ -272,10 +272,57 @@ def save_timelines():
         json.dump(out, f, indent=1)
 
 
+def save_batched():
+    """Reference gradient() / run_forward() over leading batch dims
+    (interpreter.py:161-169, :604-618), and a batch whose branch diverges."""
+    sys.path.insert(0, HERE)
+    from workloads_ref import WORKLOADS
+    import gradflow.examples as ref_examples
+
+    from paper_2509_02197_b200.workloads import make_inputs
+    from paper_2509_02197_b200.ir import adopt
+
+    cases = {}
+    rng = np.random.default_rng(9)
+    specs = [("jacobi_2d", WORKLOADS["jacobi_2d"](), {"N": 9, "TSTEPS": 3}, {"A": (3,), "B": (3,)}),
+             ("softmax", WORKLOADS["softmax"](), {"R": 6, "SM": 5}, {"x": (2, 2)}),
+             ("atax", WORKLOADS["atax"](), {"M": 6, "N": 5}, {"x": (4,)})]
+    for name, program, params, bat in specs:
+        base = make_inputs(name, adopt(program), params, 0)
+        inputs = dict(base)
+        for k, bshape in bat.items():
+            inputs[k] = rng.uniform(0.4, 1.6, bshape + base[k].shape).astype(base[k].dtype)
+        res = gradient(program, inputs, params)
+        fwd = run_forward(program, inputs, params)
+        cid = f"{name}__batch"
+        arrays = {f"in:{k}": v for k, v in inputs.items()}
+        arrays["value"] = np.asarray(res.value)
+        arrays["fwd_value"] = np.asarray(fwd.value)
+        for k, v in res.grads.items():
+            arrays[f"grad:{k}"] = np.asarray(v)
+        np.savez(os.path.join(OUT, cid + ".npz"), **arrays)
+        cases[cid] = {"workload": name, "params": params}
+        print("batched", cid, np.shape(res.value))
+    # a branch whose condition differs across the batch
+    program = ref_examples.build("branchy_scale")
+    base = make_inputs("corpus_branchy_scale", adopt(program), {"n": 8}, 0)
+    div = dict(base, s=np.array([0.3, 0.9]))
+    try:
+        gradient(program, div, {"n": 8})
+        err = None
+    except ref_errors.GradflowError as exc:
+        err = type(exc).__name__
+    np.savez(os.path.join(OUT, "corpus_branchy_scale__diverge.npz"), **{f"in:{k}": v for k, v in div.items()})
+    cases["corpus_branchy_scale__diverge"] = {"workload": "corpus_branchy_scale", "params": {"n": 8}, "error": err}
+    print("diverging batch:", err)
+    return cases
+
+
 def main():
+    batched = save_batched()
     save_timelines()
     save_config_plans()
-    index = {"control_flow": save_control_flow(), "plans_cli": save_cli_plans()}
+    index = {"control_flow": save_control_flow(), "plans_cli": save_cli_plans(), "batched": batched}
     with open(os.path.join(OUT, "index.json"), "w") as f:
         json.dump(index, f, indent=2)
     save_errors()
