@@ -43,7 +43,7 @@ from .ir import (
     pristine_inputs,
 )
 from .lowering import Lowering, LTape, NeedValues, ProgramRun, required_record
-from .runtime import NP_DTYPE, Executable
+from .runtime import NP_DTYPE, Executable, HostEnv
 
 # ---------------------------------------------------------------------------
 # bundles (what the host AD / planner hands to the engine)
@@ -421,13 +421,18 @@ def lower_gradient(program: Program, bundle: Bundle, params: dict, shapes: dict,
 
 def build_gradient_executable(program: Program, bundle: Bundle, params: dict, shapes: dict, *, trip_limit=None,
                               record=None, plan: PlanBundle | None = None, inputs: dict | None = None,
-                              seed=1.0) -> Executable:
+                              seed=1.0, pin_env=False) -> Executable:
     """``inputs`` (host or device values) are needed only by programs whose
     control flow reads runtime data; the launch list then holds the path
-    those inputs take (``Executable.decisions_hold`` re-checks it)."""
+    those inputs take (``Executable.decisions_hold`` re-checks it).
+    ``pin_env`` keeps every named array of the forward and reverse runs out
+    of the recycling arena, so ``RunResult.env`` holds all of them like the
+    reference's (interpreter.py:78-83); planned runs leave it off, since
+    their device peak is bounded by the plan's budget."""
     lw = probe_lower(lambda known: lower_gradient(program, bundle, params, shapes, trip_limit=trip_limit,
                                                   record=record, plan=plan, known=known), inputs, seed)
-    exe = Executable(lw.low, lw.inputs, lw.outputs, seed_buf=lw.seed_buf)
+    pinned = [b for b in list(lw.forward_env.values()) + list(lw.backward_env.values())] if pin_env else []
+    exe = Executable(lw.low, lw.inputs, lw.outputs, seed_buf=lw.seed_buf, pinned=pinned)
     exe.forward_env, exe.backward_env, exe.tape = lw.forward_env, lw.backward_env, lw.tape
     exe.forward_program, exe.backward_program = lw.forward_program, lw.backward_program
     return exe
@@ -507,11 +512,12 @@ def _result(exe: Executable, program: Program, inputs: dict, bundle) -> Gradient
         else:
             ref = np.asarray(inputs[ind])
             grads[ind] = np.zeros(ref.shape, dtype=NP_DTYPE[program.descriptors[ind].element_kind])
-    # env entries whose HBM was recycled by the liveness arena are omitted
-    # (inputs, the dependent and the gradients always remain)
+    # env: host numpy arrays like the reference's, copied on first access
+    # (runtime.HostEnv); entries whose HBM the liveness arena recycled (only
+    # in planned runs, whose peak is bounded by the budget) are omitted
     kept = getattr(exe, "keep_bids", None)
-    fenv = {k: exe.view(b) for k, b in exe.forward_env.items() if kept is None or b.root().bid in kept}
-    benv = {k: exe.view(b) for k, b in exe.backward_env.items() if kept is None or b.root().bid in kept}
+    fenv = HostEnv(exe, {k: b for k, b in exe.forward_env.items() if kept is None or b.root().bid in kept})
+    benv = HostEnv(exe, {k: b for k, b in exe.backward_env.items() if kept is None or b.root().bid in kept})
     fwd = RunResult(env=fenv, value=value, op_count=exe.flops, tape=exe.tape)
     bwd = RunResult(env=benv, value=None, op_count=exe.flops)
     res = GradientResult(value=value, grads=grads, forward=fwd, backward=bwd, bundle=bundle)
@@ -566,7 +572,7 @@ def gradient(program, inputs: dict, params: dict | None = None, *, seed=1.0, tri
     shapes = _check_inputs(prog, inputs, params)
     key = ("grad", fp, bfp, tuple(sorted(params.items())), tuple(sorted(shapes.items())), trip_limit)
     build = lambda: build_gradient_executable(prog, bundle_eng, params, shapes, trip_limit=trip_limit,  # noqa: E731
-                                              inputs=inputs, seed=seed)
+                                              inputs=inputs, seed=seed, pin_env=True)
     exe = _run_guarded(key, (program, bundle, bundle_eng), build, inputs, seed)
     return _result(exe, prog, inputs, bundle if bundle is not None else bundle_eng)
 
@@ -767,7 +773,7 @@ def run_forward(program, inputs: dict, params: dict | None = None, *, record=Non
     exe = Executable(low, ins, {"value": low.resolve(dep)}, use_graph=False,
                      pinned=[low.resolve(b) for b in observed])
     exe.run(inputs)
-    out_env = {k: exe.view(low.resolve(b)) for k, b in env.items()}
+    out_env = HostEnv(exe, {k: low.resolve(b) for k, b in env.items()})
     res = RunResult(env=out_env, value=exe.output_host("value"), op_count=exe.flops, tape=tape)
     res._exe = exe
     return res
@@ -808,7 +814,7 @@ def run_backward(program, backward, inputs: dict, params: dict | None = None, *,
     exe = Executable(low, ins, outputs, seed_buf=seed_buf, use_graph=False,
                      pinned=[low.resolve(b) for b in env.values()])
     exe.run({**pass_in, **extra_in}, seed)
-    out_env = {k: exe.view(low.resolve(b)) for k, b in env.items()}
+    out_env = HostEnv(exe, {k: low.resolve(b) for k, b in env.items()})
     return RunResult(env=out_env, value=None if seed_buf is None else exe.output_host("value"), op_count=exe.flops)
 
 

@@ -11,6 +11,8 @@ point the device error word is checked and mapped to DomainError.
 from __future__ import annotations
 
 import os
+import weakref
+from collections.abc import Mapping
 
 import numpy as np
 import torch
@@ -118,6 +120,38 @@ def _pool_only(t: torch.Tensor) -> bool:
     return torch._C._storage_Use_Count(t.untyped_storage()._cdata) <= 2
 
 
+class HostEnv(Mapping):
+    """``RunResult.env`` of an engine run: name -> host numpy array, copied
+    from the device on first access. Before the executable runs again (which
+    rewrites its buffers) every live HostEnv of it copies what it has not
+    read yet, so the arrays a caller holds keep the values of their own call,
+    as the reference's env does (interpreter.py:78-83)."""
+
+    __hash__ = object.__hash__  # identity (tracked in a WeakSet); Mapping equality stays by content
+
+    def __init__(self, exe, bufs: dict):
+        self._exe, self._bufs, self._host = exe, dict(bufs), {}
+        exe._live_envs.add(self)
+
+    def __getitem__(self, name):
+        got = self._host.get(name)
+        if got is None:
+            if name not in self._bufs:
+                raise KeyError(name)
+            got = self._host[name] = self._exe.view(self._bufs[name]).cpu().numpy().copy()
+        return got
+
+    def __iter__(self):
+        return iter(self._bufs)
+
+    def __len__(self):
+        return len(self._bufs)
+
+    def materialize(self):
+        for name in self._bufs:
+            self[name]
+
+
 class Executable:
     def __init__(self, low: Lowering, inputs: dict, outputs: dict, *, seed_buf: Buffer | None = None,
                  device=None, use_graph: bool | None = None, pinned=(), reuse: bool | None = None):
@@ -137,6 +171,7 @@ class Executable:
         # decision snapshots (data-dependent control flow) stay readable
         self.pinned = list(pinned) + [low.resolve(b) for slots, _, _ in low.decisions for b in slots.values()]
         self.reuse = (os.environ.get("GFB_ARENA", "1") != "0") if reuse is None else reuse
+        self._live_envs = weakref.WeakSet()
         self._allocate()
         for op in self.ops:
             op.prepare(self)
@@ -228,6 +263,9 @@ class Executable:
             op.launch(self, stream)
 
     def run(self, inputs: dict, seed=1.0, *, sync=True, clear_err=True):
+        for env in list(self._live_envs):
+            env.materialize()  # results of the previous call keep their values
+        self._live_envs.clear()
         self.load_inputs(inputs)
         if self.seed_buf is not None:
             self.view(self.seed_buf).fill_(float(seed))

@@ -133,7 +133,7 @@ def test_run_forward_then_run_backward_matches_reference(cid):
     br = run_backward(prog, b.backward, inputs, params, tape=fr.tape, forwarding=b.forwarding, seed=1.0)
     for k, ref in grads.items():
         got = br.env.get(k + "__grad")
-        got = np.zeros_like(ref) if got is None else got.cpu().numpy()
+        got = np.zeros_like(ref) if got is None else np.asarray(got)
         assert rel_err(got, ref) <= tol_for(prog), k
 
 
@@ -410,3 +410,22 @@ def test_batch_whose_branch_diverges_raises_like_the_reference():
     inputs = {k[3:]: g[k] for k in g.files if k.startswith("in:")}
     with pytest.raises(BatchDivergence):
         gradient(prog, inputs, meta["params"], bundle=b)
+
+
+def test_run_result_env_holds_host_arrays_of_every_intermediate():
+    """RunResult.env like the reference's (interpreter.py:78-83): every named
+    array of the forward / reverse run as a host numpy array, keeping the
+    values of its own call after later calls rewrite the device buffers."""
+    prog, b = _bundle("softmax")
+    params = {"R": 64, "SM": 32}
+    x1 = W.make_inputs("softmax", prog, params, 1)
+    x2 = W.make_inputs("softmax", prog, params, 2)
+    r1 = gradient(prog, x1, params, bundle=b)
+    names = set(r1.forward.env)
+    assert {"x", "w", "e", "d", "sm", "p", "O"} <= names
+    r2 = gradient(prog, x2, params, bundle=b)  # rewrites the buffers r1's env viewed
+    e1 = r1.forward.env["e"]
+    assert isinstance(e1, np.ndarray)
+    assert rel_err(e1, np.exp(x1["x"].astype(np.float64))) <= 1e-6
+    assert rel_err(r2.forward.env["e"], np.exp(x2["x"].astype(np.float64))) <= 1e-6
+    assert {"x__grad", "e__grad"} <= set(r1.backward.env)
