@@ -60,6 +60,12 @@ namespace GFB_STAR_NS {
 #ifndef GFB_STAR_CHAIN
 #define GFB_STAR_CHAIN 1
 #endif
+#ifndef GFB_STAR_BRANCHFREE
+#define GFB_STAR_BRANCHFREE 1
+#endif
+#ifndef GFB_STAR_WARPFAST
+#define GFB_STAR_WARPFAST 1
+#endif
 constexpr int tPX = 32, tPY = GFB_STAR_TPY, tPM = GFB_STAR_TPM;  // CTA tile (k, j) and planes
 constexpr int kR = GFB_STAR_KR;                                   // Z rows per thread
 constexpr int tThreads = tPX * (tPY / kR);
@@ -259,6 +265,20 @@ __device__ __forceinline__ void star_tma_body(const CUtensorMap *ymap, const Sta
     mz[u] = W.bj[kR * ty + u] & W.bk[tx];
   }
   const uint32_t mxr = ring ? (W.aj[rj] & W.ak[rk]) : 0u;
+#if GFB_STAR_WARPFAST
+  // per-warp common-case words: AND of the (j, k) words of the warp's points
+  // (ring point included); a plane whose word keeps every common bit for all
+  // of them skips the fix-ups warp-uniformly (on a tile at a j face only the
+  // warp owning the face rows and the ring warps take them)
+  uint32_t mxall = ring ? mxr : ~0u, mzall = ~0u;
+#pragma unroll
+  for (int u = 0; u < kR; ++u) {
+    mxall &= mx[u];
+    mzall &= mz[u];
+  }
+  mxall = __reduce_and_sync(0xffffffffu, mxall);
+  mzall = __reduce_and_sync(0xffffffffu, mzall);
+#endif
   const bool ysrc = MODES >= 0 ? ((MODES / 32) & 1) != 0 : d.a.srcmask == 1;
   const bool yj_in = j0 - 2 >= d.a.smlo[1] && j0 + tPY + 2 <= d.a.smhi[1];
   const bool yk_in = k0 - 2 >= d.a.smlo[2] && k0 + tPX + 2 <= d.a.smhi[2];
@@ -295,6 +315,11 @@ __device__ __forceinline__ void star_tma_body(const CUtensorMap *ymap, const Sta
   const bool jk_clean = !ysrc || (yj_in && yk_in);
   const int clean_lo = jk_clean ? (ysrc ? max(0, d.a.smlo[0] - d.p0) : 0) : 1;
   const int clean_hi = jk_clean ? (ysrc ? min(d.d0, d.a.smhi[0] - d.p0) : d.d0) : 0;
+#if GFB_STAR_WARPFAST
+  const uint32_t jka = (amode == 0) ? 0u : mxall, jkb = (bmode == 0) ? 0u : mzall;
+#else
+  const uint32_t jka = (amode == 0) ? 0u : W.jk[0], jkb = (bmode == 0) ? 0u : W.jk[1];
+#endif
   // common-case predicate patterns
   const uint32_t xmask = kArray | kRegion | (amode == 2 ? kClear : 0u) | (xwrite ? kDead : 0u);
   const uint32_t xval = amode == 0 ? 0xffffffffu : xmask;  // mode 0: base always added -> fix-up
@@ -311,7 +336,7 @@ __device__ __forceinline__ void star_tma_body(const CUtensorMap *ymap, const Sta
   auto prefetch_xo = [&](int q) {
     if (q > min(qend, d.d0 - 1)) return;
     const uint32_t mi = W.ai[q - i0 + 1];
-    if (((mi & W.jk[0]) & xfast_m) == xfast_m && amode != 0) return;
+    if (((mi & jka) & xfast_m) == xfast_m && amode != 0) return;
     const T *src = Xo + (size_t)q * ps;
 #pragma unroll
     for (int u = 0; u < kR; ++u)
@@ -320,6 +345,20 @@ __device__ __forceinline__ void star_tma_body(const CUtensorMap *ymap, const Sta
     cp_async_commit();
   };
   // X~ of one point from its tap sum; abnormal points take the fix-up
+#if GFB_STAR_BRANCHFREE
+  // branch-free fix-up: selects instead of nested branches (the boundary
+  // tiles run it for every point of every plane); the staged old value is
+  // read unconditionally and discarded by the selects where not staged
+  auto x_tilde = [&](T acc, uint32_t w, int slot, int rel, bool wb, int q) -> T {
+    const bool arr = (w & kArray) != 0, reg = (w & kRegion) != 0;
+    const bool add = amode == 0 || (amode == 2 && !(w & kClear));
+    const T xo = xst[q & 1][slot][tid];
+    T r = reg ? (add ? acc + xo : acc) : xo;
+    r = arr ? r : T(0);
+    if (wb && xwrite && arr && !(w & kDead) && !(d.skipx && !reg)) Xn[(size_t)q * ps + rel] = r;
+    return (w & kSrcB) ? r : T(0);
+  };
+#else
   auto x_tilde = [&](T acc, uint32_t w, int slot, int rel, bool wb, int q) -> T {
     if ((w & xmask) != xval) {
       if (!(w & kArray)) {
@@ -334,6 +373,7 @@ __device__ __forceinline__ void star_tma_body(const CUtensorMap *ymap, const Sta
     }
     return (w & kSrcB) ? acc : T(0);
   };
+#endif
   const T a0 = coef<T>(d.a, 0), a1 = coef<T>(d.a, 1), a2 = coef<T>(d.a, 2), a3 = coef<T>(d.a, 3),
           a4 = coef<T>(d.a, 4), a5 = coef<T>(d.a, 5), a6 = coef<T>(d.a, 6);
   const T b0 = coef<T>(d.b, 0), b1 = coef<T>(d.b, 1), b2 = coef<T>(d.b, 2), b3 = coef<T>(d.b, 3),
@@ -347,7 +387,6 @@ __device__ __forceinline__ void star_tma_body(const CUtensorMap *ymap, const Sta
     prepare_plane(0);
   }
   __syncthreads();
-  const uint32_t jka = (amode == 0) ? 0u : W.jk[0], jkb = (bmode == 0) ? 0u : W.jk[1];
 
   // Registers rolled along the march, rotated by index (three live planes):
   // yv[u][.] = Y centre values at the own X points (row u), yr[.] at the
@@ -534,6 +573,18 @@ __device__ __forceinline__ void star_tma_body(const CUtensorMap *ymap, const Sta
 #pragma unroll
         for (int u = 0; u < kR; ++u) zrow[u * rs] = z[u];
       } else {
+#if GFB_STAR_BRANCHFREE
+#pragma unroll
+        for (int u = 0; u < kR; ++u) {
+          const uint32_t w = mzi & mz[u];
+          const bool arr = (w & kArray) != 0, reg = (w & kRegion) != 0;
+          const bool add = bmode == 0 || (bmode == 2 && !(w & kClear));
+          T old = zo[u];
+          if (!kZPre && !reg && arr && !d.skipz) old = Zo[(size_t)i * ps + rel0 + u * rs];
+          const T zz = reg ? (add ? z[u] + old : z[u]) : old;
+          if (arr && (reg || !d.skipz)) zrow[u * rs] = zz;  // out of region: the twin may hold the copy
+        }
+#else
 #pragma unroll
         for (int u = 0; u < kR; ++u) {
           const uint32_t w = mzi & mz[u];
@@ -549,6 +600,7 @@ __device__ __forceinline__ void star_tma_body(const CUtensorMap *ymap, const Sta
           }
           zrow[u * rs] = zz;
         }
+#endif
       }
     }
     ysl = ysl + 1 == (unsigned)NSY ? 0u : ysl + 1;
