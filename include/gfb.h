@@ -26,7 +26,7 @@
 extern "C" {
 #endif
 
-#define GFB_ABI_VERSION 9
+#define GFB_ABI_VERSION 10
 
 #define GFB_MAX_PARAMS 8    /* map parameters (iteration-space rank) */
 #define GFB_MAX_RANK 8      /* array rank */
@@ -339,11 +339,36 @@ const char *gfb_last_error(void);
 int gfb_device_sm_count(void);
 /* sizes of gfb_space, gfb_operand, gfb_map_desc, gfb_term, gfb_gather_desc,
  * gfb_stencil_desc, gfb_star_op, gfb_star_pair_desc, gfb_contract_desc,
- * gfb_map2_desc (binding layout check); returns the count written */
+ * gfb_map2_desc, gfb_wave_desc (binding layout check); returns the count
+ * written */
 int gfb_struct_sizes(int64_t *out, int32_t cap);
 
 /* replaces Executor._exec_map / _exec_tasklet (interpreter.py:478-507, 405-426) */
 int gfb_map_launch(const gfb_map_desc *d, void *stream);
+
+/*
+ * Sequential loop nest of one tasklet (reference _exec_loop / run_level over
+ * LoopRegions whose body is a single scalar tasklet, interpreter.py:221-330,
+ * 396-426), executed by hyperplanes: the nest's iteration space is map.space
+ * (one parameter per loop, box_lo = first iterate, step = the loop's step,
+ * so box index k_p is the execution order of loop p); points with
+ * sum_p c[p] * k_p == h form hyperplane h. The host proves (lowering.py,
+ * ProgramRun._wavefront) that every pair of iterations touching one element
+ * (at least one of them writing) lies on different hyperplanes in
+ * execution order, so hyperplanes h = 0 .. hmax run in order with their
+ * points in parallel (one cooperative launch, a grid barrier between
+ * hyperplanes), and the result is the sequential nest's, element for
+ * element. `solve` is a parameter with c != 0 (its index is solved from h).
+ */
+typedef struct {
+  gfb_map_desc map;
+  int64_t c[GFB_MAX_PARAMS];
+  int64_t hmax;
+  int32_t solve;
+  int32_t _pad;
+} gfb_wave_desc;
+
+int gfb_wave_launch(const gfb_wave_desc *d, void *stream);
 /* replaces the wcr="sum" scatter of _exec_tasklet (interpreter.py:422-423) */
 int gfb_gather_launch(const gfb_gather_desc *d, void *stream);
 int64_t gfb_gather_workspace_bytes(const gfb_gather_desc *d);

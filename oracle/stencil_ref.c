@@ -267,6 +267,32 @@ int jacobi2d_gradient(int n, int tsteps, const double *A0, const double *B0, dou
   return 0;
 }
 
+/*
+ * corpus seidel_stencil (reference examples.py:159-182), forward only: the
+ * in-place Gauss-Seidel nest for t, i, j in loop order, body
+ * (mul 0.2 (add (add (add cc nn) (add ss ww)) ee)) in the reference's
+ * evaluation order, then O = sum(A). Sequential by construction (single
+ * thread); the program is linear, so parity of the engine's gradient is
+ * checked through O(A + d) - O(A) = <grad, d>.
+ */
+double seidel2d_value(int n, int tsteps, const double *A0) {
+  const int64_t total = (int64_t)n * n;
+  double *A = malloc(total * sizeof(double));
+  if (!A) return 0.0;
+  memcpy(A, A0, total * sizeof(double));
+  for (int t = 0; t < tsteps; ++t)
+    for (int i = 1; i < n - 1; ++i)
+      for (int j = 1; j < n - 1; ++j) {
+        const double cc = A[IDX2(i, j)], nn = A[IDX2(i - 1, j)], ss = A[IDX2(i + 1, j)];
+        const double ww = A[IDX2(i, j - 1)], ee = A[IDX2(i, j + 1)];
+        A[IDX2(i, j)] = 0.2 * (((cc + nn) + (ss + ww)) + ee);
+      }
+  double v = 0.0;
+  for (int64_t q = 0; q < total; ++q) v += A[q];
+  free(A);
+  return v;
+}
+
 int stencil_ref_max_threads(void) {
   set_threads(0);
   return g_threads;

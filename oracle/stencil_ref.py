@@ -24,6 +24,8 @@ def load():
             fn.restype = C.c_int
             fn.argtypes = [C.c_int, C.c_int, dp, dp, C.c_double, dp, dp, C.c_int]
         lib.stencil_ref_max_threads.restype = C.c_int
+        lib.seidel2d_value.restype = C.c_double
+        lib.seidel2d_value.argtypes = [C.c_int, C.c_int, dp]
         _LIB = lib
     return _LIB
 
@@ -47,3 +49,10 @@ def gradient(name: str, params: dict, inputs: dict, *, seed=1.0, threads=0):
 
 def max_threads() -> int:
     return int(load().stencil_ref_max_threads())
+
+
+def seidel_value(params: dict, A) -> float:
+    """Forward value of the corpus seidel_stencil (sequential C restatement)."""
+    A = np.ascontiguousarray(A, dtype=np.float64)
+    return float(load().seidel2d_value(int(params["N"]), int(params["TSTEPS"]),
+                                       A.ctypes.data_as(C.POINTER(C.c_double))))

@@ -19,7 +19,7 @@ MAXCODE = 128
 MAXCONST = 24
 MAXTAPS = 32
 MAXSRCS = 4
-ABI_VERSION = 9
+ABI_VERSION = 10
 
 F32, F64 = 0, 1
 STAR_SKIP_ZCOPY, STAR_SKIP_XCOPY = 1, 2
@@ -96,6 +96,10 @@ class ContractDesc(C.Structure):
                 ("mtab", vp), ("ntab", vp), ("ktab", vp), ("lo", i32 * 4), ("hi", i32 * 4), ("workspace", vp)]
 
 
+class WaveDesc(C.Structure):
+    _fields_ = [("map", MapDesc), ("c", i64 * P), ("hmax", i64), ("solve", i32), ("_pad", i32)]
+
+
 M2DIMS, M2OUTS, M2DEPTH = 8, 4, 6
 
 
@@ -122,6 +126,7 @@ _SIGS = [
     ("gfb_device_sm_count", i32, []),
     ("gfb_struct_sizes", i32, [C.POINTER(i64), i32]),
     ("gfb_map_launch", i32, [C.POINTER(MapDesc), vp]),
+    ("gfb_wave_launch", i32, [C.POINTER(WaveDesc), vp]),
     ("gfb_gather_launch", i32, [C.POINTER(GatherDesc), vp]),
     ("gfb_gather_workspace_bytes", i64, [C.POINTER(GatherDesc)]),
     ("gfb_stencil_launch", i32, [C.POINTER(StencilDesc), vp]),
@@ -165,11 +170,11 @@ def load(path: str | None = None):
         fn.argtypes = args
     if lib.gfb_abi_version() != ABI_VERSION:
         raise EngineError(f"libgfb ABI {lib.gfb_abi_version()} != expected {ABI_VERSION}; rebuild")
-    sizes = (i64 * 10)()
-    n = lib.gfb_struct_sizes(sizes, 10)
+    sizes = (i64 * 11)()
+    n = lib.gfb_struct_sizes(sizes, 11)
     want = [C.sizeof(Space), C.sizeof(Operand), C.sizeof(MapDesc), C.sizeof(Term), C.sizeof(GatherDesc),
             C.sizeof(StencilDesc), C.sizeof(StarOp), C.sizeof(StarPairDesc), C.sizeof(ContractDesc),
-            C.sizeof(Map2Desc)]
+            C.sizeof(Map2Desc), C.sizeof(WaveDesc)]
     got = list(sizes[:n])
     if got[: len(want)] != want:
         raise EngineError(f"struct layout mismatch between gfb.h and _lib.py: C {got} vs ctypes {want}")

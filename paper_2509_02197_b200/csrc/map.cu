@@ -5,6 +5,8 @@
 // The tasklet body runs as bytecode (gfb_common.cuh); subsets arrive as
 // affine element offsets precomputed by the host lowering, which has already
 // bounds-checked every subset over the whole iteration space.
+#include <cooperative_groups.h>
+
 #include <cstdio>
 
 #include "gfb_common.cuh"
@@ -75,6 +77,61 @@ __global__ void __launch_bounds__(256) map_pointwise_kernel(const __grid_constan
         add_as<T>(w.base, w.dtype, off, vals[o]);
       else
         atomic_add_as<T>(w.base, w.dtype, off, vals[o]);
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// sequential loop nests by hyperplanes (gfb_wave_desc)
+
+template <typename T>
+__global__ void __launch_bounds__(256) wavefront_kernel(const __grid_constant__ gfb_wave_desc w) {
+  namespace cg = cooperative_groups;
+  cg::grid_group grid = cg::this_grid();
+  const gfb_map_desc &d = w.map;
+  const int np = d.space.nparams, sv = w.solve;
+  const int64_t cs = w.c[sv], ns = d.space.box_ext[sv];
+  int64_t cand = 1;
+  for (int p = 0; p < np; ++p)
+    if (p != sv) cand *= d.space.box_ext[p];
+  const int64_t gstride = (int64_t)gridDim.x * blockDim.x;
+  const int64_t g0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  for (int64_t h = 0; h <= w.hmax; ++h) {
+    for (int64_t flat = g0; flat < cand; flat += gstride) {
+      int64_t k[GFB_MAX_PARAMS];
+      int64_t rem = flat, part = 0;
+      for (int p = np - 1; p >= 0; --p) {
+        if (p == sv) continue;
+        const int64_t e = d.space.box_ext[p];
+        k[p] = rem % e;
+        rem /= e;
+        part += w.c[p] * k[p];
+      }
+      const int64_t r = h - part;
+      if (r < 0 || r % cs != 0 || r / cs >= ns) continue;
+      k[sv] = r / cs;
+      int64_t x[GFB_MAX_PARAMS];
+      for (int p = 0; p < np; ++p) x[p] = d.space.box_lo[p] + k[p] * d.space.step[p];
+      auto fetch = [&](int q) -> T {
+        return load_as<T>(d.in[q].base, d.in[q].dtype, operand_offset(d.in[q], x, np));
+      };
+      // read-all-then-write per point, outputs in declaration order
+      T vals[GFB_MAX_OUTPUTS];
+#pragma unroll
+      for (int o = 0; o < GFB_MAX_OUTPUTS; ++o)
+        if (o < d.n_out) vals[o] = vm_eval<T>(d.code, d.arg, d.code_start[o], d.code_len[o], d.consts, fetch, d.err);
+      for (int o = 0; o < d.n_out; ++o) {
+        const gfb_operand &q = d.out[o];
+        const int64_t off = operand_offset(q, x, np);
+        if (d.wcr[o] == 0)
+          store_as<T>(q.base, q.dtype, off, vals[o]);
+        else
+          add_as<T>(q.base, q.dtype, off, vals[o]);
+      }
+    }
+    if (h < w.hmax) {
+      __threadfence();
+      grid.sync();
     }
   }
 }
@@ -247,4 +304,27 @@ extern "C" int gfb_gather_launch(const gfb_gather_desc *d, void *stream) {
   else
     gather_finish_kernel<float><<<fb, 256, 0, st>>>(*d, ny);
   return check_launch("gather_finish");
+}
+
+extern "C" int gfb_wave_launch(const gfb_wave_desc *w, void *stream) {
+  const gfb_map_desc *d = w ? &w->map : nullptr;
+  if (!d || d->space.nparams < 1 || d->space.nparams > GFB_MAX_PARAMS || d->n_in > GFB_MAX_INPUTS ||
+      d->n_out > GFB_MAX_OUTPUTS || d->n_out < 1 || w->solve < 0 || w->solve >= d->space.nparams ||
+      w->c[w->solve] <= 0 || w->hmax < 0)
+    return set_error(GFB_EINVAL, "gfb_wave_launch: bad descriptor");
+  int64_t cand = 1;
+  for (int p = 0; p < d->space.nparams; ++p)
+    if (p != w->solve) cand *= d->space.box_ext[p];
+  // one cooperative grid: every resident CTA (the grid barrier needs them all)
+  int per_sm = 0;
+  const void *fn = d->compute_f64 ? (const void *)wavefront_kernel<double> : (const void *)wavefront_kernel<float>;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, 256, 0) != cudaSuccess || per_sm < 1) per_sm = 1;
+  int64_t blocks = ceil_div(cand, 256);
+  const int64_t cap = (int64_t)sm_count() * per_sm;
+  if (blocks > cap) blocks = cap;
+  if (blocks < 1) blocks = 1;
+  void *args[] = {const_cast<gfb_wave_desc *>(w)};
+  cudaError_t e = cudaLaunchCooperativeKernel(fn, dim3((unsigned)blocks), dim3(256), args, 0, (cudaStream_t)stream);
+  if (e != cudaSuccess) return set_error(GFB_ECUDA, cudaGetErrorString(e));
+  return check_launch("wavefront");
 }

@@ -484,6 +484,115 @@ class MapOp(Op):
         L.check(rt.lib.gfb_map_launch(self._ref, stream), "map")
 
 
+class WavefrontOp(Op):
+    """A sequential loop nest of one tasklet executed by hyperplanes
+    (gfb_wave_launch): ``c`` are the hyperplane coefficients over the
+    loops' execution indices, proven dependence-respecting by
+    ``ProgramRun._wavefront``."""
+
+    family = "wavefront"
+
+    def __init__(self, space: SpaceInfo, ins: list, outs: list, code: Code, segs: list, compute_f64: bool, c):
+        self.space, self.ins, self.outs, self.code, self.segs = space, ins, outs, code, segs
+        self.compute_f64 = compute_f64
+        self.c = list(c)
+        self.reads = tuple(a.buf for a in ins) + tuple(a.buf for a, w in outs if w == 1)
+        self.writes = tuple(a.buf for a, _ in outs)
+
+    @property
+    def hmax(self) -> int:
+        return sum(c * (e - 1) for c, e in zip(self.c, self.space.ext))
+
+    @property
+    def solve(self) -> int:
+        return max(p for p, c in enumerate(self.c) if c > 0)
+
+    def remap(self, f):
+        for a in self.ins:
+            a.buf = f(a.buf)
+        for a, _ in self.outs:
+            a.buf = f(a.buf)
+        self.reads = tuple(f(b) for b in self.reads)
+        self.writes = tuple(f(b) for b in self.writes)
+
+    def prepare(self, rt):
+        w = L.WaveDesc()
+        d = w.map
+        self.space.fill(d.space)
+        d.n_in, d.n_out = len(self.ins), len(self.outs)
+        d.compute_f64 = 1 if self.compute_f64 else 0
+        for k, a in enumerate(self.ins):
+            fill_operand(d.in_[k], a, self.space.np)
+        for o, (a, wc) in enumerate(self.outs):
+            fill_operand(d.out[o], a, self.space.np)
+            d.wcr[o] = wc
+            d.code_start[o], d.code_len[o] = self.segs[o]
+        self.code.fill(d)
+        d.ncode = len(self.code.code)
+        d.err = rt.err_ptr
+        for p, c in enumerate(self.c):
+            w.c[p] = c
+        w.hmax = self.hmax
+        w.solve = self.solve
+        self.desc = w
+        self._ref = C.byref(w)
+
+    def launch(self, rt, stream):
+        L.check(rt.lib.gfb_wave_launch(self._ref, stream), "wavefront")
+
+
+def hyperplane(exts, deps):
+    """Smallest-span integer hyperplane c (c_p >= 0) with c . d >= 1 for
+    every dependence set in ``deps``; None if none with small coefficients.
+
+    A dependence set is (fixed, free): ``fixed`` maps loop position -> the
+    fixed difference of execution indices between the later and the earlier
+    iteration, ``free`` the positions whose difference is unconstrained
+    (iterators absent from the subscripts). Members: every d with those
+    components that is lexicographically positive (the later iteration
+    really is later) and |d_p| <= ext_p - 1."""
+    D = len(exts)
+
+    def ok(c):
+        for fixed, free in deps:
+            for lead in range(D):
+                # d_0..d_{lead-1} = 0, d_lead >= 1, the rest anything allowed
+                if any(fixed.get(p, 0) != 0 for p in range(lead) if p not in free):
+                    break
+                if lead not in free and fixed.get(lead, 0) <= 0:
+                    if fixed.get(lead, 0) < 0:
+                        break
+                    continue
+                if lead in free and exts[lead] < 2:
+                    continue
+                worst = 0
+                if lead in free:
+                    worst += c[lead] * 1
+                else:
+                    worst += c[lead] * fixed[lead]
+                for p in range(lead + 1, D):
+                    if p in free:
+                        worst -= c[p] * (exts[p] - 1)
+                    else:
+                        worst += c[p] * fixed.get(p, 0)
+                if worst < 1:
+                    return False
+                if lead not in free:
+                    break  # a fixed positive leading component: no later lead
+        return True
+
+    best = None
+    rng = range(0, 7)
+    for c in itertools.product(rng, repeat=D):
+        if not any(c):
+            continue
+        if ok(c):
+            span = sum(ci * (e - 1) for ci, e in zip(c, exts))
+            if best is None or span < best[0]:
+                best = (span, c)
+    return None if best is None else list(best[1])
+
+
 class GatherOp(Op):
     family = "map_gather"
 
@@ -2026,7 +2135,159 @@ class ProgramRun:
             i = eval_int(loop.update, b, f"update of '{loop.label}'")
         return out
 
+    # nests of at least this many iterations are tried as hyperplane wavefronts
+    WAVE_MIN = int(os.environ.get("GFB_WAVE_MIN", "256"))
+
+    def _wavefront(self, loop) -> bool:
+        """A perfectly nested loop nest whose innermost body is one state with
+        one scalar tasklet (the reference visits it point by point in loop
+        order, interpreter.py:221-330, 396-426), lowered to ONE launch that
+        runs hyperplanes of the iteration space in order (WavefrontOp).
+
+        Every array the tasklet writes must be accessed (read and written)
+        through subsets of the form x_p + const along each dimension (one
+        loop iterator per dimension, shared by all its accesses). Two
+        iterations X1 before X2 touch one element through accesses o1, o2
+        iff X2 - X1 = o1 - o2 on the subscripted iterators; iterators absent
+        from the subscripts (the time loop) are unconstrained. A hyperplane
+        sum_p c_p k_p (k_p = execution index of loop p) with c . (X2 - X1) >= 1
+        for all such pairs, at least one of the two a write, orders every
+        conflicting pair as the sequential nest does (hyperplane()). Returns
+        False (the caller unrolls) when the shape or the proof fails."""
+        nest, cur = [], loop
+        while True:
+            if (not isinstance(cur, LoopRegion) or cur.replay_of is not None or cur.reversed_simulate
+                    or cur.label in self.ctx):
+                return False
+            nest.append(cur)
+            if len(cur.body) != 1:
+                return False
+            inner = cur.body[0]
+            if isinstance(inner, State):
+                state = inner
+                break
+            cur = inner
+        if len(nest) > 4:  # the hyperplane search is exhaustive over small coefficients
+            return False
+        comp = [n for n in state.graph.nodes if not isinstance(n, AccessNode)]
+        if len(comp) != 1 or not isinstance(comp[0], Tasklet):
+            return False
+        t = comp[0]
+        iters = [lp.iterator for lp in nest]
+        if len(set(iters)) != len(iters) or any(i in self.bind for i in iters):
+            return False
+        for lp in nest:
+            names = free_names(lp.init) | free_names(lp.bound) | free_names(lp.update)
+            if names & (set(iters) - {lp.iterator}):
+                return False  # not rectangular
+        # recorded values inside the nest (tape) need the per-point walk
+        if self.tape is not None and self.versions is not None and self.record:
+            version_of, _ = self.versions
+            for n in state.graph.nodes:
+                if isinstance(n, AccessNode):
+                    v = version_of.get((state.label, n.id))
+                    if v is not None and self._want(n.data, v):
+                        return False
+        seqs = [self.simulate(lp) for lp in nest]
+        lo, hi, step = [], [], []
+        for sq in seqs:
+            if not sq:
+                return False
+            st = sq[1] - sq[0] if len(sq) > 1 else 1
+            if st == 0 or any(b - a != st for a, b in zip(sq, sq[1:])):
+                return False
+            lo.append((sq[0], [0] * len(nest)))
+            hi.append((sq[0] + st * len(sq), [0] * len(nest)))
+            step.append(st)
+        total = int(np.prod([len(sq) for sq in seqs], dtype=np.int64))
+        if total < self.WAVE_MIN:
+            return False
+        space = SpaceInfo(iters, lo, hi, step)
+        in_edges, out_edges = state.graph.in_edges(t.id), state.graph.out_edges(t.id)
+        written = {e.data for e in out_edges}
+        # per written array: every access is dim d = x_{p(d)} + off_d
+        accs = {}
+        for e, is_w in [(e, False) for e in in_edges] + [(e, True) for e in out_edges]:
+            if e.data not in written:
+                continue
+            forms = [affine_form(x, self.bind, tuple(iters), f"subset of '{e.data}'") for x in (e.subset or ())]
+            pos, offs = [], []
+            for c0, coefs in forms:
+                nz = [p for p, v in enumerate(coefs) if v != 0]
+                if len(nz) > 1 or (nz and coefs[nz[0]] != 1):
+                    return False
+                pos.append(nz[0] if nz else None)
+                offs.append(c0)
+            accs.setdefault(e.data, []).append((tuple(pos), tuple(offs), is_w))
+        deps = []
+        D = len(nest)
+        for data, lst in accs.items():
+            shapes = {a[0] for a in lst}
+            if len(shapes) != 1:
+                return False
+            pos = next(iter(shapes))
+            used = [p for p in pos if p is not None]
+            if len(used) != len(set(used)):
+                return False
+            free = frozenset(p for p in range(D) if p not in used)
+            for (_, o1, w1), (_, o2, w2) in itertools.product(lst, lst):
+                if not (w1 or w2):
+                    continue
+                # constant subscripts must agree for the element to be shared
+                if any(pp is None and a != b for pp, a, b in zip(pos, o1, o2)):
+                    continue
+                fixed = {}
+                for pp, a, b in zip(pos, o1, o2):
+                    if pp is None:
+                        continue
+                    dx = a - b  # X2 - X1 in iterator units
+                    if dx % step[pp]:
+                        fixed = None
+                        break
+                    fixed[pp] = dx // step[pp]
+                if fixed is None:
+                    continue
+                deps.append((fixed, free))
+        c = hyperplane([len(sq) for sq in seqs], deps)
+        if c is None:
+            return False
+        # operands (bounds-checked over the whole nest) and the body code
+        ins = {e.dst_conn: self.access(self.read(e.data), e.subset, space, f"loop nest '{loop.label}'")
+               for e in in_edges}
+        outs = [(e.src_conn, self.access(self.write(e.data), e.subset, space, f"loop nest '{loop.label}'"), e.wcr)
+                for e in out_edges]
+        self.low.flops += sum(count_ops(t.body[e.src_conn]) for e in out_edges) * total
+        for a in list(ins.values()) + [a for _, a, _ in outs]:
+            self.low.materialize(a.buf)
+        conns = list(ins)
+        if len(conns) > L.MAXIN or len(outs) > L.MAXOUT:
+            return False
+        code = Code()
+        ci = {cn: k for k, cn in enumerate(conns)}
+        segs = [code.compile(t.body[conn], ci) for conn, _, _ in outs]
+        compute_f64 = any(a.buf.kind == "real64" for a in ins.values()) or not ins
+        op = WavefrontOp(space, [ins[cn] for cn in conns], [(a, 1 if w == "sum" else 0) for _, a, w in outs],
+                         code, segs, compute_f64, c)
+        self.low.emit(op)
+        if self.tape is not None:
+            # the iterate records the per-point walk leaves for a reverse pass
+            # that replays loops (reference Tape.iterate_records); constant-
+            # step headers reverse in closed form, so only bounded record sets
+            # are kept (a replay that needs more raises MissingTapeValue)
+            key0 = tuple(cc.current for cc in self.ctx_stack)
+            n_outer = 1
+            for depth, lp in enumerate(nest):
+                if n_outer > 4096:
+                    break
+                recs = self.tape.iterate_records.setdefault(lp.label, {})
+                for outer in itertools.product(*seqs[:depth]):
+                    recs[key0 + tuple(outer)] = list(seqs[depth])
+                n_outer *= len(seqs[depth])
+        return True
+
     def loop(self, loop):
+        if os.environ.get("GFB_WAVEFRONT", "1") != "0" and self._wavefront(loop):
+            return
         if loop.replay_of is not None:
             if self.src_tape is None:
                 raise MissingInverse(

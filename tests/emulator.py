@@ -28,6 +28,7 @@ from paper_2509_02197_b200.lowering import (
     ReduceOp,
     StarPairOp,
     StencilOp,
+    WavefrontOp,
 )
 
 NPT = {L.F32: np.float32, L.F64: np.float64}
@@ -174,7 +175,9 @@ class Emulator:
         return a, o
 
     def run_op(self, op):
-        if isinstance(op, MapOp):
+        if isinstance(op, WavefrontOp):
+            self.wave(op.desc)
+        elif isinstance(op, MapOp):
             self.map(op.desc)
         elif isinstance(op, GatherOp):
             self.gather(op.desc)
@@ -356,6 +359,44 @@ class Emulator:
                 a[idx] = a[idx] + v
             else:
                 np.add.at(a, idx, v)
+
+    def wave(self, w):
+        """gfb_wave_launch: hyperplanes in order, each one's points at once
+        (read all, then write); asserts the points of a hyperplane never
+        write one element twice (the host's dependence proof)."""
+        d = w.map
+        T = np.float64 if d.compute_f64 else np.float32
+        sp = d.space
+        npar = sp.nparams
+        ks = np.stack([g.reshape(-1) for g in np.meshgrid(*[np.arange(sp.box_ext[p]) for p in range(npar)],
+                                                          indexing="ij")])
+        h = sum(int(w.c[p]) * ks[p] for p in range(npar))
+        xs = np.stack([sp.box_lo[p] + ks[p] * sp.step[p] for p in range(npar)])
+        for hv in range(int(w.hmax) + 1):
+            sel = np.nonzero(h == hv)[0]
+            if sel.size == 0:
+                continue
+            x = xs[:, sel]
+
+            def fetch(k):
+                o = d.in_[k]
+                a, base = self.arr(o.base)
+                return a[base + _offsets(o, x, npar)].astype(T)
+
+            vals = [_vm(list(d.code), list(d.arg), d.code_start[o], d.code_len[o], list(d.consts), fetch, T,
+                        self.err) for o in range(d.n_out)]
+            writers = {}  # element -> the one point of this hyperplane that writes it
+            for o in range(d.n_out):
+                q = d.out[o]
+                a, base = self.arr(q.base)
+                idx = base + _offsets(q, x, npar)
+                for pt, e in enumerate(np.broadcast_to(idx, (x.shape[1],)).tolist()):
+                    assert writers.setdefault((q.base, e), pt) == pt, "two points of one hyperplane write one element"
+                v = np.broadcast_to(np.asarray(vals[o]), idx.shape)
+                if d.wcr[o] == 0:
+                    a[idx] = v
+                else:
+                    a[idx] = a[idx] + v
 
     def gather(self, d):
         T = np.float64 if d.compute_f64 else np.float32

@@ -39,7 +39,7 @@ def _check(lw, view, prog, value, grads):
         assert rel_err(got, ref) <= tol, k
 
 
-CASES = sorted(IDX["cases"]) + sorted(c for c in IDX["examples"] if "seidel" not in c and "branchy" not in c)
+CASES = sorted(IDX["cases"]) + sorted(c for c in IDX["examples"] if "branchy" not in c)
 
 
 @pytest.mark.parametrize("cid", CASES)

@@ -260,3 +260,52 @@ def test_batch_shape_follows_the_reference_rule():
     with pytest.raises(ShapeMismatch):
         _check_inputs(prog, {"A": np.ones((2, 6, 5)), "x": x}, params, batch=(4, 3))
     assert batch_of(prog, {"A": A, "x": np.ones((5, 1))}) == ()
+
+
+# -- sequential loop nests by hyperplanes (lowering.ProgramRun._wavefront) -------
+
+
+def test_seidel_nest_lowers_to_two_wavefront_launches():
+    """The corpus Gauss-Seidel nest (reference examples.py:159-182) runs as
+    one hyperplane launch per direction instead of one launch per point;
+    the emulated launch list reproduces the reference golden exactly and the
+    reference op_count."""
+    from conftest import load_case
+    from paper_2509_02197_b200.lowering import WavefrontOp
+
+    prog, b = _bundle("corpus_seidel_stencil")
+    inputs, value, grads, op_count = load_case("corpus_seidel_stencil__N40_TSTEPS10")
+    params = {"N": 40, "TSTEPS": 10}
+    lw = lower_gradient(prog, b, params, _check_inputs(prog, inputs, params))
+    waves = [op for op in lw.low.ops if isinstance(op, WavefrontOp)]
+    assert len(waves) == 2 and len(lw.low.ops) <= 4
+    assert waves[0].c == [2, 1, 1]  # forward: 2t + i + j
+    em, view = E.execute(lw.low, inputs, lw.inputs, lw.seed_buf)
+    assert rel_err(view(lw.outputs["value"]), value) <= 1e-13
+    assert rel_err(view(lw.outputs["grad:A"]), grads["A"]) <= 1e-13
+    assert lw.low.flops == op_count
+
+
+def test_hyperplane_respects_every_dependence():
+    from paper_2509_02197_b200.lowering import hyperplane
+
+    # 2-D in-place recurrence x[i] = f(x[i-1]) inside a time loop: (t free, i)
+    deps = [({1: 1}, frozenset({0})), ({1: -1}, frozenset({0})), ({1: 0}, frozenset({0}))]
+    c = hyperplane([5, 7], deps)
+    assert c is not None
+    for d_t in range(-4, 5):
+        for d_i in range(-6, 7):
+            lexpos = d_t > 0 or (d_t == 0 and d_i > 0)
+            if lexpos and d_i in (1, -1, 0):
+                assert c[0] * d_t + c[1] * d_i >= 1
+    # a dependence no small hyperplane can order: A[i] += B[j] over (i, j)
+    # with i free inside j ... (every i conflicts with every other i)
+    assert hyperplane([3, 50], [({}, frozenset({0, 1}))]) is None
+
+
+def test_seidel_oracle_is_pinned_to_the_reference_golden():
+    from conftest import load_case
+    from oracle import stencil_ref as S
+
+    inputs, value, _, _ = load_case("corpus_seidel_stencil__N40_TSTEPS10")
+    assert rel_err(S.seidel_value({"N": 40, "TSTEPS": 10}, inputs["A"]), value) <= 1e-13
