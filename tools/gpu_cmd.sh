@@ -1,2 +1,3 @@
-timeout 600 ncu --set full --import-source on --clock-control none -k regex:star_pair --launch-skip 1 -c 1 -o gpurun_out/r2_star_fwd python tools/prof_stencil.py heat_3d 512 4 > gpurun_out/r2_ncu_full.log 2>&1
-timeout 600 ncu --set full --import-source on --clock-control none -k regex:star_pair --launch-skip 4 -c 1 -o gpurun_out/r2_star_adj2 python tools/prof_stencil.py heat_3d 512 4 >> gpurun_out/r2_ncu_full.log 2>&1
+python -m pytest tests/test_gpu.py tests/test_gpu_r2.py -q -x -k "heat or jacobi or golden or stencil or medium" > gpurun_out/r2_chain_tests.log 2>&1
+python tools/bench_all.py --no-cpu --steps 20 --only C2/heat_3d,C1/jacobi_2d > gpurun_out/r2_chain.jsonl 2> gpurun_out/r2_chain.err
+GFB_STENCIL_CHAIN=0 python tools/bench_all.py --no-cpu --steps 20 --only C2/heat_3d >> gpurun_out/r2_chain.jsonl 2>> gpurun_out/r2_chain.err
