@@ -66,6 +66,9 @@ namespace GFB_STAR_NS {
 #ifndef GFB_STAR_WARPFAST
 #define GFB_STAR_WARPFAST 1
 #endif
+#ifndef GFB_STAR_STEADY
+#define GFB_STAR_STEADY 1
+#endif
 constexpr int tPX = 32, tPY = GFB_STAR_TPY, tPM = GFB_STAR_TPM;  // CTA tile (k, j) and planes
 constexpr int kR = GFB_STAR_KR;                                   // Z rows per thread
 constexpr int tThreads = tPX * (tPY / kR);
@@ -423,20 +426,27 @@ __device__ __forceinline__ void star_tma_body(const CUtensorMap *ymap, const Sta
   // the start of the step; other instantiations load it in the fix-up (only
   // the out-of-region copies of the first timesteps need it)
   constexpr bool kZPre = MODES < 0 || (MODES % 4) == 0 || (MODES % 4) == 2;
-  auto step = [&](auto S, int q) {
+  // ST (steady): a plane inside the segment's steady range [qs, qe) --
+  // common X and Z planes, owned, loaded and clean, TMA issue in range -- so
+  // every guard of the general step folds away at compile time
+  int qe_steady = 0;
+  auto step = [&](auto S, int q, auto ST) {
     constexpr int M = decltype(S)::value, C = (M + 1) % 3, P = (M + 2) % 3;
+    constexpr bool steady = decltype(ST)::value;
+    if (!steady) {
 #pragma unroll
-    for (int u = 0; u < kR; ++u) xv[u][P] = T(0);
+      for (int u = 0; u < kR; ++u) xv[u][P] = T(0);
+    }
     // old Z values the fix-ups of Z(i) need (plane not common): loaded
     // before the X sweep so their latency overlaps it
     const int i = HAS_I ? q - 1 : q;
-    const bool zon = i >= i0 && i < i1;
-    const uint32_t mzi = zon ? W.bi[i - i0] : 0u;
-    const bool zfast = ((mzi & jkb) & zmask) == zmask;
+    const bool zon = steady || (i >= i0 && i < i1);
+    const uint32_t mzi = (!steady && zon) ? W.bi[i - i0] : 0u;
+    const bool zfast = steady || ((mzi & jkb) & zmask) == zmask;
     T zo[kR];
 #pragma unroll
     for (int u = 0; u < kR; ++u) zo[u] = T(0);
-    if (kZPre && zon && !zfast) {
+    if (!steady && kZPre && zon && !zfast) {
       const T *zold = Zo + (size_t)i * ps + rel0;
 #pragma unroll
       for (int u = 0; u < kR; ++u) {
@@ -446,10 +456,10 @@ __device__ __forceinline__ void star_tma_body(const CUtensorMap *ymap, const Sta
         if (need) zo[u] = zold[u * rs];
       }
     }
-    if (q < d.d0) {
+    if (steady || q < d.d0) {
       if (tid == 0) {
         const int pn = q + 1 + kDist;
-        if (pn > pre_hi && pn <= yhi) {
+        if (steady || (pn > pre_hi && pn <= yhi)) {
           asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
           issue(pn);
         }
@@ -458,8 +468,8 @@ __device__ __forceinline__ void star_tma_body(const CUtensorMap *ymap, const Sta
         // plane q + 2 is needed by X(q + 1): land it and mask it now; the
         // barrier below orders this before any read of it
         const int pn = q + 2;
-        if (pn <= yhi && pn > qbeg + 1) mbar_wait(&mbar[wsl], wph);
-        if (pn <= qend + 1 && pn > qbeg + 1 && (pn < clean_lo || pn >= clean_hi)) prepare_plane(pn);
+        if (steady || (pn <= yhi && pn > qbeg + 1)) mbar_wait(&mbar[wsl], wph);
+        if (!steady && pn <= qend + 1 && pn > qbeg + 1 && (pn < clean_lo || pn >= clean_hi)) prepare_plane(pn);
       }
       const T *yc = ys + ysl * YSS;
       const T *yp = ys + (ysl + 1 == (unsigned)NSY ? 0u : ysl + 1) * YSS;
@@ -470,11 +480,11 @@ __device__ __forceinline__ void star_tma_body(const CUtensorMap *ymap, const Sta
 #else
       T *xw = xs + ((unsigned)(q - qbeg) % (unsigned)NXS) * XS;
 #endif
-      const uint32_t mi = W.ai[q - i0 + 1];
-      const bool fast = ((mi & jka) & xfast_m) == xfast_m;
-      const bool own = q >= i0 && q < i1;
+      const uint32_t mi = steady ? 0u : W.ai[q - i0 + 1];
+      const bool fast = steady || ((mi & jka) & xfast_m) == xfast_m;
+      const bool own = steady || (q >= i0 && q < i1);
       if (!fast) cp_async_wait_all();  // this thread's staged old values of plane q
-      prefetch_xo(q + 1);
+      if (!steady || q + 1 >= qe_steady) prefetch_xo(q + 1);
       if (HAS_I) {
 #pragma unroll
         for (int u = 0; u < kR; ++u) yv[u][P] = yp[yo0 + u * YK];
@@ -613,17 +623,66 @@ __device__ __forceinline__ void star_tma_body(const CUtensorMap *ymap, const Sta
   using I1 = std::integral_constant<int, 1>;
   using I2 = std::integral_constant<int, 2>;
 #if GFB_STAR_UNROLL
+  // steady range: X plane q and Z plane q - 1 common (warp-uniform words),
+  // q owned, its TMA issue and wait inside the segment's ranges, plane q + 2
+  // clean. Each warp finds it with ballots over 32 planes at a time (all
+  // warps agree: the words are the CTA's plane words AND the warp's own).
+  int qs = qbeg, qe = qbeg;
+  if (HAS_I && GFB_STAR_STEADY) {
+    const int lo = max(max(i0 + 1, qbeg), clean_lo - 2);
+    const int hi = min(min(min(i1, d.d0), yhi - kDist), clean_hi - 2);  // exclusive
+    const int lane = threadIdx.x & 31;
+    bool found = false;
+    for (int c = lo; c < hi; c += 32) {
+      const int q = c + lane;
+      bool ok = q < hi;
+      if (ok) {
+        const uint32_t mi = W.ai[q - i0 + 1], mz = W.bi[q - 1 - i0];
+        ok = ((mi & jka) & xfast_m) == xfast_m && ((mz & jkb) & zmask) == zmask;
+      }
+      const uint32_t bad = __ballot_sync(0xffffffffu, !ok && q < hi), good = __ballot_sync(0xffffffffu, ok);
+      if (!found) {
+        if (good) {
+          qs = c + __ffs(good) - 1;
+          found = true;
+          const uint32_t after = bad & ~((2u << (__ffs(good) - 1)) - 1u);  // failures past the first good
+          if (after) {
+            qe = c + __ffs(after) - 1;
+            break;
+          }
+          qe = min(c + 32, hi);
+        }
+      } else {
+        if (bad) {
+          qe = c + __ffs(bad) - 1;
+          break;
+        }
+        qe = min(c + 32, hi);
+      }
+    }
+    // align to the 3-step unroll (slot indices are compile-time)
+    qs = qbeg + (qs - qbeg + 2) / 3 * 3;
+    qe = qe > qs ? qs + (qe - qs) / 3 * 3 : qs;
+  }
+  qe_steady = qe;
+  // one loop, two bodies: steady 3-blocks inside [qs, qe), general otherwise
   for (int q = qbeg; q <= qend; q += 3) {
-    step(I0{}, q);
+    if (q >= qs && q + 3 <= qe) {
+      step(I0{}, q, std::true_type{});
+      step(I1{}, q + 1, std::true_type{});
+      step(I2{}, q + 2, std::true_type{});
+      continue;
+    }
+    step(I0{}, q, std::false_type{});
     if (q + 1 > qend) break;
-    step(I1{}, q + 1);
+    step(I1{}, q + 1, std::false_type{});
     if (q + 2 > qend) break;
-    step(I2{}, q + 2);
+    step(I2{}, q + 2, std::false_type{});
   }
 #else
   // one step body, registers rotated by moves (smaller code)
   for (int q = qbeg; q <= qend; ++q) {
-    step(I0{}, q);
+    step(I0{}, q, std::false_type{});
 #pragma unroll
     for (int u = 0; u < kR; ++u) {
       yv[u][0] = yv[u][1];
