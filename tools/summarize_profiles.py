@@ -71,8 +71,8 @@ def ncu_full(tag):
     rows = list(csv.reader(io.StringIO(raw)))
     hdr, units = rows[0], rows[1]
     idx = {h: i for i, h in enumerate(hdr)}
-    out = ["ncu --set full --clock-control none --import-source on -k regex:star_pair -c 4 "
-           "python tools/prof_stencil.py heat_3d 512 3", ""]
+    out = ["ncu --set full --clock-control none --import-source on -k regex:star_pair --launch-skip 1 -c 4 "
+           "python tools/prof_stencil.py heat_3d 512 4", ""]
     traffic = []
     for n, r in enumerate(rows[2:]):
         out.append(f"launch {n}: {r[idx['Kernel Name']]}  grid {r[idx.get('launch__grid_size', 0)]}")
@@ -95,8 +95,46 @@ def ncu_full(tag):
         json.dump({"star_pair": {"dram_bytes_per_launch": sum(traffic) / len(traffic),
                                  "launches": len(traffic),
                                  "source": f"profiles/{tag}_ncu_star_pair.txt (dram__bytes_read.sum + "
-                                           "dram__bytes_write.sum, heat_3d 512^3, first forward launches)"}},
+                                           "dram__bytes_write.sum, heat_3d 512^3, launches 1-4: steady forward and adjoint timesteps)"}},
                   f, indent=1)
+
+
+def ncu_lines(tag):
+    """Per-source-line instruction / stall attribution of the captured
+    star-pair launches (tools/ncu_lines.py over nvdisasm's line table)."""
+    rep = os.path.join(OUT, "prof_top.ncu-rep")
+    obj = os.path.join(REPO, "build", "obj", "star_tma.o")
+    if not (os.path.exists(rep) and os.path.exists(obj)):
+        return
+    import tempfile
+
+    tmp = tempfile.mkdtemp()
+    src_csv = os.path.join(tmp, "src.csv")
+    with open(src_csv, "w") as f:
+        subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass"], stdout=f,
+                       stderr=subprocess.DEVNULL)
+    subprocess.run(["cuobjdump", "-xelf", "all", obj], cwd=tmp, capture_output=True)
+    cubins = [c for c in os.listdir(tmp) if c.endswith(".cubin")]
+    sass = os.path.join(tmp, "all.sass")
+    with open(sass, "w") as f:
+        subprocess.run(["nvdisasm", "-g", "-c"] + [os.path.join(tmp, c) for c in cubins], stdout=f)
+    kernels = [r.split('"')[3] for r in open(src_csv) if r.startswith('"Kernel Name"')]
+    out = []
+    src = os.path.join(REPO, "paper_2509_02197_b200", "csrc", "star_tma.cu")
+    seen = set()
+    for k, name in enumerate(kernels):
+        modes = name.split("(int)")[-1].split(">")[0]
+        if modes in seen:
+            continue
+        seen.add(modes)
+        mangled = f"_ZN3gfb6tile3220star_pair_tma_kernelIdLb1ELi{modes}EEEv14CUtensorMap_stNS_11StarPairDevE"
+        r = subprocess.run([sys.executable, os.path.join(REPO, "tools", "ncu_lines.py"), mangled, sass, src_csv,
+                            str(k), src, "140", "900"], capture_output=True, text=True)
+        lines = r.stdout.splitlines()
+        body = [l for l in lines[2:] if l.strip() and float(l.split()[0]) >= 2.0]
+        out += [f"== {name} (MODES {modes}): M warp instructions, stall samples, source line", *lines[:2], *body, ""]
+    with open(os.path.join(PROF, f"{tag}_ncu_star_lines.txt"), "w") as f:
+        f.write("\n".join(out))
 
 
 def main():
@@ -115,6 +153,7 @@ def main():
             shutil.copy(os.path.join(OUT, src), os.path.join(PROF, dst))
     launches(tag)
     ncu_full(tag)
+    ncu_lines(tag)
     print("\n".join(sorted(os.listdir(PROF))))
 
 
