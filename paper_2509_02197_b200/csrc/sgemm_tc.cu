@@ -24,6 +24,7 @@
 #include <cudaTypedefs.h>
 
 #include <algorithm>
+#include <type_traits>
 
 #include "gfb_common.cuh"
 #include "gfb_internal.h"
@@ -220,7 +221,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
                    : "r"(taddr));
     }
     asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-    if (csn == 1 && !partial) {
+    if (csn == 1) {
       // row-major C: transpose the warp's 32 rows x kGrp columns through
       // (now idle) stage memory so lanes walk consecutive columns of a row
       float *scr = S.a[0][0] + warp * (32 * (kGrp + 1));
@@ -233,8 +234,9 @@ __global__ void __launch_bounds__(kTcThreads, 1)
           const int rm = m0 + quarter * 32 + r;
           if (rm >= M || gn >= N) continue;
           const float x = scr[r * (kGrp + 1) + lane];
-          float *o = C + (int64_t)rm * csm + gn;
-          *o = accumulate ? *o + x : x;
+          // split-K partials are laid out like C ([z][m][n] here)
+          float *o = partial ? partial + ((int64_t)blockIdx.z * M + rm) * N + gn : C + (int64_t)rm * csm + gn;
+          *o = accumulate && !partial ? *o + x : x;
         }
       }
       __syncwarp();
@@ -255,7 +257,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
       if (gn >= N) continue;
       const float x = nslab > 0 ? __uint_as_float(v[j]) : 0.f;
       if (partial)
-        partial[((int64_t)blockIdx.z * M + gm) * N + gn] = x;
+        partial[((int64_t)blockIdx.z * N + gn) * M + gm] = x;  // column-major C: [z][n][m], lanes coalesced
       else
         C[(int64_t)gm * csm + (int64_t)gn * csn] = accumulate ? old[j] + x : x;
     }
@@ -267,20 +269,23 @@ __global__ void __launch_bounds__(kTcThreads, 1)
 
 // ---------------------------------------------------------------------------
 // TMA-fed variant (16-byte aligned operands): one elected producer thread
-// streams raw fp32 k-slabs by cp.async.bulk.tensor into a ring; six splitter
-// warps turn each raw slab into the hi / lo TF32 operands (in place for
-// K-major slabs, which TMA already writes in the SWIZZLE_128B canonical
-// layout; through a transpose for MN-major ones); one elected thread issues
-// the MMAs. Global loads no longer wait on the staging threads, so a CTA
-// keeps several slabs of HBM traffic in flight (the skinny, weight-streaming
-// mlp shapes are HBM-bound).
+// streams raw fp32 k-slabs by cp.async.bulk.tensor into a ring in the
+// SWIZZLE_128B canonical layout of either major (K-major: one box of 32 k x
+// rows; MN-major: one 32 (MN) x 32 (k) box per 128-byte atom, described to
+// the MMA as MN-major); the tensor core truncates fp32 operands to TF32
+// itself (checked bit for bit against an explicit hi copy), so the raw slab
+// IS the hi operand and six splitter warps only write lo = x - trunc(x),
+// elementwise at the same offsets; one elected thread issues the MMAs.
+// Global loads no longer wait on the staging threads, so a CTA keeps several
+// slabs of HBM traffic in flight (the skinny, weight-streaming mlp shapes are
+// HBM-bound).
 constexpr int kTmaSplitWarps = 6;
 
 template <int BN, bool AKM, bool BKM, bool SK = false>
 struct TmaCfg {
   static constexpr int kRawA = kTcM * kTcK * 4, kRawB = BN * kTcK * 4;  // bytes
-  // per stage: raw A (= hi A when K-major), [hi A], lo A, raw B, [hi B], lo B
-  static constexpr int kStage = kRawA * (AKM ? 2 : 3) + kRawB * (BKM ? 2 : 3);
+  // per stage: raw A (= hi A), lo A, raw B (= hi B), lo B
+  static constexpr int kStage = 2 * (kRawA + kRawB);
   // SK (short k: at most two slabs per CTA): one stage, so several CTAs
   // share an SM and one CTA's epilogue overlaps another's loads
   static constexpr int kStages = SK ? 1 : ((200 * 1024) / kStage > 4 ? 4 : (200 * 1024) / kStage);
@@ -292,6 +297,18 @@ __device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap *map
       "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];"
       ::"r"(dst), "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(bar)
       : "memory");
+}
+
+// one raw slab: K-major = a (32 k) x rows box at (k0, mn0); MN-major = one
+// 32 (MN) x 32 (k) box per atom at (mn0 + 32 a, k0)
+template <int ROWS, bool KM>
+__device__ __forceinline__ void load_slab(uint32_t dst, const CUtensorMap *map, uint32_t bar, int k0, int mn0) {
+  if constexpr (KM) {
+    tma_load_2d(dst, map, bar, k0, mn0);
+  } else {
+#pragma unroll
+    for (int a = 0; a < ROWS / 32; ++a) tma_load_2d(dst + a * (kTcK * 128), map, bar, mn0 + 32 * a, k0);
+  }
 }
 
 __device__ __forceinline__ void tc_mbar_init_n(uint64_t *bar, uint32_t n) {
@@ -307,35 +324,35 @@ __device__ __forceinline__ void tc_mbar_expect_tx(uint64_t *bar, uint32_t bytes)
                : "memory");
 }
 
-// split one raw slab of `rows` rows into hi / lo K-major SW128 operands
-template <int ROWS, bool KM>
-__device__ __forceinline__ void split_slab(uint32_t raw, uint32_t hi, uint32_t lo, int st) {
+// lo operand of one raw slab of `rows` rows (either major: elementwise, the
+// same canonical offsets as the raw slab)
+template <int ROWS>
+__device__ __forceinline__ void split_slab(uint32_t raw, uint32_t lo, int st) {
   constexpr int kNSt = kTmaSplitWarps * 32;
-  if constexpr (KM) {
-    // raw is already the canonical layout: elementwise, hi written in place
-    for (int c = st; c < ROWS * 8; c += kNSt) {
-      float4 x;
-      asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
-                   : "=f"(x.x), "=f"(x.y), "=f"(x.z), "=f"(x.w)
-                   : "r"(raw + c * 16));
-      const float4 h = make_float4(tf32_hi(x.x), tf32_hi(x.y), tf32_hi(x.z), tf32_hi(x.w));
-      sts128(raw + c * 16, h);
-      sts128(lo + c * 16, make_float4(x.x - h.x, x.y - h.y, x.z - h.z, x.w - h.w));
-    }
-  } else {
-    // raw[k][r] (r contiguous): chunk (r, kc) gathers k = 4kc..4kc+3 of row r
-    for (int c = st; c < ROWS * 8; c += kNSt) {
-      const int r = c % ROWS, kc = c / ROWS;
-      float v[4];
-#pragma unroll
-      for (int j = 0; j < 4; ++j)
-        asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v[j]) : "r"(raw + ((kc * 4 + j) * ROWS + r) * 4));
-      const float4 h = make_float4(tf32_hi(v[0]), tf32_hi(v[1]), tf32_hi(v[2]), tf32_hi(v[3]));
-      const uint32_t o = sw128(r, kc * 4);
-      sts128(hi + o, h);
-      sts128(lo + o, make_float4(v[0] - h.x, v[1] - h.y, v[2] - h.z, v[3] - h.w));
-    }
+#pragma unroll 2
+  for (int c = st; c < ROWS * 8; c += kNSt) {
+    float4 x;
+    asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+                 : "=f"(x.x), "=f"(x.y), "=f"(x.z), "=f"(x.w)
+                 : "r"(raw + c * 16));
+    sts128(lo + c * 16, make_float4(x.x - tf32_hi(x.x), x.y - tf32_hi(x.y), x.z - tf32_hi(x.z), x.w - tf32_hi(x.w)));
   }
+}
+
+// UMMA descriptor of an MN-major tf32 operand. The only MN-major layout the
+// tensor core takes for 32-bit types is "128B swizzle with 32-byte atoms"
+// (layout type 1; TMA's SWIZZLE_128B_ATOM_32B writes it): 128-byte MN rows
+// whose 32-byte granules are XOR-ed with the row index mod 4. Here: 32-element
+// MN atoms of 32 k rows (4 KiB apart: leading byte offset), 4-row k groups
+// 512 B apart (stride byte offset)
+__device__ __forceinline__ uint64_t umma_desc_sw128_mn(uint32_t saddr) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3FFFu);
+  d |= (uint64_t)((kTcK * 128) >> 4) << 16;
+  d |= (uint64_t)(512 >> 4) << 32;
+  d |= (uint64_t)1 << 46;
+  d |= (uint64_t)1 << 61;
+  return d;
 }
 
 template <int BN, bool AKM, bool BKM, bool SK>
@@ -357,10 +374,9 @@ __global__ void __launch_bounds__(kTcThreads, 1)
   // (one N = 2 BN MMA over the adjacent hi | lo rows of B): two MMAs per
   // k-step instead of three, a third less shared-memory operand traffic
   constexpr int kCols = 2 * BN < 32 ? 32 : 2 * BN;
-  // stage layout (byte offsets): rawA | hiA (MN-major only) | loA | rawB | hiB | loB
-  constexpr int oRawA = 0, oHiA = AKM ? 0 : Cfg::kRawA, oLoA = AKM ? Cfg::kRawA : 2 * Cfg::kRawA;
-  constexpr int oRawB = oLoA + Cfg::kRawA, oHiB = BKM ? oRawB : oRawB + Cfg::kRawB;
-  constexpr int oLoB = oHiB + Cfg::kRawB;
+  // stage layout (byte offsets): rawA | loA | rawB | loB (lo right after hi
+  // along the operand's rows: one MMA reads B's hi | lo as 2 BN rows)
+  constexpr int oRawA = 0, oLoA = Cfg::kRawA, oRawB = 2 * Cfg::kRawA, oLoB = oRawB + Cfg::kRawB;
   const uint32_t sbase = tc_smem(base);
 
   if (warp == 0) {
@@ -390,34 +406,36 @@ __global__ void __launch_bounds__(kTcThreads, 1)
         const uint32_t st = sbase + s * Cfg::kStage;
         const int k0 = kb + t * kTcK;
         tc_mbar_expect_tx(&full[s], Cfg::kRawA + Cfg::kRawB);
-        if (AKM)
-          tma_load_2d(st + oRawA, &amap, tc_smem(&full[s]), k0, m0);
-        else
-          tma_load_2d(st + oRawA, &amap, tc_smem(&full[s]), m0, k0);
-        if (BKM)
-          tma_load_2d(st + oRawB, &bmap, tc_smem(&full[s]), k0, n0);
-        else
-          tma_load_2d(st + oRawB, &bmap, tc_smem(&full[s]), n0, k0);
+        load_slab<kTcM, AKM>(st + oRawA, &amap, tc_smem(&full[s]), k0, m0);
+        load_slab<BN, BKM>(st + oRawB, &bmap, tc_smem(&full[s]), k0, n0);
       }
     }
   } else if (warp == 1) {
     if (lane == 0) {  // MMA issuer
-      const uint32_t idesc2 = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)((2 * BN) >> 3) << 17) |
+      // operand majors: bit 15 (A) / 16 (B) set = MN-major
+      constexpr uint32_t kMaj = (AKM ? 0u : 1u << 15) | (BKM ? 0u : 1u << 16);
+      const uint32_t idesc2 = (1u << 4) | (2u << 7) | (2u << 10) | kMaj | ((uint32_t)((2 * BN) >> 3) << 17) |
                               ((uint32_t)(kTcM >> 4) << 24);
-      const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(BN >> 3) << 17) |
+      const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | kMaj | ((uint32_t)(BN >> 3) << 17) |
                              ((uint32_t)(kTcM >> 4) << 24);
+      // one MMA k-step (8 tf32): 32 B along a K-major row, one 8-row k group
+      // (1 KiB) of an MN-major atom
+      auto desc = [](uint32_t a, int ks, auto km) {
+        return decltype(km)::value ? umma_desc_sw128(a + ks * 32) : umma_desc_sw128_mn(a + ks * 1024);
+      };
       for (int t = 0; t < nslab; ++t) {
         const int s = t % S;
         tc_mbar_wait(&split[s], (uint32_t)((t / S) & 1));
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         const uint32_t st = sbase + s * Cfg::kStage;
-        const uint32_t ah = st + oHiA, al = st + oLoA, bh = st + oHiB, bl = st + oLoB;
+        const uint32_t ah = st + oRawA, al = st + oLoA, bh = st + oRawB;
+        using AK = std::integral_constant<bool, AKM>;
+        using BK = std::integral_constant<bool, BKM>;
 #pragma unroll
         for (int ks = 0; ks < kTcK / 8; ++ks) {
-          const uint32_t off = ks * 32;
           const int acc = (t > 0 || ks > 0) ? 1 : 0;
-          tc_mma(tmem, umma_desc_sw128(ah + off), umma_desc_sw128(bh + off), idesc2, acc);  // [B_hi | B_lo]
-          tc_mma(tmem, umma_desc_sw128(al + off), umma_desc_sw128(bh + off), idesc, 1);
+          tc_mma(tmem, desc(ah, ks, AK{}), desc(bh, ks, BK{}), idesc2, acc);  // [B_hi | B_lo]
+          tc_mma(tmem, desc(al, ks, AK{}), desc(bh, ks, BK{}), idesc, 1);
         }
         tc_commit(&empty[s]);
       }
@@ -429,8 +447,8 @@ __global__ void __launch_bounds__(kTcThreads, 1)
       const int s = t % S;
       tc_mbar_wait(&full[s], (uint32_t)((t / S) & 1));
       const uint32_t st = sbase + s * Cfg::kStage;
-      split_slab<kTcM, AKM>(st + oRawA, st + oHiA, st + oLoA, st_id);
-      split_slab<BN, BKM>(st + oRawB, st + oHiB, st + oLoB, st_id);
+      split_slab<kTcM>(st + oRawA, st + oLoA, st_id);
+      split_slab<BN>(st + oRawB, st + oLoB, st_id);
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       __syncwarp();
       if (lane == 0) tc_mbar_arrive(&split[s]);
@@ -464,7 +482,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 #pragma unroll
     for (int j = 0; j < kGrp; ++j) v[j] = __float_as_uint(__uint_as_float(v[j]) + __uint_as_float(v2[j]));
-    if (csn == 1 && !partial) {
+    if (csn == 1) {
       float *scr = reinterpret_cast<float *>(base) + warp * (32 * (kGrp + 1));
 #pragma unroll
       for (int j = 0; j < kGrp; ++j) scr[lane * (kGrp + 1) + j] = nslab > 0 ? __uint_as_float(v[j]) : 0.f;
@@ -475,8 +493,9 @@ __global__ void __launch_bounds__(kTcThreads, 1)
           const int rm = m0 + quarter * 32 + r;
           if (rm >= M || gn >= N) continue;
           const float x = scr[r * (kGrp + 1) + lane];
-          float *o = C + (int64_t)rm * csm + gn;
-          *o = accumulate ? *o + x : x;
+          // split-K partials are laid out like C ([z][m][n] here)
+          float *o = partial ? partial + ((int64_t)blockIdx.z * M + rm) * N + gn : C + (int64_t)rm * csm + gn;
+          *o = accumulate && !partial ? *o + x : x;
         }
       }
       __syncwarp();
@@ -497,7 +516,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
       if (gn >= N) continue;
       const float x = nslab > 0 ? __uint_as_float(v[j]) : 0.f;
       if (partial)
-        partial[((int64_t)blockIdx.z * M + gm) * N + gn] = x;
+        partial[((int64_t)blockIdx.z * N + gn) * M + gm] = x;  // column-major C: [z][n][m], lanes coalesced
       else
         C[(int64_t)gm * csm + (int64_t)gn * csn] = accumulate ? old[j] + x : x;
     }
@@ -522,14 +541,14 @@ static PFN_cuTensorMapEncodeTiled_v12000 tc_encode_fn() {
 // 2-D fp32 tensor map: inner extent `inner` (contiguous), `outer` rows of
 // `ld` elements, box (bi, bo)
 static bool tc_map(CUtensorMap *map, const float *p, int64_t inner, int64_t outer, int64_t ld, int bi, int bo,
-                   bool swz) {
+                   CUtensorMapSwizzle swz) {
   cuuint64_t dims[2] = {(cuuint64_t)inner, (cuuint64_t)outer};
   cuuint64_t strides[1] = {(cuuint64_t)(ld * 4)};
   cuuint32_t box[2] = {(cuuint32_t)bi, (cuuint32_t)bo};
   cuuint32_t estr[2] = {1, 1};
   return tc_encode_fn()(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float *>(p), dims, strides, box, estr,
                         CU_TENSOR_MAP_INTERLEAVE_NONE,
-                        swz ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE,
+                        swz,
                         CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
@@ -538,8 +557,9 @@ static int launch_tma_k(dim3 grid, int M, int N, int K, const float *A, int64_t 
                       float *C, int64_t csm, int64_t csn, int accumulate, float *partial, int kchunk,
                       cudaStream_t st) {
   CUtensorMap am, bm;
-  const bool ok = (AKM ? tc_map(&am, A, K, M, lda, kTcK, kTcM, true) : tc_map(&am, A, M, K, lda, kTcM, kTcK, false)) &&
-                  (BKM ? tc_map(&bm, B, K, N, ldb, kTcK, BN, true) : tc_map(&bm, B, N, K, ldb, BN, kTcK, false));
+  constexpr CUtensorMapSwizzle kK = CU_TENSOR_MAP_SWIZZLE_128B, kMN = CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B;
+  const bool ok = (AKM ? tc_map(&am, A, K, M, lda, kTcK, kTcM, kK) : tc_map(&am, A, M, K, lda, 32, kTcK, kMN)) &&
+                  (BKM ? tc_map(&bm, B, K, N, ldb, kTcK, BN, kK) : tc_map(&bm, B, N, K, ldb, 32, kTcK, kMN));
   if (!ok) return -1;
   constexpr int smem = TmaCfg<BN, AKM, BKM, SK>::kSmem;
   ensure_smem(sgemm_tma_kernel<BN, AKM, BKM, SK>, smem);
@@ -578,14 +598,20 @@ static bool tma_ok(const float *A, int64_t lda, const float *B, int64_t ldb) {
          (reinterpret_cast<uintptr_t>(A) & 15) == 0 && (reinterpret_cast<uintptr_t>(B) & 15) == 0;
 }
 
+// C (+)= the fixed-order sum of the ns split-K partials, which are laid out
+// like C (row-major [z][m][n] when csn == 1, else column-major [z][n][m]) so
+// both the partial stores and this pass are coalesced
 __global__ void tc_splits_finish(int64_t M, int64_t N, int64_t ns, const float *__restrict__ partial, float *C,
                                  int64_t csm, int64_t csn, int accumulate) {
   const int64_t MN = M * N;
+  const bool rows = csn == 1;
+  const int64_t inner = rows ? N : M;
   for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < MN; e += (int64_t)gridDim.x * blockDim.x) {
     float s = 0.f;
-    for (int64_t q = 0; q < ns; ++q) s += partial[q * MN + e];
-    const int64_t m = e / N, n = e - m * N;
-    float *c = C + m * csm + n * csn;
+#pragma unroll 4
+    for (int64_t q = 0; q < ns; ++q) s += __ldg(partial + q * MN + e);
+    const int64_t o = e / inner, i = e - o * inner;
+    float *c = rows ? C + o * csm + i : C + i * csm + o * csn;
     *c = accumulate ? *c + s : s;
   }
 }

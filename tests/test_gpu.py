@@ -349,7 +349,8 @@ def test_planned_device_payload_respects_the_budget(cid):
 
 
 @pytest.mark.parametrize("ta,tb", [(0, 0), (1, 0), (0, 1), (1, 1)])
-@pytest.mark.parametrize("M,N,K", [(64, 4096, 512), (130, 70, 33), (512, 96, 1024), (7, 300, 2000)])
+@pytest.mark.parametrize("M,N,K", [(64, 4096, 512), (130, 70, 33), (512, 96, 1024), (7, 300, 2000),
+                                   (100, 4000, 260), (1000, 36, 1024), (4096, 1024, 64)])
 def test_fp32_matmul_tensor_core_3xtf32(M, N, K, ta, tb):
     """gfb_matmul fp32 (tcgen05 3xTF32 path, split-K for skinny shapes)
     against an fp64 product, with and without accumulation, through the C ABI."""

@@ -1,1 +1,3 @@
-python bench.py --steps 10 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/r2_bench3.log 2>&1
+cd $GRAFT_REPO_ROOT
+timeout 600 python -m pytest tests/test_gpu.py -q -x -k "3xtf32 or mlp or C4" > gpurun_out/t_mm.log 2>&1; tail -3 gpurun_out/t_mm.log
+cd tools/lab && python mm_time.py 2>&1 | tee ../../gpurun_out/mm_time_mn.log

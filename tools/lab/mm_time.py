@@ -32,20 +32,25 @@ def timeit(fn):
     return ts[len(ts) // 2] * 1e3
 
 
-tot_ours = tot_cub = 0
-for M, N, K, ta, tb, lab in SHAPES:
-    A = torch.rand((K, M) if ta else (M, K), device="cuda") + 0.1
-    B = torch.rand((N, K) if tb else (K, N), device="cuda") + 0.1
-    C = torch.empty((M, N), device="cuda")
-    ws = torch.empty(max(lib.gfb_matmul_workspace_bytes(L.F32, ta, tb, M, N, K), 16), dtype=torch.uint8, device="cuda")
-    f = lambda: lib.gfb_matmul(L.F32, ta, tb, M, N, K, A.data_ptr(), A.shape[1], B.data_ptr(), B.shape[1], C.data_ptr(), N, 0, ws.data_ptr(), cs())
-    ours = timeit(f)
-    ref = (A.double().T if ta else A.double()) @ (B.double().T if tb else B.double())
-    err = ((C.double() - ref).abs() / ref.abs().clamp(min=1)).max().item()
-    opA = A.T if ta else A
-    opB = B.T if tb else B
-    cub = timeit(lambda: torch.matmul(opA, opB, out=C))
-    byts = 4 * (M * K + K * N + M * N)
-    tot_ours += ours; tot_cub += cub
-    print(f"{lab:16s} M={M:5d} N={N:5d} K={K:5d}  ours {ours:7.1f} us ({byts/ours/1e3:6.0f} GB/s, {2*M*N*K/ours/1e6:6.1f} TF/s) err {err:.1e}   cublas-fp32 {cub:7.1f} us", flush=True)
-print(f"total ours {tot_ours:.1f} us, cublas fp32 {tot_cub:.1f} us")
+def main():
+    tot_ours = tot_cub = 0
+    for M, N, K, ta, tb, lab in SHAPES:
+        A = torch.rand((K, M) if ta else (M, K), device="cuda") + 0.1
+        B = torch.rand((N, K) if tb else (K, N), device="cuda") + 0.1
+        C = torch.empty((M, N), device="cuda")
+        ws = torch.empty(max(lib.gfb_matmul_workspace_bytes(L.F32, ta, tb, M, N, K), 16), dtype=torch.uint8, device="cuda")
+        f = lambda: lib.gfb_matmul(L.F32, ta, tb, M, N, K, A.data_ptr(), A.shape[1], B.data_ptr(), B.shape[1], C.data_ptr(), N, 0, ws.data_ptr(), cs())
+        ours = timeit(f)
+        ref = (A.double().T if ta else A.double()) @ (B.double().T if tb else B.double())
+        err = ((C.double() - ref).abs() / ref.abs().clamp(min=1)).max().item()
+        opA = A.T if ta else A
+        opB = B.T if tb else B
+        cub = timeit(lambda: torch.matmul(opA, opB, out=C))
+        byts = 4 * (M * K + K * N + M * N)
+        tot_ours += ours; tot_cub += cub
+        print(f"{lab:16s} M={M:5d} N={N:5d} K={K:5d}  ours {ours:7.1f} us ({byts/ours/1e3:6.0f} GB/s, {2*M*N*K/ours/1e6:6.1f} TF/s) err {err:.1e}   cublas-fp32 {cub:7.1f} us", flush=True)
+    print(f"total ours {tot_ours:.1f} us, cublas fp32 {tot_cub:.1f} us")
+
+
+if __name__ == "__main__":
+    main()

@@ -20,6 +20,8 @@ import sys
 REPO = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 OUT = os.path.join(REPO, "gpurun_out")
 PROF = os.path.join(REPO, "profiles")
+sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+import ncu_rep  # noqa: E402
 
 
 def launches(tag):
@@ -49,46 +51,13 @@ def launches(tag):
             f.write(f"{name[:90]:90s} {n:8d} {t:12.1f} {t / n:10.2f} {t / tot:6.3f}\n")
 
 
-METRICS = [
-    ("gpu__time_duration.sum", "duration"),
-    ("dram__bytes_read.sum", "dram read"),
-    ("dram__bytes_write.sum", "dram write"),
-    ("smsp__inst_executed.sum", "warp instructions"),
-    ("sm__inst_issued.avg.pct_of_peak_sustained_active", "issue active %"),
-    ("sm__warps_active.avg.pct_of_peak_sustained_active", "warps active %"),
-    ("launch__registers_per_thread", "registers/thread"),
-    ("l1tex__data_pipe_lsu_wavefronts_mem_shared_op_ld.sum", "smem load wavefronts"),
-    ("l1tex__data_bank_conflicts_pipe_lsu_mem_shared_op_ld.sum", "smem load bank conflicts"),
-    ("dram__throughput.avg.pct_of_peak_sustained_elapsed", "dram throughput %"),
-]
-
-
 def ncu_full(tag):
     rep = os.path.join(OUT, "prof_top.ncu-rep")
     if not os.path.exists(rep):
         return
-    raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
-    rows = list(csv.reader(io.StringIO(raw)))
-    hdr, units = rows[0], rows[1]
-    idx = {h: i for i, h in enumerate(hdr)}
+    lines, traffic = ncu_rep.summarize(rep)
     out = ["ncu --set full --clock-control none --import-source on -k regex:star_pair --launch-skip 1 -c 4 "
-           "python tools/prof_stencil.py heat_3d 512 4", ""]
-    traffic = []
-    for n, r in enumerate(rows[2:]):
-        out.append(f"launch {n}: {r[idx['Kernel Name']]}  grid {r[idx.get('launch__grid_size', 0)]}")
-        for key, label in METRICS:
-            if key in idx:
-                out.append(f"  {label:28s} {r[idx[key]]:>16s} {units[idx[key]]}")
-        st = {h: float(r[i]) for h, i in idx.items()
-              if h.startswith("smsp__pcsamp_warps_issue_stalled") and not h.endswith("not_issued") and r[i]}
-        tot = sum(st.values()) or 1.0
-        out.append("  stall samples: " + ", ".join(
-            f"{k.replace('smsp__pcsamp_warps_issue_stalled_', '')} {v / tot * 100:.0f}%"
-            for k, v in sorted(st.items(), key=lambda kv: -kv[1])[:8]))
-        rd = float(r[idx["dram__bytes_read.sum"]]) * (1e9 if units[idx["dram__bytes_read.sum"]] == "Gbyte" else 1e6)
-        wr = float(r[idx["dram__bytes_write.sum"]]) * (1e9 if units[idx["dram__bytes_write.sum"]] == "Gbyte" else 1e6)
-        traffic.append(rd + wr)
-        out.append("")
+           "python tools/prof_stencil.py heat_3d 512 4", ""] + lines
     with open(os.path.join(PROF, f"{tag}_ncu_star_pair.txt"), "w") as f:
         f.write("\n".join(out))
     with open(os.path.join(PROF, "ncu_traffic.json"), "w") as f:
