@@ -356,9 +356,10 @@ __device__ __forceinline__ uint64_t umma_desc_sw128_mn(uint32_t saddr) {
 }
 
 template <int BN, bool AKM, bool BKM, bool SK>
-__global__ void __launch_bounds__(kTcThreads, 1)
-    sgemm_tma_kernel(const __grid_constant__ CUtensorMap amap, const __grid_constant__ CUtensorMap bmap, int M,
-                     int N, int K, float *C, int64_t csm, int64_t csn, int accumulate, float *partial, int kchunk) {
+__global__ void __launch_bounds__(kTcThreads, 2)  // <= 128 registers: two short-k CTAs per SM
+    sgemm_tma_kernel(const __grid_constant__ CUtensorMap amap, const __grid_constant__ CUtensorMap bmap,
+                     const __grid_constant__ CUtensorMap cmap, int M, int N, int K, float *C, int64_t csm,
+                     int64_t csn, int accumulate, float *partial, int kchunk, int cmode) {
   using Cfg = TmaCfg<BN, AKM, BKM, SK>;
   constexpr int S = Cfg::kStages;
   extern __shared__ __align__(1024) unsigned char tm_raw[];
@@ -458,8 +459,9 @@ __global__ void __launch_bounds__(kTcThreads, 1)
   if (nslab > 0) tc_mbar_wait(done, 0);
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
 
-  // epilogue (as sgemm_tc_kernel): warp w reads TMEM lane quarter w % 4 and
-  // column half w / 4; the ring is idle now and serves as transpose scratch
+  // epilogue: warp w reads TMEM lane quarter w % 4 and column half w / 4;
+  // the ring is idle now and stages the TMA stores (or serves as transpose
+  // scratch for the split-K partials)
   const int quarter = warp & 3, half = warp >> 2;
   const int row = quarter * 32 + lane, gm = m0 + row;
   constexpr int kHalf = BN / 2 < 8 ? 8 : BN / 2;
@@ -482,6 +484,48 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 #pragma unroll
     for (int j = 0; j < kGrp; ++j) v[j] = __float_as_uint(__uint_as_float(v[j]) + __uint_as_float(v2[j]));
+    if constexpr (kGrp == 32) {
+      if (cmode) {
+        // stage the warp's 32 x 32 block (4 KiB slot per warp and column
+        // group) and write it with one TMA store (a TMA add-reduction when
+        // accumulating); the tensor map clips rows / columns past M / N
+        const uint32_t stg = sbase + (uint32_t)(warp * (kHalf / 32) + (c0 - half * kHalf) / 32) * 4096u;
+        if (nslab == 0) {
+#pragma unroll
+          for (int j = 0; j < kGrp; ++j) v[j] = 0u;
+        }
+        if (cmode == 1) {  // row-major C: row = lane, SWIZZLE_128B rows of 32 columns
+#pragma unroll
+          for (int c = 0; c < 8; ++c)
+            sts128(stg + lane * 128 + ((c ^ (lane & 7)) << 4),
+                   make_float4(__uint_as_float(v[4 * c]), __uint_as_float(v[4 * c + 1]),
+                               __uint_as_float(v[4 * c + 2]), __uint_as_float(v[4 * c + 3])));
+        } else {  // column-major C: row = column j, lanes along m
+#pragma unroll
+          for (int j = 0; j < kGrp; ++j)
+            asm volatile("st.shared.f32 [%0], %1;" ::"r"(stg + j * 128 + lane * 4), "f"(__uint_as_float(v[j]))
+                         : "memory");
+        }
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        __syncwarp();
+        if (lane == 0) {
+          const int x0 = cmode == 1 ? n0 + c0 : m0 + quarter * 32, x1 = cmode == 1 ? m0 + quarter * 32 : n0 + c0;
+          if (accumulate)
+            asm volatile(
+                "cp.reduce.async.bulk.tensor.2d.global.shared::cta.add.tile.bulk_group [%0, {%1, %2}], [%3];" ::"l"(
+                    reinterpret_cast<uint64_t>(&cmap)),
+                "r"(x0), "r"(x1), "r"(stg)
+                : "memory");
+          else
+            asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];" ::"l"(
+                             reinterpret_cast<uint64_t>(&cmap)),
+                         "r"(x0), "r"(x1), "r"(stg)
+                         : "memory");
+          asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+        }
+        continue;
+      }
+    }
     if (csn == 1) {
       float *scr = reinterpret_cast<float *>(base) + warp * (32 * (kGrp + 1));
 #pragma unroll
@@ -521,6 +565,8 @@ __global__ void __launch_bounds__(kTcThreads, 1)
         C[(int64_t)gm * csm + (int64_t)gn * csn] = accumulate ? old[j] + x : x;
     }
   }
+  // the staged blocks must stay in shared memory until the stores read them
+  if (cmode && lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
   if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kCols));
@@ -561,10 +607,23 @@ static int launch_tma_k(dim3 grid, int M, int N, int K, const float *A, int64_t 
   const bool ok = (AKM ? tc_map(&am, A, K, M, lda, kTcK, kTcM, kK) : tc_map(&am, A, M, K, lda, 32, kTcK, kMN)) &&
                   (BKM ? tc_map(&bm, B, K, N, ldb, kTcK, BN, kK) : tc_map(&bm, B, N, K, ldb, 32, kTcK, kMN));
   if (!ok) return -1;
+  // TMA-store epilogue: whole C (not split-K partials), 16-byte aligned rows,
+  // 32-column groups (BN >= 64)
+  CUtensorMap cm{};
+  int cmode = 0;
+  static const bool no_cstore = getenv("GFB_TC_NO_TMA_STORE") != nullptr;
+  if (!no_cstore && BN >= 64 && !partial && (reinterpret_cast<uintptr_t>(C) & 15) == 0) {
+    if (csn == 1 && csm % 4 == 0 && tc_map(&cm, C, N, M, csm, 32, 32, CU_TENSOR_MAP_SWIZZLE_128B))
+      cmode = 1;
+    else if (csm == 1 && csn % 4 == 0 && tc_map(&cm, C, M, N, csn, 32, 32, CU_TENSOR_MAP_SWIZZLE_NONE))
+      cmode = 2;
+  }
   constexpr int smem = TmaCfg<BN, AKM, BKM, SK>::kSmem;
+  static_assert(BN < 64 || TmaCfg<BN, AKM, BKM, SK>::kStages * TmaCfg<BN, AKM, BKM, SK>::kStage >= 8 * (BN / 64) * 4096,
+                "epilogue staging exceeds the ring");
   ensure_smem(sgemm_tma_kernel<BN, AKM, BKM, SK>, smem);
-  sgemm_tma_kernel<BN, AKM, BKM, SK><<<grid, kTcThreads, smem, st>>>(am, bm, M, N, K, C, csm, csn, accumulate, partial,
-                                                                 kchunk);
+  sgemm_tma_kernel<BN, AKM, BKM, SK><<<grid, kTcThreads, smem, st>>>(am, bm, cm, M, N, K, C, csm, csn, accumulate,
+                                                                     partial, kchunk, cmode);
   return 0;
 }
 

@@ -443,6 +443,8 @@ class Executable:
         # host's per-launch latency); ~40 us of host time per launch
         torch.cuda._sleep(int(min(len(self.ops) * 40e-6, 2.0) * 2e9))
         for op in self.ops:
+            if getattr(op, "elided", False):
+                continue  # an alias, not a launch
             a = torch.cuda.Event(enable_timing=True)
             b = torch.cuda.Event(enable_timing=True)
             a.record(stream)

@@ -1,3 +1,5 @@
-cd $GRAFT_REPO_ROOT
-timeout 600 python -m pytest tests/test_gpu.py -q -x -k "3xtf32 or mlp or C4" > gpurun_out/t_mm.log 2>&1; tail -3 gpurun_out/t_mm.log
-cd tools/lab && python mm_time.py 2>&1 | tee ../../gpurun_out/mm_time_mn.log
+cd $GRAFT_REPO_ROOT/tools/lab
+for lib in default sk2; do for bn in 128 64; do
+  if [ $lib = default ]; then unset GFB_LIBRARY; else export GFB_LIBRARY=$GRAFT_REPO_ROOT/build/var/$lib.so; fi
+  echo "== $lib bn=$bn"; GFB_TC_SK_BN=$bn python mm_time.py 2>&1 | grep -E "K=   64|total" | cut -c1-60
+done; done
