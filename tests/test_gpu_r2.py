@@ -197,6 +197,27 @@ def test_branch_guarding_a_domain_error_takes_the_other_arm():
         assert rel_err(eng.gradient(inputs).value, value) <= 1e-12, tag
 
 
+@pytest.mark.parametrize("cid", sorted(R2IDX["fd"]))
+def test_finite_difference_oracle_across_branch_boundaries(cid):
+    """The GPU FD oracle rides the batch axis like the reference's
+    (verification.py:95-120): where the probe batch diverges at a branch it
+    probes pairwise, and a pair straddling the boundary comes back NaN at
+    the same elements as the reference's."""
+    from paper_2509_02197_b200 import finite_difference_gradient
+
+    meta = R2IDX["fd"][cid]
+    prog, _ = _bundle(meta["program"], R2)
+    g = np.load(os.path.join(R2, cid + ".npz"))
+    inputs = {k[3:]: g[k] for k in g.files if k.startswith("in:")}
+    fd = finite_difference_gradient(prog, inputs, meta["params"])
+    for k in prog.independents:
+        want = g["fd:" + k]
+        got = np.asarray(fd[k])
+        assert np.array_equal(np.isnan(got), np.isnan(want)), (cid, got, want)
+        ok = ~np.isnan(want)
+        assert np.allclose(got[ok], want[ok], rtol=1e-6, atol=1e-6), (cid, got, want)
+
+
 # -- the reference CLI's plan artifacts ------------------------------------------------
 
 

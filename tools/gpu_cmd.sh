@@ -1,5 +1,2 @@
-cd $GRAFT_REPO_ROOT/tools/lab
-for lib in default sk2; do for bn in 128 64; do
-  if [ $lib = default ]; then unset GFB_LIBRARY; else export GFB_LIBRARY=$GRAFT_REPO_ROOT/build/var/$lib.so; fi
-  echo "== $lib bn=$bn"; GFB_TC_SK_BN=$bn python mm_time.py 2>&1 | grep -E "K=   64|total" | cut -c1-60
-done; done
+cd $GRAFT_REPO_ROOT
+timeout 900 python -m pytest tests/test_gpu_r2.py tests/test_gpu.py -q -k "finite_difference or batch" 2>&1 | grep -E "Error|assert|passed|failed" | head -30

@@ -318,11 +318,39 @@ def save_batched():
     return cases
 
 
+def save_fd():
+    """The reference finite-difference oracle (verification.py:53-120) where
+    its probe batch diverges at a branch: pairwise fallback, NaN for probe
+    pairs that straddle the branch boundary."""
+    from gradflow.verification import finite_difference_gradient
+
+    cases = {}
+    prog, _ = loop_branch()
+    for t in (1.0, 1.5, 2.0, -1.0):
+        fd = finite_difference_gradient(prog, {"t": np.array(t)}, {})
+        tag = f"loop_branch__fd_t{t:+g}".replace("+", "p").replace("-", "m").replace(".", "_")
+        np.savez(os.path.join(OUT, tag + ".npz"), **{"in:t": np.array(t)}, **{"fd:t": np.asarray(fd["t"])})
+        cases[tag] = {"program": "loop_branch", "params": {}}
+        print("fd", tag, fd["t"])
+    prog, _ = guarded_log()
+    x = np.random.default_rng(6).uniform(0.4, 1.6, 9)
+    for tag, x0 in (("zero", 0.0), ("pos", x[0])):
+        xi = x.copy()
+        xi[0] = x0
+        fd = finite_difference_gradient(prog, {"x": xi}, {"N": 9})
+        cid = f"guarded_log__fd_{tag}"
+        np.savez(os.path.join(OUT, cid + ".npz"), **{"in:x": xi}, **{"fd:x": np.asarray(fd["x"])})
+        cases[cid] = {"program": "guarded_log", "params": {"N": 9}}
+        print("fd", cid, fd["x"])
+    return cases
+
+
 def main():
     batched = save_batched()
     save_timelines()
     save_config_plans()
-    index = {"control_flow": save_control_flow(), "plans_cli": save_cli_plans(), "batched": batched}
+    index = {"control_flow": save_control_flow(), "plans_cli": save_cli_plans(), "batched": batched,
+             "fd": save_fd()}
     with open(os.path.join(OUT, "index.json"), "w") as f:
         json.dump(index, f, indent=2)
     save_errors()
