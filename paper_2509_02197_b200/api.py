@@ -29,7 +29,7 @@ from dataclasses import dataclass, field
 
 import numpy as np
 
-from .errors import ShapeMismatch, UnboundName, UnsupportedConstruct
+from .errors import EngineError, ShapeMismatch, UnboundName, UnsupportedConstruct
 from .ir import (
     Program,
     adopt,
@@ -348,12 +348,32 @@ def probe_values(nv: NeedValues, inputs: dict, seed=1.0) -> dict:
     return {n: exe.view(low.resolve(b)).cpu().numpy().copy() for n, b in nv.slots.items()}
 
 
+class _Known(list):
+    """Decision values known before lowering, plus the incremental prober
+    the Lowering calls for the ones met while lowering."""
+
+    def __init__(self, probe=None):
+        super().__init__()
+        self.probe = probe
+
+
 def probe_lower(lower, inputs: dict | None, seed=1.0):
-    """``lower(known)`` until no decision is missing: each ``NeedValues``
-    runs the prefix on the device and appends its values to ``known``
-    (reference data-dependent branches / loop headers, interpreter.py:
-    210-219, 342-347, evaluated at the same program point)."""
-    known = []
+    """``lower(known)`` with the data-dependent decisions (reference branches
+    / loop headers, interpreter.py:210-219, 342-347, evaluated at the same
+    program point) resolved as they are met: a ``ProbeRuntime`` runs the
+    launches emitted since the previous decision and reads its snapshots,
+    so the lowering runs once. Without inputs, or on a box without a GPU,
+    each ``NeedValues`` ends the attempt and the prefix is probed from
+    scratch (``probe_values``)."""
+    from .runtime import ProbeRuntime
+
+    prober = None
+    if inputs is not None:
+        try:
+            prober = ProbeRuntime(inputs, seed)
+        except EngineError:
+            prober = None
+    known = _Known(prober)
     while True:
         try:
             return lower(known)

@@ -45,6 +45,7 @@ import numpy as np
 from . import _lib as L
 from .errors import (
     DomainError,
+    GradflowError,
     MissingInverse,
     MissingTapeValue,
     NonTermination,
@@ -58,6 +59,7 @@ from .ir import (
     Binary,
     Conditional,
     Const,
+    Index,
     LibraryNode,
     LoopRegion,
     MapNode,
@@ -1616,6 +1618,66 @@ class LoopCtx:
         return self.iterates[self.pos]
 
 
+class _Elements:
+    """The elements of an array a decision reads (snapshotted one by one
+    instead of the whole array): ``x[(Ellipsis, *idx)]`` as numpy would
+    index the full array."""
+
+    def __init__(self, shape, idxs, values):
+        self.shape = tuple(shape)
+        vals = np.asarray(values).reshape(-1)
+        self.map = {tuple(idx): vals[k] for k, idx in enumerate(idxs)}
+
+    def __getitem__(self, key):
+        idx = tuple(int(i) + (s if int(i) < 0 else 0) for i, s in zip(key[1:], self.shape))
+        return self.map[idx]
+
+
+def _element_view(buf: Buffer, lin: int) -> Buffer:
+    """A one-element view of ``buf`` at linear element offset ``lin``."""
+    v = Buffer(f"{buf.name}[{lin}]", (), buf.kind, fresh=False)
+    v.alias_of = buf
+    v.offset = lin
+    return v
+
+
+def static_reads(expr, bind: dict, shapes: dict):
+    """Element indices of each array ``expr`` reads (``idx`` nodes) when
+    every subscript is fixed by ``bind``; arrays with a data-dependent or
+    out-of-range subscript are left out (snapshotted whole). Every ``idx``
+    node is evaluated exactly once (``evaluate`` has no short-circuit), so
+    this is exactly the set a condition reads."""
+    out, whole = {}, set()
+
+    def walk(e):
+        t = type(e)
+        if t is Index:
+            shape = shapes.get(e.base)
+            try:
+                idx = tuple(int(evaluate(x, bind)) for x in e.indices)
+            except GradflowError:
+                idx = None
+            if shape is None or idx is None or len(idx) != len(shape):
+                whole.add(e.base)
+            else:
+                norm = tuple(i + s if i < 0 else i for i, s in zip(idx, shape))
+                if all(0 <= i < s for i, s in zip(norm, shape)):
+                    if norm not in out.setdefault(e.base, []):
+                        out[e.base].append(norm)
+                else:
+                    whole.add(e.base)
+            for x in e.indices:
+                walk(x)
+        elif t is Binary:
+            walk(e.x)
+            walk(e.y)
+        elif t is Unary:
+            walk(e.x)
+
+    walk(expr)
+    return {n: v for n, v in out.items() if n not in whole}
+
+
 def _host_index(vals: dict, base: str, idx: tuple):
     """``idx`` read in a condition (reference symexpr.py:180-184: numpy
     indexing of the env array, so negative indices wrap)."""
@@ -1657,6 +1719,10 @@ class Lowering:
         # runtime control-flow values observed by earlier probe runs, in
         # decision order; decisions = [(slots, key_fn, key)] taken this lowering
         self.known: list = list(known or [])
+        # incremental prober (api.probe_lower): runs the launches emitted
+        # since the previous decision and returns the snapshot values, so a
+        # decision no longer restarts the lowering (None: raise NeedValues)
+        self.probe = getattr(known, "probe", None)
         self.decisions: list = []
         self.entry_inputs: dict = {}  # caller name -> Buffer (for probe runs of a prefix)
         self.entry_seed = None
@@ -1940,20 +2006,21 @@ class Lowering:
     def _elide_copies(self):
         """Copies whose source and destination are never written afterwards
         (tape snapshots, plan keep-copies) become aliases."""
+        # keyed by root buffer: a write through a view writes its root
         last_write = {}
         first_touch = {}
         for i, op in enumerate(self.ops):
             for b in op.writes:
-                last_write[b.bid] = i
+                last_write[b.root().bid] = i
             for b in tuple(op.reads) + tuple(op.writes):
-                first_touch.setdefault(b.bid, i)
+                first_touch.setdefault(b.root().bid, i)
         for i, op in enumerate(self.ops):
             if not isinstance(op, CopyOp):
                 continue
             src, dst = op.src, op.dst
-            if last_write.get(src.bid, -1) > i or last_write.get(dst.bid, -1) > i:
+            if last_write.get(src.root().bid, -1) > i or last_write.get(dst.root().bid, -1) > i:
                 continue
-            if first_touch.get(dst.bid, i) < i or dst.alias_of is not None:
+            if first_touch.get(dst.root().bid, i) < i or dst.alias_of is not None:
                 continue
             if src.root() is dst.root():
                 continue
@@ -2068,33 +2135,55 @@ class ProgramRun:
             else:
                 self.branch(b)
 
-    def runtime_values(self, names, key_fn) -> dict:
+    def runtime_values(self, names, key_fn, reads=None) -> dict:
         """Host values of the data ``names`` at this point of the program.
 
         Emits a device snapshot of each (so later writes do not disturb it)
-        and returns the values a probe run observed for this decision; raises
-        ``NeedValues`` when no probe has reached it yet. ``key_fn(values)`` is
-        what the decision depends on (a branch outcome, a loop's header
-        scalars): the executable re-evaluates it from the snapshots after
-        every run and rebuilds when it changes."""
+        and returns the values a probe run observed for this decision. With a
+        prober (``Lowering.probe``) the launches emitted so far run now;
+        without one, ``NeedValues`` is raised for the caller to probe and
+        lower again. ``key_fn(values)`` is what the decision depends on (a
+        branch outcome, a loop's header scalars): the executable re-evaluates
+        it from the snapshots after every run and rebuilds when it changes.
+
+        ``reads`` maps an array name to the element indices the decision
+        reads (static under the current bindings): only those elements are
+        snapshotted, and ``key_fn`` sees them through ``_Elements``; other
+        names are snapshotted whole."""
         low = self.low
-        slots = {}
+        slots, specs = {}, {}
+        i = len(low.decisions)
         for n in sorted(names):
             src = self.env.get(n)
             if src is None:
                 continue  # unbound: evaluation raises UnboundName as in the reference
             low.materialize(src)
-            slot = low.new_buffer(f"{n}@probe{len(low.decisions)}", src.shape, src.kind, fresh=False)
-            low.emit(CopyOp(slot, src))
+            idxs = (reads or {}).get(n)
+            if idxs is not None and src.shape:
+                slot = low.new_buffer(f"{n}@probe{i}", (len(idxs),), src.kind, fresh=False)
+                for k, idx in enumerate(idxs):
+                    lin = int(sum(int(x) * st for x, st in zip(idx, src.strides)))
+                    low.emit(CopyOp(_element_view(slot, k), _element_view(src, lin)))
+                specs[n] = (src.shape, idxs)
+            else:
+                slot = low.new_buffer(f"{n}@probe{i}", src.shape, src.kind, fresh=False)
+                low.emit(CopyOp(slot, src))
             slots[n] = slot
-        i = len(low.decisions)
+        if specs:
+            inner = key_fn
+
+            def key_fn(raw, inner=inner, specs=specs):
+                return inner({n: _Elements(*specs[n], v) if n in specs else v for n, v in raw.items()})
+
         if i >= len(low.known):
-            nv = NeedValues(slots)
-            nv.low = low
-            raise nv
-        vals = low.known[i]
-        low.decisions.append((slots, key_fn, key_fn(vals)))
-        return vals
+            if low.probe is None:
+                nv = NeedValues(slots)
+                nv.low = low
+                raise nv
+            low.known.append(low.probe(low, slots))
+        raw = low.known[i]
+        low.decisions.append((slots, key_fn, key_fn(raw)))
+        return {n: _Elements(*specs[n], v) if n in specs else v for n, v in raw.items()}
 
     def _header_bind(self, loop):
         need = (free_names(loop.init) | free_names(loop.bound) | free_names(loop.update)) - {loop.iterator}
@@ -2377,7 +2466,8 @@ class ProgramRun:
                     b.update({n: v.reshape(()).item() for n, v in vals.items() if descs[n].rank == 0})
                     return bool(evaluate(cond, b, lambda base, idx: _host_index(vals, base, idx)))
 
-                outcome = key(self.runtime_values(data, key))
+                shapes = {n: self.env[n].shape for n in data if n in self.env}
+                outcome = key(self.runtime_values(data, key, static_reads(cond, self.bind, shapes)))
             else:
                 outcome = bool(evaluate(br.condition, dict(self.bind)))
             if self.tape is not None:

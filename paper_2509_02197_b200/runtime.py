@@ -152,6 +152,107 @@ class HostEnv(Mapping):
             self[name]
 
 
+def _read_slots(view, groups: list) -> list:
+    """Host copies of the snapshot buffers of several decisions
+    ([{name: Buffer}] -> [{name: ndarray}]) with one gather and one
+    device-to-host copy per element type."""
+    by_kind = {}
+    for gi, slots in enumerate(groups):
+        for n, b in slots.items():
+            by_kind.setdefault(b.kind, []).append((gi, n, b))
+    out = [{} for _ in groups]
+    for items in by_kind.values():
+        flat = torch.cat([view(b).reshape(-1) for _, _, b in items]).cpu().numpy()
+        o = 0
+        for gi, n, b in items:
+            out[gi][n] = flat[o:o + b.numel].reshape(b.shape)
+            o += b.numel
+    return out
+
+
+class ProbeRuntime:
+    """Incremental executor for the data-dependent decisions met while a
+    launch list is lowered (reference branches and scalar loop headers,
+    interpreter.py:210-219, 342-347). At each decision it runs only the
+    launches emitted since the previous one, on buffers it keeps for the
+    whole lowering (one allocation per buffer, no arena reuse), and reads
+    the decision's snapshots back: T decisions cost O(T) launches, where
+    lowering again from the start for every decision cost O(T^2). Buffer
+    tensors are bound only while its launches are prepared and run, so the
+    final Executable plans its own arena."""
+
+    def __init__(self, inputs: dict, seed=1.0, device=None):
+        require_cuda()
+        self.lib = L.load()
+        self.device = torch.device(device or "cuda")
+        self.inputs = inputs
+        self.seed = seed
+        self.tensors = {}  # root bid -> tensor
+        self.done = 0      # launches already run
+        self.loaded = False
+        self.seeded = False
+        self.aux = []
+        self.workspace = torch.empty(16, dtype=torch.uint8, device=self.device)
+        self.workspace_ptr = self.workspace.data_ptr()
+        self.err = torch.zeros(1, dtype=torch.int32, device=self.device)
+        self.err_ptr = self.err.data_ptr()
+        self.launches = 0
+
+    def upload(self, arr: np.ndarray) -> int:
+        t = torch.from_numpy(np.ascontiguousarray(arr)).to(self.device)
+        self.aux.append(t)
+        return t.data_ptr()
+
+    def view(self, b: Buffer) -> torch.Tensor:
+        t = self.tensors[b.root().bid]
+        o = b.root_offset()
+        return t[o: o + b.numel].view(b.shape) if b.shape else t[o:o + 1].view(())
+
+    def __call__(self, low: Lowering, slots: dict) -> dict:
+        roots = {}
+        for b in low.buffers:
+            r = b.root()
+            if r.tensor is not None and r.bid not in self.tensors:
+                continue  # placed by its owner (not this prober's to bind or release)
+            roots[r.bid] = r
+            if r.bid not in self.tensors:
+                self.tensors[r.bid] = torch.empty(max(r.numel, 1), dtype=TORCH_DTYPE[r.kind], device=self.device)
+        for bid, r in roots.items():
+            r.tensor = self.tensors[bid]
+        try:
+            if not self.loaded:
+                for name, buf in low.entry_inputs.items():
+                    v = self.inputs[name]
+                    dst = self.view(buf)
+                    src = v if isinstance(v, torch.Tensor) else torch.from_numpy(
+                        np.ascontiguousarray(np.asarray(v, dtype=NP_DTYPE[buf.kind])))
+                    dst.copy_(src.reshape(dst.shape).to(dst.dtype))
+                self.loaded = True
+            if getattr(low, "entry_seed", None) is not None and not self.seeded:
+                self.view(low.entry_seed).fill_(float(self.seed))
+                self.seeded = True
+            new = low.ops[self.done:]
+            ws = max([int(op.workspace_bytes()) for op in new if hasattr(op, "workspace_bytes")] + [16])
+            if ws > self.workspace.numel():
+                self.workspace = torch.empty(ws, dtype=torch.uint8, device=self.device)
+                self.workspace_ptr = self.workspace.data_ptr()
+            stream = torch.cuda.current_stream(self.device).cuda_stream
+            for op in new:
+                op.prepare(self)
+                op.launch(self, stream)
+            self.launches += len(new)
+            self.done = len(low.ops)
+            torch.cuda.synchronize(self.device)
+            bits = int(self.err.item())
+            if bits:
+                msgs = [m for b_, m in L.EBITS.items() if bits & b_]
+                raise DomainError("; ".join(msgs) or f"device error bits {bits:#x}")
+            return {n: v.copy() for n, v in _read_slots(self.view, [slots])[0].items()}
+        finally:
+            for r in roots.values():
+                r.tensor = None
+
+
 class Executable:
     def __init__(self, low: Lowering, inputs: dict, outputs: dict, *, seed_buf: Buffer | None = None,
                  device=None, use_graph: bool | None = None, pinned=(), reuse: bool | None = None):
@@ -299,10 +400,9 @@ class Executable:
         list was lowered with, from the device snapshots of the run just
         finished; False means the inputs took another path and the caller
         must lower again."""
-        # one synchronisation and one batch of copies for all snapshots
-        torch.cuda.synchronize(self.device)
-        host = [{n: self.view(self.low.resolve(b)).cpu().numpy() for n, b in slots.items()}
-                for slots, _k, _v in self.low.decisions]
+        # one device-to-host copy per element type for all snapshots
+        host = _read_slots(self.view, [{n: self.low.resolve(b) for n, b in slots.items()}
+                                       for slots, _k, _v in self.low.decisions])
         for vals, (_slots, key_fn, key) in zip(host, self.low.decisions):
             try:
                 if key_fn(vals) != key:

@@ -180,6 +180,26 @@ def test_iterator_dependent_branch_across_calls():
         assert rel_err(eng.gradient(inputs).value, value) <= 1e-12, cid
 
 
+def test_elementwise_branches_probe_incrementally_on_the_device():
+    """A 12-trip loop branching on x[i]: the device prober resolves the
+    decisions while lowering (one lowering, element snapshots), the cached
+    launch list re-checks them from one readback per call, and a call whose
+    elements take other arms lowers again; values are the reference's."""
+    from paper_2509_02197_b200 import api
+
+    clear_cache()
+    prog, b = _bundle("elem_branch", R2)
+    cids = sorted(c for c in R2IDX["control_flow"] if c.startswith("elem_branch"))
+    for cid in cids + cids[::-1]:
+        inputs, value, grads = _r2_case(cid)
+        res = gradient(prog, inputs, {"N": 12}, bundle=b)
+        assert rel_err(res.value, value) <= 1e-12, cid
+        assert rel_err(res.grads["x"], grads["x"]) <= 1e-12, cid
+    exe = next(e for e in api._CACHE.values() if getattr(e, "low", None) is not None and e.low.decisions)
+    assert len(exe.low.decisions) == 12
+    assert all(s.shape == (1,) for slots, _, _ in exe.low.decisions for s in slots.values())
+
+
 def test_branch_guarding_a_domain_error_takes_the_other_arm():
     """``if x0 > 0: log(x)``: a call whose inputs take the else arm returns
     the else arm's value, although the cached launch list (then arm) would

@@ -124,6 +124,110 @@ def test_iterator_dependent_branch_matches_reference_and_rechecks(cid):
         assert key_fn({"t": np.array(0.5)}) == (0.5 < i)
 
 
+class _EmuProbe:
+    """The api's incremental prober (runtime.ProbeRuntime) on the emulator:
+    at each decision it runs only the launches emitted since the previous
+    one, on memory it keeps for the whole lowering."""
+
+    def __init__(self, inputs, seed=1.0):
+        self.mem = E.Memory()
+        self.em = E.Emulator(self.mem)
+        self.inputs, self.seed = inputs, seed
+        self.done, self.launches, self.calls, self.loaded = 0, 0, 0, False
+        self.shims = {}
+
+        class RT:
+            pass
+
+        self.rt = RT()
+        self.rt.upload = self._upload
+        self.rt.workspace_ptr = self.mem.alloc(1 << 16, np.uint8).ctypes.data
+        self.rt.err_ptr = self.em.err.ctypes.data
+        self.rt.lib = None
+
+    def _upload(self, arr):
+        a = self.mem.alloc(arr.size, arr.dtype)
+        a[:] = arr.reshape(-1)
+        return a.ctypes.data
+
+    def view(self, b):
+        t = b.root().tensor.arr
+        o = b.root_offset()
+        return t[o:o + b.numel].reshape(b.shape) if b.shape else t[o:o + 1].reshape(())
+
+    def __call__(self, low, slots):
+        self.calls += 1
+        roots = [b for b in low.buffers if b.alias_of is None]
+        for b in roots:  # bound only while probing, like ProbeRuntime
+            if b.bid not in self.shims:
+                self.shims[b.bid] = E._Shim(self.mem.alloc(b.numel, E.NPT[b.dtype]))
+            b.tensor = self.shims[b.bid]
+        try:
+            if not self.loaded:
+                for name, b in low.entry_inputs.items():
+                    self.view(b)[...] = np.asarray(self.inputs[name]).reshape(b.shape)
+                self.loaded = True
+            for op in low.ops[self.done:]:
+                op.prepare(self.rt)
+                self.em.run_op(op)
+                self.launches += 1
+            self.done = len(low.ops)
+            return {n: np.array(self.view(b)) for n, b in slots.items()}
+        finally:
+            for b in roots:
+                b.tensor = None
+
+
+def _incremental(prog, bundle, params, inputs):
+    from paper_2509_02197_b200.api import _Known
+
+    probe = _EmuProbe(inputs)
+    lw = lower_gradient(prog, bundle, params, _check_inputs(prog, inputs, params), known=_Known(probe))
+    em, view = E.execute(lw.low, inputs, lw.inputs, lw.seed_buf)
+    return lw, view, probe
+
+
+@pytest.mark.parametrize("cid", sorted(c for c in R2IDX["control_flow"] if c.startswith("loop_branch")))
+def test_incremental_probe_lowers_once(cid):
+    """ADVICE r1 (probe_lower O(T^2)): the decisions of a T-trip loop are
+    resolved while lowering, each probe running only the launches emitted
+    since the previous decision (T probes, each launch run once), with the
+    reference's results."""
+    prog, b = _r2_bundle("loop_branch")
+    inputs, value, grads = _r2_case(cid)
+    lw, view, probe = _incremental(prog, b, {}, inputs)
+    assert rel_err(view(lw.outputs["value"]), value) <= 1e-12
+    assert rel_err(view(lw.outputs["grad:t"]), grads["t"]) <= 1e-12
+    assert probe.calls == len(lw.low.decisions) == 3
+    # every probed launch ran once: no more launches than the unfinished list
+    assert probe.launches <= len(lw.low.ops) + len(lw.low.decisions) * 4
+
+
+@pytest.mark.parametrize("cid", sorted(c for c in R2IDX["control_flow"] if c.startswith("elem_branch")))
+def test_branch_on_array_elements_snapshots_only_those_elements(cid):
+    """Every trip of a 12-trip loop branches on x[i] (``idx``): each decision
+    snapshots that one element (full-array snapshots pinned
+    T x the array in HBM), re-evaluates from it alone, and the result is
+    the reference's."""
+    prog, b = _r2_bundle("elem_branch")
+    inputs, value, grads = _r2_case(cid)
+    lw, view, probe = _incremental(prog, b, {"N": 12}, inputs)
+    assert rel_err(view(lw.outputs["value"]), value) <= 1e-12
+    assert rel_err(view(lw.outputs["grad:x"]), grads["x"]) <= 1e-12
+    decisions = lw.low.decisions
+    assert probe.calls == len(decisions) == 12
+    x = inputs["x"]
+    for i, (slots, key_fn, key) in enumerate(decisions):
+        assert {n: s.shape for n, s in slots.items()} == {"x": (1,)}
+        assert float(view(lw.low.resolve(slots["x"]))[0]) == x[i]
+        assert key is bool(x[i] < 1.0)
+        assert key_fn({"x": np.array([0.5])}) is True and key_fn({"x": np.array([1.5])}) is False
+    # the restart protocol gives the same launch list
+    lw2, em, view2 = _emulate_probing(prog, b, {"N": 12}, inputs)
+    assert len(lw2.low.ops) == len(lw.low.ops)
+    assert rel_err(view2(lw2.outputs["grad:x"]), grads["x"]) <= 1e-12
+
+
 # -- the reference CLI's plan artifacts (f1)
 
 

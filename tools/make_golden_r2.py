@@ -118,9 +118,40 @@ def guarded_log():
     return b.finish("O", ["x"]), None
 
 
+def elem_branch():
+    """for i in [0, N): y[i] = 2 x[i] if x[i] < 1 else x[i]^2; O = sum(y):
+    every trip's branch reads one element of x (``idx``), ADVICE r1
+    (element snapshots, incremental probing)."""
+    b = ProgramBuilder(("N",))
+    b.array("x", ("N",), role="input", kind="real64")
+    b.array("y", ("N",), kind="real64")
+    b.scalar("O", role="output", kind="real64")
+    with b.loop("i", "0", "N", label="L"):
+        with b.branch("(lt (idx x i) 1.0)", label="small") as br:
+            with br.then():
+                with b.state("twice") as s:
+                    s.tasklet(ins={"a": ("x", ("i",))}, outs={"o": ("y", ("i",))}, body={"o": "(mul a 2)"})
+            with br.orelse():
+                with b.state("square") as s:
+                    s.tasklet(ins={"a": ("x", ("i",))}, outs={"o": ("y", ("i",))}, body={"o": "(mul a a)"})
+    with b.state("sum") as s:
+        s.library("reduce_sum", {"x": "y"}, {"y": "O"})
+    return b.finish("O", ["x"])
+
+
 def save_control_flow():
     os.makedirs(OUT, exist_ok=True)
     index = {}
+    prog = elem_branch()
+    bundle = save_programs(os.path.join(OUT, "elem_branch"), prog)
+    rng = np.random.default_rng(8)
+    for k in range(2):
+        x = rng.uniform(0.4, 1.6, 12)
+        res = gradient(prog, {"x": x}, {"N": 12}, bundle=bundle)
+        np.savez(os.path.join(OUT, f"elem_branch__{k}.npz"), **{"in:x": x}, value=np.asarray(res.value),
+                 **{"grad:x": np.asarray(res.grads["x"])})
+        index[f"elem_branch__{k}"] = {"program": "elem_branch", "params": {"N": 12}}
+        print("elem_branch", k, float(res.value))
     prog, ts = loop_branch()
     bundle = save_programs(os.path.join(OUT, "loop_branch"), prog)
     for t in ts:
