@@ -18,4 +18,11 @@ python bench.py --steps 2 --warmup 1 --no-cpu-baseline --no-e2e > gpurun_out/ben
 python tools/prof_stencil.py heat_3d 512 4 > gpurun_out/plain2.log 2>&1 && \
   timeout 600 ncu --set full --clock-control none --import-source on -k regex:star_pair --launch-skip 1 -c 4 \
   -o gpurun_out/prof_top python tools/prof_stencil.py heat_3d 512 4 > gpurun_out/ncu2.log 2>&1
+# the mlp GEMMs: the W2 forward (skinny, weight-streaming) and W2 gradient (K = 64)
+(cd tools/lab && python mm_time.py > ../../gpurun_out/mm_time.log 2>&1)
+for sh in "64 4096 4096 0 0" "4096 4096 64 1 0"; do
+  tag=$(echo $sh | tr ' ' _)
+  (cd tools/lab && timeout 300 ncu --set full --clock-control none -k regex:sgemm_tma --launch-skip 2 -c 1 \
+    -o ../../gpurun_out/gemm_$tag python mm_one.py $sh > ../../gpurun_out/ncu_gemm_$tag.log 2>&1)
+done
 echo done

@@ -106,6 +106,24 @@ def ncu_lines(tag):
         f.write("\n".join(out))
 
 
+def ncu_gemm(tag):
+    """The mlp GEMM captures (tools/lab/mm_one.py) and the nine-shape timing
+    table (tools/lab/mm_time.py)."""
+    reps = sorted(f for f in os.listdir(OUT) if f.startswith("gemm_") and f.endswith(".ncu-rep"))
+    if not reps:
+        return
+    out = []
+    t = os.path.join(OUT, "mm_time.log")
+    if os.path.exists(t):
+        out += ["tools/lab/mm_time.py (graph replay, median of 30):", open(t).read(), ""]
+    for r in reps:
+        shape = r[len("gemm_"):-len(".ncu-rep")].replace("_", " ")
+        out.append(f"ncu --set full -k regex:sgemm_tma python tools/lab/mm_one.py {shape}")
+        out += ncu_rep.summarize(os.path.join(OUT, r))[0]
+    with open(os.path.join(PROF, f"{tag}_ncu_gemm.txt"), "w") as f:
+        f.write("\n".join(out))
+
+
 def main():
     tag = sys.argv[1] if len(sys.argv) > 1 else "r01"
     os.makedirs(PROF, exist_ok=True)
@@ -123,6 +141,7 @@ def main():
     launches(tag)
     ncu_full(tag)
     ncu_lines(tag)
+    ncu_gemm(tag)
     print("\n".join(sorted(os.listdir(PROF))))
 
 
