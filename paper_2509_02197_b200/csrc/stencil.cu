@@ -41,6 +41,11 @@ struct StencilGeom {
 template <typename T, int MAXT, int NTC = 0, int CM = 0>
 __global__ void __launch_bounds__(kSX *kSY) stencil_kernel(const __grid_constant__ gfb_stencil_desc d,
                                                            const __grid_constant__ StencilGeom g) {
+  // launched with programmatic dependent launch: everything before the
+  // wait overlaps the previous launch's drain; global memory after it. The
+  // successor is released only as CTAs finish (an early trigger lets its
+  // waiting CTAs take the slots of this grid's later waves)
+  pdl_wait();
   const int64_t k = g.lo2 + (int64_t)blockIdx.x * kSX + threadIdx.x;
   const int64_t j = g.lo1 + (int64_t)blockIdx.y * kSY + threadIdx.y;
   if (k >= g.lo2 + g.e2 || j >= g.lo1 + g.e1) return;
@@ -87,6 +92,7 @@ __global__ void __launch_bounds__(kSX *kSY) stencil_kernel(const __grid_constant
       if (t < nt) acc += (T)d.tap_coef[t] * v[t];
     dst[off] = acc;
   }
+  pdl_trigger();
 }
 
 }  // namespace gfb
@@ -142,18 +148,18 @@ extern "C" int gfb_stencil_launch(const gfb_stencil_desc *d, void *stream) {
   cudaStream_t st = (cudaStream_t)stream;
 #define GFB_STENCIL_LAUNCH(MT)                                      \
   if (d->dtype == GFB_F64)                                          \
-    stencil_kernel<double, MT><<<grid, block, 0, st>>>(*d, g);      \
+    launch_pdl(stencil_kernel<double, MT>, grid, block, 0, st, *d, g); \
   else                                                              \
-    stencil_kernel<float, MT><<<grid, block, 0, st>>>(*d, g);
+    launch_pdl(stencil_kernel<float, MT>, grid, block, 0, st, *d, g);
   const bool cm1 = (d->clear_mode == 1 || d->clear_mode == 3) && !g.any_masked;
   const bool cm2 = d->clear_mode == 2 && g.any_masked;
   if (d->ntaps == 7 && (cm1 || cm2)) {  // heat_3d sweeps (forward / adjoint)
     if (d->dtype == GFB_F64) {
-      if (cm1) stencil_kernel<double, 8, 7, 1><<<grid, block, 0, st>>>(*d, g);
-      else stencil_kernel<double, 8, 7, 2><<<grid, block, 0, st>>>(*d, g);
+      if (cm1) launch_pdl(stencil_kernel<double, 8, 7, 1>, grid, block, 0, st, *d, g);
+      else launch_pdl(stencil_kernel<double, 8, 7, 2>, grid, block, 0, st, *d, g);
     } else {
-      if (cm1) stencil_kernel<float, 8, 7, 1><<<grid, block, 0, st>>>(*d, g);
-      else stencil_kernel<float, 8, 7, 2><<<grid, block, 0, st>>>(*d, g);
+      if (cm1) launch_pdl(stencil_kernel<float, 8, 7, 1>, grid, block, 0, st, *d, g);
+      else launch_pdl(stencil_kernel<float, 8, 7, 2>, grid, block, 0, st, *d, g);
     }
   } else if (d->ntaps <= 8) {
     GFB_STENCIL_LAUNCH(8)
