@@ -48,6 +48,8 @@ __device__ __forceinline__ double block_sum(double v) {
 template <typename TI>
 __global__ void __launch_bounds__(kThreads) reduce_pass1(const TI *__restrict__ x, int64_t n,
                                                          double *__restrict__ part) {
+  pdl_wait();  // programmatic dependent launch: global memory after the wait
+  PdlRelease pdl_release_;
   double acc[4] = {0.0, 0.0, 0.0, 0.0};
   const int64_t stride = (int64_t)gridDim.x * kThreads;
   const int64_t t0 = (int64_t)blockIdx.x * kThreads + threadIdx.x;
@@ -78,6 +80,8 @@ __global__ void __launch_bounds__(kThreads) reduce_pass1(const TI *__restrict__ 
 template <typename TI, typename TO>
 __global__ void __launch_bounds__(kThreads) reduce_single(const TI *__restrict__ x, int64_t n, TO *out,
                                                           int accumulate) {
+  pdl_wait();  // programmatic dependent launch: global memory after the wait
+  PdlRelease pdl_release_;
   double acc = 0.0;
   for (int64_t i = threadIdx.x; i < n; i += kThreads) acc += (double)x[i];
   double s = block_sum<TI>(acc);
@@ -90,6 +94,8 @@ __global__ void __launch_bounds__(kThreads) reduce_single(const TI *__restrict__
 template <typename TO>
 __global__ void __launch_bounds__(kThreads) reduce_pass2(const double *__restrict__ part, int64_t nb, TO *out,
                                                          int accumulate) {
+  pdl_wait();  // programmatic dependent launch: global memory after the wait
+  PdlRelease pdl_release_;
   double acc = 0.0;
   for (int64_t i = threadIdx.x; i < nb; i += kThreads) acc += part[i];
   double s = block_sum<TO>(acc);
@@ -106,6 +112,8 @@ template <typename T>
 __global__ void __launch_bounds__(kThreads) ew_kernel(int op, T c, const T *__restrict__ a, int64_t n_a,
                                                       const T *__restrict__ b, int64_t n_b, T *out, int64_t n,
                                                       int accumulate, uint32_t *err) {
+  pdl_wait();  // programmatic dependent launch: global memory after the wait
+  PdlRelease pdl_release_;
   const int64_t stride = (int64_t)gridDim.x * kThreads;
   for (int64_t i = (int64_t)blockIdx.x * kThreads + threadIdx.x; i < n; i += stride) {
     T x = a[n_a == 1 ? 0 : i];
@@ -159,6 +167,8 @@ __device__ __forceinline__ T ew_apply(T x, T y, T c, uint32_t &bad) {
 template <typename T, int OP, bool HASB>
 __global__ void __launch_bounds__(kThreads) ew_vec_kernel(T c, const T *__restrict__ a, const T *__restrict__ b,
                                                           T *out, int64_t nv, int accumulate, uint32_t *err) {
+  pdl_wait();  // programmatic dependent launch: global memory after the wait
+  PdlRelease pdl_release_;
   using V = typename EwVec<T>::V;
   constexpr int W = EwVec<T>::W;
   const V *av = reinterpret_cast<const V *>(a);
@@ -192,7 +202,7 @@ static bool ew_vec_launch(int op, T c, const T *a, int64_t n_a, const T *b, int6
   if (n % W || n_a != n || !al(a) || !al(out) || (b && (n_b != n || !al(b)))) return false;
   const int64_t nv = n / W;
   const unsigned blocks = (unsigned)stream_blocks(nv, 2);
-#define GFB_EW(OPC, HB) ew_vec_kernel<T, OPC, HB><<<blocks, kThreads, 0, st>>>(c, a, b, out, nv, accumulate, err)
+#define GFB_EW(OPC, HB) launch_pdl(ew_vec_kernel<T, OPC, HB>, blocks, kThreads, 0, st, c, a, b, out, nv, accumulate, err)
   if (!b) {
     if (op == GFB_OP_IN) GFB_EW(GFB_OP_IN, false);
     else if (op == GFB_OP_MUL) GFB_EW(-1, false);
@@ -212,6 +222,8 @@ static bool ew_vec_launch(int op, T c, const T *a, int64_t n_a, const T *b, int6
 template <typename T>
 __global__ void __launch_bounds__(kThreads) broadcast_kernel(const void *src, int32_t src_dtype, double scale,
                                                              T *out, int64_t n, int accumulate) {
+  pdl_wait();  // programmatic dependent launch: global memory after the wait
+  PdlRelease pdl_release_;
   double v = scale;
   if (src) v *= (src_dtype == GFB_F64 ? *(const double *)src : (double)*(const float *)src);
   const T tv = (T)v;
@@ -239,6 +251,8 @@ template <typename T>
 __global__ void __launch_bounds__(kThreads) fill_box_kernel(T *dst, int64_t d1, int64_t d2, int64_t lo0,
                                                             int64_t lo1, int64_t lo2, int64_t e0, int64_t e1,
                                                             int64_t e2, T value) {
+  pdl_wait();  // programmatic dependent launch: global memory after the wait
+  PdlRelease pdl_release_;
   const int64_t total = e0 * e1 * e2;
   const int64_t stride = (int64_t)gridDim.x * kThreads;
   for (int64_t f = (int64_t)blockIdx.x * kThreads + threadIdx.x; f < total; f += stride) {
@@ -261,7 +275,7 @@ extern "C" int gfb_reduce_sum(const void *x, int32_t xdtype, int64_t n, void *ou
   int64_t nb = reduce_blocks(n);
   double *part = (double *)workspace;
   if (n > 0 && nb == 1) {
-#define GFB_RS(TI, TO) reduce_single<TI, TO><<<1, kThreads, 0, st>>>((const TI *)x, n, (TO *)out, accumulate)
+#define GFB_RS(TI, TO) launch_pdl(reduce_single<TI, TO>, 1, kThreads, 0, st, (const TI *)x, n, (TO *)out, accumulate)
     if (xdtype == GFB_F64) {
       if (odtype == GFB_F64) GFB_RS(double, double); else GFB_RS(double, float);
     } else {
@@ -274,14 +288,14 @@ extern "C" int gfb_reduce_sum(const void *x, int32_t xdtype, int64_t n, void *ou
     nb = 1;
     cudaMemsetAsync(part, 0, 8, st);
   } else if (xdtype == GFB_F64) {
-    reduce_pass1<double><<<(unsigned)nb, kThreads, 0, st>>>((const double *)x, n, part);
+    launch_pdl(reduce_pass1<double>, (unsigned)nb, kThreads, 0, st, (const double *)x, n, part);
   } else {
-    reduce_pass1<float><<<(unsigned)nb, kThreads, 0, st>>>((const float *)x, n, part);
+    launch_pdl(reduce_pass1<float>, (unsigned)nb, kThreads, 0, st, (const float *)x, n, part);
   }
   if (odtype == GFB_F64)
-    reduce_pass2<double><<<1, kThreads, 0, st>>>(part, nb, (double *)out, accumulate);
+    launch_pdl(reduce_pass2<double>, 1, kThreads, 0, st, part, nb, (double *)out, accumulate);
   else
-    reduce_pass2<float><<<1, kThreads, 0, st>>>(part, nb, (float *)out, accumulate);
+    launch_pdl(reduce_pass2<float>, 1, kThreads, 0, st, part, nb, (float *)out, accumulate);
   return check_launch("reduce_sum");
 }
 
@@ -298,10 +312,10 @@ extern "C" int gfb_elementwise(int32_t op, double c, const void *a, int64_t n_a,
     return check_launch("elementwise");
   unsigned blocks = (unsigned)stream_blocks(n, 4);
   if (dtype == GFB_F64)
-    ew_kernel<double><<<blocks, kThreads, 0, st>>>(op, c, (const double *)a, n_a, (const double *)b, n_b,
+    launch_pdl(ew_kernel<double>, blocks, kThreads, 0, st, op, c, (const double *)a, n_a, (const double *)b, n_b,
                                                    (double *)out, n, accumulate, err);
   else
-    ew_kernel<float><<<blocks, kThreads, 0, st>>>(op, (float)c, (const float *)a, n_a, (const float *)b, n_b,
+    launch_pdl(ew_kernel<float>, blocks, kThreads, 0, st, op, (float)c, (const float *)a, n_a, (const float *)b, n_b,
                                                   (float *)out, n, accumulate, err);
   return check_launch("elementwise");
 }
@@ -312,9 +326,9 @@ extern "C" int gfb_broadcast(const void *src, int32_t src_dtype, double scale, v
   cudaStream_t st = (cudaStream_t)stream;
   unsigned blocks = (unsigned)stream_blocks(n, 4);
   if (dtype == GFB_F64)
-    broadcast_kernel<double><<<blocks, kThreads, 0, st>>>(src, src_dtype, scale, (double *)out, n, accumulate);
+    launch_pdl(broadcast_kernel<double>, blocks, kThreads, 0, st, src, src_dtype, scale, (double *)out, n, accumulate);
   else
-    broadcast_kernel<float><<<blocks, kThreads, 0, st>>>(src, src_dtype, scale, (float *)out, n, accumulate);
+    launch_pdl(broadcast_kernel<float>, blocks, kThreads, 0, st, src, src_dtype, scale, (float *)out, n, accumulate);
   return check_launch("broadcast");
 }
 
@@ -333,10 +347,10 @@ extern "C" int gfb_fill_box(void *dst, int32_t dtype, int32_t rank, const int64_
   cudaStream_t st = (cudaStream_t)stream;
   unsigned blocks = (unsigned)stream_blocks(total, 4);
   if (dtype == GFB_F64)
-    fill_box_kernel<double><<<blocks, kThreads, 0, st>>>((double *)dst, D[1], D[2], L[0], L[1], L[2], E[0], E[1],
+    launch_pdl(fill_box_kernel<double>, blocks, kThreads, 0, st, (double *)dst, D[1], D[2], L[0], L[1], L[2], E[0], E[1],
                                                          E[2], value);
   else
-    fill_box_kernel<float><<<blocks, kThreads, 0, st>>>((float *)dst, D[1], D[2], L[0], L[1], L[2], E[0], E[1],
+    launch_pdl(fill_box_kernel<float>, blocks, kThreads, 0, st, (float *)dst, D[1], D[2], L[0], L[1], L[2], E[0], E[1],
                                                         E[2], (float)value);
   return check_launch("fill_box");
 }

@@ -182,4 +182,11 @@ __host__ __device__ __forceinline__ int64_t ceil_div(int64_t a, int64_t b) { ret
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 
+// releases the successor launch when the thread leaves the kernel (any
+// return path): its CTAs then start only as this grid drains, instead of
+// holding slots the grid's later waves need
+struct PdlRelease {
+  __device__ __forceinline__ ~PdlRelease() { pdl_trigger(); }
+};
+
 }  // namespace gfb

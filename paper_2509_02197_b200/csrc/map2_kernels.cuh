@@ -282,6 +282,8 @@ __device__ __forceinline__ void m2_points(const gfb_map2_desc &d, At &at, uint32
 template <typename T, int V, int LAYOUT, typename Body>
 __global__ void __launch_bounds__(256) map2_pointwise_kernel(const __grid_constant__ gfb_map2_desc d, int32_t rows,
                                                              int32_t cpr, uint64_t magic) {
+  pdl_wait();  // programmatic dependent launch: global memory after the wait
+  PdlRelease pdl_release_;
   __shared__ int32_t sbase[kM2Warps][kM2Bases];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int nd = d.ndim;
@@ -326,6 +328,8 @@ __global__ void __launch_bounds__(256) map2_pointwise_kernel(const __grid_consta
 template <typename T, int V, bool ROW1, typename Body>
 __global__ void __launch_bounds__(256) map2_reduce_inner_kernel(const __grid_constant__ gfb_map2_desc d,
                                                                 int32_t rows) {
+  pdl_wait();  // programmatic dependent launch: global memory after the wait
+  PdlRelease pdl_release_;
   __shared__ int32_t sbase[kM2Warps][kM2Bases];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int nd = d.ndim;
@@ -367,6 +371,8 @@ __global__ void __launch_bounds__(256) map2_reduce_inner_kernel(const __grid_con
 // column sums: lane = column, V rows per warp iteration (V loads in flight)
 template <typename T, int V, typename Body>
 __global__ void __launch_bounds__(256) map2_reduce_outer_kernel(const __grid_constant__ gfb_map2_desc d) {
+  pdl_wait();  // programmatic dependent launch: global memory after the wait
+  PdlRelease pdl_release_;
   __shared__ T red[kM2Warps][32];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int32_t R = (int32_t)d.ext[0], E = (int32_t)d.ext[1];
@@ -406,6 +412,8 @@ __global__ void __launch_bounds__(256) map2_reduce_outer_kernel(const __grid_con
 
 template <typename T>
 __global__ void __launch_bounds__(1024) map2_finish_kernel(const __grid_constant__ gfb_map2_desc d) {
+  pdl_wait();  // programmatic dependent launch: global memory after the wait
+  PdlRelease pdl_release_;
   // 32 columns x 32 split groups per CTA: group g sums splits g, g + 32, ...
   // (a few L2 round trips per thread instead of nsplit), then the groups are
   // added in order (deterministic)
@@ -462,6 +470,8 @@ struct M2FetchVec4 {
 template <typename Body, bool FLAT>
 __global__ void __launch_bounds__(256) map2_pointwise_vec4_kernel(const __grid_constant__ gfb_map2_desc d,
                                                                   int32_t rows, int32_t cpr) {
+  pdl_wait();  // programmatic dependent launch: global memory after the wait
+  PdlRelease pdl_release_;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int32_t E = (int32_t)d.ext[1];
   const int32_t items = FLAT ? (int32_t)ceil_div((int64_t)rows * E, 128) : rows * cpr;
@@ -498,6 +508,8 @@ __global__ void __launch_bounds__(256) map2_pointwise_vec4_kernel(const __grid_c
 template <typename Body>
 __global__ void __launch_bounds__(256) map2_reduce_inner_vec4_kernel(const __grid_constant__ gfb_map2_desc d,
                                                                      int32_t rows) {
+  pdl_wait();  // programmatic dependent launch: global memory after the wait
+  PdlRelease pdl_release_;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int32_t E = (int32_t)d.ext[1];
   for (int32_t row = blockIdx.x * kM2Warps + w; row < rows; row += gridDim.x * kM2Warps) {
@@ -550,6 +562,8 @@ __device__ __forceinline__ void m2_prefetch(const gfb_map2_desc &d, const int32_
 template <typename Body, bool FLAT, int U>
 __global__ void __launch_bounds__(256) map2_pointwise_ilp_kernel(const __grid_constant__ gfb_map2_desc d,
                                                                  int32_t rows, int32_t cpr) {
+  pdl_wait();  // programmatic dependent launch: global memory after the wait
+  PdlRelease pdl_release_;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int32_t E = (int32_t)d.ext[1];
   const int32_t items = FLAT ? (int32_t)ceil_div((int64_t)rows * E, 128) : rows * cpr;
@@ -596,6 +610,8 @@ __global__ void __launch_bounds__(256) map2_pointwise_ilp_kernel(const __grid_co
 template <typename Body, int U>
 __global__ void __launch_bounds__(256) map2_reduce_row_ilp_kernel(const __grid_constant__ gfb_map2_desc d,
                                                                   int32_t rows) {
+  pdl_wait();  // programmatic dependent launch: global memory after the wait
+  PdlRelease pdl_release_;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int32_t E = (int32_t)d.ext[1];
   for (int32_t r0 = (blockIdx.x * kM2Warps + w) * U; r0 < rows; r0 += gridDim.x * kM2Warps * U) {
@@ -659,6 +675,8 @@ struct M2FetchVec4Row {
 template <typename Body>
 __global__ void __launch_bounds__(256) map2_reduce_outer_vec4_kernel(const __grid_constant__ gfb_map2_desc d,
                                                                      int qpr) {
+  pdl_wait();  // programmatic dependent launch: global memory after the wait
+  PdlRelease pdl_release_;
   __shared__ float4 red[kM2Warps][32];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int32_t R = (int32_t)d.ext[0], E = (int32_t)d.ext[1];
@@ -761,9 +779,9 @@ inline int launch_map2(const gfb_map2_desc &d, cudaStream_t st) {
               const int64_t items = E < 128 ? ceil_div(rows * E, 128) : rows * cpr;
               const int64_t blocks = std::max<int64_t>(std::min<int64_t>(ceil_div(items, kM2Warps * U), cap * 4), 1);
               if (E < 128)
-                map2_pointwise_ilp_kernel<Body, true, U><<<(unsigned)blocks, 256, 0, st>>>(d, (int32_t)rows, 1);
+                launch_pdl(map2_pointwise_ilp_kernel<Body, true, U>, (unsigned)blocks, 256, 0, st, d, (int32_t)rows, 1);
               else
-                map2_pointwise_ilp_kernel<Body, false, U><<<(unsigned)blocks, 256, 0, st>>>(d, (int32_t)rows,
+                launch_pdl(map2_pointwise_ilp_kernel<Body, false, U>, (unsigned)blocks, 256, 0, st, d, (int32_t)rows,
                                                                                               (int32_t)cpr);
               return check_launch("map2");
             }
@@ -771,11 +789,11 @@ inline int launch_map2(const gfb_map2_desc &d, cudaStream_t st) {
           if (E < 128) {
             const int64_t blocks =
                 std::max<int64_t>(std::min<int64_t>(ceil_div(rows * E, 128 * kM2Warps), cap * 4), 1);
-            map2_pointwise_vec4_kernel<Body, true><<<(unsigned)blocks, 256, 0, st>>>(d, (int32_t)rows, 1);
+            launch_pdl(map2_pointwise_vec4_kernel<Body, true>, (unsigned)blocks, 256, 0, st, d, (int32_t)rows, 1);
           } else {
             const int64_t blocks =
                 std::max<int64_t>(std::min<int64_t>(ceil_div(rows * cpr, kM2Warps), cap * 4), 1);
-            map2_pointwise_vec4_kernel<Body, false><<<(unsigned)blocks, 256, 0, st>>>(d, (int32_t)rows,
+            launch_pdl(map2_pointwise_vec4_kernel<Body, false>, (unsigned)blocks, 256, 0, st, d, (int32_t)rows,
                                                                                        (int32_t)cpr);
           }
           return check_launch("map2");
@@ -788,12 +806,12 @@ inline int launch_map2(const gfb_map2_desc &d, cudaStream_t st) {
               constexpr int U = 4;
               const int64_t blocks =
                   std::max<int64_t>(std::min<int64_t>(ceil_div(rows, kM2Warps * U), cap * 4), 1);
-              map2_reduce_row_ilp_kernel<Body, U><<<(unsigned)blocks, 256, 0, st>>>(d, (int32_t)rows);
+              launch_pdl(map2_reduce_row_ilp_kernel<Body, U>, (unsigned)blocks, 256, 0, st, d, (int32_t)rows);
               return check_launch("map2");
             }
           }
           const int64_t blocks = std::max<int64_t>(std::min<int64_t>(ceil_div(rows, kM2Warps), cap * 4), 1);
-          map2_reduce_inner_vec4_kernel<Body><<<(unsigned)blocks, 256, 0, st>>>(d, (int32_t)rows);
+          launch_pdl(map2_reduce_inner_vec4_kernel<Body>, (unsigned)blocks, 256, 0, st, d, (int32_t)rows);
           return check_launch("map2");
         }
       }
@@ -801,9 +819,9 @@ inline int launch_map2(const gfb_map2_desc &d, cudaStream_t st) {
         if (d.mode == 2) {
           const int qpr = (int)std::min<int64_t>(E, 128) / 4;
           dim3 grid((unsigned)ceil_div(E, 128), (unsigned)d.nsplit);
-          map2_reduce_outer_vec4_kernel<Body><<<grid, 256, 0, st>>>(d, qpr);
+          launch_pdl(map2_reduce_outer_vec4_kernel<Body>, grid, 256, 0, st, d, qpr);
           if (d.nsplit > 1) {
-            map2_finish_kernel<T><<<(unsigned)ceil_div(E, 32), 1024, 0, st>>>(d);
+            launch_pdl(map2_finish_kernel<T>, (unsigned)ceil_div(E, 32), 1024, 0, st, d);
           }
           return check_launch("map2");
         }
@@ -817,13 +835,13 @@ inline int launch_map2(const gfb_map2_desc &d, cudaStream_t st) {
         const uint64_t magic = (((uint64_t)1 << 40) + (uint64_t)E - 1) / (uint64_t)E;
         const int64_t blocks =
             std::max<int64_t>(std::min<int64_t>(ceil_div(rows * E, 32 * V * kM2Warps), cap * 4), 1);
-        map2_pointwise_kernel<T, V, 1, Body><<<(unsigned)blocks, 256, 0, st>>>(d, (int32_t)rows, (int32_t)cpr, magic);
+        launch_pdl(map2_pointwise_kernel<T, V, 1, Body>, (unsigned)blocks, 256, 0, st, d, (int32_t)rows, (int32_t)cpr, magic);
       } else {
         const int64_t blocks = std::max<int64_t>(std::min<int64_t>(ceil_div(rows * cpr, kM2Warps), cap * 4), 1);
         if (nd == 2)
-          map2_pointwise_kernel<T, V, 0, Body><<<(unsigned)blocks, 256, 0, st>>>(d, (int32_t)rows, (int32_t)cpr, 0);
+          launch_pdl(map2_pointwise_kernel<T, V, 0, Body>, (unsigned)blocks, 256, 0, st, d, (int32_t)rows, (int32_t)cpr, 0);
         else
-          map2_pointwise_kernel<T, V, 2, Body><<<(unsigned)blocks, 256, 0, st>>>(d, (int32_t)rows, (int32_t)cpr, 0);
+          launch_pdl(map2_pointwise_kernel<T, V, 2, Body>, (unsigned)blocks, 256, 0, st, d, (int32_t)rows, (int32_t)cpr, 0);
       }
     }
   }
@@ -831,17 +849,17 @@ inline int launch_map2(const gfb_map2_desc &d, cudaStream_t st) {
     if (d.mode == 1) {
       const int64_t blocks = std::max<int64_t>(std::min<int64_t>(ceil_div(rows, kM2Warps), cap * 4), 1);
       if (nd == 2)
-        map2_reduce_inner_kernel<T, V, true, Body><<<(unsigned)blocks, 256, 0, st>>>(d, (int32_t)rows);
+        launch_pdl(map2_reduce_inner_kernel<T, V, true, Body>, (unsigned)blocks, 256, 0, st, d, (int32_t)rows);
       else
-        map2_reduce_inner_kernel<T, V, false, Body><<<(unsigned)blocks, 256, 0, st>>>(d, (int32_t)rows);
+        launch_pdl(map2_reduce_inner_kernel<T, V, false, Body>, (unsigned)blocks, 256, 0, st, d, (int32_t)rows);
     }
   }
   if constexpr (MODE == -1 || MODE == 2) {
     if (d.mode == 2) {
       dim3 grid((unsigned)ceil_div(E, 32), (unsigned)d.nsplit);
-      map2_reduce_outer_kernel<T, V, Body><<<grid, 256, 0, st>>>(d);
+      launch_pdl(map2_reduce_outer_kernel<T, V, Body>, grid, 256, 0, st, d);
       if (d.nsplit > 1) {
-        map2_finish_kernel<T><<<(unsigned)ceil_div(E, 32), 1024, 0, st>>>(d);
+        launch_pdl(map2_finish_kernel<T>, (unsigned)ceil_div(E, 32), 1024, 0, st, d);
       }
     }
   }

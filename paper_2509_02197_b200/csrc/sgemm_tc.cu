@@ -50,6 +50,8 @@ template <int BN, bool TA, bool TB>
 __global__ void __launch_bounds__(kTcThreads, 1)
     sgemm_tc_kernel(int M, int N, int K, const float *__restrict__ A, int64_t lda, const float *__restrict__ B,
                     int64_t ldb, float *C, int64_t csm, int64_t csn, int accumulate, float *partial, int kchunk) {
+  pdl_wait();  // programmatic dependent launch: global memory after the wait
+  PdlRelease pdl_release_;
   extern __shared__ __align__(1024) unsigned char tc_raw[];
   // align the dynamic region to 1 KiB by hand (the runtime guarantees 16 B)
   TcSmem<BN> &S = *reinterpret_cast<TcSmem<BN> *>((reinterpret_cast<uintptr_t>(tc_raw) + 1023) & ~(uintptr_t)1023);
@@ -360,6 +362,7 @@ __global__ void __launch_bounds__(kTcThreads, 2)  // <= 128 registers: two short
     sgemm_tma_kernel(const __grid_constant__ CUtensorMap amap, const __grid_constant__ CUtensorMap bmap,
                      const __grid_constant__ CUtensorMap cmap, int M, int N, int K, float *C, int64_t csm,
                      int64_t csn, int accumulate, float *partial, int kchunk, int cmode) {
+  PdlRelease pdl_release_;
   using Cfg = TmaCfg<BN, AKM, BKM, SK>;
   constexpr int S = Cfg::kStages;
   extern __shared__ __align__(1024) unsigned char tm_raw[];
@@ -398,6 +401,9 @@ __global__ void __launch_bounds__(kTcThreads, 2)  // <= 128 registers: two short
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem = *tmem_slot;
+  // programmatic dependent launch: the TMEM allocation and barrier set-up
+  // above overlap the previous launch's drain; global memory after the wait
+  pdl_wait();
 
   if (warp == 0) {
     if (lane == 0) {  // producer
@@ -622,7 +628,7 @@ static int launch_tma_k(dim3 grid, int M, int N, int K, const float *A, int64_t 
   static_assert(BN < 64 || TmaCfg<BN, AKM, BKM, SK>::kStages * TmaCfg<BN, AKM, BKM, SK>::kStage >= 8 * (BN / 64) * 4096,
                 "epilogue staging exceeds the ring");
   ensure_smem(sgemm_tma_kernel<BN, AKM, BKM, SK>, smem);
-  sgemm_tma_kernel<BN, AKM, BKM, SK><<<grid, kTcThreads, smem, st>>>(am, bm, cm, M, N, K, C, csm, csn, accumulate,
+  launch_pdl(sgemm_tma_kernel<BN, AKM, BKM, SK>, grid, kTcThreads, smem, st, am, bm, cm, M, N, K, C, csm, csn, accumulate,
                                                                      partial, kchunk, cmode);
   return 0;
 }
@@ -662,6 +668,8 @@ static bool tma_ok(const float *A, int64_t lda, const float *B, int64_t ldb) {
 // both the partial stores and this pass are coalesced
 __global__ void tc_splits_finish(int64_t M, int64_t N, int64_t ns, const float *__restrict__ partial, float *C,
                                  int64_t csm, int64_t csn, int accumulate) {
+  pdl_wait();  // programmatic dependent launch: global memory after the wait
+  PdlRelease pdl_release_;
   const int64_t MN = M * N;
   const bool rows = csn == 1;
   const int64_t inner = rows ? N : M;
@@ -705,7 +713,7 @@ static void launch_tc(dim3 grid, int M, int N, int K, const float *A, int64_t ld
                       cudaStream_t st) {
   const size_t smem = sizeof(TcSmem<BN>) + 1024;
   ensure_smem(sgemm_tc_kernel<BN, TA, TB>, (int)smem);
-  sgemm_tc_kernel<BN, TA, TB><<<grid, kTcThreads, smem, st>>>(M, N, K, A, lda, B, ldb, C, csm, csn, accumulate,
+  launch_pdl(sgemm_tc_kernel<BN, TA, TB>, grid, kTcThreads, smem, st, M, N, K, A, lda, B, ldb, C, csm, csn, accumulate,
                                                                partial, kchunk);
 }
 
@@ -769,7 +777,7 @@ int sgemm_tc(int ta, int tb, int64_t M, int64_t N, int64_t K, const float *A, in
                      (int)chunk, st);
   if (nz > 1) {
     const unsigned blocks = (unsigned)std::min<int64_t>(ceil_div(M * N, 256), (int64_t)sm_count() * 8);
-    tc_splits_finish<<<blocks, 256, 0, st>>>(M, N, nz, partial, C, csm, csn, accumulate);
+    launch_pdl(tc_splits_finish, blocks, 256, 0, st, M, N, nz, partial, C, csm, csn, accumulate);
   }
   return check_launch("sgemm_tc");
 }
