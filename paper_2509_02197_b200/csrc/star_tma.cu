@@ -325,7 +325,7 @@ __device__ __forceinline__ void star_tma_body(const CUtensorMap *ymap, const Sta
 #endif
   // common-case predicate patterns
   const uint32_t xmask = kArray | kRegion | (amode == 2 ? kClear : 0u) | (xwrite ? kDead : 0u);
-  const uint32_t xval = amode == 0 ? 0xffffffffu : xmask;  // mode 0: base always added -> fix-up
+  [[maybe_unused]] const uint32_t xval = amode == 0 ? 0xffffffffu : xmask;  // mode 0: base always added -> fix-up
   const uint32_t zmask = kArray | kRegion | (bmode == 2 ? kClear : 0u);
   const uint32_t zval = bmode == 0 ? 0xffffffffu : zmask;
   const uint32_t xfast_m = xmask | kSrcB;
