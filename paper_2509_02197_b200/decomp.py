@@ -154,6 +154,11 @@ class HaloOp(Op):
         self.done = torch.cuda.Event()
         self.done.record(comm_stream)
 
+    def algorithmic_bytes(self) -> int:
+        """Bytes the exchange moves out of this rank (both neighbours)."""
+        nb = (self.plan.rank > 0) + (self.plan.rank < self.plan.world - 1)
+        return sum(nb * w * (b.numel // b.shape[0]) * b.itemsize for b, w in self.items)
+
 
 class HaloWaitOp(Op):
     """The compute stream waits for a HaloOp's exchange (before the edge
@@ -174,7 +179,7 @@ class HaloWaitOp(Op):
             self.halo.done = None
 
     def algorithmic_bytes(self) -> int:
-        return sum(2 * w * (b.numel // b.shape[0]) * b.itemsize for b, w in self.items)
+        return 0
 
 
 class AllReduceOp(Op):

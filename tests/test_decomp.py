@@ -77,6 +77,13 @@ def _run_rank(rank, world, port, params, q):
                 em.run_op(op)
         value = float(view(dl.outputs["value"]))
         g = view(dl.outputs["grad:A"]).numpy()
+        # what bench.py's per-launch roofline pass and launch count read of
+        # every op of a decomposed list (communication ops included)
+        import bench
+
+        for op in dl.low.ops:
+            assert op.algorithmic_bytes() >= 0
+            assert bench.kernels_per_op(op) >= 0
         lo, hi = plan.own_local
         q.put((rank, value, plan.own_lo, plan.own_hi, g[lo:hi].copy()))
     finally:

@@ -7,6 +7,8 @@ make -C oracle -s
 timeout 900 python -m pytest tests -m gpu -q > gpurun_out/pytest_gpu.log 2>&1; echo rc=$? >> gpurun_out/pytest_gpu.log
 timeout 600 python bench.py > gpurun_out/bench.jsonl 2> gpurun_out/bench.err; echo rc=$? >> gpurun_out/bench.err
 timeout 600 python bench.py --impl reference > gpurun_out/bench_ref.jsonl 2> gpurun_out/bench_ref.err
+# the slab-decomposition path at one rank (communication-free rewrite, graph captured)
+timeout 600 python bench.py --force-slab --steps 5 --no-cpu-baseline > gpurun_out/bench_slab1.jsonl 2> gpurun_out/bench_slab1.err
 timeout 1500 python tools/bench_all.py --steps 10 --plans > gpurun_out/configs.jsonl 2> gpurun_out/configs.err
 timeout 600 python tools/op_table.py > gpurun_out/ops.txt 2>&1
 # launch list of the bench command (cold-cache serialised times: compare shares)

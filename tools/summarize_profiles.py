@@ -135,6 +135,7 @@ def main():
     if lines:
         open(os.path.join(PROF, f"{tag}_bench.jsonl"), "w").write("\n".join(lines) + "\n")
     for src, dst in (("configs.jsonl", f"{tag}_configs.jsonl"), ("ops.txt", f"{tag}_ops.txt"),
+                     ("bench_slab1.jsonl", f"{tag}_bench_slab1.jsonl"),
                      ("pytest_gpu.log", f"{tag}_pytest_gpu.log")):
         if os.path.exists(os.path.join(OUT, src)):
             shutil.copy(os.path.join(OUT, src), os.path.join(PROF, dst))
