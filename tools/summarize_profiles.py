@@ -134,8 +134,11 @@ def main():
             lines += [l for l in open(p).read().splitlines() if l.startswith("{")]
     if lines:
         open(os.path.join(PROF, f"{tag}_bench.jsonl"), "w").write("\n".join(lines) + "\n")
+    p = os.path.join(OUT, "bench_slab1.jsonl")
+    if os.path.exists(p):
+        keep = [l for l in open(p).read().splitlines() if l.startswith("{")]
+        open(os.path.join(PROF, f"{tag}_bench_slab1.jsonl"), "w").write("\n".join(keep) + "\n")
     for src, dst in (("configs.jsonl", f"{tag}_configs.jsonl"), ("ops.txt", f"{tag}_ops.txt"),
-                     ("bench_slab1.jsonl", f"{tag}_bench_slab1.jsonl"),
                      ("pytest_gpu.log", f"{tag}_pytest_gpu.log")):
         if os.path.exists(os.path.join(OUT, src)):
             shutil.copy(os.path.join(OUT, src), os.path.join(PROF, dst))
