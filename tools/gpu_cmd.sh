@@ -1,4 +1,5 @@
-cd $GRAFT_REPO_ROOT/tools/lab
-timeout 300 ncu --set full --import-source on --clock-control none -k regex:"sgemm_tma" --launch-skip 2 -c 1 -o ../../gpurun_out/mm4_k64 python mm_one.py 4096 4096 64 1 0 > ../../gpurun_out/ncu_mm4.log 2>&1
-timeout 300 ncu --set full --import-source on --clock-control none -k regex:"sgemm_tma" --launch-skip 2 -c 1 -o ../../gpurun_out/mm4_w2 python mm_one.py 64 4096 4096 0 0 > ../../gpurun_out/ncu_mm4b.log 2>&1
-ls ../../gpurun_out | grep mm4
+cd $GRAFT_REPO_ROOT
+for r in 1 2; do for v in cur s1; do
+  if [ $v = cur ]; then unset GFB_LIBRARY; else export GFB_LIBRARY=$GRAFT_REPO_ROOT/build/var/$v.so; fi
+  timeout 120 python tools/time_star.py
+done; done
