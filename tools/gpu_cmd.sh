@@ -1,5 +1,3 @@
 cd $GRAFT_REPO_ROOT
-for r in 1 2; do for v in cur s1; do
-  if [ $v = cur ]; then unset GFB_LIBRARY; else export GFB_LIBRARY=$GRAFT_REPO_ROOT/build/var/$v.so; fi
-  timeout 120 python tools/time_star.py
-done; done
+timeout 900 python -m pytest tests/test_gpu.py tests/test_gpu_r2.py -q -x -k "lockstep or slab or group or heat or c5 or C5" 2>&1 | tail -2
+timeout 600 python tools/host_overhead.py 2>&1 | tail -12
