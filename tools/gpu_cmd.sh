@@ -1,4 +1,3 @@
 cd $GRAFT_REPO_ROOT
-for t in 0 8 10 12 16 20 24 30; do
-  echo "== tpm $t"; GFB_STAR_TPM_SET=$t timeout 300 python tools/host_overhead.py 2>&1 | grep -E "single|of 8|60 planes"
-done
+timeout 600 python -m pytest tests/test_gpu.py -q -x -k "3xtf32 or mlp or C4" 2>&1 | tail -2
+cd tools/lab; for r in 1 2; do python mm_time.py 2>&1 | cut -c1-60; done
