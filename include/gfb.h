@@ -26,7 +26,7 @@
 extern "C" {
 #endif
 
-#define GFB_ABI_VERSION 11
+#define GFB_ABI_VERSION 10
 
 #define GFB_MAX_PARAMS 8    /* map parameters (iteration-space rank) */
 #define GFB_MAX_RANK 8      /* array rank */
@@ -245,9 +245,6 @@ typedef struct {
    * produced for local planes [zlo, zhi). Single device: 0, 0, dims[0]. */
   int64_t plane0, zlo, zhi;
   int64_t global_d0;
-  /* optional second plane range [zlo2, zhi2) produced by the same launch
-   * (the two edge ranges of a slab; zhi2 <= zlo2: none) */
-  int64_t zlo2, zhi2;
 } gfb_star_pair_desc;
 
 /*

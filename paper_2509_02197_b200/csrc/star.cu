@@ -214,9 +214,7 @@ __global__ void __launch_bounds__(kPX *kPY, 2) star_pair_kernel(const __grid_con
   __shared__ uint32_t s_and_a, s_or_a, s_and_b, s_or_b;
   const int tx = threadIdx.x, ty = threadIdx.y, tid = ty * kPX + tx;
   const int k0 = blockIdx.x * kPX, j0 = blockIdx.y * kPY;
-  const bool second = (int)blockIdx.z >= d.nz1;
-  const int i0 = second ? d.zlo2 + ((int)blockIdx.z - d.nz1) * kPM : d.zlo + (int)blockIdx.z * kPM;
-  const int i1 = min(i0 + kPM, second ? d.zhi2 : d.zhi);
+  const int i0 = d.zlo + blockIdx.z * kPM, i1 = min(i0 + kPM, d.zhi);
   star_prologue(d, i0, i1, tid, aj, ak, bj, bk, ai, bi, s_and_a, s_or_a, s_and_b, s_or_b);  // descriptor only
   pdl_wait();
   pdl_trigger();  // after the wait: at most one launch waits ahead of the running one
@@ -354,18 +352,13 @@ extern "C" int gfb_star_pair_launch(const gfb_star_pair_desc *s, void *stream) {
     d.gd0 = (int32_t)(s->global_d0 > 0 ? s->global_d0 : dims[0]);
     d.zlo = (int32_t)s->zlo;
     d.zhi = (int32_t)(s->zhi > s->zlo ? s->zhi : dims[0]);
-    d.zlo2 = (int32_t)s->zlo2;
-    d.zhi2 = (int32_t)(s->zhi2 > s->zlo2 ? s->zhi2 : s->zlo2);
   } else {
     d.p0 = 0;
     d.gd0 = 1;
     d.zlo = 0;
     d.zhi = 1;
-    d.zlo2 = d.zhi2 = 0;
   }
   if (d.zlo < 0 || d.zhi > d.d0 || d.zlo >= d.zhi) return set_error(GFB_EINVAL, "gfb_star_pair_launch: bad plane range");
-  if (d.zhi2 > d.zlo2 && (d.zlo2 < 0 || d.zhi2 > d.d0 || (d.zlo2 < d.zhi && d.zhi2 > d.zlo)))
-    return set_error(GFB_EINVAL, "gfb_star_pair_launch: bad second plane range");
   fill_star_op(d.a, s->a, pad);
   fill_star_op(d.b, s->b, pad);
   d.y = s->y;
@@ -379,9 +372,7 @@ extern "C" int gfb_star_pair_launch(const gfb_star_pair_desc *s, void *stream) {
     d.dhi[r] = padded ? (1 << 30) : (int32_t)s->dead_hi[r - pad];
   }
   dim3 block(kPX, kPY);
-  d.nz1 = (int32_t)ceil_div(d.zhi - d.zlo, kPM);
-  dim3 grid((unsigned)ceil_div(d.d2, kPX), (unsigned)ceil_div(d.d1, kPY),
-            (unsigned)(d.nz1 + ceil_div(d.zhi2 - d.zlo2, kPM)));
+  dim3 grid((unsigned)ceil_div(d.d2, kPX), (unsigned)ceil_div(d.d1, kPY), (unsigned)ceil_div(d.zhi - d.zlo, kPM));
   cudaStream_t st = (cudaStream_t)stream;
   // the TMA kernel runs masks as data (source-mask form); general masks use the L1 kernel
   if (d.a.srcmask >= 0 && d.b.srcmask >= 0) {

@@ -27,8 +27,6 @@ struct StarPairDev {
   int32_t d0, d1, d2;   // local extents
   int32_t p0, gd0;      // global index of local plane 0, global extent of dim 0
   int32_t zlo, zhi;     // local planes to produce
-  int32_t zlo2, zhi2;   // optional second range (zhi2 <= zlo2: none)
-  int32_t nz1;          // grid.z blocks of the first range (the rest cover the second)
   int32_t xwrite;  // write X back (outside the dead box)
   int32_t skipz, skipx;  // out-of-region Z copy / X write-back already in place
   int32_t tpm;           // planes per CTA (TMA kernel)

@@ -718,9 +718,7 @@ __global__ void __launch_bounds__(tThreads, HAS_I ? 512 / tThreads : 768 / tThre
   __shared__ TmaWords words;
   __shared__ T xst[2][kR + 1][tThreads];  // staged old X values (fix-up points), by plane parity
   const int tid = threadIdx.y * tPX + threadIdx.x;
-  const bool second = (int)blockIdx.z >= d.nz1;
-  const int i0 = second ? d.zlo2 + ((int)blockIdx.z - d.nz1) * d.tpm : d.zlo + (int)blockIdx.z * d.tpm;
-  const int i1 = min(i0 + d.tpm, second ? d.zhi2 : d.zhi);
+  const int i0 = d.zlo + blockIdx.z * d.tpm, i1 = min(i0 + d.tpm, d.zhi);
   tma_prologue(d, i0, blockIdx.y * tPY, blockIdx.x * tPX, tid, words);  // descriptor only
   pdl_wait();
   pdl_trigger();  // after the wait: at most one launch waits ahead of the running one
@@ -753,13 +751,10 @@ static int launch_tma_m(const CUtensorMap &map, const StarPairDev &d, cudaStream
   // tile-column segment in one wave of resident CTAs (2 per SM); small
   // domains get short marches rather than idle SMs or a straggler wave
   StarPairDev dd = d;
-  const int64_t tiles = ceil_div(d.d2, tPX) * ceil_div(d.d1, tPY);
-  const int64_t planes = (d.zhi - d.zlo) + std::max(0, d.zhi2 - d.zlo2);
+  const int64_t tiles = ceil_div(d.d2, tPX) * ceil_div(d.d1, tPY), planes = d.zhi - d.zlo;
   const int64_t slots = 2 * (int64_t)sm_count();
   dd.tpm = (int32_t)std::max<int64_t>(2, std::min<int64_t>(tPM, ceil_div(planes * tiles, slots)));
-  dd.nz1 = (int32_t)ceil_div(d.zhi - d.zlo, dd.tpm);
-  dim3 grid((unsigned)ceil_div(d.d2, tPX), (unsigned)ceil_div(d.d1, tPY),
-            (unsigned)(dd.nz1 + ceil_div(std::max(0, d.zhi2 - d.zlo2), dd.tpm)));
+  dim3 grid((unsigned)ceil_div(d.d2, tPX), (unsigned)ceil_div(d.d1, tPY), (unsigned)ceil_div(planes, dd.tpm));
   launch_pdl(star_pair_tma_kernel<T, HAS_I, MODES>, grid, dim3(tPX, tPY / kR), sm, st, map, dd);
   return check_launch("star_pair_tma");
 }

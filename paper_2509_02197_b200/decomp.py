@@ -13,8 +13,8 @@ after star-pair fusion and ping-pong placement) is rewritten per rank:
     - the same kernel on the interior planes [own_lo + 2, own_hi - 2), which
       read no halo plane and run on the compute stream WHILE the exchange
       is in flight;
-    - a wait for the exchange (HaloWaitOp), then ONE launch of the kernel on
-      the two edge plane ranges (two planes at each slab end);
+    - a wait for the exchange (HaloWaitOp), then the kernel on the two edge
+      plane ranges (two planes at each slab end);
   masks / regions stay in global coordinates (plane0 in the descriptor);
 * a reduction over a decomposed array becomes a local reduction over the
   owned planes plus an all-reduce of the scalar (the reference's dependent
@@ -246,13 +246,12 @@ def decompose(lw, plan: SlabPlan, comm) -> DistLowered:
     ol, oh = plan.own_local
     w = plan.halo
 
-    def pair_on(op, zr, zr2=None):
+    def pair_on(op, zr):
         new = StarPairOp(op.a, op.b, op.fa, op.fb, op.xwrite, op.dead)
         new.X, new.Y, new.Z = loc(op.X), loc(op.Y), loc(op.Z)
         new.xout, new.zout = loc(op.xout), loc(op.zout)
         new.skip_zcopy, new.skip_xcopy = op.skip_zcopy, op.skip_xcopy
         new.plane0, new.zrange, new.global_d0 = plan.loc_lo, zr, plan.N
-        new.zrange2 = zr2
         new._refresh()
         low.emit(new)
 
@@ -271,9 +270,9 @@ def decompose(lw, plan: SlabPlan, comm) -> DistLowered:
             if hi_edge[0] > lo_edge[1]:
                 pair_on(op, (lo_edge[1], hi_edge[0]))
             low.emit(HaloWaitOp(halo))
-            # both edge ranges in one launch (two tiny launches cost a
-            # launch latency each; measured 2 x 16.7 us per timestep at 8 ranks)
-            pair_on(op, lo_edge, hi_edge if hi_edge[1] > hi_edge[0] else None)
+            pair_on(op, lo_edge)
+            if hi_edge[1] > hi_edge[0]:
+                pair_on(op, hi_edge)
         elif isinstance(op, ReduceOp) and op.x.root().shape == shape:
             if op.accumulate:
                 raise UnsupportedConstruct("slab decomposition: accumulating reduction")

@@ -1562,7 +1562,6 @@ class StarPairOp(Op):
         # slab placement (decomp.py): global plane of local plane 0, local
         # planes produced, global extent of dim 0; single device: whole array
         self.plane0, self.zrange, self.global_d0 = 0, None, None
-        self.zrange2 = None  # a second local plane range of the same launch (a slab's two edges)
         self._refresh()
 
     def _refresh(self):
@@ -1596,7 +1595,6 @@ class StarPairOp(Op):
                 d.dead_lo[r], d.dead_hi[r] = self.dead[r]
         d.plane0 = self.plane0
         d.zlo, d.zhi = self.zrange if self.zrange is not None else (0, self.Z.shape[0])
-        d.zlo2, d.zhi2 = self.zrange2 if self.zrange2 is not None else (0, 0)
         d.global_d0 = self.global_d0 if self.global_d0 is not None else self.Z.shape[0]
         self.desc = d
         self._ref = C.byref(d)

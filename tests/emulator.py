@@ -487,8 +487,6 @@ class Emulator:
 
         zsel = np.zeros(ys[0].shape, dtype=bool)
         zsel[zlo:zhi] = True
-        if rank == 3 and d.zhi2 > d.zlo2:
-            zsel[d.zlo2:d.zhi2] = True
         if d.flags & L.STAR_SKIP_ZCOPY:  # out-of-region copies are left to the twin
             zsel &= inside(d.b.lo, d.b.hi)
         zv[zsel] = Zn[zsel]
@@ -502,8 +500,6 @@ class Emulator:
                 dead[...] = False
             own = np.zeros(ys[0].shape, dtype=bool)
             own[zlo:zhi] = True
-            if rank == 3 and d.zhi2 > d.zlo2:
-                own[d.zlo2:d.zhi2] = True
             out = view(d.xout)
             sel = ~dead & own
             if d.flags & L.STAR_SKIP_XCOPY:

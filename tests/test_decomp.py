@@ -132,17 +132,16 @@ def _ops_of(world, rank, params):
 
 def test_timestep_splits_into_overlapped_interior_and_edges():
     """Per fused timestep: exchange, interior planes (no halo read, run while
-    the exchange is in flight), wait, then one launch over both edge plane
-    ranges."""
+    the exchange is in flight), wait, then the two edge plane ranges."""
     params = {"N": 64, "TSTEPS": 3}
     ops = _ops_of(4, 1, params)
     plan = SlabPlan(64, 4, 1)
     ol, oh = plan.own_local
     kinds = [type(op).__name__ for op in ops]
     first = kinds.index("HaloOp")
-    assert kinds[first:first + 4] == ["HaloOp", "StarPairOp", "HaloWaitOp", "StarPairOp"]
-    pairs = [op for op in ops[first:first + 4] if isinstance(op, StarPairOp)]
-    assert [(p.zrange, p.zrange2) for p in pairs] == [((ol + 2, oh - 2), None), ((ol, ol + 2), (oh - 2, oh))]
+    assert kinds[first:first + 5] == ["HaloOp", "StarPairOp", "HaloWaitOp", "StarPairOp", "StarPairOp"]
+    pairs = [op for op in ops[first:first + 5] if isinstance(op, StarPairOp)]
+    assert [p.zrange for p in pairs] == [(ol + 2, oh - 2), (ol, ol + 2), (oh - 2, oh)]
     # interior: its source planes [zlo - 2, zhi + 2) are owned, never halo
     zlo, zhi = pairs[0].zrange
     assert zlo - 2 >= ol and zhi + 2 <= oh
