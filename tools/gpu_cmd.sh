@@ -1,3 +1,5 @@
 cd $GRAFT_REPO_ROOT
-timeout 600 python -m pytest tests/test_gpu.py -q -x -k "3xtf32 or mlp or C4" 2>&1 | tail -2
-cd tools/lab; for r in 1 2; do python mm_time.py 2>&1 | cut -c1-60; done
+timeout 900 python -m pytest tests/test_gpu.py tests/test_gpu_r2.py -q -x -k "lockstep or slab or group or heat or c5 or C5" 2>&1 | tail -2
+timeout 120 python tools/time_star.py
+timeout 120 python tools/time_star.py
+timeout 300 python tools/host_overhead.py 2>&1 | grep -E "single|slab rank"
