@@ -115,6 +115,8 @@ def kernels_per_op(op) -> int:
 
     if isinstance(op, CopyOp):
         return 0  # device-to-device memcpy or elided alias, not a kernel
+    if isinstance(getattr(op, "edges", None), list):
+        return len(op.edges)  # a slab's edge ranges (decomp.EdgeOp)
     if op.family in ("halo", "halo_wait", "allreduce"):
         return 0  # NCCL communication, not one of the engine's kernels
     if isinstance(op, ReduceOp):

@@ -13,8 +13,12 @@ after star-pair fusion and ping-pong placement) is rewritten per rank:
     - the same kernel on the interior planes [own_lo + 2, own_hi - 2), which
       read no halo plane and run on the compute stream WHILE the exchange
       is in flight;
-    - a wait for the exchange (HaloWaitOp), then the kernel on the two edge
-      plane ranges (two planes at each slab end);
+    - the kernel on the two edge plane ranges (two planes at each slab end)
+      on the communication stream right behind the exchange, so a
+      timestep's edges run beside its interior (EdgeOp; StreamMark /
+      StreamJoin carry the cross-stream order: the interior of timestep
+      t + 1 waits for the edges of t, the edges of t wait for the interior
+      of t - 1, whose planes they read);
   masks / regions stay in global coordinates (plane0 in the descriptor);
 * a reduction over a decomposed array becomes a local reduction over the
   owned planes plus an all-reduce of the scalar (the reference's dependent
@@ -107,8 +111,9 @@ class HaloOp(Op):
 
     family = "halo"
 
-    def __init__(self, items, plan: SlabPlan, comm):
+    def __init__(self, items, plan: SlabPlan, comm, first=False):
         self.items, self.plan, self.comm = list(items), plan, comm
+        self.first = first  # first timestep of a chain: join the compute stream
         self.reads = tuple(b for b, _ in self.items)
         self.writes = tuple(b for b, _ in self.items)
 
@@ -144,15 +149,14 @@ class HaloOp(Op):
             return
         import torch
 
-        # the exchange starts once everything issued so far on the compute
-        # stream (the previous timestep's edge planes) is done, and runs
-        # beside the interior kernel that follows; HaloWaitOp joins it
-        compute = torch.cuda.current_stream(rt.device)
-        comm_stream.wait_stream(compute)
+        # the exchange sends the edge planes of the previous timestep, which
+        # ran on this stream; the first timestep of a chain starts from what
+        # the compute stream produced (inputs, seeds, broadcasts)
+        if self.first:
+            comm_stream.wait_stream(torch.cuda.current_stream(rt.device))
+            rt._ev_int = rt._ev_int_prev = rt._ev_edges = None
         with torch.cuda.stream(comm_stream):
             self.comm.run_exchange(ops)
-        self.done = torch.cuda.Event()
-        self.done.record(comm_stream)
 
     def algorithmic_bytes(self) -> int:
         """Bytes the exchange moves out of this rank (both neighbours)."""
@@ -160,26 +164,85 @@ class HaloOp(Op):
         return sum(nb * w * (b.numel // b.shape[0]) * b.itemsize for b, w in self.items)
 
 
-class HaloWaitOp(Op):
-    """The compute stream waits for a HaloOp's exchange (before the edge
-    planes, which read the halo)."""
+class StreamMark(Op):
+    """After a timestep's interior on the compute stream: record it (the
+    next timestep's edges read its planes)."""
 
     family = "halo_wait"
 
-    def __init__(self, halo: HaloOp):
-        self.halo = halo
+    def __init__(self):
         self.reads = self.writes = ()
 
     def launch(self, rt, stream):
-        ev = getattr(self.halo, "done", None)
-        if ev is not None:
-            import torch
+        if getattr(rt, "comm_stream", None) is None:
+            return
+        import torch
 
-            torch.cuda.current_stream(rt.device).wait_event(ev)
-            self.halo.done = None
+        ev = torch.cuda.Event()
+        ev.record(torch.cuda.current_stream(rt.device))
+        rt._ev_int_prev, rt._ev_int = getattr(rt, "_ev_int", None), ev
 
     def algorithmic_bytes(self) -> int:
         return 0
+
+
+class StreamJoin(Op):
+    """The compute stream waits for the latest edges (before a timestep's
+    interior, which reads the previous edge planes, and before any other
+    launch that reads the slab)."""
+
+    family = "halo_wait"
+
+    def __init__(self):
+        self.reads = self.writes = ()
+
+    def launch(self, rt, stream):
+        ev = getattr(rt, "_ev_edges", None)
+        if getattr(rt, "comm_stream", None) is None or ev is None:
+            return
+        import torch
+
+        torch.cuda.current_stream(rt.device).wait_event(ev)
+
+    def algorithmic_bytes(self) -> int:
+        return 0
+
+
+class EdgeOp(Op):
+    """A timestep's two edge plane ranges (StarPairOps) on the communication
+    stream right behind their exchange, beside the interior on the compute
+    stream; they wait for the previous timestep's interior."""
+
+    family = "star_pair"
+
+    def __init__(self, edges):
+        self.edges = list(edges)  # StarPairOps of the edge plane ranges
+        self.reads = tuple(b for p in self.edges for b in p.reads)
+        self.writes = tuple(b for p in self.edges for b in p.writes)
+
+    def prepare(self, rt):
+        for p in self.edges:
+            p.prepare(rt)
+
+    def launch(self, rt, stream):
+        comm_stream = getattr(rt, "comm_stream", None)
+        if comm_stream is None:
+            for p in self.edges:
+                p.launch(rt, stream)
+            return
+        import torch
+
+        prev = getattr(rt, "_ev_int_prev", None)
+        if prev is not None:
+            comm_stream.wait_event(prev)
+        for p in self.edges:
+            p.launch(rt, comm_stream.cuda_stream)
+        ev = torch.cuda.Event()
+        ev.record(comm_stream)
+        rt._ev_edges = ev
+
+    def algorithmic_bytes(self) -> int:
+        return sum(p.algorithmic_bytes() for p in self.edges)
 
 
 class AllReduceOp(Op):
@@ -246,15 +309,18 @@ def decompose(lw, plan: SlabPlan, comm) -> DistLowered:
     ol, oh = plan.own_local
     w = plan.halo
 
-    def pair_on(op, zr):
+    def pair_on(op, zr, emit=True):
         new = StarPairOp(op.a, op.b, op.fa, op.fb, op.xwrite, op.dead)
         new.X, new.Y, new.Z = loc(op.X), loc(op.Y), loc(op.Z)
         new.xout, new.zout = loc(op.xout), loc(op.zout)
         new.skip_zcopy, new.skip_xcopy = op.skip_zcopy, op.skip_xcopy
         new.plane0, new.zrange, new.global_d0 = plan.loc_lo, zr, plan.N
         new._refresh()
-        low.emit(new)
+        if emit:
+            low.emit(new)
+        return new
 
+    in_chain = False  # inside a run of timesteps (edges may be in flight)
     for op in ops:
         if isinstance(op, StarPairOp):
             if solo:
@@ -263,17 +329,24 @@ def decompose(lw, plan: SlabPlan, comm) -> DistLowered:
             items = [(loc(op.Y), 2)]
             if op.X.root() is not op.Y.root():
                 items.append((loc(op.X), 1))
-            halo = HaloOp(items, plan, comm)
-            low.emit(halo)
+            low.emit(HaloOp(items, plan, comm, first=not in_chain))
             # interior planes read no halo plane: they overlap the exchange
+            # and the edges (which follow the exchange on its stream)
             lo_edge, hi_edge = (ol, min(ol + w, oh)), (max(oh - w, ol + w), oh)
+            low.emit(StreamJoin())
             if hi_edge[0] > lo_edge[1]:
                 pair_on(op, (lo_edge[1], hi_edge[0]))
-            low.emit(HaloWaitOp(halo))
-            pair_on(op, lo_edge)
+            low.emit(StreamMark())
+            edges = [pair_on(op, lo_edge, emit=False)]
             if hi_edge[1] > hi_edge[0]:
-                pair_on(op, hi_edge)
-        elif isinstance(op, ReduceOp) and op.x.root().shape == shape:
+                edges.append(pair_on(op, hi_edge, emit=False))
+            low.emit(EdgeOp(edges))
+            in_chain = True
+            continue
+        if in_chain:
+            low.emit(StreamJoin())  # everything else runs after the edges
+            in_chain = False
+        if isinstance(op, ReduceOp) and op.x.root().shape == shape:
             if op.accumulate:
                 raise UnsupportedConstruct("slab decomposition: accumulating reduction")
             low.emit(ReduceOp(own_view(loc(op.x)), loc(op.out), False))
@@ -285,6 +358,8 @@ def decompose(lw, plan: SlabPlan, comm) -> DistLowered:
             low.emit(FillOp(loc(op.dst), whole_box(loc(op.dst).shape), op.value))
         else:
             raise UnsupportedConstruct(f"slab decomposition does not handle '{op.family}' launches")
+    if in_chain:
+        low.emit(StreamJoin())
     inputs = {k: loc(b) for k, b in lw.inputs.items()}
     outputs = {k: loc(b) for k, b in lw.outputs.items()}
     seed = loc(lw.seed_buf) if lw.seed_buf is not None else None
@@ -334,8 +409,10 @@ class SlabEngine:
         # one rank: no communication op, so the list is captured in a CUDA
         # graph like the single-device engine; several ranks run it eagerly
         # with the exchanges on a communication stream
+        # several ranks: launches on two streams, so no buffer may share
+        # memory with another by liveness in list order (reuse off)
         self.exe = Executable(self.dl.low, self.dl.inputs, self.dl.outputs, seed_buf=self.dl.seed_buf,
-                              device=self.device, use_graph=world == 1)
+                              device=self.device, use_graph=world == 1, reuse=world == 1)
         if world > 1:
             self.exe.comm_stream = torch.cuda.Stream(self.device)
         self.group = group

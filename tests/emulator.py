@@ -175,7 +175,10 @@ class Emulator:
         return a, o
 
     def run_op(self, op):
-        if isinstance(op, WavefrontOp):
+        if isinstance(getattr(op, "edges", None), list):  # decomp.EdgeOp: its star pairs in order
+            for p in op.edges:
+                self.run_op(p)
+        elif isinstance(op, WavefrontOp):
             self.wave(op.desc)
         elif isinstance(op, MapOp):
             self.map(op.desc)

@@ -15,7 +15,17 @@ import torch.multiprocessing as mp
 import emulator as E
 from paper_2509_02197_b200 import workloads as W
 from paper_2509_02197_b200.api import lower_gradient
-from paper_2509_02197_b200.decomp import AllReduceOp, HaloOp, HaloWaitOp, SlabPlan, StarPairOp, TorchComm, decompose
+from paper_2509_02197_b200.decomp import (
+    AllReduceOp,
+    EdgeOp,
+    HaloOp,
+    SlabPlan,
+    StarPairOp,
+    StreamJoin,
+    StreamMark,
+    TorchComm,
+    decompose,
+)
 
 
 def _free_port():
@@ -71,8 +81,11 @@ def _run_rank(rank, world, port, params, q):
                 op.launch(rt, None)
             elif isinstance(op, AllReduceOp):
                 op.run(view)
-            elif isinstance(op, HaloWaitOp):
-                op.launch(rt, None)  # no exchange in flight on the emulator: a no-op
+            elif isinstance(op, (StreamJoin, StreamMark)):
+                op.launch(rt, None)  # no streams on the emulator: a no-op
+            elif isinstance(op, EdgeOp):
+                for p in op.edges:  # the list order is a valid schedule
+                    em.run_op(p)
             else:
                 em.run_op(op)
         value = float(view(dl.outputs["value"]))
@@ -132,22 +145,27 @@ def _ops_of(world, rank, params):
 
 def test_timestep_splits_into_overlapped_interior_and_edges():
     """Per fused timestep: exchange, interior planes (no halo read, run while
-    the exchange is in flight), wait, then the two edge plane ranges."""
+    the exchange and the edges are in flight), then the two edge plane
+    ranges behind the exchange on its stream, with the cross-stream order
+    carried by a join (interior after the previous edges) and a mark."""
     params = {"N": 64, "TSTEPS": 3}
     ops = _ops_of(4, 1, params)
     plan = SlabPlan(64, 4, 1)
     ol, oh = plan.own_local
     kinds = [type(op).__name__ for op in ops]
     first = kinds.index("HaloOp")
-    assert kinds[first:first + 5] == ["HaloOp", "StarPairOp", "HaloWaitOp", "StarPairOp", "StarPairOp"]
-    pairs = [op for op in ops[first:first + 5] if isinstance(op, StarPairOp)]
+    assert kinds[first:first + 5] == ["HaloOp", "StreamJoin", "StarPairOp", "StreamMark", "EdgeOp"]
+    assert kinds[first + 5] == "HaloOp" and not ops[first + 5].first and ops[first].first
+    pairs = [ops[first + 2]] + ops[first + 4].edges
     assert [p.zrange for p in pairs] == [(ol + 2, oh - 2), (ol, ol + 2), (oh - 2, oh)]
+    # the chain ends with a join before anything else reads the slab
+    last = max(i for i, k in enumerate(kinds) if k == "EdgeOp")
+    assert kinds[last + 1] == "StreamJoin"
     # interior: its source planes [zlo - 2, zhi + 2) are owned, never halo
     zlo, zhi = pairs[0].zrange
     assert zlo - 2 >= ol and zhi + 2 <= oh
-    assert ops[first + 2].halo is ops[first]
 
 
 def test_single_rank_has_no_communication():
     ops = _ops_of(1, 0, {"N": 24, "TSTEPS": 3})
-    assert not any(isinstance(op, (HaloOp, HaloWaitOp, AllReduceOp)) for op in ops)
+    assert not any(isinstance(op, (HaloOp, StreamJoin, StreamMark, EdgeOp, AllReduceOp)) for op in ops)

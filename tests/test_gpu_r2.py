@@ -257,6 +257,96 @@ def test_run_planned_on_reference_cli_artifacts(cid):
 # -- multi-GPU path reachable from the drop-in API ---------------------------------
 
 
+class _PairComm:
+    """NCCL's grouped send/recv between the two ranks of a one-GPU test: each
+    rank's exchange records an event on its communication stream; once both
+    have posted, a copy stream waits for both, copies every peer send view
+    into the matching receive view (posting order) and both communication
+    streams wait for it -- the rendezvous NCCL performs. No kernel waits on
+    another; only stream events order the copies."""
+
+    def __init__(self):
+        self.posted, self.rank = {}, 0
+        self.xs = torch.cuda.Stream()
+
+    def plan_exchange(self, pairs):
+        return pairs
+
+    def run_exchange(self, ops):
+        ev = torch.cuda.Event()
+        ev.record()
+        self.posted[self.rank] = (ops, ev, torch.cuda.current_stream())
+        if len(self.posted) < 2:
+            return
+        for _, e, _ in self.posted.values():
+            self.xs.wait_event(e)
+        with torch.cuda.stream(self.xs):
+            for r in (0, 1):
+                rcvs = [rcv for peer, _, rcv in self.posted[r][0] if peer == 1 - r]
+                snds = [snd for peer, snd, _ in self.posted[1 - r][0] if peer == r]
+                for snd, rcv in zip(snds, rcvs):
+                    rcv.copy_(snd)
+        done = torch.cuda.Event()
+        done.record(self.xs)
+        for _, _, st in self.posted.values():
+            st.wait_event(done)
+        self.posted = {}
+
+    def exchange(self, pairs):
+        self.run_exchange(pairs)
+
+    def allreduce_sum(self, t):
+        self.posted.setdefault("sum", []).append(t)
+        if len(self.posted["sum"]) == 2:
+            a, b_ = self.posted.pop("sum")
+            tot = a + b_
+            a.copy_(tot)
+            b_.copy_(tot)
+
+
+def test_two_rank_slab_with_concurrent_edges_on_one_gpu():
+    """Two ranks' decomposed lists with their real stream schedule: the edge
+    ranges run on each rank's communication stream behind the exchange,
+    beside the interior on the compute stream (decomp.EdgeOp / StreamJoin /
+    StreamMark); repeated runs reproduce the single-device gradient."""
+    from paper_2509_02197_b200.api import lower_gradient
+    from paper_2509_02197_b200.decomp import SlabPlan, decompose
+    from paper_2509_02197_b200.runtime import Executable
+
+    params = {"N": 96, "TSTEPS": 8}
+    prog, b = _bundle("heat_3d")
+    shapes = W.input_shapes(prog, params)
+    full = W.make_inputs("heat_3d", prog, params, 0)
+    ref = gradient(prog, full, params, bundle=b)
+    comm = _PairComm()
+    ranks = []
+    for r in range(2):
+        lw = lower_gradient(prog, b, params, shapes, fuse_small=True)
+        plan = SlabPlan(params["N"], 2, r)
+        dl = decompose(lw, plan, comm)
+        exe = Executable(dl.low, dl.inputs, dl.outputs, seed_buf=dl.seed_buf, use_graph=False, reuse=False)
+        exe.comm_stream = torch.cuda.Stream()
+        ranks.append((plan, dl, exe))
+    stream = torch.cuda.current_stream()
+    for rep in range(3):
+        for plan, dl, exe in ranks:
+            exe.load_inputs({k: torch.from_numpy(np.ascontiguousarray(plan.local_slice(v))).cuda()
+                             for k, v in full.items()})
+            exe.view(dl.seed_buf).fill_(1.0)
+            exe.err.zero_()
+        for k in range(len(ranks[0][1].low.ops)):
+            for r, (plan, dl, exe) in enumerate(ranks):
+                comm.rank = r
+                dl.low.ops[k].launch(exe, stream.cuda_stream)
+        torch.cuda.synchronize()
+        for plan, dl, exe in ranks:
+            exe.check()
+            assert abs(exe.output_host("value") - ref.value) / abs(ref.value) <= 1e-12, rep
+            lo, hi = plan.own_local
+            got = exe.output("grad:A")[lo:hi].cpu().numpy()
+            assert rel_err(got, ref.grads["A"][plan.own_lo:plan.own_hi]) <= 1e-12, rep
+
+
 def test_gradient_over_a_process_group_single_rank():
     """``gradient(..., group=pg)`` slab-decomposes the caller's program over
     the group (decomp.SlabEngine). With one rank the list carries no

@@ -80,7 +80,9 @@ rows = exe.timed_eager(loc)
 tot = {}
 for fam, op, ms in rows:
     key = fam
-    if fam == "star_pair":
+    if isinstance(getattr(op, "edges", None), list):
+        key = f"edges ({len(op.edges)} ranges)"
+    elif fam == "star_pair":
         lo, hi = op.zrange
         key = f"star_pair[{hi - lo} planes]"
     tot.setdefault(key, [0, 0.0])
