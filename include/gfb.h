@@ -26,7 +26,7 @@
 extern "C" {
 #endif
 
-#define GFB_ABI_VERSION 10
+#define GFB_ABI_VERSION 11
 
 #define GFB_MAX_PARAMS 8    /* map parameters (iteration-space rank) */
 #define GFB_MAX_RANK 8      /* array rank */
@@ -245,6 +245,8 @@ typedef struct {
    * produced for local planes [zlo, zhi). Single device: 0, 0, dims[0]. */
   int64_t plane0, zlo, zhi;
   int64_t global_d0;
+  /* planes per CTA of the 3-D kernel (0: chosen from the launch's size) */
+  int64_t tpm_hint;
 } gfb_star_pair_desc;
 
 /*

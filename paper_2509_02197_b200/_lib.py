@@ -19,7 +19,7 @@ MAXCODE = 128
 MAXCONST = 24
 MAXTAPS = 32
 MAXSRCS = 4
-ABI_VERSION = 10
+ABI_VERSION = 11
 
 F32, F64 = 0, 1
 STAR_SKIP_ZCOPY, STAR_SKIP_XCOPY = 1, 2
@@ -86,7 +86,7 @@ class StarPairDesc(C.Structure):
     _fields_ = [("rank", i32), ("dtype", i32), ("xwrite", i32), ("flags", i32), ("dims", i64 * 3),
                 ("a", StarOp), ("b", StarOp), ("y", vp), ("xold", vp), ("xout", vp), ("zold", vp), ("zout", vp),
                 ("dead_lo", i64 * 3), ("dead_hi", i64 * 3), ("plane0", i64), ("zlo", i64), ("zhi", i64),
-                ("global_d0", i64)]
+                ("global_d0", i64), ("tpm_hint", i64)]
 
 
 class ContractDesc(C.Structure):

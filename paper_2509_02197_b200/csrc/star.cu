@@ -359,6 +359,7 @@ extern "C" int gfb_star_pair_launch(const gfb_star_pair_desc *s, void *stream) {
     d.zhi = 1;
   }
   if (d.zlo < 0 || d.zhi > d.d0 || d.zlo >= d.zhi) return set_error(GFB_EINVAL, "gfb_star_pair_launch: bad plane range");
+  d.tpm = (int32_t)(s->tpm_hint > 0 && s->tpm_hint < (1 << 20) ? s->tpm_hint : 0);
   fill_star_op(d.a, s->a, pad);
   fill_star_op(d.b, s->b, pad);
   d.y = s->y;

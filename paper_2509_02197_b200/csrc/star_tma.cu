@@ -753,7 +753,8 @@ static int launch_tma_m(const CUtensorMap &map, const StarPairDev &d, cudaStream
   StarPairDev dd = d;
   const int64_t tiles = ceil_div(d.d2, tPX) * ceil_div(d.d1, tPY), planes = d.zhi - d.zlo;
   const int64_t slots = 2 * (int64_t)sm_count();
-  dd.tpm = (int32_t)std::max<int64_t>(2, std::min<int64_t>(tPM, ceil_div(planes * tiles, slots)));
+  dd.tpm = d.tpm >= 2 ? std::min<int32_t>(d.tpm, tPM)  // the caller's choice (slab interiors)
+                      : (int32_t)std::max<int64_t>(2, std::min<int64_t>(tPM, ceil_div(planes * tiles, slots)));
   dim3 grid((unsigned)ceil_div(d.d2, tPX), (unsigned)ceil_div(d.d1, tPY), (unsigned)ceil_div(planes, dd.tpm));
   launch_pdl(star_pair_tma_kernel<T, HAS_I, MODES>, grid, dim3(tPX, tPY / kR), sm, st, map, dd);
   return check_launch("star_pair_tma");

@@ -1562,6 +1562,7 @@ class StarPairOp(Op):
         # slab placement (decomp.py): global plane of local plane 0, local
         # planes produced, global extent of dim 0; single device: whole array
         self.plane0, self.zrange, self.global_d0 = 0, None, None
+        self.tpm_hint = 0  # planes per CTA of the 3-D kernel (0: the launch chooses)
         self._refresh()
 
     def _refresh(self):
@@ -1596,6 +1597,7 @@ class StarPairOp(Op):
         d.plane0 = self.plane0
         d.zlo, d.zhi = self.zrange if self.zrange is not None else (0, self.Z.shape[0])
         d.global_d0 = self.global_d0 if self.global_d0 is not None else self.Z.shape[0]
+        d.tpm_hint = self.tpm_hint
         self.desc = d
         self._ref = C.byref(d)
 

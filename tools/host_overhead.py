@@ -56,7 +56,7 @@ dev = {k: torch.from_numpy(v).cuda() for k, v in full.items()}
 h, d = measure(exe, dev)
 print(f"single device, eager: {len(exe.ops)} ops, host {h:.2f} ms, device {d:.2f} ms per step")
 del exe
-for world in (2, 8):
+for world in (2, 4, 8):
     lw = lower_gradient(prog, b, params, shapes, fuse_small=True)
     plan = SlabPlan(params["N"], world, 0)
     dl = decompose(lw, plan, NullComm())
