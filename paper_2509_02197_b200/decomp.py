@@ -212,9 +212,10 @@ class StreamJoin(Op):
 class EdgeOp(Op):
     """A timestep's two edge plane ranges (StarPairOps) on the communication
     stream right behind their exchange, beside the interior on the compute
-    stream; they wait for the previous timestep's interior."""
+    stream; they wait for the previous timestep's interior. A family of its
+    own: per-launch CUDA-event timings on the compute stream do not see it."""
 
-    family = "star_pair"
+    family = "star_pair_edge"
 
     def __init__(self, edges):
         self.edges = list(edges)  # StarPairOps of the edge plane ranges
