@@ -158,6 +158,10 @@ def test_timestep_splits_into_overlapped_interior_and_edges():
     assert kinds[first + 5] == "HaloOp" and not ops[first + 5].first and ops[first].first
     pairs = [ops[first + 2]] + ops[first + 4].edges
     assert [p.zrange for p in pairs] == [(ol + 2, oh - 2), (ol, ol + 2), (oh - 2, oh)]
+    # the interior carries the slab's planes-per-CTA choice, the edges none
+    from paper_2509_02197_b200.decomp import SLAB_INTERIOR_TPM
+
+    assert [p.tpm_hint for p in pairs] == [SLAB_INTERIOR_TPM, 0, 0]
     # the chain ends with a join before anything else reads the slab
     last = max(i for i, k in enumerate(kinds) if k == "EdgeOp")
     assert kinds[last + 1] == "StreamJoin"
