@@ -1,4 +1,9 @@
 cd $GRAFT_REPO_ROOT
-timeout 900 python -m pytest tests/test_gpu.py tests/test_gpu_r2.py -q -x -k "concurrent_edges or lockstep or slab or group or c5 or heat" 2>&1 | tail -2
-timeout 120 python tools/time_star.py
-timeout 300 python tools/host_overhead.py 2>&1 | grep -E "single|slab rank 0 of"
+for mm in 2 1; do for f in 4 8 16; do
+  echo "== march_min $mm fill $f"; GFB_STENCIL_MARCH_MIN=$mm GFB_STENCIL_FILL=$f python tools/bench_all.py --only C2/heat_3d --no-cpu 2>&1 | python -c "
+import sys,json
+for l in sys.stdin:
+    try: d=json.loads(l)
+    except Exception: continue
+    print(d['config'], d['ms_per_step'])
+"; done; done

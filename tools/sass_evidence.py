@@ -1,6 +1,8 @@
 """SASS evidence of the Blackwell data paths in libgfb.so (cuobjdump):
 which kernels issue tcgen05 MMAs (UTCHMMA), TMEM loads (LDTM), TMA loads
-(UTMALDG), 1-D bulk copies (UBLKCP), mbarrier transaction waits (SYNCS), cp.async (LDGSTS) and DMMA.
+(UTMALDG), TMA stores / add-reductions (UTMASTG / UTMAREDG), 1-D bulk copies
+(UBLKCP), mbarrier transaction waits (SYNCS), cp.async (LDGSTS), DMMA and the
+programmatic-dependent-launch wait / trigger (ACQBULK / PREEXIT).
 
     python tools/sass_evidence.py > profiles/rNN_sass_evidence.txt
 """
@@ -10,8 +12,8 @@ import re
 import subprocess
 
 LIB = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "paper_2509_02197_b200", "libgfb.so")
-OPS = ["UTCHMMA", "UTCBAR", "LDTM", "UTMALDG", "UBLKCP", "SYNCS.ARRIVE.TRANS64", "SYNCS.PHASECHK.TRANS64.TRYWAIT", "LDGSTS",
-       "DMMA", "FFMA", "DFMA"]
+OPS = ["UTCHMMA", "UTCBAR", "LDTM", "UTMALDG", "UTMASTG", "UTMAREDG", "UBLKCP", "SYNCS.ARRIVE.TRANS64",
+       "SYNCS.PHASECHK.TRANS64.TRYWAIT", "LDGSTS", "DMMA", "FFMA", "DFMA", "ACQBULK", "PREEXIT"]
 
 sass = subprocess.run(["cuobjdump", "-sass", LIB], capture_output=True, text=True).stdout
 per = collections.OrderedDict()
