@@ -26,7 +26,7 @@
 extern "C" {
 #endif
 
-#define GFB_ABI_VERSION 11
+#define GFB_ABI_VERSION 12
 
 #define GFB_MAX_PARAMS 8    /* map parameters (iteration-space rank) */
 #define GFB_MAX_RANK 8      /* array rank */
@@ -458,6 +458,35 @@ int gfb_copy(void *dst, const void *src, int64_t bytes, void *stream);
  * `nplanes` contiguous outer-dimension planes starting at plane `p0`. */
 int gfb_plane_copy(void *dst, const void *src, int64_t plane_elems,
                    int32_t dtype, int64_t nplanes, void *stream);
+
+/* K15: the halo exchange of a slab-decomposed stencil timestep over NCCL
+ * (the engine's Python path posts the same exchange through
+ * torch.distributed, decomp.HaloOp). Each array is a contiguous local slab
+ * whose outermost dimension holds [own_lo - width, own_hi + width) halo and
+ * owned planes; the owned planes next to each neighbour are sent and the
+ * neighbour's are received into the halo:
+ *   lower: send [own_lo, own_lo + w)  recv [own_lo - w, own_lo)
+ *   upper: send [own_hi - w, own_hi)  recv [own_hi, own_hi + w)
+ * all in one NCCL group on `stream`. `nccl_comm` is the caller's ncclComm_t;
+ * NCCL is resolved at run time (the libnccl.so.2 already in the process, or
+ * the system one), so the library has no link-time NCCL dependency. */
+#define GFB_MAX_HALO 4
+typedef struct {
+  void *base;           /* local slab, contiguous, halo planes included */
+  int64_t plane_bytes;  /* bytes of one outermost-dimension plane */
+  int64_t planes;       /* local planes (halo included) */
+  int64_t own_lo, own_hi;
+  int64_t width;        /* halo planes per side */
+} gfb_halo_array;
+
+typedef struct {
+  int32_t n;            /* arrays exchanged in one group (<= GFB_MAX_HALO) */
+  int32_t lower, upper; /* neighbour ranks in the communicator; -1: none */
+  int32_t _pad;
+  gfb_halo_array a[GFB_MAX_HALO];
+} gfb_halo_desc;
+
+int gfb_halo_exchange(const gfb_halo_desc *d, void *nccl_comm, void *stream);
 
 #ifdef __cplusplus
 }

@@ -19,7 +19,7 @@ MAXCODE = 128
 MAXCONST = 24
 MAXTAPS = 32
 MAXSRCS = 4
-ABI_VERSION = 11
+ABI_VERSION = 12
 
 F32, F64 = 0, 1
 STAR_SKIP_ZCOPY, STAR_SKIP_XCOPY = 1, 2
@@ -120,6 +120,18 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libgfb.so")
 
 # (name, restype, argtypes)
+class HaloArray(C.Structure):
+    _fields_ = [("base", vp), ("plane_bytes", i64), ("planes", i64), ("own_lo", i64), ("own_hi", i64),
+                ("width", i64)]
+
+
+MAX_HALO = 4
+
+
+class HaloDesc(C.Structure):
+    _fields_ = [("n", i32), ("lower", i32), ("upper", i32), ("_pad", i32), ("a", HaloArray * MAX_HALO)]
+
+
 _SIGS = [
     ("gfb_abi_version", i32, []),
     ("gfb_last_error", C.c_char_p, []),
@@ -147,6 +159,7 @@ _SIGS = [
     ("gfb_rank2", i32, [i32, i64, i64, vp, vp, vp, vp, vp, i64, i32, vp]),
     ("gfb_copy", i32, [vp, vp, i64, vp]),
     ("gfb_plane_copy", i32, [vp, vp, i64, i32, i64, vp]),
+    ("gfb_halo_exchange", i32, [C.POINTER(HaloDesc), vp, vp]),
 ]
 
 EXPORTED = tuple(name for name, _, _ in _SIGS)
@@ -170,11 +183,11 @@ def load(path: str | None = None):
         fn.argtypes = args
     if lib.gfb_abi_version() != ABI_VERSION:
         raise EngineError(f"libgfb ABI {lib.gfb_abi_version()} != expected {ABI_VERSION}; rebuild")
-    sizes = (i64 * 11)()
-    n = lib.gfb_struct_sizes(sizes, 11)
+    sizes = (i64 * 12)()
+    n = lib.gfb_struct_sizes(sizes, 12)
     want = [C.sizeof(Space), C.sizeof(Operand), C.sizeof(MapDesc), C.sizeof(Term), C.sizeof(GatherDesc),
             C.sizeof(StencilDesc), C.sizeof(StarOp), C.sizeof(StarPairDesc), C.sizeof(ContractDesc),
-            C.sizeof(Map2Desc), C.sizeof(WaveDesc)]
+            C.sizeof(Map2Desc), C.sizeof(WaveDesc), C.sizeof(HaloDesc)]
     got = list(sizes[:n])
     if got[: len(want)] != want:
         raise EngineError(f"struct layout mismatch between gfb.h and _lib.py: C {got} vs ctypes {want}")

@@ -87,13 +87,13 @@ extern "C" int gfb_plane_copy(void *dst, const void *src, int64_t plane_elems, i
 // Layout self-check for foreign bindings (ctypes in _lib.py): sizes of the
 // descriptor structs in declaration order.
 extern "C" int gfb_struct_sizes(int64_t *out, int32_t cap) {
-  const int64_t s[11] = {(int64_t)sizeof(gfb_space),       (int64_t)sizeof(gfb_operand),
+  const int64_t s[12] = {(int64_t)sizeof(gfb_space),       (int64_t)sizeof(gfb_operand),
                         (int64_t)sizeof(gfb_map_desc),    (int64_t)sizeof(gfb_term),
                         (int64_t)sizeof(gfb_gather_desc), (int64_t)sizeof(gfb_stencil_desc),
                         (int64_t)sizeof(gfb_star_op),     (int64_t)sizeof(gfb_star_pair_desc),
                         (int64_t)sizeof(gfb_contract_desc), (int64_t)sizeof(gfb_map2_desc),
-                        (int64_t)sizeof(gfb_wave_desc)};
-  int n = cap < 11 ? cap : 11;
+                        (int64_t)sizeof(gfb_wave_desc),   (int64_t)sizeof(gfb_halo_desc)};
+  int n = cap < 12 ? cap : 12;
   for (int i = 0; i < n; ++i) out[i] = s[i];
   return n;
 }

@@ -347,6 +347,50 @@ def test_two_rank_slab_with_concurrent_edges_on_one_gpu():
             assert rel_err(got, ref.grads["A"][plan.own_lo:plan.own_hi]) <= 1e-12, rep
 
 
+def test_c_abi_halo_exchange_over_nccl():
+    """K15 (gfb_halo_exchange) through the C ABI with a real NCCL
+    communicator: one rank that is its own lower and upper neighbour (NCCL
+    send / receive to self), so each halo receives the owned planes the same
+    call sends: [own_lo, own_lo + w) into the lower halo, [own_hi - w, own_hi)
+    into the upper one, for two arrays in one group."""
+    import ctypes as C
+
+    from paper_2509_02197_b200 import _lib as L
+
+    nccl = C.CDLL("libnccl.so.2")  # the library torch loaded
+
+    class UniqueId(C.Structure):
+        _fields_ = [("internal", C.c_char * 128)]
+
+    uid = UniqueId()
+    assert nccl.ncclGetUniqueId(C.byref(uid)) == 0
+    comm = C.c_void_p()
+    torch.cuda.set_device(0)
+    assert nccl.ncclCommInitRank(C.byref(comm), 1, uid, 0) == 0
+    try:
+        lib = L.load()
+        planes, w = 12, 2
+        xs = [torch.arange(planes * 40, dtype=dt, device="cuda").reshape(planes, 40) + 1
+              for dt in (torch.float64, torch.float32)]
+        want = [x.clone() for x in xs]
+        for x in want:
+            x[:w] = x[w:2 * w]
+            x[planes - w:] = x[planes - 2 * w:planes - w]
+        d = L.HaloDesc()
+        d.n, d.lower, d.upper = 2, 0, 0
+        for i, x in enumerate(xs):
+            a = d.a[i]
+            a.base, a.plane_bytes, a.planes = x.data_ptr(), x[0].numel() * x.element_size(), planes
+            a.own_lo, a.own_hi, a.width = w, planes - w, w
+        stream = torch.cuda.current_stream().cuda_stream
+        L.check(lib.gfb_halo_exchange(C.byref(d), comm, stream), "halo_exchange")
+        torch.cuda.synchronize()
+        for x, y in zip(xs, want):
+            assert torch.equal(x, y)
+    finally:
+        nccl.ncclCommDestroy(comm)
+
+
 def test_gradient_over_a_process_group_single_rank():
     """``gradient(..., group=pg)`` slab-decomposes the caller's program over
     the group (decomp.SlabEngine). With one rank the list carries no

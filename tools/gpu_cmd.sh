@@ -1,5 +1,2 @@
 cd $GRAFT_REPO_ROOT
-for r in 1 2; do
-timeout 120 python tools/time_star.py
-GFB_LIBRARY=$GRAFT_REPO_ROOT/build/var/tpy64.so timeout 120 python tools/time_star.py
-done
+timeout 600 python -m pytest tests/test_gpu_r2.py tests/test_abi.py -q -x -k "halo or abi or declared or workspace" 2>&1 | tail -3
