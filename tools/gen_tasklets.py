@@ -189,6 +189,15 @@ def body_code(words, segs, umask=0) -> str:
                     if a[0] != nm:
                         stmts.append(f"{nm}[0] = {a[0]}[0];")
                     stmts.append(f"m2_binary<T, 1>({BIN[op]}, {nm}, {b[0]}, vm ? 1u : 0u, bad);")
+                elif op == L.OP_DIV and b[1] and not a[1]:
+                    # a vector over a per-lane scalar (a row value): one
+                    # reciprocal per lane, then products (<= 1.5 ulp from
+                    # the correctly rounded quotient; zero still raises)
+                    if a[0] != f"s{depth}":
+                        stmts.append(f"m2_copy<T, V>(s{depth}, {a[0]});")
+                    maxd = max(maxd, depth + 1)
+                    stmts.append(f"m2_div_scalar<T, V>(s{depth}, {b[0]}[0], vm, bad);")
+                    stack.append((f"s{depth}", False))
                 else:
                     # destination slot s{depth}; the right operand goes to s{depth + 1}
                     bv = as_vec(b, depth + 1) if b[1] else b[0]
@@ -230,6 +239,13 @@ def generate() -> str:
         "__device__ __forceinline__ void m2_copy(T (&x)[V], const T (&y)[V]) {",
         "#pragma unroll",
         "  for (int v = 0; v < V; ++v) x[v] = y[v];",
+        "}",
+        "template <typename T, int V>",
+        "__device__ __forceinline__ void m2_div_scalar(T (&x)[V], T c, uint32_t vm, uint32_t &bad) {",
+        "  if (vm && c == T(0)) bad |= GFB_EBIT_DIV0;",
+        "  const T rc = T(1) / c;",
+        "#pragma unroll",
+        "  for (int v = 0; v < V; ++v) x[v] = x[v] * rc;",
         "}",
         "",
     ]

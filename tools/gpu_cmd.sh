@@ -1,2 +1,9 @@
 cd $GRAFT_REPO_ROOT
-timeout 600 python -m pytest tests/test_gpu_r2.py tests/test_abi.py -q -x -k "halo or abi or declared or workspace" 2>&1 | tail -3
+timeout 1500 python -m pytest tests -m gpu -q -x 2>&1 | tail -2
+for r in 1 2; do python tools/bench_all.py --only C4/softmax,C4/mlp --no-cpu --plans 2>&1 | python -c "
+import sys,json
+for l in sys.stdin:
+    try: d=json.loads(l)
+    except Exception: continue
+    print(d['config'], d['ms_per_step'])
+"; done
