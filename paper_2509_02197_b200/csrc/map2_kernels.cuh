@@ -546,15 +546,31 @@ struct M2Cached {
   }
 };
 
-template <int U>
-__device__ __forceinline__ void m2_prefetch(const gfb_map2_desc &d, const int32_t (&row)[U], const int32_t (&i0)[U],
-                                            const uint32_t (&vm)[U], float (&c)[U][kM2CacheIn][4]) {
+// the inputs of U items for a generated body: input count and which inputs
+// are row scalars (stride 0 along the row on the 16-byte paths) are
+// compile-time, so the loads of all items of one input issue back to back
+template <typename Body, int U>
+__device__ __forceinline__ void m2_prefetch_static(const gfb_map2_desc &d, const int32_t (&row)[U],
+                                                   const int32_t (&i0)[U], const uint32_t (&vm)[U],
+                                                   float (&c)[U][kM2CacheIn][4]) {
+  static_assert(Body::kNIn <= kM2CacheIn, "generated ILP bodies take at most four inputs");
 #pragma unroll
-  for (int u = 0; u < U; ++u) {
-    M2FetchVec4 f{d, row[u], i0[u], vm[u]};
+  for (int k = 0; k < Body::kNIn; ++k) {
+    const gfb_m2_operand &o = d.in[k];
+    const float *base = (const float *)o.base + (int32_t)o.c0;
+    const int32_t s0 = (int32_t)o.s[0];
 #pragma unroll
-    for (int k = 0; k < kM2CacheIn; ++k)
-      if (k < d.n_in) f(k, c[u][k]);
+    for (int u = 0; u < U; ++u) {
+      const float *p = base + s0 * row[u];
+      if (!vm[u]) {
+        c[u][k][0] = c[u][k][1] = c[u][k][2] = c[u][k][3] = 1.f;
+      } else if ((Body::kRowScalar >> k) & 1u) {
+        c[u][k][0] = c[u][k][1] = c[u][k][2] = c[u][k][3] = p[0];
+      } else {
+        const float4 q = *reinterpret_cast<const float4 *>(p + i0[u]);
+        c[u][k][0] = q.x, c[u][k][1] = q.y, c[u][k][2] = q.z, c[u][k][3] = q.w;
+      }
+    }
   }
 }
 
@@ -585,11 +601,12 @@ __global__ void __launch_bounds__(256) map2_pointwise_ilp_kernel(const __grid_co
       }
     }
     float c[U][kM2CacheIn][4];
-    m2_prefetch<U>(d, row, i0, vm, c);
+    m2_prefetch_static<Body, U>(d, row, i0, vm, c);
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       M2Cached fetch{c[u]};
-      for (int o = 0; o < d.n_out; ++o) {
+#pragma unroll
+      for (int o = 0; o < Body::kNOut; ++o) {
         float r[4];
         Body::template eval<float, 4>(d, o, fetch, vm[u], r);
         if (!vm[u]) continue;
@@ -624,7 +641,7 @@ __global__ void __launch_bounds__(256) map2_reduce_row_ilp_kernel(const __grid_c
       vm[u] = (row[u] < rows && i0[u] < E) ? 0xFu : 0u;
     }
     float c[U][kM2CacheIn][4];
-    m2_prefetch<U>(d, row, i0, vm, c);
+    m2_prefetch_static<Body, U>(d, row, i0, vm, c);
     float acc[U];
 #pragma unroll
     for (int u = 0; u < U; ++u) {

@@ -256,6 +256,8 @@ def generate() -> str:
         out += [
             f"struct GenBody{i} {{  // mode {mode}, {'fp64' if f64 else 'fp32'}, {n_in} inputs, {len(segs)} outputs"
             + (f", row-scalar inputs 0x{umask:x}" if umask else ""),
+            f"  static constexpr int kNIn = {n_in}, kNOut = {len(segs)};",
+            f"  static constexpr uint32_t kRowScalar = 0x{umask:x}u;  // inputs with stride 0 along the row",
             "  template <typename T, int V, typename F>",
             "  static __device__ __forceinline__ void eval(const gfb_map2_desc &d, int o, F &fetch, uint32_t vm,",
             "                                              T (&r)[V]) {",
