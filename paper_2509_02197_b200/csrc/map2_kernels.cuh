@@ -577,7 +577,7 @@ __device__ __forceinline__ void m2_prefetch_static(const gfb_map2_desc &d, const
 // pointwise, U warp items per iteration (generated bodies, n_in <= 4)
 template <typename Body, bool FLAT, int U>
 __global__ void __launch_bounds__(256) map2_pointwise_ilp_kernel(const __grid_constant__ gfb_map2_desc d,
-                                                                 int32_t rows, int32_t cpr) {
+                                                                 int32_t rows, int32_t cpr, uint64_t magic) {
   pdl_wait();  // programmatic dependent launch: global memory after the wait
   PdlRelease pdl_release_;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
@@ -591,7 +591,8 @@ __global__ void __launch_bounds__(256) map2_pointwise_ilp_kernel(const __grid_co
       const int32_t it = it0 + u;
       if (FLAT) {
         const int32_t f = it * 128 + lane * 4;
-        row[u] = f / E;
+        // f / E by a precomputed multiplier (exact for f < 2^24, E < 128)
+        row[u] = (int32_t)(((uint64_t)(uint32_t)f * magic) >> 40);
         i0[u] = f - row[u] * E;
         vm[u] = (it < items && row[u] < rows) ? 0xFu : 0u;
       } else {
@@ -796,10 +797,11 @@ inline int launch_map2(const gfb_map2_desc &d, cudaStream_t st) {
               const int64_t items = E < 128 ? ceil_div(rows * E, 128) : rows * cpr;
               const int64_t blocks = std::max<int64_t>(std::min<int64_t>(ceil_div(items, kM2Warps * U), cap * 4), 1);
               if (E < 128)
-                launch_pdl(map2_pointwise_ilp_kernel<Body, true, U>, (unsigned)blocks, 256, 0, st, d, (int32_t)rows, 1);
+                launch_pdl(map2_pointwise_ilp_kernel<Body, true, U>, (unsigned)blocks, 256, 0, st, d, (int32_t)rows, 1,
+                           (((uint64_t)1 << 40) + (uint64_t)E - 1) / (uint64_t)E);
               else
                 launch_pdl(map2_pointwise_ilp_kernel<Body, false, U>, (unsigned)blocks, 256, 0, st, d, (int32_t)rows,
-                                                                                              (int32_t)cpr);
+                           (int32_t)cpr, (uint64_t)0);
               return check_launch("map2");
             }
           }
