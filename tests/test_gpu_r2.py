@@ -238,6 +238,29 @@ def test_finite_difference_oracle_across_branch_boundaries(cid):
         assert np.allclose(got[ok], want[ok], rtol=1e-6, atol=1e-6), (cid, got, want)
 
 
+def test_finite_difference_probe_batches_in_chunks():
+    """The FD probe batch is cut into chunks of at most FD_CHUNK_BYTES;
+    batch elements are independent, so any chunking gives the same
+    gradient (here: 3 probe pairs per chunk against one batch)."""
+    from paper_2509_02197_b200 import fd
+
+    prog, _ = _bundle("elem_branch", R2)
+    inputs = {"x": np.random.default_rng(4).uniform(0.4, 1.6, 12)}
+    whole = fd.finite_difference_gradient(prog, inputs, {"N": 12})["x"]
+    old = fd.FD_CHUNK_BYTES
+    try:
+        fd.FD_CHUNK_BYTES = 2 * 8 * 12 * 3
+        chunked = fd.finite_difference_gradient(prog, inputs, {"N": 12})["x"]
+    finally:
+        fd.FD_CHUNK_BYTES = old
+    assert np.array_equal(np.isnan(whole), np.isnan(chunked))
+    ok = ~np.isnan(whole)
+    assert np.array_equal(whole[ok], chunked[ok])
+    # elements near 1.0 straddle the branch; the rest are 2 or 2x
+    x = inputs["x"]
+    assert np.allclose(whole[ok], np.where(x < 1.0, 2.0, 2.0 * x)[ok], rtol=1e-6)
+
+
 # -- the reference CLI's plan artifacts ------------------------------------------------
 
 
