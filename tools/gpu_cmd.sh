@@ -1,2 +1,4 @@
-cd $GRAFT_REPO_ROOT
-timeout 600 python -m pytest tests/test_gpu_r2.py -q -x -k "finite_difference" 2>&1 | tail -2
+cd $GRAFT_REPO_ROOT/tools/lab
+for cfg in "4 1" "2 1" "2 2" "1 2" "8 1"; do set -- $cfg
+  echo "== div $1 mul $2"; GFB_TC_SPLIT_DIV=$1 GFB_TC_SPLIT_MUL=$2 python mm_time.py 2>&1 | grep -E "x@W1|r2@W3|z3g@W3\^T|z1g@W1\^T|r1@W2|z2g@W2\^T|total" | cut -c1-60
+done
