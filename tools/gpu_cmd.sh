@@ -1,3 +1,9 @@
 cd $GRAFT_REPO_ROOT
-timeout 600 python -c "import __graft_entry__ as g; g.smoke(); print('smoke ok')" 2>&1 | tail -1
-timeout 1500 python -m pytest tests -m gpu -q 2>&1 | tail -1
+for m in 1 2 4; do
+  echo "== small_mul $m"; GFB_STAR_SMALL_MUL=$m python tools/bench_all.py --only C2/jacobi_2d,C1/jacobi_2d --no-cpu 2>&1 | python -c "
+import sys,json
+for l in sys.stdin:
+    try: d=json.loads(l)
+    except Exception: continue
+    print(d['config'], d['ms_per_step'])
+"; done
